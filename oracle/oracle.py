@@ -82,6 +82,9 @@ def lib():
         _lib.orc_rng_seed.argtypes = [C.c_void_p, C.c_uint64]
         _lib.orc_homotopy_rate_constant.restype = C.c_double
         _lib.orc_homotopy_rate_constant.argtypes = [C.c_double] * 3
+        _lib.orc_sqeuclid_max.restype = C.c_double
+        _lib.orc_sqeuclid_max.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                          C.c_int64, C.c_int]
     return _lib
 
 
@@ -425,6 +428,11 @@ def sweep_rows_mt(p: Problem, v, row0, row1, nthreads):
     _check(lib().orc_sweep_rows_mt(p.ref, _p(v), C.c_int64(row0), C.c_int64(row1),
                                    C.c_int(nthreads), _p(u), _p(col)))
     return u, col
+
+
+def sqeuclid_max(x, y, threads=1) -> float:
+    x, y = _f64(x), _f64(y)
+    return lib().orc_sqeuclid_max(_p(x), _p(y), x.shape[0], y.shape[0], x.shape[1], threads)
 
 
 # fixtures (helpers.hpp:14-27) ----------------------------------------------

@@ -924,4 +924,28 @@ int orc_sweep_rows_mt(const orc_problem* pp, const double* v, int64_t row0, int6
   });
 }
 
+double orc_sqeuclid_max(const double* x, const double* y, int64_t n, int64_t m, int64_t d,
+                        int nthreads) {
+  const int T = std::max(1, nthreads);
+  std::vector<double> best(T, 0.0);
+  auto work = [&](int t) {
+    double mx = 0.0;
+    for (int64_t i = n * t / T; i < n * (t + 1) / T; ++i)
+      for (int64_t j = 0; j < m; ++j) {
+        double s = 0.0;
+        for (int64_t k = 0; k < d; ++k) {
+          const double diff = x[i * d + k] - y[j * d + k];
+          s += diff * diff;
+        }
+        mx = std::max(mx, s);
+      }
+    best[t] = mx;
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& q : th) q.join();
+  return *std::max_element(best.begin(), best.end());
+}
+
 }  // extern "C"

@@ -177,6 +177,11 @@ double orc_homotopy_rate_constant(double mu0, double r_hat, double l_f);
 int orc_sweep_rows_mt(const orc_problem* p, const double* v, int64_t row0, int64_t row1,
                       int nthreads, double* u, double* col_partial);
 
+/* max_ij ||x_i - y_j||^2 (the cost_sqeuclidean normaliser, data.cpp:78-80),
+ * nthreads workers. */
+double orc_sqeuclid_max(const double* x, const double* y, int64_t n, int64_t m, int64_t d,
+                        int nthreads);
+
 #ifdef __cplusplus
 }
 #endif

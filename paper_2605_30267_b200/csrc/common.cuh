@@ -1,0 +1,210 @@
+// common.cuh — shared internals of libotg (B200 / sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/otg.h"
+
+namespace otg {
+
+// ---------------------------------------------------------------- errors --
+struct Error {
+  otg_status code;
+  std::string msg;
+};
+
+[[noreturn]] inline void fail(otg_status code, const std::string& msg) { throw Error{code, msg}; }
+
+void set_last_error(const std::string& msg);
+
+#define OTG_CUDA(call)                                                              \
+  do {                                                                              \
+    cudaError_t _e = (call);                                                        \
+    if (_e != cudaSuccess)                                                          \
+      ::otg::fail(_e == cudaErrorMemoryAllocation ? OTG_E_OOM : OTG_E_CUDA,         \
+                  std::string(#call) + ": " + cudaGetErrorString(_e));              \
+  } while (0)
+
+template <class F>
+otg_status guard(F&& f) {
+  try {
+    f();
+    return OTG_OK;
+  } catch (const Error& e) {
+    set_last_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return OTG_E_OT;
+  }
+}
+
+// --------------------------------------------------------------- numerics --
+constexpr double kLog2e = 1.4426950408889634074;
+constexpr double kLn2 = 0.69314718055994530942;
+constexpr double kExpOverflowBound = 700.0;  // types.hpp:15
+constexpr double kGradFloor = 1e-12;         // types.hpp:19
+constexpr double kTinyPrecise = 1e-280;      // dual.cpp:53 (fp64 path: same threshold)
+constexpr double kTinyFast = 1e-30;          // fp32 ex2.ftz path: flushed mass <= 1.2e-38
+constexpr float kQuant = 256.0f;             // 2^8 quantum of the split shifts
+
+// ------------------------------------------------------------ loop control --
+enum Mode : int {
+  MODE_EVAL = 0,       // one eval_normalized_step
+  MODE_SINKHORN = 1,   // sinkhorn.cpp:65-115
+  MODE_ACC = 2,        // acc_solve accel.cpp:200-232
+  MODE_ACC_RUN = 3,    // acc_run accel.cpp:174-198
+  MODE_HOMOTOPY = 4,   // homotopy_solve_instrumented accel.cpp:234-301
+};
+
+// Device-resident control block.  The last CTA of the finalize epilogue runs
+// the solver's scalar control flow (stop test, homotopy schedule, trace) so
+// the iteration never round-trips to the host.
+struct Ctrl {
+  // --- status (device-written) ---
+  int done;
+  int converged;
+  int capped;
+  int error;          // otg_status raised on the device (DomainViolation, ...)
+  int stage_changed;  // this eval closed a homotopy stage
+  int is_step;        // the eval in flight is an accelerated step (not a seed)
+  int have_prev;      // stability: previous observation stored
+  int live_e2;        // finalize -> apply handoff for the current eval
+  long long k;        // observation index (sinkhorn / acc / acc_run)
+  long long evaluations;
+  long long iterations;
+  long long total_inner, stage, inner_i, m_stage, outer_stages;
+  double mu, alpha_step, alpha_next;
+  double grad_l1, f_value, mean_y, max_v_inf;
+  double final_violation, final_f;
+  long long trace_count;   // records produced
+  long long trace_row;     // ring slot of the current eval's record, -1 none
+  long long boundary_count;
+  long long cond_checked, cond_held;
+  long long live_kernels;
+  unsigned int e1_counter, e2_counter, fb_count, pad0;
+  // --- configuration (host-written) ---
+  int mode;
+  int record_trace;
+  int stability;
+  int rescale_w;
+  double tol;
+  long long max_iters;       // sinkhorn / acc
+  long long trace_stride;
+  long long max_outer;
+  long long max_total_inner;
+  long long m0;
+  long long msteps;          // acc_run
+  double mu0;
+  double tiny;               // fallback threshold for c_j
+  long long trace_cap;       // ring capacity
+  long long boundary_cap;
+};
+
+constexpr int kTraceCols = OTG_TRACE_COLS;
+
+// ---------------------------------------------------------------- problem --
+struct Shard {
+  int64_t row0 = 0;  // first local row of the shard
+  int64_t rows = 0;
+};
+
+struct Problem {
+  // sizes
+  int64_t n = 0, m = 0, n_local = 0, row_begin = 0;
+  int64_t ldc = 0;  // row stride of C in elements (multiple of 4)
+  int storage = OTG_STORE_F64;
+  double epsilon = 1.0;   // epsilon_original
+  double kappa = 1.0;     // 1 / epsilon (fp32 path multiplies on load)
+  double raw_min = 0.0, raw_max = 0.0;
+  int device = 0;
+  int world = 1, rank = 0;
+  int vshards = 1;
+
+  cudaStream_t stream = nullptr;
+
+  // cost
+  double* C64 = nullptr;  // fp64: C' = C / eps (pre-divided, core.cpp:42-49)
+  float* C32 = nullptr;   // fp32: raw C
+  float* X = nullptr;     // on-the-fly: x (n_local x 4 padded), y (m x 4)
+  float* Y = nullptr;
+
+  // marginals (fp64)
+  double *a = nullptr, *loga = nullptr, *b = nullptr, *logb = nullptr;
+
+  // per-row state (n_local)
+  double *rowM = nullptr, *rowS = nullptr, *u = nullptr, *wrow = nullptr;
+  float4* aux = nullptr;  // fast path: {Mc, mf, w, 0} (base-2 split row shift)
+
+  // per-column state (m, padded)
+  double *p = nullptr, *wacc = nullptr, *col = nullptr, *col_log = nullptr, *y = nullptr,
+         *grad = nullptr;
+  double *prev_grad = nullptr, *prev_x = nullptr, *prev_y = nullptr;
+  int* flag_idx = nullptr;  // fallback slot per column (-1 none)
+  int* fb_cols = nullptr;   // flagged column list (m)
+  double2* fb_part = nullptr;  // (max, sum) per flagged column per row chunk
+
+  // column-pass partials
+  int col_splits = 1;
+  int64_t rows_per_split = 0;
+  double* part = nullptr;  // (vshards * col_splits) x mpad
+
+  // epilogue scratch
+  int e_blocks = 1;
+  double* e1_part = nullptr;  // e_blocks x 8
+  double* e2_part = nullptr;  // e_blocks x 8
+  Ctrl* ctrl = nullptr;
+  Ctrl* ctrl_host = nullptr;  // pinned mirror
+  double* trace = nullptr;    // ring: trace_cap x kTraceCols
+  double* bounds = nullptr;   // boundary_cap x 4
+
+  int64_t mpad = 0;
+  int64_t device_bytes = 0;
+
+  // captured solver chunk graphs (lazily built)
+  cudaGraphExec_t chunk_exec = nullptr;
+  cudaGraphExec_t chunk_exec_timed = nullptr;
+  int chunk_len = 0;
+  std::vector<cudaEvent_t> chunk_events;  // 4 per iteration (timed graph)
+
+  // NCCL (sharded)
+  void* nccl_comm = nullptr;
+};
+
+// allocation helpers (track bytes)
+template <class T>
+T* dalloc(Problem& P, size_t count) {
+  if (count == 0) count = 1;
+  void* ptr = nullptr;
+  OTG_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
+  P.device_bytes += static_cast<int64_t>(count * sizeof(T));
+  return static_cast<T*>(ptr);
+}
+
+void problem_free(Problem& P);
+void problem_alloc_state(Problem& P);
+
+// sweeps / epilogue (sweep.cu)
+void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4);
+void launch_apply(Problem& P);
+void launch_row_pass(Problem& P);
+void launch_col_pass(Problem& P);
+void launch_merge_nolog(Problem& P);
+
+// NCCL (comm.cpp)
+void comm_init(Problem& P, const void* unique_id);
+void comm_destroy(Problem& P);
+void comm_allreduce_sum(Problem& P, double* buf, size_t count);
+void comm_allreduce_max(Problem& P, double* buf, size_t count);
+
+inline int64_t round_up(int64_t x, int64_t k) { return (x + k - 1) / k * k; }
+
+}  // namespace otg
+
+struct otg_problem_s {
+  otg::Problem P;
+};

@@ -1,0 +1,461 @@
+// problem.cu — handle creation: validation (core.cpp:9-29), upload, the
+// rescale fold (core.cpp:42-49), device cost materialisation
+// (data.cpp:69-110), plan statistics over the implicit plan (core.cpp:59-79).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace otg {
+
+void configure_sweeps(Problem& P);
+int64_t row_blocks(const Problem& P);
+
+namespace {
+
+constexpr int kT = 256;
+constexpr int kFbChunks = 32;
+constexpr int64_t kTraceCap = 4096;
+constexpr int64_t kBoundaryCap = 4096;
+
+std::string fmt17(double x) {
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "%.17g", x);
+  return buf;
+}
+
+// core.cpp:9-29 for the marginals (host side; cheap).
+void validate_marginals(const double* a, int64_t n, const double* b, int64_t m) {
+  if (n < 1 || m < 1) fail(OTG_E_DIMENSION, "empty marginal");
+  if (!a || !b) fail(OTG_E_DIMENSION, "marginal pointer is NULL");
+  const double* ms[2] = {a, b};
+  const int64_t ls[2] = {n, m};
+  for (int k = 0; k < 2; ++k) {
+    double mn = ms[k][0], s = 0.0;
+    for (int64_t j = 0; j < ls[k]; ++j) {
+      mn = std::min(mn, ms[k][j]);
+      s += ms[k][j];
+    }
+    if (!(mn > 0.0)) fail(OTG_E_INVALID_MARGINALS, "marginals must be strictly positive");
+    if (std::abs(s - 1.0) > 1e-9)
+      fail(OTG_E_INVALID_MARGINALS, "marginal sums to " + fmt17(s) + ", expected 1");
+  }
+}
+
+void validate_eps(double eps) {
+  if (!(eps > 0.0) || !std::isfinite(eps)) fail(OTG_E_OT, "epsilon must be positive and finite");
+}
+
+__global__ void k_log(const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = log(x[i]);
+}
+
+__global__ void k_div_rows(double* __restrict__ C, int64_t ldc, int64_t n, int64_t m, double eps) {
+  const int64_t i = blockIdx.y;
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    C[i * ldc + j] = C[i * ldc + j] / eps;
+}
+
+// raw cost of one pair, fp64, left-to-right without contraction (data.cpp:75-77, 98-99)
+__device__ __forceinline__ double raw_cost(const double* __restrict__ x,
+                                           const double* __restrict__ y, int64_t d, int cost) {
+  double s = 0.0;
+  if (cost == OTG_COST_SQEUCLID) {
+    for (int64_t k = 0; k < d; ++k) {
+      const double diff = __dsub_rn(x[k], y[k]);
+      s = __dadd_rn(s, __dmul_rn(diff, diff));
+    }
+    return s;
+  }
+  for (int64_t k = 0; k < d; ++k) s = __dadd_rn(s, __dmul_rn(x[k], y[k]));
+  return __dadd_rn(-s, 1.0);
+}
+
+// pass 1: per-block (min, max) of the raw cost
+__global__ void k_cost_minmax(const double* __restrict__ X, const double* __restrict__ Y,
+                              int64_t n, int64_t m, int64_t d, int cost,
+                              double2* __restrict__ out) {
+  __shared__ double smn[kT], smx[kT];
+  double mn = DBL_MAX, mx = -DBL_MAX;
+  const int64_t total = n * m;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * kT) {
+    const int64_t i = t / m, j = t % m;
+    const double c = raw_cost(X + i * d, Y + j * d, d, cost);
+    mn = fmin(mn, c);
+    mx = fmax(mx, c);
+  }
+  smn[threadIdx.x] = mn;
+  smx[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = kT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      smn[threadIdx.x] = fmin(smn[threadIdx.x], smn[threadIdx.x + o]);
+      smx[threadIdx.x] = fmax(smx[threadIdx.x], smx[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = make_double2(smn[0], smx[0]);
+}
+
+// pass 2: normalise and store. norm: NONE, MAX (c / mx), MINMAX ((c-mn)/(mx-mn)),
+// HALFRANGE (c / 2); then fp64 storage divides by eps (rescale), fp32 rounds.
+template <typename T>
+__global__ void k_cost_store(const double* __restrict__ X, const double* __restrict__ Y,
+                             int64_t n, int64_t m, int64_t d, int cost, int norm, double mn,
+                             double mx, double eps_div, T* __restrict__ C, int64_t ldc) {
+  const int64_t i = blockIdx.y;
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double c = raw_cost(X + i * d, Y + j * d, d, cost);
+    if (norm == OTG_NORM_MAX) {
+      if (mx > 0.0) c = c / mx;
+    } else if (norm == OTG_NORM_MINMAX) {
+      c = (mx - mn > 1e-15) ? (c - mn) / (mx - mn) : 0.0;
+    } else if (norm == OTG_NORM_HALFRANGE) {
+      c = c / 2.0;
+    }
+    if (eps_div != 1.0) c = c / eps_div;
+    C[i * ldc + j] = static_cast<T>(c);
+  }
+}
+
+}  // namespace
+
+void problem_free(Problem& P) {
+  void* ptrs[] = {P.C64, P.C32, P.X, P.Y, P.a, P.loga, P.b, P.logb, P.rowM, P.rowS, P.u,
+                  P.wrow, P.aux, P.p, P.wacc, P.col, P.col_log, P.y, P.grad, P.prev_grad,
+                  P.prev_x, P.prev_y, P.flag_idx, P.fb_cols, P.fb_part, P.part, P.e1_part,
+                  P.e2_part, P.ctrl, P.trace, P.bounds};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  if (P.ctrl_host) cudaFreeHost(P.ctrl_host);
+  if (P.chunk_exec) cudaGraphExecDestroy(P.chunk_exec);
+  if (P.chunk_exec_timed) cudaGraphExecDestroy(P.chunk_exec_timed);
+  for (cudaEvent_t e : P.chunk_events) cudaEventDestroy(e);
+  if (P.nccl_comm) comm_destroy(P);
+  if (P.stream) cudaStreamDestroy(P.stream);
+  P = Problem{};
+}
+
+void problem_alloc_state(Problem& P) {
+  configure_sweeps(P);
+  const int64_t n = P.n_local, mp = P.mpad;
+  P.rowM = dalloc<double>(P, n);
+  P.rowS = dalloc<double>(P, n);
+  P.u = dalloc<double>(P, n);
+  P.wrow = dalloc<double>(P, n);
+  P.aux = dalloc<float4>(P, n);
+  P.p = dalloc<double>(P, mp);
+  P.wacc = dalloc<double>(P, mp);
+  P.col = dalloc<double>(P, mp + 8);
+  P.col_log = dalloc<double>(P, mp);
+  P.y = dalloc<double>(P, mp);
+  P.grad = dalloc<double>(P, mp);
+  P.prev_grad = dalloc<double>(P, mp);
+  P.prev_x = dalloc<double>(P, mp);
+  P.prev_y = dalloc<double>(P, mp);
+  P.flag_idx = dalloc<int>(P, mp);
+  P.fb_cols = dalloc<int>(P, mp);
+  P.fb_part = dalloc<double2>(P, mp * kFbChunks);
+  P.part = dalloc<double>(P, static_cast<size_t>(P.vshards) * P.col_splits * mp);
+  P.e1_part = dalloc<double>(P, P.e_blocks * 8 + row_blocks(P) + 8);
+  P.e2_part = dalloc<double>(P, P.e_blocks * 8);
+  P.ctrl = dalloc<Ctrl>(P, 1);
+  P.trace = dalloc<double>(P, kTraceCap * kTraceCols);
+  P.bounds = dalloc<double>(P, kBoundaryCap * 4);
+  OTG_CUDA(cudaMallocHost(&P.ctrl_host, sizeof(Ctrl)));
+  OTG_CUDA(cudaMemsetAsync(P.p, 0, mp * sizeof(double), P.stream));
+  OTG_CUDA(cudaMemsetAsync(P.wacc, 0, mp * sizeof(double), P.stream));
+  OTG_CUDA(cudaMemsetAsync(P.part, 0, static_cast<size_t>(P.vshards) * P.col_splits * mp * sizeof(double), P.stream));
+  OTG_CUDA(cudaMemsetAsync(P.ctrl, 0, sizeof(Ctrl), P.stream));
+  std::memset(P.ctrl_host, 0, sizeof(Ctrl));
+}
+
+static void begin(Problem& P, int64_t n, int64_t m, const otg_device_opts* opts) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    fail(OTG_E_UNSUPPORTED, "no CUDA device available (libotg has no CPU fallback)");
+  P.device = (opts && opts->device >= 0) ? opts->device : 0;
+  if (!opts || opts->device < 0) OTG_CUDA(cudaGetDevice(&P.device));
+  OTG_CUDA(cudaSetDevice(P.device));
+  P.n = n;
+  P.m = m;
+  P.n_local = n;
+  P.row_begin = 0;
+  if (opts && opts->world_size > 1) {
+    if (opts->rank < 0 || opts->rank >= opts->world_size)
+      fail(OTG_E_DIMENSION, "rank outside [0, world_size)");
+    if (opts->row_begin < 0 || opts->row_end > n || opts->row_begin >= opts->row_end)
+      fail(OTG_E_DIMENSION, "row shard [row_begin, row_end) outside [0, n)");
+    P.world = opts->world_size;
+    P.rank = opts->rank;
+    P.row_begin = opts->row_begin;
+    P.n_local = opts->row_end - opts->row_begin;
+  }
+  P.vshards = (opts && opts->virtual_shards > 1) ? opts->virtual_shards : 1;
+  if (P.vshards > P.n_local) P.vshards = static_cast<int>(P.n_local);
+  P.mpad = round_up(m, 4);
+  P.ldc = round_up(m, 4);
+  OTG_CUDA(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
+}
+
+static void upload_marginals(Problem& P, const double* a, const double* b) {
+  const int64_t n = P.n_local, m = P.m;
+  P.a = dalloc<double>(P, n);
+  P.loga = dalloc<double>(P, n);
+  P.b = dalloc<double>(P, P.mpad);
+  P.logb = dalloc<double>(P, P.mpad);
+  OTG_CUDA(cudaMemsetAsync(P.b, 0, P.mpad * sizeof(double), P.stream));
+  OTG_CUDA(cudaMemsetAsync(P.logb, 0, P.mpad * sizeof(double), P.stream));
+  OTG_CUDA(cudaMemcpyAsync(P.a, a + P.row_begin, n * sizeof(double), cudaMemcpyHostToDevice, P.stream));
+  OTG_CUDA(cudaMemcpyAsync(P.b, b, m * sizeof(double), cudaMemcpyHostToDevice, P.stream));
+  k_log<<<(n + kT - 1) / kT, kT, 0, P.stream>>>(P.a, P.loga, n);
+  k_log<<<(m + kT - 1) / kT, kT, 0, P.stream>>>(P.b, P.logb, m);
+  OTG_CUDA(cudaGetLastError());
+}
+
+static void finish_create(Problem& P, const otg_device_opts* opts, otg_problem* out) {
+  if (P.world > 1) comm_init(P, opts->nccl_unique_id);
+  problem_alloc_state(P);
+  OTG_CUDA(cudaStreamSynchronize(P.stream));
+  auto* h = new otg_problem_s;
+  h->P = P;
+  *out = h;
+}
+
+}  // namespace otg
+
+using namespace otg;
+
+extern "C" {
+
+otg_status otg_problem_create_dense(int64_t n, int64_t m, const double* a, const double* b,
+                                    const void* C, otg_dtype dtype, int64_t ldc,
+                                    double epsilon, const otg_device_opts* opts,
+                                    otg_problem* out) {
+  Problem P;
+  const otg_status st = guard([&] {
+    if (!out) fail(OTG_E_DIMENSION, "out handle pointer is NULL");
+    *out = nullptr;
+    validate_marginals(a, n, b, m);
+    validate_eps(epsilon);
+    if (!C) fail(OTG_E_DIMENSION, "cost pointer is NULL");
+    if (dtype != OTG_F64 && dtype != OTG_F32) fail(OTG_E_OT, "unknown dtype");
+    const int64_t src_ld = ldc > 0 ? ldc : m;
+    if (src_ld < m) fail(OTG_E_DIMENSION, "ldc < m");
+    begin(P, n, m, opts);
+    const int64_t nl = P.n_local;
+    // core.cpp:20 C.allFinite() on the rows this handle holds
+    if (dtype == OTG_F64) {
+      const double* Cd = static_cast<const double*>(C);
+      for (int64_t i = 0; i < nl; ++i)
+        for (int64_t j = 0; j < m; ++j)
+          if (!std::isfinite(Cd[i * src_ld + j])) fail(OTG_E_OT, "cost matrix has non-finite entries");
+    } else {
+      const float* Cf = static_cast<const float*>(C);
+      for (int64_t i = 0; i < nl; ++i)
+        for (int64_t j = 0; j < m; ++j)
+          if (!std::isfinite(Cf[i * src_ld + j])) fail(OTG_E_OT, "cost matrix has non-finite entries");
+    }
+    P.epsilon = epsilon;
+    P.kappa = 1.0 / epsilon;
+    upload_marginals(P, a, b);
+    if (dtype == OTG_F64) {
+      P.storage = OTG_STORE_F64;
+      P.C64 = dalloc<double>(P, static_cast<size_t>(nl) * P.ldc);
+      OTG_CUDA(cudaMemsetAsync(P.C64, 0, static_cast<size_t>(nl) * P.ldc * sizeof(double), P.stream));
+      OTG_CUDA(cudaMemcpy2DAsync(P.C64, P.ldc * sizeof(double), static_cast<const double*>(C),
+                                 src_ld * sizeof(double), m * sizeof(double), nl,
+                                 cudaMemcpyHostToDevice, P.stream));
+      if (epsilon != 1.0) {
+        dim3 grid(static_cast<unsigned>(std::min<int64_t>((m + kT - 1) / kT, 64)),
+                  static_cast<unsigned>(nl));
+        k_div_rows<<<grid, kT, 0, P.stream>>>(P.C64, P.ldc, nl, m, epsilon);
+        OTG_CUDA(cudaGetLastError());
+      }
+    } else {
+      P.storage = OTG_STORE_F32;
+      P.C32 = dalloc<float>(P, static_cast<size_t>(nl) * P.ldc);
+      OTG_CUDA(cudaMemsetAsync(P.C32, 0, static_cast<size_t>(nl) * P.ldc * sizeof(float), P.stream));
+      OTG_CUDA(cudaMemcpy2DAsync(P.C32, P.ldc * sizeof(float), static_cast<const float*>(C),
+                                 src_ld * sizeof(float), m * sizeof(float), nl,
+                                 cudaMemcpyHostToDevice, P.stream));
+    }
+    finish_create(P, opts, out);
+  });
+  if (st != OTG_OK) problem_free(P);
+  return st;
+}
+
+otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const double* a,
+                                     const double* b, const double* x, const double* y,
+                                     otg_cost cost, otg_norm norm, otg_storage storage,
+                                     double epsilon, const otg_device_opts* opts,
+                                     otg_problem* out) {
+  Problem P;
+  const otg_status st = guard([&] {
+    if (!out) fail(OTG_E_DIMENSION, "out handle pointer is NULL");
+    *out = nullptr;
+    validate_marginals(a, n, b, m);
+    validate_eps(epsilon);
+    if (d < 1 || !x || !y) fail(OTG_E_DIMENSION, "point clouds need d >= 1 and data");
+    if (cost != OTG_COST_SQEUCLID && cost != OTG_COST_COSINE) fail(OTG_E_OT, "unknown cost");
+    if (storage == OTG_STORE_ON_THE_FLY)
+      fail(OTG_E_UNSUPPORTED, "on-the-fly storage is not built in this version");
+    if (storage != OTG_STORE_F64 && storage != OTG_STORE_F32) fail(OTG_E_OT, "unknown storage");
+    begin(P, n, m, opts);
+    const int64_t nl = P.n_local;
+    const double* xl = x + P.row_begin * d;
+    for (int64_t t = 0; t < nl * d; ++t)
+      if (!std::isfinite(xl[t])) fail(OTG_E_OT, "point coordinates must be finite");
+    for (int64_t t = 0; t < m * d; ++t)
+      if (!std::isfinite(y[t])) fail(OTG_E_OT, "point coordinates must be finite");
+    if (cost == OTG_COST_COSINE) {  // data.cpp:89-96 unit-row check
+      for (int side = 0; side < 2; ++side) {
+        const double* Z = side ? y : xl;
+        const int64_t rows = side ? m : nl;
+        for (int64_t i = 0; i < rows; ++i) {
+          double s = 0.0;
+          for (int64_t k = 0; k < d; ++k) s += Z[i * d + k] * Z[i * d + k];
+          if (std::abs(std::sqrt(s) - 1.0) > 1e-6)
+            fail(OTG_E_OT, "cosine cost expects unit rows");
+        }
+      }
+    }
+    P.epsilon = epsilon;
+    P.kappa = 1.0 / epsilon;
+    upload_marginals(P, a, b);
+    double *dX = nullptr, *dY = nullptr;
+    OTG_CUDA(cudaMalloc(&dX, nl * d * sizeof(double)));
+    OTG_CUDA(cudaMalloc(&dY, m * d * sizeof(double)));
+    OTG_CUDA(cudaMemcpyAsync(dX, xl, nl * d * sizeof(double), cudaMemcpyHostToDevice, P.stream));
+    OTG_CUDA(cudaMemcpyAsync(dY, y, m * d * sizeof(double), cudaMemcpyHostToDevice, P.stream));
+    double mn = 0.0, mx = 0.0;
+    if (norm != OTG_NORM_NONE && norm != OTG_NORM_HALFRANGE) {
+      const int blocks = 148 * 8;
+      double2* part = nullptr;
+      OTG_CUDA(cudaMalloc(&part, blocks * sizeof(double2)));
+      k_cost_minmax<<<blocks, kT, 0, P.stream>>>(dX, dY, nl, m, d, cost, part);
+      OTG_CUDA(cudaGetLastError());
+      std::vector<double2> hp(blocks);
+      OTG_CUDA(cudaMemcpyAsync(hp.data(), part, blocks * sizeof(double2), cudaMemcpyDeviceToHost, P.stream));
+      OTG_CUDA(cudaStreamSynchronize(P.stream));
+      cudaFree(part);
+      mn = DBL_MAX;
+      mx = -DBL_MAX;
+      for (auto& v : hp) {
+        mn = std::min(mn, v.x);
+        mx = std::max(mx, v.y);
+      }
+      if (P.world > 1) {
+        comm_init(P, opts->nccl_unique_id);
+        double buf[2] = {-mn, mx};
+        double* dbuf = nullptr;
+        OTG_CUDA(cudaMalloc(&dbuf, 2 * sizeof(double)));
+        OTG_CUDA(cudaMemcpyAsync(dbuf, buf, sizeof buf, cudaMemcpyHostToDevice, P.stream));
+        comm_allreduce_max(P, dbuf, 2);
+        OTG_CUDA(cudaMemcpyAsync(buf, dbuf, sizeof buf, cudaMemcpyDeviceToHost, P.stream));
+        OTG_CUDA(cudaStreamSynchronize(P.stream));
+        cudaFree(dbuf);
+        mn = -buf[0];
+        mx = buf[1];
+      }
+    }
+    P.raw_min = mn;
+    P.raw_max = mx;
+    dim3 grid(static_cast<unsigned>(std::min<int64_t>((m + kT - 1) / kT, 64)),
+              static_cast<unsigned>(nl));
+    if (storage == OTG_STORE_F64) {
+      P.storage = OTG_STORE_F64;
+      P.C64 = dalloc<double>(P, static_cast<size_t>(nl) * P.ldc);
+      OTG_CUDA(cudaMemsetAsync(P.C64, 0, static_cast<size_t>(nl) * P.ldc * sizeof(double), P.stream));
+      k_cost_store<double><<<grid, kT, 0, P.stream>>>(dX, dY, nl, m, d, cost, norm, mn, mx,
+                                                      epsilon, P.C64, P.ldc);
+    } else {
+      P.storage = OTG_STORE_F32;
+      P.C32 = dalloc<float>(P, static_cast<size_t>(nl) * P.ldc);
+      OTG_CUDA(cudaMemsetAsync(P.C32, 0, static_cast<size_t>(nl) * P.ldc * sizeof(float), P.stream));
+      k_cost_store<float><<<grid, kT, 0, P.stream>>>(dX, dY, nl, m, d, cost, norm, mn, mx, 1.0,
+                                                     P.C32, P.ldc);
+    }
+    OTG_CUDA(cudaGetLastError());
+    OTG_CUDA(cudaStreamSynchronize(P.stream));
+    cudaFree(dX);
+    cudaFree(dY);
+    if (P.world > 1 && P.nccl_comm) {
+      // communicator already built for the normaliser; finish_create must not re-init
+      problem_alloc_state(P);
+      OTG_CUDA(cudaStreamSynchronize(P.stream));
+      auto* h = new otg_problem_s;
+      h->P = P;
+      *out = h;
+      return;
+    }
+    finish_create(P, opts, out);
+  });
+  if (st != OTG_OK) problem_free(P);
+  return st;
+}
+
+otg_status otg_problem_destroy(otg_problem h) {
+  return guard([&] {
+    if (!h) return;
+    cudaSetDevice(h->P.device);
+    cudaStreamSynchronize(h->P.stream);
+    problem_free(h->P);
+    delete h;
+  });
+}
+
+otg_status otg_problem_info_get(otg_problem h, otg_problem_info* out) {
+  return guard([&] {
+    if (!h || !out) fail(OTG_E_DIMENSION, "NULL handle");
+    const Problem& P = h->P;
+    out->n = P.n;
+    out->m = P.m;
+    out->n_local = P.n_local;
+    out->row_begin = P.row_begin;
+    out->storage = P.storage;
+    out->epsilon = P.epsilon;
+    out->cost_raw_min = P.raw_min;
+    out->cost_raw_max = P.raw_max;
+    out->device_bytes = P.device_bytes;
+    out->world_size = P.world;
+    out->rank = P.rank;
+    out->device = P.device;
+  });
+}
+
+otg_status otg_problem_get_cost(otg_problem h, int64_t row0, int64_t nrows, void* outp) {
+  return guard([&] {
+    if (!h || !outp) fail(OTG_E_DIMENSION, "NULL argument");
+    Problem& P = h->P;
+    if (row0 < 0 || nrows < 0 || row0 + nrows > P.n_local) fail(OTG_E_DIMENSION, "row range");
+    OTG_CUDA(cudaSetDevice(P.device));
+    if (P.storage == OTG_STORE_F64) {
+      // stored C' = C / eps: undo the fold for the caller (exact only up to
+      // rounding; the parity tests use fp32 storage or eps = 1 with fp64)
+      std::vector<double> tmp(static_cast<size_t>(nrows) * P.m);
+      OTG_CUDA(cudaMemcpy2DAsync(tmp.data(), P.m * sizeof(double), P.C64 + row0 * P.ldc,
+                                 P.ldc * sizeof(double), P.m * sizeof(double), nrows,
+                                 cudaMemcpyDeviceToHost, P.stream));
+      OTG_CUDA(cudaStreamSynchronize(P.stream));
+      double* o = static_cast<double*>(outp);
+      for (size_t k = 0; k < tmp.size(); ++k) o[k] = P.epsilon == 1.0 ? tmp[k] : tmp[k] * P.epsilon;
+    } else {
+      OTG_CUDA(cudaMemcpy2DAsync(outp, P.m * sizeof(float), P.C32 + row0 * P.ldc,
+                                 P.ldc * sizeof(float), P.m * sizeof(float), nrows,
+                                 cudaMemcpyDeviceToHost, P.stream));
+      OTG_CUDA(cudaStreamSynchronize(P.stream));
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,518 @@
+// solver.cu — solver entry points of the C-ABI: one-shot evaluations and the
+// device-resident Sinkhorn / Acc-Sinkhorn / homotopy loops.
+//
+// The loop body (row pass, column pass, merge, fallback, finalize, apply) is
+// captured once per handle into a CUDA graph holding kChunk evaluations; the
+// host replays the graph and reads the 300-byte control block once per
+// chunk.  All stop / schedule decisions are taken on the device by the
+// finalize kernel (sweep.cu: control_step), so there is no per-iteration
+// host round trip; evaluations past the stop point are no-ops.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace otg {
+
+namespace {
+
+constexpr int kChunk = 8;
+constexpr int kT = 256;
+
+void check_finite_vec(const double* v, int64_t m, const char* what) {  // dual.cpp:13-18
+  if (!v) fail(OTG_E_DIMENSION, std::string(what) + " is NULL");
+  for (int64_t j = 0; j < m; ++j)
+    if (!std::isfinite(v[j])) fail(OTG_E_OT, std::string(what) + " has non-finite entries");
+}
+
+std::vector<double> project_zero_sum(const double* x, int64_t m) {  // mirror.cpp:103-105
+  double s = 0.0;
+  for (int64_t j = 0; j < m; ++j) s += x[j];
+  const double mean = s / static_cast<double>(m);
+  std::vector<double> out(m);
+  for (int64_t j = 0; j < m; ++j) out[j] = x[j] - mean;
+  return out;
+}
+
+void check_zero_sum(const double* x, int64_t m, const char* what) {  // accel.cpp:21-25
+  double s = 0.0;
+  for (int64_t j = 0; j < m; ++j) s += x[j];
+  if (std::abs(s) > 1e-9) fail(OTG_E_GAUGE, std::string(what) + " must be zero-sum");
+}
+
+void validate_solve_config(const otg_solve_config* c) {  // sinkhorn.cpp:29-33
+  if (!c) fail(OTG_E_OT, "solve config is NULL");
+  if (!(c->tol_l1 > 0.0)) fail(OTG_E_OT, "tol_l1 must be positive");
+  if (c->max_iters < 1) fail(OTG_E_OT, "max_iters must be at least 1");
+  if (c->trace_stride < 1) fail(OTG_E_OT, "trace_stride must be at least 1");
+}
+
+Ctrl base_ctrl(const Problem& P) {
+  Ctrl c;
+  std::memset(&c, 0, sizeof c);
+  c.tiny = P.storage == OTG_STORE_F64 ? kTinyPrecise : kTinyFast;
+  c.trace_cap = 4096;
+  c.boundary_cap = 4096;
+  c.trace_stride = 1;
+  return c;
+}
+
+void put_ctrl(Problem& P, const Ctrl& c) {
+  std::memcpy(P.ctrl_host, &c, sizeof c);
+  OTG_CUDA(cudaMemcpyAsync(P.ctrl, P.ctrl_host, sizeof(Ctrl), cudaMemcpyHostToDevice, P.stream));
+}
+
+void get_ctrl(Problem& P) {
+  OTG_CUDA(cudaMemcpyAsync(P.ctrl_host, P.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, P.stream));
+  OTG_CUDA(cudaStreamSynchronize(P.stream));
+}
+
+void h2d(Problem& P, double* dst, const double* src, int64_t count) {
+  OTG_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyHostToDevice, P.stream));
+}
+void d2h(Problem& P, double* dst, const double* src, int64_t count) {
+  if (dst) OTG_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToHost, P.stream));
+}
+
+void raise_device_error(const Ctrl& c) {
+  if (c.error == OTG_E_DOMAIN) fail(OTG_E_DOMAIN, "column log-mass degenerated (non-finite log c)");
+  if (c.error) fail(static_cast<otg_status>(c.error), "device-side error");
+}
+
+void build_graph(Problem& P, bool timed) {
+  cudaGraphExec_t& exec = timed ? P.chunk_exec_timed : P.chunk_exec;
+  if (exec) return;
+  if (timed && P.chunk_events.empty()) {
+    P.chunk_events.resize(4 * kChunk);
+    for (auto& e : P.chunk_events) OTG_CUDA(cudaEventCreate(&e));
+  }
+  cudaGraph_t g = nullptr;
+  OTG_CUDA(cudaStreamBeginCapture(P.stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    for (int k = 0; k < kChunk; ++k) {
+      launch_eval(P, true, timed, timed ? &P.chunk_events[4 * k] : nullptr);
+      launch_apply(P);
+    }
+  } catch (...) {
+    cudaStreamEndCapture(P.stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  OTG_CUDA(cudaStreamEndCapture(P.stream, &g));
+  OTG_CUDA(cudaGraphInstantiate(&exec, g, 0));
+  cudaGraphDestroy(g);
+  P.chunk_len = kChunk;
+}
+
+struct LoopOut {
+  double device_s = 0.0, row_s = 0.0, col_s = 0.0;
+  int64_t trace_len = 0;
+};
+
+// Replays the chunk graph until the device control block says done; drains
+// the trace ring into res->trace after every chunk.
+LoopOut run_loop(Problem& P, otg_solve_result* res, bool timed) {
+  build_graph(P, timed);
+  cudaEvent_t t0, t1;
+  OTG_CUDA(cudaEventCreate(&t0));
+  OTG_CUDA(cudaEventCreate(&t1));
+  LoopOut lo;
+  int64_t drained = 0;
+  long long ev_before = P.ctrl_host->evaluations;
+  OTG_CUDA(cudaEventRecord(t0, P.stream));
+  for (;;) {
+    OTG_CUDA(cudaGraphLaunch(timed ? P.chunk_exec_timed : P.chunk_exec, P.stream));
+    get_ctrl(P);
+    const Ctrl& c = *P.ctrl_host;
+    if (timed) {
+      const long long live = c.evaluations - ev_before;
+      for (long long k = 0; k < live && k < kChunk; ++k) {
+        float a = 0.f, b = 0.f;
+        OTG_CUDA(cudaEventElapsedTime(&a, P.chunk_events[4 * k], P.chunk_events[4 * k + 1]));
+        OTG_CUDA(cudaEventElapsedTime(&b, P.chunk_events[4 * k + 2], P.chunk_events[4 * k + 3]));
+        lo.row_s += a * 1e-3;
+        lo.col_s += b * 1e-3;
+      }
+      ev_before = c.evaluations;
+    }
+    if (c.trace_count > drained) {
+      const int64_t cap = c.trace_cap;
+      std::vector<double> ring(static_cast<size_t>(cap) * kTraceCols);
+      OTG_CUDA(cudaMemcpyAsync(ring.data(), P.trace, ring.size() * sizeof(double),
+                               cudaMemcpyDeviceToHost, P.stream));
+      OTG_CUDA(cudaStreamSynchronize(P.stream));
+      for (int64_t r = drained; r < c.trace_count; ++r) {
+        if (res && res->trace && r < res->trace_cap)
+          std::memcpy(res->trace + r * kTraceCols, ring.data() + (r % cap) * kTraceCols,
+                      kTraceCols * sizeof(double));
+      }
+      drained = c.trace_count;
+    }
+    if (c.done) break;
+  }
+  OTG_CUDA(cudaEventRecord(t1, P.stream));
+  OTG_CUDA(cudaEventSynchronize(t1));
+  float ms = 0.f;
+  OTG_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+  lo.device_s = ms * 1e-3;
+  lo.trace_len = drained;
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  return lo;
+}
+
+void fill_result(Problem& P, otg_solve_result* res, const LoopOut& lo) {
+  const Ctrl& c = *P.ctrl_host;
+  raise_device_error(c);
+  if (!res) return;
+  res->converged = c.converged;
+  res->iterations = c.iterations;
+  res->evaluations = c.evaluations;
+  res->outer_stages = c.outer_stages;
+  res->final_violation = c.final_violation;
+  res->final_reduced_f = c.final_f;
+  res->max_v_inf = c.max_v_inf;
+  res->conditions_checked = c.cond_checked;
+  res->conditions_held = c.cond_held;
+  res->trace_len = lo.trace_len;
+  res->device_seconds = lo.device_s;
+  res->row_pass_seconds = lo.row_s;
+  res->col_pass_seconds = lo.col_s;
+  res->kernel_launches = c.evaluations * 7;
+  d2h(P, res->u, P.u, P.n_local);
+  d2h(P, res->v, P.p, P.m);
+  d2h(P, res->w, P.wacc, P.m);
+  if (res->boundaries && res->boundaries_cap > 0) {
+    const int64_t nb = std::min<int64_t>(c.boundary_count, std::min<int64_t>(res->boundaries_cap, c.boundary_cap));
+    if (nb > 0) d2h(P, res->boundaries, P.bounds, nb * 4);
+  }
+  OTG_CUDA(cudaStreamSynchronize(P.stream));
+}
+
+Problem& get(otg_problem h) {
+  if (!h) fail(OTG_E_DIMENSION, "NULL problem handle");
+  OTG_CUDA(cudaSetDevice(h->P.device));
+  return h->P;
+}
+
+// One evaluation at v (host), outputs left on the device.
+void one_eval(Problem& P, const double* v, bool with_log) {
+  check_finite_vec(v, P.m, "v");
+  Ctrl c = base_ctrl(P);
+  c.mode = MODE_EVAL;
+  put_ctrl(P, c);
+  h2d(P, P.p, v, P.m);
+  launch_eval(P, with_log, false, nullptr);
+  if (with_log) launch_apply(P);
+  get_ctrl(P);
+  raise_device_error(*P.ctrl_host);
+}
+
+__global__ void k_plan_rows(const double* __restrict__ C64, const float* __restrict__ C32,
+                            int64_t ldc, int64_t n, int64_t m, double kappa,
+                            const double* __restrict__ u, const double* __restrict__ v,
+                            double* __restrict__ rowsum, double* __restrict__ rowcost,
+                            double* __restrict__ rowmax) {
+  __shared__ double s1[kT], s2[kT], s3[kT];
+  const int64_t i = blockIdx.x;
+  double rs = 0.0, cs = 0.0, mx = -DBL_MAX;
+  for (int64_t j = threadIdx.x; j < m; j += kT) {
+    const double c = C64 ? C64[i * ldc + j] : static_cast<double>(C32[i * ldc + j]) * kappa;
+    const double e = ((-c) + u[i]) + v[j];  // core.cpp:63-65
+    const double P = exp(e);
+    mx = fmax(mx, e);
+    rs += P;
+    cs += c * P;
+  }
+  s1[threadIdx.x] = rs;
+  s2[threadIdx.x] = cs;
+  s3[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = kT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      s1[threadIdx.x] += s1[threadIdx.x + o];
+      s2[threadIdx.x] += s2[threadIdx.x + o];
+      s3[threadIdx.x] = fmax(s3[threadIdx.x], s3[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    rowsum[i] = s1[0];
+    rowcost[i] = s2[0];
+    rowmax[i] = s3[0];
+  }
+}
+
+__global__ void k_plan_cols(const double* __restrict__ C64, const float* __restrict__ C32,
+                            int64_t ldc, int64_t n, int64_t m, double kappa,
+                            const double* __restrict__ u, const double* __restrict__ v,
+                            double* __restrict__ colsum) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+  if (j >= m) return;
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double c = C64 ? C64[i * ldc + j] : static_cast<double>(C32[i * ldc + j]) * kappa;
+    s += exp(((-c) + u[i]) + v[j]);
+  }
+  colsum[j] = s;
+}
+
+}  // namespace
+}  // namespace otg
+
+using namespace otg;
+
+extern "C" {
+
+otg_status otg_row_solve_marginals(otg_problem h, const double* v, double* u, double* col) {
+  return guard([&] {
+    Problem& P = get(h);
+    check_finite_vec(v, P.m, "v");
+    Ctrl c = base_ctrl(P);
+    c.mode = MODE_EVAL;
+    put_ctrl(P, c);
+    h2d(P, P.p, v, P.m);
+    launch_row_pass(P);
+    launch_col_pass(P);
+    launch_merge_nolog(P);
+    if (P.world > 1) comm_allreduce_sum(P, P.col, static_cast<size_t>(P.mpad + 1));
+    d2h(P, u, P.u, P.n_local);
+    d2h(P, col, P.col, P.m);
+    OTG_CUDA(cudaStreamSynchronize(P.stream));
+  });
+}
+
+otg_status otg_row_solve_marginals_log(otg_problem h, const double* v, double* u, double* col,
+                                       double* col_log) {
+  return guard([&] {
+    Problem& P = get(h);
+    one_eval(P, v, true);
+    d2h(P, u, P.u, P.n_local);
+    d2h(P, col, P.col, P.m);
+    d2h(P, col_log, P.col_log, P.m);
+    OTG_CUDA(cudaStreamSynchronize(P.stream));
+  });
+}
+
+otg_status otg_eval_normalized_step(otg_problem h, const double* v, otg_step_eval* out) {
+  return guard([&] {
+    Problem& P = get(h);
+    one_eval(P, v, true);
+    if (out) {
+      d2h(P, out->v_next, P.y, P.m);
+      d2h(P, out->u, P.u, P.n_local);
+      d2h(P, out->grad, P.grad, P.m);
+      OTG_CUDA(cudaStreamSynchronize(P.stream));
+      out->grad_l1 = P.ctrl_host->grad_l1;
+      out->f_value = P.ctrl_host->f_value;
+    }
+  });
+}
+
+otg_status otg_sinkhorn_solve(otg_problem h, const double* v0, const otg_solve_config* cfg,
+                              otg_solve_result* res) {
+  return guard([&] {
+    Problem& P = get(h);
+    validate_solve_config(cfg);
+    std::vector<double> zero;
+    if (!v0) {
+      zero.assign(P.m, 0.0);
+      v0 = zero.data();
+    }
+    check_finite_vec(v0, P.m, "v0");
+    const std::vector<double> v = project_zero_sum(v0, P.m);  // sinkhorn.cpp:77
+    Ctrl c = base_ctrl(P);
+    c.mode = MODE_SINKHORN;
+    c.tol = cfg->tol_l1;
+    c.max_iters = cfg->max_iters;
+    c.record_trace = cfg->record_trace;
+    c.trace_stride = cfg->trace_stride;
+    put_ctrl(P, c);
+    h2d(P, P.p, v.data(), P.m);
+    const LoopOut lo = run_loop(P, res, res && res->time_sweeps);
+    fill_result(P, res, lo);
+  });
+}
+
+static void start_acc(Problem& P, Ctrl& c, const double* x0, const double* w0, double mu) {
+  c.mu = mu;
+  c.alpha_next = std::sqrt(2.0 * mu);  // accel.cpp:149
+  c.alpha_step = c.alpha_next;
+  put_ctrl(P, c);
+  h2d(P, P.p, x0, P.m);
+  if (w0)
+    h2d(P, P.wacc, w0, P.m);
+  else
+    OTG_CUDA(cudaMemsetAsync(P.wacc, 0, P.m * sizeof(double), P.stream));
+}
+
+otg_status otg_acc_solve(otg_problem h, const double* v0, double mu, const otg_solve_config* cfg,
+                         otg_solve_result* res) {
+  return guard([&] {
+    Problem& P = get(h);
+    validate_solve_config(cfg);
+    if (!(mu > 0.0) || !(mu < 1.0)) fail(OTG_E_OT, "mu must lie in (0, 1)");
+    std::vector<double> zero;
+    if (!v0) {
+      zero.assign(P.m, 0.0);
+      v0 = zero.data();
+    }
+    check_finite_vec(v0, P.m, "v0");
+    const std::vector<double> x0 = project_zero_sum(v0, P.m);  // accel.cpp:207
+    Ctrl c = base_ctrl(P);
+    c.mode = MODE_ACC;
+    c.tol = cfg->tol_l1;
+    c.max_iters = cfg->max_iters;
+    c.record_trace = cfg->record_trace;
+    c.trace_stride = cfg->trace_stride;
+    start_acc(P, c, x0.data(), nullptr, mu);
+    const LoopOut lo = run_loop(P, res, res && res->time_sweeps);
+    fill_result(P, res, lo);
+  });
+}
+
+otg_status otg_acc_run(otg_problem h, const double* x0, const double* w0, double mu,
+                       int64_t m_steps, int record_trace, int64_t trace_stride,
+                       const otg_instr* instr, otg_solve_result* res) {
+  return guard([&] {
+    Problem& P = get(h);
+    if (m_steps < 0) fail(OTG_E_OT, "acc_run needs m >= 0");
+    check_finite_vec(x0, P.m, "x0");
+    check_finite_vec(w0, P.m, "w0");
+    if (!(mu > 0.0) || !(mu < 1.0)) fail(OTG_E_OT, "mu must lie in (0, 1)");
+    check_zero_sum(x0, P.m, "x0");
+    check_zero_sum(w0, P.m, "w0");
+    Ctrl c = base_ctrl(P);
+    c.mode = MODE_ACC_RUN;
+    c.msteps = m_steps;
+    c.record_trace = record_trace;
+    c.trace_stride = trace_stride > 0 ? trace_stride : 1;
+    c.stability = instr && instr->stability;
+    start_acc(P, c, x0, w0, mu);
+    const LoopOut lo = run_loop(P, res, res && res->time_sweeps);
+    fill_result(P, res, lo);
+  });
+}
+
+otg_status otg_homotopy_solve(otg_problem h, const otg_homotopy_config* cfg,
+                              const otg_instr* instr, otg_solve_result* res) {
+  return guard([&] {
+    Problem& P = get(h);
+    if (!cfg) fail(OTG_E_OT, "homotopy config is NULL");
+    if (!(cfg->mu0 > 0.0) || !(cfg->mu0 < 1.0) || cfg->m0 < 1 || cfg->max_outer < 1)
+      fail(OTG_E_OT, "homotopy schedule needs mu0 in (0, 1), m0 >= 1, max_outer >= 1");
+    if (!(cfg->tol_l1 > 0.0)) fail(OTG_E_OT, "tol_l1 must be positive");
+    if (cfg->max_total_inner < 1) fail(OTG_E_OT, "max_total_inner must be at least 1");
+    if (cfg->trace_stride < 1) fail(OTG_E_OT, "trace_stride must be at least 1");
+    Ctrl c = base_ctrl(P);
+    c.mode = MODE_HOMOTOPY;
+    c.tol = cfg->tol_l1;
+    c.m0 = cfg->m0;
+    c.max_outer = cfg->max_outer;
+    c.max_total_inner = cfg->max_total_inner;
+    c.rescale_w = cfg->rescale_w_across_stages;
+    c.record_trace = cfg->record_trace;
+    c.trace_stride = cfg->trace_stride;
+    c.stability = instr && instr->stability;
+    c.mu0 = cfg->mu0;
+    const std::vector<double> zero(P.m, 0.0);
+    start_acc(P, c, zero.data(), nullptr, cfg->mu0);
+    const LoopOut lo = run_loop(P, res, res && res->time_sweeps);
+    fill_result(P, res, lo);
+  });
+}
+
+otg_status otg_plan_stats(otg_problem h, const double* u, const double* v, otg_plan_summary* out) {
+  return guard([&] {
+    Problem& P = get(h);
+    if (!out) fail(OTG_E_DIMENSION, "NULL output");
+    check_finite_vec(u, P.n_local, "u");
+    check_finite_vec(v, P.m, "v");
+    const int64_t n = P.n_local, m = P.m;
+    double *du = nullptr, *dv = nullptr, *rs = nullptr, *rc = nullptr, *rm = nullptr, *cs = nullptr;
+    OTG_CUDA(cudaMalloc(&du, n * sizeof(double)));
+    OTG_CUDA(cudaMalloc(&dv, m * sizeof(double)));
+    OTG_CUDA(cudaMalloc(&rs, n * sizeof(double)));
+    OTG_CUDA(cudaMalloc(&rc, n * sizeof(double)));
+    OTG_CUDA(cudaMalloc(&rm, n * sizeof(double)));
+    OTG_CUDA(cudaMalloc(&cs, m * sizeof(double)));
+    h2d(P, du, u, n);
+    h2d(P, dv, v, m);
+    k_plan_rows<<<static_cast<unsigned>(n), kT, 0, P.stream>>>(P.C64, P.C32, P.ldc, n, m, P.kappa,
+                                                               du, dv, rs, rc, rm);
+    k_plan_cols<<<static_cast<unsigned>((m + kT - 1) / kT), kT, 0, P.stream>>>(
+        P.C64, P.C32, P.ldc, n, m, P.kappa, du, dv, cs);
+    OTG_CUDA(cudaGetLastError());
+    std::vector<double> hrs(n), hrc(n), hrm(n), hcs(m);
+    d2h(P, hrs.data(), rs, n);
+    d2h(P, hrc.data(), rc, n);
+    d2h(P, hrm.data(), rm, n);
+    d2h(P, hcs.data(), cs, m);
+    OTG_CUDA(cudaStreamSynchronize(P.stream));
+    for (double* q : {du, dv, rs, rc, rm, cs}) cudaFree(q);
+    double top = -DBL_MAX, cost = 0.0, viol = 0.0, vc = 0.0;
+    for (int64_t i = 0; i < n; ++i) top = std::max(top, hrm[i]);
+    out->max_exponent = top;
+    if (top > kExpOverflowBound) fail(OTG_E_OVERFLOW, "plan exponent exceeds bound");
+    std::vector<double> hb(m), ha(n);
+    OTG_CUDA(cudaMemcpy(hb.data(), P.b, m * sizeof(double), cudaMemcpyDeviceToHost));
+    OTG_CUDA(cudaMemcpy(ha.data(), P.a, n * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n; ++i) {
+      cost += hrc[i];
+      viol += std::abs(hrs[i] - ha[i]);
+    }
+    for (int64_t j = 0; j < m; ++j) vc += std::abs(hcs[j] - hb[j]);
+    out->marginal_violation_l1 = viol + vc;
+    out->primal_cost = cost * P.epsilon;  // (eps_original / eps) with eps = 1 (core.cpp:77-79)
+    if (out->row_sums) std::memcpy(out->row_sums, hrs.data(), n * sizeof(double));
+    if (out->col_sums) std::memcpy(out->col_sums, hcs.data(), m * sizeof(double));
+  });
+}
+
+otg_status otg_time_sweeps(otg_problem h, const double* v, int reps, double ms[3],
+                           double bytes[2]) {
+  return guard([&] {
+    Problem& P = get(h);
+    if (reps < 1) reps = 1;
+    one_eval(P, v, true);  // warm
+    cudaEvent_t e[4];
+    for (auto& x : e) OTG_CUDA(cudaEventCreate(&x));
+    double acc[3] = {0, 0, 0};
+    for (int r = 0; r < reps; ++r) {
+      Ctrl c = base_ctrl(P);
+      c.mode = MODE_EVAL;
+      put_ctrl(P, c);
+      h2d(P, P.p, v, P.m);
+      OTG_CUDA(cudaEventRecord(e[0], P.stream));
+      launch_row_pass(P);
+      OTG_CUDA(cudaEventRecord(e[1], P.stream));
+      launch_col_pass(P);
+      OTG_CUDA(cudaEventRecord(e[2], P.stream));
+      launch_merge_nolog(P);
+      OTG_CUDA(cudaEventRecord(e[3], P.stream));
+      OTG_CUDA(cudaEventSynchronize(e[3]));
+      float a = 0, b = 0, c2 = 0;
+      OTG_CUDA(cudaEventElapsedTime(&a, e[0], e[1]));
+      OTG_CUDA(cudaEventElapsedTime(&b, e[1], e[2]));
+      OTG_CUDA(cudaEventElapsedTime(&c2, e[2], e[3]));
+      acc[0] += a;
+      acc[1] += b;
+      acc[2] += c2;
+    }
+    for (auto& x : e) cudaEventDestroy(x);
+    if (ms)
+      for (int k = 0; k < 3; ++k) ms[k] = acc[k] / reps;
+    if (bytes) {
+      const double elem = P.storage == OTG_STORE_F64 ? 8.0 : 4.0;
+      const double nm = static_cast<double>(P.n_local) * static_cast<double>(P.m);
+      bytes[0] = nm * elem + P.m * 8.0 + P.n_local * 8.0 * 8;      // C + p + row outputs
+      bytes[1] = nm * elem + P.m * 8.0 + P.n_local * 16.0 +
+                 static_cast<double>(P.col_splits) * P.vshards * P.m * 8.0;  // C + aux + partials
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,940 @@
+// sweep.cu — the O(nm) evaluation of the normalised Sinkhorn map on sm_100a.
+//
+// One evaluation at the column potential p (reference: eval_normalized_step,
+// sinkhorn.cpp:51-63 -> row_solve_marginals_log, dual.cpp:44-70 ->
+// row_solve_marginals, dual.cpp:29-42) is this launch sequence on the
+// handle's stream:
+//
+//   K1 row pass     M_i = max_j (p_j - C'_ij), S_i = sum_j exp(. - M_i),
+//                   u_i = (log a_i - M_i) - log S_i, w_i = a_i / S_i
+//   K2 column pass  partial c_j = sum_{i in split} w_i exp(p_j - C'_ij - M_i)
+//   E1a merge       c_j = sum of partials (fixed order); flag c_j < tiny
+//   K5 fallback     exact column log-sum-exp for flagged columns (dual.cpp:53-69)
+//   E1b finalize    log c, grad = c - b, |grad|_1, mean(y), f; LAST CTA runs the
+//                   solver's scalar control flow (stop test, homotopy schedule,
+//                   trace) on the device
+//   E2  apply       S(p) = y - mean(y) (mirror.cpp:103-105) fused with the
+//                   Acc-Sinkhorn extrapolation (accel.cpp:161-169) and the
+//                   stability-condition sums (diag.cpp:107-146)
+//
+// Two numeric paths:
+//  * fp64 storage ("precise"): C' = C / eps stored in fp64, every exponential
+//    is the IEEE fp64 exp of the reference's own expression -> per-iterate
+//    parity to ~1e-13.
+//  * fp32 storage ("fast"): C fp32 read once per pass with 128-bit streaming
+//    loads.  Row pass: exponent argument formed in fp64 (DFMA) with an online
+//    max, rounded to fp32 only after the max shift, MUFU ex2, fp64 partial
+//    sums.  Column pass: all-fp32 exact cancellation - the row shift and the
+//    column potential are split into a 2^-8-quantised part (exactly
+//    representable, differences exact) and a small remainder, so
+//    fmaf(-C, kappa_hi, Vc - Mc) cancels the large magnitudes inside one FMA
+//    and only the small result is rounded; fp32 accumulation flushed into
+//    fp64 every 16 rows.
+//
+// All kernels read the control block first and return at once after the
+// solve stopped, so a captured chunk of evaluations can run past the stop
+// point harmlessly.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace otg {
+
+namespace {
+
+constexpr int kRowThreads = 256;
+constexpr int kColThreads = 128;
+constexpr int kColUnroll = 8;
+constexpr int kAuxTile = 256;
+constexpr int kEThreads = 256;
+constexpr int kFbChunks = 32;
+constexpr int kFlushRows = 16;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float4 ld_stream(const float4* ptr) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(ptr));
+  return r;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide reductions for blockDim == NT (multiple of 32); result valid in
+// every thread.  Deterministic: fixed shuffle tree then fixed warp order.
+template <int NT>
+__device__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+#pragma unroll
+  for (int k = 0; k < NT / 32; ++k) r += sh[k];
+  return r;
+}
+template <int NT>
+__device__ double block_max(double v, double* sh) {
+  v = warp_max(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = -DBL_MAX;
+#pragma unroll
+  for (int k = 0; k < NT / 32; ++k) r = fmax(r, sh[k]);
+  return r;
+}
+
+// Quantised split of a base-2 value: hi is a multiple of 2^-8 (exact in fp32
+// for |x| < 2^15), lo = x - hi rounded to fp32 (|lo| <= 2^-9).
+__device__ __forceinline__ void split_q(double x2, float& hi, float& lo) {
+  const double h = rint(x2 * 256.0) * (1.0 / 256.0);
+  hi = static_cast<float>(h);
+  lo = static_cast<float>(x2 - h);
+}
+
+// ------------------------------------------------------------------ K1 ----
+// fp64 storage: exact restatement of dual.cpp:34-38 for one row per G threads.
+template <int G>
+__global__ void __launch_bounds__(kRowThreads)
+k_row_precise(const double* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
+              const double* __restrict__ p, const double* __restrict__ a,
+              const double* __restrict__ loga, double* __restrict__ rowM,
+              double* __restrict__ rowS, double* __restrict__ u, double* __restrict__ wrow,
+              double* __restrict__ rowpart, const Ctrl* __restrict__ ctrl) {
+  if (ctrl->done) return;
+  constexpr int RPB = kRowThreads / G;
+  __shared__ double sh[kRowThreads / 32];
+  __shared__ double ua_sh[RPB];
+  const int sub = threadIdx.x / G, lane = threadIdx.x % G;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * RPB + sub;
+  const bool valid = i < n;
+  const double* Ci = C + (valid ? i : 0) * ldc;
+  double mx = -INFINITY;
+  if (valid)
+    for (int64_t j = lane; j < m; j += G) mx = fmax(mx, (-Ci[j]) + p[j]);
+  double s = 0.0;
+  if (G == 32) {
+    mx = warp_max(mx);
+    if (valid)
+      for (int64_t j = lane; j < m; j += G) s += exp(((-Ci[j]) + p[j]) - mx);
+    s = warp_sum(s);
+  } else {
+    mx = block_max<kRowThreads>(mx, sh);
+    for (int64_t j = lane; j < m; j += G) s += exp(((-Ci[j]) + p[j]) - mx);
+    s = block_sum<kRowThreads>(s, sh);
+  }
+  if (lane == 0) {
+    double ua = 0.0;
+    if (valid) {
+      const double ui = (loga[i] - mx) - log(s);
+      rowM[i] = mx;
+      rowS[i] = s;
+      u[i] = ui;
+      wrow[i] = a[i] / s;
+      ua = ui * a[i];
+    }
+    ua_sh[sub] = ua;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < RPB; ++k) t += ua_sh[k];
+    rowpart[blockIdx.x] = t;
+  }
+}
+
+// fp32 storage: R rows per CTA; every thread streams float4 columns of the R
+// rows, the column potential is loaded once per CTA column-chunk and reused
+// across the R rows.
+template <int R>
+__global__ void __launch_bounds__(kRowThreads)
+k_row_fast(const float* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
+           const double* __restrict__ p, double kappa, const double* __restrict__ a,
+           const double* __restrict__ loga, double* __restrict__ rowM,
+           double* __restrict__ rowS, double* __restrict__ u, double* __restrict__ wrow,
+           float4* __restrict__ aux, double* __restrict__ rowpart,
+           const Ctrl* __restrict__ ctrl) {
+  if (ctrl->done) return;
+  __shared__ double sh[kRowThreads / 32];
+  __shared__ double resM[R], resS[R];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * R;
+  const float* Cr[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) Cr[r] = C + (r0 + r < n ? r0 + r : n - 1) * ldc;
+  double mr[R], sr[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    mr[r] = -INFINITY;
+    sr[r] = 0.0;
+  }
+  const int64_t nq = m >> 2;
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  for (int64_t q = threadIdx.x; q < nq; q += kRowThreads) {
+    const double2 pa = __ldg(p2 + 2 * q), pb = __ldg(p2 + 2 * q + 1);
+    float4 c[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) c[r] = ld_stream(reinterpret_cast<const float4*>(Cr[r]) + q);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double t0 = fma(-static_cast<double>(c[r].x), kappa, pa.x);
+      const double t1 = fma(-static_cast<double>(c[r].y), kappa, pa.y);
+      const double t2 = fma(-static_cast<double>(c[r].z), kappa, pb.x);
+      const double t3 = fma(-static_cast<double>(c[r].w), kappa, pb.y);
+      const double cm = fmax(fmax(t0, t1), fmax(t2, t3));
+      if (cm > mr[r]) {
+        sr[r] *= exp(mr[r] - cm);
+        mr[r] = cm;
+      }
+      const double mm = mr[r];
+      const float e = ex2_approx(static_cast<float>(t0 - mm) * static_cast<float>(kLog2e)) +
+                      ex2_approx(static_cast<float>(t1 - mm) * static_cast<float>(kLog2e)) +
+                      ex2_approx(static_cast<float>(t2 - mm) * static_cast<float>(kLog2e)) +
+                      ex2_approx(static_cast<float>(t3 - mm) * static_cast<float>(kLog2e));
+      sr[r] += static_cast<double>(e);
+    }
+  }
+  // ragged tail (m % 4 columns)
+  for (int64_t j = 4 * nq + threadIdx.x; j < m; j += kRowThreads) {
+    const double pj = p[j];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double t = fma(-static_cast<double>(Cr[r][j]), kappa, pj);
+      if (t > mr[r]) {
+        sr[r] *= exp(mr[r] - t);
+        mr[r] = t;
+      }
+      sr[r] += static_cast<double>(
+          ex2_approx(static_cast<float>(t - mr[r]) * static_cast<float>(kLog2e)));
+    }
+  }
+  // per row: exact max, then each thread rescales its partial once (fp64 exp)
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const double M = block_max<kRowThreads>(mr[r], sh);
+    const double s = sr[r] > 0.0 ? sr[r] * exp(mr[r] - M) : 0.0;
+    const double S = block_sum<kRowThreads>(s, sh);
+    if (threadIdx.x == 0) {
+      resM[r] = M;
+      resS[r] = S;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < R) {
+    const int r = threadIdx.x;
+    const int64_t i = r0 + r;
+    if (i < n) {
+      const double M = resM[r], S = resS[r];
+      const double ui = (loga[i] - M) - log(S);
+      const double wi = a[i] / S;
+      rowM[i] = M;
+      rowS[i] = S;
+      u[i] = ui;
+      wrow[i] = wi;
+      float hi, lo;
+      split_q(M * kLog2e, hi, lo);
+      aux[i] = make_float4(hi, lo, static_cast<float>(wi), 0.0f);
+      resS[r] = ui * a[i];
+    } else {
+      resS[r] = 0.0;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) t += resS[r];
+    rowpart[blockIdx.x] = t;
+  }
+}
+
+// ------------------------------------------------------------------ K2 ----
+// fp64: partial c_j = sum_i exp(((-C'_ij) + p_j) - M_i) * w_i  (dual.cpp:36,41)
+__global__ void __launch_bounds__(kColThreads)
+k_col_precise(const double* __restrict__ C, int64_t ldc, int64_t m,
+              const double* __restrict__ p, const double* __restrict__ rowM,
+              const double* __restrict__ wrow, int64_t row_lo, int64_t row_hi,
+              int64_t rows_per_split, double* __restrict__ part, int64_t mpad,
+              const Ctrl* __restrict__ ctrl) {
+  if (ctrl->done) return;
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * kColThreads + threadIdx.x;
+  const int64_t i0 = row_lo + static_cast<int64_t>(blockIdx.y) * rows_per_split;
+  const int64_t i1 = min(i0 + rows_per_split, row_hi);
+  double acc = 0.0;
+  if (j < m) {
+    const double pj = p[j];
+    for (int64_t i = i0; i < i1; ++i) acc += exp(((-C[i * ldc + j]) + pj) - rowM[i]) * wrow[i];
+  }
+  part[static_cast<int64_t>(blockIdx.y) * mpad + j] = acc;
+}
+
+// fp32: thread owns 4 consecutive columns, loops over the split's rows.
+__global__ void __launch_bounds__(kColThreads)
+k_col_fast(const float* __restrict__ C, int64_t ldc, int64_t m, const double* __restrict__ p,
+           float kh, float kl, const float4* __restrict__ aux, int64_t row_lo, int64_t row_hi,
+           int64_t rows_per_split, double* __restrict__ part, int64_t mpad,
+           const Ctrl* __restrict__ ctrl) {
+  if (ctrl->done) return;
+  __shared__ float4 sh_aux[kAuxTile];
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * kColThreads + threadIdx.x;
+  const int64_t j0 = 4 * q;
+  const int64_t i0 = row_lo + static_cast<int64_t>(blockIdx.y) * rows_per_split;
+  const int64_t i1 = min(i0 + rows_per_split, row_hi);
+  float Vc[4], vf[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double pj = (j0 + k < m) ? p[j0 + k] : 0.0;
+    split_q(pj * kLog2e, Vc[k], vf[k]);
+  }
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  double acc64[4] = {0.0, 0.0, 0.0, 0.0};
+  const bool active = j0 < m;
+  const float4* Cq = reinterpret_cast<const float4*>(C + (active ? j0 : 0));
+  const int64_t ldq = ldc >> 2;
+  for (int64_t t0 = i0; t0 < i1; t0 += kAuxTile) {
+    const int64_t tn = min(static_cast<int64_t>(kAuxTile), i1 - t0);
+    __syncthreads();
+    for (int k = threadIdx.x; k < tn; k += kColThreads) sh_aux[k] = aux[t0 + k];
+    __syncthreads();
+    if (!active) continue;
+    int k = 0;
+    for (; k + kColUnroll <= tn; k += kColUnroll) {
+      float4 c[kColUnroll];
+#pragma unroll
+      for (int r = 0; r < kColUnroll; ++r) c[r] = ld_stream(Cq + (t0 + k + r) * ldq);
+#pragma unroll
+      for (int r = 0; r < kColUnroll; ++r) {
+        const float4 ax = sh_aux[k + r];
+        const float cc[4] = {c[r].x, c[r].y, c[r].z, c[r].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float A = Vc[e] - ax.x;  // exact: both multiples of 2^-8
+          const float g = fmaf(-cc[e], kl, vf[e] - ax.y);
+          const float t = fmaf(-cc[e], kh, A) + g;
+          acc[e] = fmaf(ax.z, ex2_approx(t), acc[e]);
+        }
+      }
+      if (((k + kColUnroll) % kFlushRows) == 0) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          acc64[e] += static_cast<double>(acc[e]);
+          acc[e] = 0.f;
+        }
+      }
+    }
+    for (; k < tn; ++k) {
+      const float4 cv = ld_stream(Cq + (t0 + k) * ldq);
+      const float4 ax = sh_aux[k];
+      const float cc[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float A = Vc[e] - ax.x;
+        const float g = fmaf(-cc[e], kl, vf[e] - ax.y);
+        const float t = fmaf(-cc[e], kh, A) + g;
+        acc[e] = fmaf(ax.z, ex2_approx(t), acc[e]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      acc64[e] += static_cast<double>(acc[e]);
+      acc[e] = 0.f;
+    }
+  }
+  if (active) {
+    double* dst = part + static_cast<int64_t>(blockIdx.y) * mpad + j0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dst[e] = acc64[e];
+  }
+}
+
+// ----------------------------------------------------------------- E1a ----
+// c_j = sum over shards of (sum over the shard's splits of the partials); the
+// inner sum is what one rank holds, the outer sum stands in for the allreduce.
+// Block 0 also folds the row-pass partials of <u, a> into col[mpad].
+__global__ void __launch_bounds__(kEThreads)
+k_merge(const double* __restrict__ part, int nshards, int splits, int64_t m, int64_t mpad,
+        double* __restrict__ col, double* __restrict__ col_log, int* __restrict__ flag_idx,
+        int* __restrict__ fb_cols, const double* __restrict__ rowpart, int64_t nrowpart,
+        int flag, Ctrl* __restrict__ ctrl) {
+  if (ctrl->done) return;
+  __shared__ double sh[kEThreads / 32];
+  if (blockIdx.x == 0) {
+    double t = 0.0;
+    for (int64_t k = threadIdx.x; k < nrowpart; k += kEThreads) t += rowpart[k];
+    t = block_sum<kEThreads>(t, sh);
+    if (threadIdx.x == 0) col[mpad] = t;
+  }
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * kEThreads + threadIdx.x;
+  if (j >= m) return;
+  double c = 0.0;
+  for (int s = 0; s < nshards; ++s) {
+    double loc = 0.0;
+    for (int k = 0; k < splits; ++k) loc += part[(static_cast<int64_t>(s) * splits + k) * mpad + j];
+    c += loc;
+  }
+  col[j] = c;
+  if (flag) {
+    if (c >= ctrl->tiny) {
+      col_log[j] = log(c);
+      flag_idx[j] = -1;
+    } else {
+      const unsigned slot = atomicAdd(&ctrl->fb_count, 1u);
+      fb_cols[slot] = static_cast<int>(j);
+      flag_idx[j] = static_cast<int>(slot);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K5 ----
+// Exact column log-sum-exp (dual.cpp:54-69) for flagged columns, split over
+// row chunks: fb_part[f][chunk] = (max_i t_ij, sum_i exp(t_ij - max)).
+template <bool PRECISE>
+__global__ void __launch_bounds__(kEThreads)
+k_fallback(const double* __restrict__ C64, const float* __restrict__ C32, int64_t ldc,
+           int64_t n, double kappa, const double* __restrict__ u, const double* __restrict__ p,
+           const int* __restrict__ fb_cols, double2* __restrict__ fb_part,
+           const Ctrl* __restrict__ ctrl) {
+  if (ctrl->done) return;
+  const unsigned nf = ctrl->fb_count;
+  if (nf == 0) return;
+  __shared__ double sh[kEThreads / 32];
+  const int64_t rpc = (n + kFbChunks - 1) / kFbChunks;
+  const int64_t items = static_cast<int64_t>(nf) * kFbChunks;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t f = it / kFbChunks, ch = it % kFbChunks;
+    const int64_t j = fb_cols[f];
+    const double vj = p[j];
+    const int64_t i0 = ch * rpc, i1 = min(n, i0 + rpc);
+    double top = -INFINITY;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += kEThreads) {
+      const double t = PRECISE ? (u[i] + vj) - C64[i * ldc + j]
+                               : fma(-static_cast<double>(C32[i * ldc + j]), kappa, u[i] + vj);
+      top = fmax(top, t);
+    }
+    top = block_max<kEThreads>(top, sh);
+    double s = 0.0;
+    if (top > -INFINITY)
+      for (int64_t i = i0 + threadIdx.x; i < i1; i += kEThreads) {
+        const double t = PRECISE ? (u[i] + vj) - C64[i * ldc + j]
+                                 : fma(-static_cast<double>(C32[i * ldc + j]), kappa, u[i] + vj);
+        s += exp(t - top);
+      }
+    s = block_sum<kEThreads>(s, sh);
+    if (threadIdx.x == 0) fb_part[f * kFbChunks + ch] = make_double2(top, s);
+  }
+}
+
+// --------------------------------------------------------------- control --
+__device__ void push_trace(Ctrl* C, double* trace, long long iter, double viol, double f,
+                           double mu, double alpha) {
+  const long long row = C->trace_count % C->trace_cap;
+  double* r = trace + row * kTraceCols;
+  r[0] = static_cast<double>(iter);
+  r[1] = 0.0;
+  r[2] = viol;
+  r[3] = viol;
+  r[4] = f;
+  r[5] = mu;
+  r[6] = alpha;
+  for (int k = 7; k < kTraceCols; ++k) r[k] = __longlong_as_double(0x7ff8000000000000LL);
+  C->trace_row = row;
+  C->trace_count += 1;
+}
+
+__device__ void push_boundary(Ctrl* C, double* bounds) {
+  if (C->boundary_count < C->boundary_cap) {
+    double* r = bounds + C->boundary_count * 4;
+    r[0] = static_cast<double>(C->stage);
+    r[1] = C->mu;
+    r[2] = C->alpha_next;
+    r[3] = static_cast<double>(C->total_inner);
+  }
+  C->boundary_count += 1;
+}
+
+// Scalar control flow after one evaluation (one thread).  Mirrors
+// sinkhorn.cpp:80-113, accel.cpp:176-197, 211-230, 245-301.
+__device__ void control_step(Ctrl* C, double* trace, double* bounds, double gl, double f) {
+  const long long ev = ++C->evaluations;
+  const bool seed = ev == 1;
+  C->grad_l1 = gl;
+  C->f_value = f;
+  C->trace_row = -1;
+  C->stage_changed = 0;
+  C->final_violation = gl;
+  C->final_f = f;
+  const bool rec = C->record_trace != 0;
+  const long long stride = C->trace_stride;
+  switch (C->mode) {
+    case MODE_EVAL:
+      C->done = 1;
+      break;
+    case MODE_SINKHORN: {
+      const long long k = C->k;
+      const bool done = gl < C->tol || k >= C->max_iters;
+      if (rec && (k % stride == 0 || done)) push_trace(C, trace, k, gl, f, 0.0, 0.0);
+      if (done) {
+        C->converged = gl < C->tol;
+        C->iterations = k;
+        C->done = 1;
+      } else {
+        C->k = k + 1;
+      }
+      break;
+    }
+    case MODE_ACC: {
+      const long long k = C->k;
+      C->is_step = !seed;
+      C->alpha_step = C->alpha_next;
+      const bool done = gl < C->tol || k >= C->max_iters;
+      if (rec && (k % stride == 0 || done)) push_trace(C, trace, k, gl, f, C->mu, C->alpha_step);
+      if (done) {
+        C->converged = gl < C->tol;
+        C->iterations = k;
+        C->done = 1;
+      } else {
+        C->k = k + 1;
+      }
+      break;
+    }
+    case MODE_ACC_RUN: {
+      const long long k = C->k;
+      C->is_step = !seed;
+      C->alpha_step = C->alpha_next;
+      const bool terminal = k == C->msteps;
+      if (rec && (k % stride == 0 || terminal))
+        push_trace(C, trace, k, gl, f, C->mu, C->alpha_step);
+      if (terminal) {
+        C->iterations = C->msteps;
+        C->done = 1;
+      } else {
+        C->k = k + 1;
+      }
+      break;
+    }
+    case MODE_HOMOTOPY: {
+      C->is_step = !seed;
+      C->alpha_step = C->alpha_next;
+      const long long cap = C->max_total_inner;
+      if (seed) {
+        const bool conv = gl < C->tol;
+        C->converged = conv;
+        if (rec) push_trace(C, trace, 0, gl, f, C->mu, C->alpha_step);
+        if (conv) {
+          C->done = 1;
+        } else {
+          C->stage = 0;
+          C->outer_stages = 1;
+          C->inner_i = 0;
+          C->m_stage = C->m0;
+          push_boundary(C, bounds);
+        }
+      } else {
+        C->total_inner += 1;
+        C->inner_i += 1;
+        const bool conv = gl < C->tol;
+        C->converged = conv;
+        const bool terminal = conv || C->total_inner >= cap;
+        if (rec && (C->total_inner % stride == 0 || terminal))
+          push_trace(C, trace, C->total_inner, gl, f, C->mu, C->alpha_step);
+        if (conv) {
+          C->done = 1;
+        } else {
+          if (C->inner_i == C->m_stage) {
+            if (C->stage + 1 < C->max_outer) {
+              C->stage += 1;
+              C->mu /= 2.0;
+              C->alpha_next = sqrt(2.0 * C->mu);
+              C->m_stage = static_cast<long long>(floor(sqrt(2.0) * static_cast<double>(C->m_stage))) + 1;
+              C->inner_i = 0;
+              C->outer_stages += 1;
+              C->stage_changed = 1;
+              push_boundary(C, bounds);
+            } else {
+              C->done = 1;
+            }
+          }
+          if (!C->done && C->total_inner >= cap) {
+            C->capped = 1;
+            C->done = 1;
+          }
+        }
+      }
+      C->iterations = C->total_inner;
+      break;
+    }
+    default:
+      C->done = 1;
+  }
+  C->live_e2 = 1;
+}
+
+// ----------------------------------------------------------------- E1b ----
+__global__ void __launch_bounds__(kEThreads)
+k_finalize(int64_t m, int64_t mpad, const double* __restrict__ p, const double* __restrict__ b,
+           const double* __restrict__ logb, double* __restrict__ col,
+           double* __restrict__ col_log, const int* __restrict__ flag_idx,
+           const double2* __restrict__ fb_part, double* __restrict__ y,
+           double* __restrict__ grad, double* __restrict__ e1_part, double* __restrict__ trace,
+           double* __restrict__ bounds, Ctrl* __restrict__ ctrl) {
+  if (ctrl->done) return;
+  __shared__ double sh[kEThreads / 32];
+  __shared__ bool last;
+  double s_abs = 0.0, s_y = 0.0, s_pb = 0.0, mx_p = 0.0, bad = 0.0;
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * kEThreads + threadIdx.x; j < m;
+       j += static_cast<int64_t>(gridDim.x) * kEThreads) {
+    double c = col[j], cl;
+    const int slot = flag_idx[j];
+    if (slot >= 0) {
+      double top = -INFINITY;
+      for (int k = 0; k < kFbChunks; ++k) top = fmax(top, fb_part[slot * kFbChunks + k].x);
+      double s = 0.0;
+      for (int k = 0; k < kFbChunks; ++k) {
+        const double2 fp = fb_part[slot * kFbChunks + k];
+        if (fp.y > 0.0) s += fp.y * exp(fp.x - top);
+      }
+      cl = top + log(s);
+      c = exp(cl);
+      col[j] = c;
+      col_log[j] = cl;
+    } else {
+      cl = col_log[j];
+    }
+    if (!isfinite(cl)) bad = 1.0;
+    const double g = c - b[j];
+    grad[j] = g;
+    const double pj = p[j];
+    const double yj = pj + (logb[j] - cl);
+    y[j] = yj;
+    s_abs += fabs(g);
+    s_y += yj;
+    s_pb += pj * b[j];
+    mx_p = fmax(mx_p, fabs(pj));
+  }
+  s_abs = block_sum<kEThreads>(s_abs, sh);
+  s_y = block_sum<kEThreads>(s_y, sh);
+  s_pb = block_sum<kEThreads>(s_pb, sh);
+  mx_p = block_max<kEThreads>(mx_p, sh);
+  bad = block_max<kEThreads>(bad, sh);
+  if (threadIdx.x == 0) {
+    double* dst = e1_part + blockIdx.x * 8;
+    dst[0] = s_abs;
+    dst[1] = s_y;
+    dst[2] = s_pb;
+    dst[3] = mx_p;
+    dst[4] = bad;
+    __threadfence();
+    const unsigned prev = atomicAdd(&ctrl->e1_counter, 1u);
+    last = prev == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  double gl = 0.0, sy = 0.0, pb = 0.0, mp = 0.0, bd = 0.0;
+  for (unsigned k = 0; k < gridDim.x; ++k) {
+    const volatile double* src = e1_part + k * 8;
+    gl += src[0];
+    sy += src[1];
+    pb += src[2];
+    mp = fmax(mp, src[3]);
+    bd = fmax(bd, src[4]);
+  }
+  Ctrl* C = ctrl;
+  C->e1_counter = 0;
+  C->fb_count = 0;
+  const double ua = col[mpad];
+  const double f = (1.0 - ua) - pb;
+  C->mean_y = sy / static_cast<double>(m);
+  C->max_v_inf = fmax(C->max_v_inf, mp);
+  if (bd > 0.0) {  // check_col_log_finite (sinkhorn.cpp:20-25)
+    C->error = OTG_E_DOMAIN;
+    C->done = 1;
+    C->live_e2 = 0;
+    return;
+  }
+  control_step(C, trace, bounds, gl, f);
+}
+
+// ------------------------------------------------------------------ E2 ----
+__device__ __forceinline__ double expm1_over_z(double z) {  // mirror.cpp:21-24
+  if (fabs(z) < 1e-8) return 1.0 + z / 2.0 + z * z / 6.0;
+  return expm1(z) / z;
+}
+
+__global__ void __launch_bounds__(kEThreads)
+k_apply(int64_t m, const double* __restrict__ b, double* __restrict__ p,
+        double* __restrict__ wacc, double* __restrict__ y, const double* __restrict__ grad,
+        double* __restrict__ prev_grad, double* __restrict__ prev_x,
+        double* __restrict__ prev_y, double* __restrict__ e2_part, double* __restrict__ trace,
+        Ctrl* __restrict__ ctrl) {
+  if (!ctrl->live_e2) return;
+  __shared__ double sh[kEThreads / 32];
+  __shared__ bool last;
+  const int mode = ctrl->mode;
+  const bool done = ctrl->done != 0;
+  const double mean = ctrl->mean_y;
+  const bool step = ctrl->is_step != 0;
+  const double al = ctrl->alpha_step, an = ctrl->alpha_next;
+  const bool resc = ctrl->stage_changed && ctrl->rescale_w;
+  const bool stab = ctrl->stability != 0 && mode >= MODE_ACC_RUN;
+  const bool have_prev = ctrl->have_prev != 0;
+  double c1 = 0.0, br = 0.0, c2 = 0.0, qq = 0.0, drift = 0.0, ginf = 0.0, dom = 0.0;
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * kEThreads + threadIdx.x; j < m;
+       j += static_cast<int64_t>(gridDim.x) * kEThreads) {
+    const double S = y[j] - mean;  // project_zero_sum (mirror.cpp:103-105)
+    if (mode == MODE_EVAL) {
+      y[j] = S;
+      continue;
+    }
+    if (mode == MODE_SINKHORN) {
+      if (!done) p[j] = S;
+      continue;
+    }
+    const double x = p[j];
+    double w = wacc[j];
+    if (step) w = (w + (al * al - 2.0) * x + 2.0 * S) / (1.0 + al);  // accel.cpp:168
+    if (stab) {
+      const double yn = w / al;
+      const double g1 = grad[j];
+      if (have_prev) {
+        const double g0 = prev_grad[j], bj = b[j];
+        ginf = fmax(ginf, fabs(g0));
+        const double r0 = g0 / bj, r1 = g1 / bj;
+        if (r0 <= -1.0 || r1 <= -1.0) {
+          dom = 1.0;
+        } else {
+          const double D0 = bj * expm1_over_z(log1p(r0));
+          const double D1 = bj * expm1_over_z(log1p(r1));
+          c1 += g0 * g0 * D1 / (D0 * D0);
+          br += g0 - bj * log1p(r0);
+          const double vk = prev_y[j] - prev_x[j], vk1 = yn - x;
+          c2 += (D1 - D0) * (vk * vk);
+          qq += D1 * (vk1 * vk1);
+          drift = fmax(drift, fabs(D1 - D0));
+        }
+      }
+      prev_grad[j] = g1;
+      prev_x[j] = x;
+      prev_y[j] = yn;
+    }
+    if (resc) w *= an / al;  // accel.cpp:279
+    wacc[j] = w;
+    if (!done) p[j] = (w + S) / (1.0 + an);  // accel.cpp:161
+  }
+  if (!stab) {
+    // no cross-block bookkeeping needed beyond releasing the handoff
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned prev = atomicAdd(&ctrl->e2_counter, 1u);
+      if (prev == gridDim.x - 1) {
+        ctrl->e2_counter = 0;
+        ctrl->live_e2 = 0;
+      }
+    }
+    return;
+  }
+  c1 = block_sum<kEThreads>(c1, sh);
+  br = block_sum<kEThreads>(br, sh);
+  c2 = block_sum<kEThreads>(c2, sh);
+  qq = block_sum<kEThreads>(qq, sh);
+  drift = block_max<kEThreads>(drift, sh);
+  ginf = block_max<kEThreads>(ginf, sh);
+  dom = block_max<kEThreads>(dom, sh);
+  if (threadIdx.x == 0) {
+    double* dst = e2_part + blockIdx.x * 8;
+    dst[0] = c1;
+    dst[1] = br;
+    dst[2] = c2;
+    dst[3] = qq;
+    dst[4] = drift;
+    dst[5] = ginf;
+    dst[6] = dom;
+    __threadfence();
+    const unsigned prev = atomicAdd(&ctrl->e2_counter, 1u);
+    last = prev == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  double t[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (unsigned k = 0; k < gridDim.x; ++k) {
+    const volatile double* src = e2_part + k * 8;
+    for (int q = 0; q < 4; ++q) t[q] += src[q];
+    for (int q = 4; q < 7; ++q) t[q] = fmax(t[q], src[q]);
+  }
+  Ctrl* C = ctrl;
+  if (have_prev) {
+    double cells[5];
+    bool valid = true;
+    if (t[5] < kGradFloor) {  // diag.cpp:116-123: skipped, counts as held, not checked
+      cells[0] = cells[1] = cells[2] = cells[3] = cells[4] = 0.0;
+    } else if (t[6] > 0.0) {  // DomainViolation caught by the observer (accel.cpp:68)
+      valid = false;
+    } else {
+      const double coef = (4.0 - al * al - 2.0 * sqrt(al)) / (2.0 * al * (1.0 + al) * (1.0 + al));
+      cells[0] = t[0];
+      cells[1] = coef * t[1];
+      cells[2] = t[2];
+      cells[3] = pow(al, 1.5) * t[3];
+      cells[4] = t[4];
+      C->cond_checked += 1;
+      C->cond_held += (cells[0] < cells[1] && cells[2] < cells[3]) ? 1 : 0;
+    }
+    if (valid && C->trace_row >= 0) {
+      double* r = trace + C->trace_row * kTraceCols;
+      for (int q = 0; q < 5; ++q) r[7 + q] = cells[q];
+    }
+  }
+  C->have_prev = 1;
+  C->e2_counter = 0;
+  C->live_e2 = 0;
+}
+
+int e_grid(int64_t m) {
+  const int64_t blocks = (m + kEThreads - 1) / kEThreads;
+  return static_cast<int>(blocks < 296 ? blocks : 296);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- launch ---
+int64_t rows_per_cta_fast(const Problem& P) { return P.n_local >= 8 ? 8 : 1; }
+
+void configure_sweeps(Problem& P) {
+  // column-pass split: enough CTAs to fill 148 SMs several times over
+  const int64_t colblocks =
+      P.storage == OTG_STORE_F64 ? (P.m + kColThreads - 1) / kColThreads
+                                 : (P.m + 4 * kColThreads - 1) / (4 * kColThreads);
+  const int64_t shard_rows = (P.n_local + P.vshards - 1) / P.vshards;
+  int64_t splits = (4 * 148 + colblocks - 1) / colblocks;
+  splits = std::max<int64_t>(1, std::min<int64_t>(splits, (shard_rows + 63) / 64));
+  P.col_splits = static_cast<int>(splits);
+  P.rows_per_split = (shard_rows + splits - 1) / splits;
+  P.e_blocks = e_grid(P.m);
+}
+
+int64_t row_blocks(const Problem& P) {
+  if (P.storage == OTG_STORE_F64) {
+    const int G = P.m <= 2048 ? 32 : kRowThreads;
+    const int64_t rpb = kRowThreads / G;
+    return (P.n_local + rpb - 1) / rpb;
+  }
+  const int64_t R = rows_per_cta_fast(P);
+  return (P.n_local + R - 1) / R;
+}
+
+double* g_rowpart_dummy = nullptr;
+
+void launch_row_pass(Problem& P) {
+  const int64_t blocks = row_blocks(P);
+  double* rowpart = P.e1_part + P.e_blocks * 8;  // scratch after the E1 partials
+  if (P.storage == OTG_STORE_F64) {
+    if (P.m <= 2048)
+      k_row_precise<32><<<blocks, kRowThreads, 0, P.stream>>>(
+          P.C64, P.ldc, P.n_local, P.m, P.p, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, rowpart,
+          P.ctrl);
+    else
+      k_row_precise<kRowThreads><<<blocks, kRowThreads, 0, P.stream>>>(
+          P.C64, P.ldc, P.n_local, P.m, P.p, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, rowpart,
+          P.ctrl);
+  } else {
+    if (rows_per_cta_fast(P) == 8)
+      k_row_fast<8><<<blocks, kRowThreads, 0, P.stream>>>(
+          P.C32, P.ldc, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow,
+          P.aux, rowpart, P.ctrl);
+    else
+      k_row_fast<1><<<blocks, kRowThreads, 0, P.stream>>>(
+          P.C32, P.ldc, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow,
+          P.aux, rowpart, P.ctrl);
+  }
+  OTG_CUDA(cudaGetLastError());
+}
+
+void launch_col_pass(Problem& P) {
+  const int64_t shard_rows = (P.n_local + P.vshards - 1) / P.vshards;
+  const double k2 = P.kappa * kLog2e;
+  const float kh = static_cast<float>(k2);
+  const float kl = static_cast<float>(k2 - static_cast<double>(kh));
+  for (int s = 0; s < P.vshards; ++s) {
+    const int64_t lo = s * shard_rows, hi = std::min(P.n_local, lo + shard_rows);
+    double* part = P.part + static_cast<int64_t>(s) * P.col_splits * P.mpad;
+    if (P.storage == OTG_STORE_F64) {
+      dim3 grid(static_cast<unsigned>((P.m + kColThreads - 1) / kColThreads), P.col_splits);
+      k_col_precise<<<grid, kColThreads, 0, P.stream>>>(P.C64, P.ldc, P.m, P.p, P.rowM, P.wrow,
+                                                        lo, hi, P.rows_per_split, part, P.mpad,
+                                                        P.ctrl);
+    } else {
+      dim3 grid(static_cast<unsigned>((P.m + 4 * kColThreads - 1) / (4 * kColThreads)),
+                P.col_splits);
+      k_col_fast<<<grid, kColThreads, 0, P.stream>>>(P.C32, P.ldc, P.m, P.p, kh, kl, P.aux, lo,
+                                                     hi, P.rows_per_split, part, P.mpad, P.ctrl);
+    }
+  }
+  OTG_CUDA(cudaGetLastError());
+}
+
+static void launch_merge(Problem& P, bool flag) {
+  const int64_t blocks = (P.m + kEThreads - 1) / kEThreads;
+  double* rowpart = P.e1_part + P.e_blocks * 8;
+  k_merge<<<blocks, kEThreads, 0, P.stream>>>(P.part, P.vshards, P.col_splits, P.m, P.mpad,
+                                              P.col, P.col_log, P.flag_idx, P.fb_cols, rowpart,
+                                              row_blocks(P), flag ? 1 : 0, P.ctrl);
+  OTG_CUDA(cudaGetLastError());
+}
+
+void launch_merge_nolog(Problem& P) { launch_merge(P, false); }
+
+void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
+  if (timed) OTG_CUDA(cudaEventRecord(ev4[0], P.stream));
+  launch_row_pass(P);
+  if (timed) OTG_CUDA(cudaEventRecord(ev4[1], P.stream));
+  if (timed) OTG_CUDA(cudaEventRecord(ev4[2], P.stream));
+  launch_col_pass(P);
+  if (timed) OTG_CUDA(cudaEventRecord(ev4[3], P.stream));
+  launch_merge(P, with_log);
+  if (P.world > 1) comm_allreduce_sum(P, P.col, static_cast<size_t>(P.mpad + 1));
+  if (!with_log) return;
+  if (P.storage == OTG_STORE_F64)
+    k_fallback<true><<<296, kEThreads, 0, P.stream>>>(P.C64, nullptr, P.ldc, P.n_local, P.kappa,
+                                                      P.u, P.p, P.fb_cols, P.fb_part, P.ctrl);
+  else
+    k_fallback<false><<<296, kEThreads, 0, P.stream>>>(nullptr, P.C32, P.ldc, P.n_local,
+                                                       P.kappa, P.u, P.p, P.fb_cols, P.fb_part,
+                                                       P.ctrl);
+  OTG_CUDA(cudaGetLastError());
+  k_finalize<<<P.e_blocks, kEThreads, 0, P.stream>>>(P.m, P.mpad, P.p, P.b, P.logb, P.col,
+                                                     P.col_log, P.flag_idx, P.fb_part, P.y,
+                                                     P.grad, P.e1_part, P.trace, P.bounds,
+                                                     P.ctrl);
+  OTG_CUDA(cudaGetLastError());
+}
+
+void launch_apply(Problem& P) {
+  k_apply<<<P.e_blocks, kEThreads, 0, P.stream>>>(P.m, P.b, P.p, P.wacc, P.y, P.grad,
+                                                  P.prev_grad, P.prev_x, P.prev_y, P.e2_part,
+                                                  P.trace, P.ctrl);
+  OTG_CUDA(cudaGetLastError());
+}
+
+int64_t rowpart_len(const Problem& P) { return row_blocks(P); }
+
+}  // namespace otg
