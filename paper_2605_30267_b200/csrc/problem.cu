@@ -56,7 +56,7 @@ __global__ void k_log(const double* __restrict__ x, double* __restrict__ y, int6
 }
 
 __global__ void k_div_rows(double* __restrict__ C, int64_t ldc, int64_t n, int64_t m, double eps) {
-  const int64_t i = blockIdx.y;
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y)
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
        j += static_cast<int64_t>(gridDim.x) * blockDim.x)
     C[i * ldc + j] = C[i * ldc + j] / eps;
@@ -110,7 +110,7 @@ template <typename T>
 __global__ void k_cost_store(const double* __restrict__ X, const double* __restrict__ Y,
                              int64_t n, int64_t m, int64_t d, int cost, int norm, double mn,
                              double mx, double eps_div, T* __restrict__ C, int64_t ldc) {
-  const int64_t i = blockIdx.y;
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y)
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
        j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     double c = raw_cost(X + i * d, Y + j * d, d, cost);
@@ -276,7 +276,7 @@ otg_status otg_problem_create_dense(int64_t n, int64_t m, const double* a, const
                                  cudaMemcpyHostToDevice, P.stream));
       if (epsilon != 1.0) {
         dim3 grid(static_cast<unsigned>(std::min<int64_t>((m + kT - 1) / kT, 64)),
-                  static_cast<unsigned>(nl));
+                  static_cast<unsigned>(std::min<int64_t>(nl, 65535)));
         k_div_rows<<<grid, kT, 0, P.stream>>>(P.C64, P.ldc, nl, m, epsilon);
         OTG_CUDA(cudaGetLastError());
       }
@@ -371,7 +371,7 @@ otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const doub
     P.raw_min = mn;
     P.raw_max = mx;
     dim3 grid(static_cast<unsigned>(std::min<int64_t>((m + kT - 1) / kT, 64)),
-              static_cast<unsigned>(nl));
+              static_cast<unsigned>(std::min<int64_t>(nl, 65535)));
     if (storage == OTG_STORE_F64) {
       P.storage = OTG_STORE_F64;
       P.C64 = dalloc<double>(P, static_cast<size_t>(nl) * P.ldc);
