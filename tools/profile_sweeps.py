@@ -1,0 +1,14 @@
+"""Profiling driver: one cfg3-shaped problem (rows x 65536, fp32), a few evaluations,
+then one isolated row pass + column pass (for ncu -k regex:k_row|k_col)."""
+import sys
+sys.path.insert(0, '.')
+import numpy as np
+from paper_2605_30267_b200 import ot
+
+rows = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+m = 65536
+x, y = ot.gen_config(3, rows, m, 3)
+p = ot.TransportProblem.from_points(np.full(rows, 1.0 / rows), np.full(m, 1.0 / m), x, y, 1e-3)
+r = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=3))
+ms, by = ot.time_sweeps(p, r.potentials.v, reps=1)
+print("rows", rows, "ms", ms, "GB/s row", by[0] / ms[0] / 1e6, "col", by[1] / ms[1] / 1e6)
