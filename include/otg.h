@@ -109,6 +109,9 @@ typedef struct {
   double cost_raw_max;     /* CostMatrix::raw_max                           */
   int64_t device_bytes;    /* device memory held by the handle              */
   int world_size, rank, device;
+  int sweep_mode;          /* 0: fp64 two-pass, 1: fp32 two-pass, 2: fp32 fused */
+  int sweep_clusters;      /* fused: co-resident 8-CTA clusters (persistent)  */
+  int col_splits;          /* two-pass: row splits of the column pass         */
 } otg_problem_info;
 
 /* StepEval (sinkhorn.hpp:18-24): caller-owned output buffers, any may be NULL. */
@@ -177,6 +180,8 @@ typedef struct {
   double row_pass_seconds; /* summed row-pass launch times (time_sweeps)    */
   double col_pass_seconds; /* summed column-pass launch times (time_sweeps) */
   int64_t kernel_launches; /* live (non-skipped) kernels launched           */
+  int64_t row_redos;     /* fp32 row pass: rows recomputed exactly because
+                            the shift estimate was loose (diagnostic)       */
 } otg_solve_result;
 
 /* plan_from_potentials + marginal_violation_l1 + primal_cost

@@ -27,7 +27,8 @@ class ProblemInfo(C.Structure):
                 ("row_begin", C.c_int64), ("storage", C.c_int), ("epsilon", C.c_double),
                 ("cost_raw_min", C.c_double), ("cost_raw_max", C.c_double),
                 ("device_bytes", C.c_int64), ("world_size", C.c_int), ("rank", C.c_int),
-                ("device", C.c_int)]
+                ("device", C.c_int), ("sweep_mode", C.c_int), ("sweep_clusters", C.c_int),
+                ("col_splits", C.c_int)]
 
 
 class StepEvalC(C.Structure):
@@ -61,7 +62,7 @@ class SolveResultC(C.Structure):
                 ("boundaries", C.c_void_p), ("boundaries_cap", C.c_int64),
                 ("time_sweeps", C.c_int), ("device_seconds", C.c_double),
                 ("row_pass_seconds", C.c_double), ("col_pass_seconds", C.c_double),
-                ("kernel_launches", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("row_redos", C.c_int64)]
 
 
 class PlanSummaryC(C.Structure):

@@ -86,7 +86,12 @@ struct Ctrl {
   long long boundary_count;
   long long cond_checked, cond_held;
   long long live_kernels;
-  unsigned int e1_counter, e2_counter, fb_count, pad0;
+  unsigned int e1_counter, e2_counter, fb_count, redo_count;
+  // fp32 row pass: shift estimate from the previous evaluation (sweep.cu)
+  int shift_valid;    // rowM2 / vq describe the previous point, dmax2 the step
+  int pad1;
+  double dmax2;       // max_j (p_new - p_old)_j * log2(e)
+  long long redo_total;  // rows redone exactly over the solve (diagnostic)
   // --- configuration (host-written) ---
   int mode;
   int record_trace;
@@ -139,6 +144,11 @@ struct Problem {
   // per-row state (n_local)
   double *rowM = nullptr, *rowS = nullptr, *u = nullptr, *wrow = nullptr;
   float4* aux = nullptr;  // fast path: {Mc, mf, w, 0} (base-2 split row shift)
+  double* rowM2 = nullptr;  // fast path: base-2 row max of the previous evaluation
+  int* rowJ = nullptr;      // fast path: its argmax column
+  double* dq = nullptr;     // fast path: (p_new - p_old) * log2(e) per column
+  int* redo_rows = nullptr; // rows whose shift estimate was off (exact redo)
+  float* vq = nullptr;      // fast path: split column potential (Vc[mpad], vf[mpad])
 
   // per-column state (m, padded)
   double *p = nullptr, *wacc = nullptr, *col = nullptr, *col_log = nullptr, *y = nullptr,
@@ -147,6 +157,10 @@ struct Problem {
   int* flag_idx = nullptr;  // fallback slot per column (-1 none)
   int* fb_cols = nullptr;   // flagged column list (m)
   double2* fb_part = nullptr;  // (max, sum) per flagged column per row chunk
+
+  // single-pass fused sweep (fused.cu), fp32 storage only
+  int fused = 0, fused_qpt = 0, fused_W = 0, fused_slots = 0, fused_smem = 0,
+      fused_clusters = 0;
 
   // column-pass partials
   int col_splits = 1;
@@ -194,6 +208,10 @@ void launch_apply(Problem& P);
 void launch_row_pass(Problem& P);
 void launch_col_pass(Problem& P);
 void launch_merge_nolog(Problem& P);
+void launch_sweeps(Problem& P, bool timed, cudaEvent_t* ev4);
+bool fused_configure(Problem& P);
+void launch_fused(Problem& P, double* rowpart);
+int partial_rows(const Problem& P);  // rows of P.part the merge sums
 
 // NCCL (comm.cpp)
 void comm_init(Problem& P, const void* unique_id);

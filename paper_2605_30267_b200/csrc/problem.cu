@@ -130,7 +130,9 @@ __global__ void k_cost_store(const double* __restrict__ X, const double* __restr
 
 void problem_free(Problem& P) {
   void* ptrs[] = {P.C64, P.C32, P.X, P.Y, P.a, P.loga, P.b, P.logb, P.rowM, P.rowS, P.u,
-                  P.wrow, P.aux, P.p, P.wacc, P.col, P.col_log, P.y, P.grad, P.prev_grad,
+                  P.wrow, P.aux, P.rowM2, P.rowJ, P.dq, P.redo_rows, P.vq, P.p, P.wacc, P.col,
+                  P.col_log,
+                  P.y, P.grad, P.prev_grad,
                   P.prev_x, P.prev_y, P.flag_idx, P.fb_cols, P.fb_part, P.part, P.e1_part,
                   P.e2_part, P.ctrl, P.trace, P.bounds};
   for (void* q : ptrs)
@@ -146,12 +148,18 @@ void problem_free(Problem& P) {
 
 void problem_alloc_state(Problem& P) {
   configure_sweeps(P);
+  fused_configure(P);
   const int64_t n = P.n_local, mp = P.mpad;
   P.rowM = dalloc<double>(P, n);
   P.rowS = dalloc<double>(P, n);
   P.u = dalloc<double>(P, n);
   P.wrow = dalloc<double>(P, n);
   P.aux = dalloc<float4>(P, n);
+  P.rowM2 = dalloc<double>(P, n);
+  P.rowJ = dalloc<int>(P, n);
+  P.dq = dalloc<double>(P, mp);
+  P.redo_rows = dalloc<int>(P, n);
+  P.vq = dalloc<float>(P, 2 * mp);
   P.p = dalloc<double>(P, mp);
   P.wacc = dalloc<double>(P, mp);
   P.col = dalloc<double>(P, mp + 8);
@@ -164,7 +172,9 @@ void problem_alloc_state(Problem& P) {
   P.flag_idx = dalloc<int>(P, mp);
   P.fb_cols = dalloc<int>(P, mp);
   P.fb_part = dalloc<double2>(P, mp * kFbChunks);
-  P.part = dalloc<double>(P, static_cast<size_t>(P.vshards) * P.col_splits * mp);
+  const size_t prow = std::max<size_t>(static_cast<size_t>(P.vshards) * P.col_splits,
+                                       static_cast<size_t>(P.fused_clusters));
+  P.part = dalloc<double>(P, prow * mp);
   P.e1_part = dalloc<double>(P, P.e_blocks * 8 + row_blocks(P) + 8);
   P.e2_part = dalloc<double>(P, P.e_blocks * 8);
   P.ctrl = dalloc<Ctrl>(P, 1);
@@ -173,7 +183,7 @@ void problem_alloc_state(Problem& P) {
   OTG_CUDA(cudaMallocHost(&P.ctrl_host, sizeof(Ctrl)));
   OTG_CUDA(cudaMemsetAsync(P.p, 0, mp * sizeof(double), P.stream));
   OTG_CUDA(cudaMemsetAsync(P.wacc, 0, mp * sizeof(double), P.stream));
-  OTG_CUDA(cudaMemsetAsync(P.part, 0, static_cast<size_t>(P.vshards) * P.col_splits * mp * sizeof(double), P.stream));
+  OTG_CUDA(cudaMemsetAsync(P.part, 0, prow * mp * sizeof(double), P.stream));
   OTG_CUDA(cudaMemsetAsync(P.ctrl, 0, sizeof(Ctrl), P.stream));
   std::memset(P.ctrl_host, 0, sizeof(Ctrl));
 }
@@ -202,7 +212,8 @@ static void begin(Problem& P, int64_t n, int64_t m, const otg_device_opts* opts)
   P.vshards = (opts && opts->virtual_shards > 1) ? opts->virtual_shards : 1;
   if (P.vshards > P.n_local) P.vshards = static_cast<int>(P.n_local);
   P.mpad = round_up(m, 4);
-  P.ldc = round_up(m, 4);
+  // rows padded to whole 8-CTA-cluster slices of 16-byte multiples (fused.cu)
+  P.ldc = round_up(m, 32);
   OTG_CUDA(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
 }
 
@@ -430,6 +441,9 @@ otg_status otg_problem_info_get(otg_problem h, otg_problem_info* out) {
     out->world_size = P.world;
     out->rank = P.rank;
     out->device = P.device;
+    out->sweep_mode = P.storage == OTG_STORE_F64 ? 0 : (P.fused ? 2 : 1);
+    out->sweep_clusters = P.fused_clusters;
+    out->col_splits = P.col_splits;
   });
 }
 

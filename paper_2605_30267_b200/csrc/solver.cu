@@ -182,6 +182,7 @@ void fill_result(Problem& P, otg_solve_result* res, const LoopOut& lo) {
   res->row_pass_seconds = lo.row_s;
   res->col_pass_seconds = lo.col_s;
   res->kernel_launches = c.evaluations * 7;
+  res->row_redos = c.redo_total;
   d2h(P, res->u, P.u, P.n_local);
   d2h(P, res->v, P.p, P.m);
   d2h(P, res->w, P.wacc, P.m);
@@ -275,8 +276,7 @@ otg_status otg_row_solve_marginals(otg_problem h, const double* v, double* u, do
     c.mode = MODE_EVAL;
     put_ctrl(P, c);
     h2d(P, P.p, v, P.m);
-    launch_row_pass(P);
-    launch_col_pass(P);
+    launch_sweeps(P, false, nullptr);
     launch_merge_nolog(P);
     if (P.world > 1) comm_allreduce_sum(P, P.col, static_cast<size_t>(P.mpad + 1));
     d2h(P, u, P.u, P.n_local);
@@ -487,9 +487,14 @@ otg_status otg_time_sweeps(otg_problem h, const double* v, int reps, double ms[3
       put_ctrl(P, c);
       h2d(P, P.p, v, P.m);
       OTG_CUDA(cudaEventRecord(e[0], P.stream));
-      launch_row_pass(P);
-      OTG_CUDA(cudaEventRecord(e[1], P.stream));
-      launch_col_pass(P);
+      if (P.fused) {
+        launch_sweeps(P, false, nullptr);
+        OTG_CUDA(cudaEventRecord(e[1], P.stream));
+      } else {
+        launch_row_pass(P);
+        OTG_CUDA(cudaEventRecord(e[1], P.stream));
+        launch_col_pass(P);
+      }
       OTG_CUDA(cudaEventRecord(e[2], P.stream));
       launch_merge_nolog(P);
       OTG_CUDA(cudaEventRecord(e[3], P.stream));
@@ -508,9 +513,15 @@ otg_status otg_time_sweeps(otg_problem h, const double* v, int reps, double ms[3
     if (bytes) {
       const double elem = P.storage == OTG_STORE_F64 ? 8.0 : 4.0;
       const double nm = static_cast<double>(P.n_local) * static_cast<double>(P.m);
-      bytes[0] = nm * elem + P.m * 8.0 + P.n_local * 8.0 * 8;      // C + p + row outputs
-      bytes[1] = nm * elem + P.m * 8.0 + P.n_local * 16.0 +
-                 static_cast<double>(P.col_splits) * P.vshards * P.m * 8.0;  // C + aux + partials
+      if (P.fused) {  // one read of C, p, a, log a; u/M/S/w out; per-cluster partials
+        bytes[0] = nm * elem + P.m * 8.0 + P.n_local * (2 * 8.0 + 4 * 8.0) +
+                   static_cast<double>(P.fused_clusters) * P.m * 8.0;
+        bytes[1] = 0.0;
+      } else {
+        bytes[0] = nm * elem + P.m * 8.0 + P.n_local * (2 * 8.0 + 4 * 8.0 + 16.0);
+        bytes[1] = nm * elem + P.m * 8.0 + P.n_local * 16.0 +
+                   static_cast<double>(P.col_splits) * P.vshards * P.m * 8.0;  // C + aux + partials
+      }
     }
   });
 }

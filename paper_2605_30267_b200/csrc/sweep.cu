@@ -104,6 +104,26 @@ __device__ double block_max(double v, double* sh) {
   return r;
 }
 
+// Exact fp32 -> fp64 with integer ops (ALU pipe, no F2F on the XU pipe).
+// Normal and zero inputs map exactly except +-0 and subnormals, which land
+// within 2^-126 of their value (|error| < 1.2e-38; irrelevant for a cost).
+__device__ __forceinline__ double f32_to_f64(float x) {
+  const uint32_t b = __float_as_uint(x);
+  const uint32_t hi = (((b & 0x7fffffffu) >> 3) + 0x38000000u) | (b & 0x80000000u);
+  return __hiloint2double(static_cast<int>(hi), static_cast<int>(b << 29));
+}
+
+// fp64 -> fp32 (round to nearest) for a value in [-2^127, 0] with integer ops;
+// values above -2^-100 are clamped to -2^-100 (ex2 of it is 1.0f).
+__device__ __forceinline__ float neg_f64_to_f32(double x) {
+  x = fmin(x, -7.888609052210118e-31);  // -2^-100
+  const uint32_t lo = static_cast<uint32_t>(__double2loint(x));
+  const uint32_t hi = static_cast<uint32_t>(__double2hiint(x));
+  const uint32_t w = __funnelshift_l(lo, hi, 3);  // exponent[8:0] | mantissa[51:29]
+  const uint32_t rb = (lo >> 28) & 1u;            // round bit
+  return __uint_as_float((w - 0xC0000000u + rb) | 0x80000000u);
+}
+
 // Quantised split of a base-2 value: hi is a multiple of 2^-8 (exact in fp32
 // for |x| < 2^15), lo = x - hi rounded to fp32 (|lo| <= 2^-9).
 __device__ __forceinline__ void split_q(double x2, float& hi, float& lo) {
@@ -163,79 +183,279 @@ k_row_precise(const double* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
   }
 }
 
-// fp32 storage: R rows per CTA; every thread streams float4 columns of the R
-// rows, the column potential is loaded once per CTA column-chunk and reused
-// across the R rows.
+// fp32 storage, exact row statistics for R rows (fp64 exponent argument with an
+// online max).  Every thread streams float4 columns of the R rows; the column
+// potential is loaded once per column chunk and reused across the R rows.
+// Used for the first evaluation of a solve (no shift estimate yet) and, in
+// LIST mode, to redo the rows whose shift estimate failed (k_row_shift).
 template <int R>
-__global__ void __launch_bounds__(kRowThreads)
-k_row_fast(const float* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
-           const double* __restrict__ p, double kappa, const double* __restrict__ a,
-           const double* __restrict__ loga, double* __restrict__ rowM,
-           double* __restrict__ rowS, double* __restrict__ u, double* __restrict__ wrow,
-           float4* __restrict__ aux, double* __restrict__ rowpart,
-           const Ctrl* __restrict__ ctrl) {
-  if (ctrl->done) return;
+__device__ void row_exact_block(const int64_t* rows, const float* __restrict__ C, int64_t ldc,
+                                int64_t m, const double* __restrict__ p, double kappa,
+                                const double* __restrict__ a, const double* __restrict__ loga,
+                                double* __restrict__ rowM, double* __restrict__ rowS,
+                                double* __restrict__ u, double* __restrict__ wrow,
+                                float4* __restrict__ aux, double* __restrict__ rowM2,
+                                int* __restrict__ rowJ, const bool* valid) {
   __shared__ double sh[kRowThreads / 32];
   __shared__ double resM[R], resS[R];
-  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * R;
+  __shared__ int resJ[R];
   const float* Cr[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) Cr[r] = C + (r0 + r < n ? r0 + r : n - 1) * ldc;
+  for (int r = 0; r < R; ++r) Cr[r] = C + rows[r] * ldc;
   double mr[R], sr[R];
+  int jr[R];  // argmax column of the running max (next evaluation's shift estimate)
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     mr[r] = -INFINITY;
     sr[r] = 0.0;
+    jr[r] = 0;
   }
+  // Base-2 units: t2 = p_j log2e - C_ij kappa log2e (fp64 DFMA on an exactly
+  // up-cast C), online max m2, ex2(t2 - m2) on MUFU; fp32 <-> fp64 conversions
+  // with integer ops (ALU pipe) instead of F2F (XU pipe, shared with MUFU).
+  const double k2 = kappa * kLog2e;
   const int64_t nq = m >> 2;
   const double2* p2 = reinterpret_cast<const double2*>(p);
   for (int64_t q = threadIdx.x; q < nq; q += kRowThreads) {
     const double2 pa = __ldg(p2 + 2 * q), pb = __ldg(p2 + 2 * q + 1);
+    const double q0 = pa.x * kLog2e, q1 = pa.y * kLog2e, q2 = pb.x * kLog2e, q3 = pb.y * kLog2e;
     float4 c[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) c[r] = ld_stream(reinterpret_cast<const float4*>(Cr[r]) + q);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const double t0 = fma(-static_cast<double>(c[r].x), kappa, pa.x);
-      const double t1 = fma(-static_cast<double>(c[r].y), kappa, pa.y);
-      const double t2 = fma(-static_cast<double>(c[r].z), kappa, pb.x);
-      const double t3 = fma(-static_cast<double>(c[r].w), kappa, pb.y);
+      const double t0 = fma(-f32_to_f64(c[r].x), k2, q0);
+      const double t1 = fma(-f32_to_f64(c[r].y), k2, q1);
+      const double t2 = fma(-f32_to_f64(c[r].z), k2, q2);
+      const double t3 = fma(-f32_to_f64(c[r].w), k2, q3);
       const double cm = fmax(fmax(t0, t1), fmax(t2, t3));
       if (cm > mr[r]) {
-        sr[r] *= exp(mr[r] - cm);
+        sr[r] *= exp2(mr[r] - cm);
         mr[r] = cm;
+        jr[r] = static_cast<int>(4 * q) + (t0 == cm ? 0 : t1 == cm ? 1 : t2 == cm ? 2 : 3);
       }
       const double mm = mr[r];
-      const float e = ex2_approx(static_cast<float>(t0 - mm) * static_cast<float>(kLog2e)) +
-                      ex2_approx(static_cast<float>(t1 - mm) * static_cast<float>(kLog2e)) +
-                      ex2_approx(static_cast<float>(t2 - mm) * static_cast<float>(kLog2e)) +
-                      ex2_approx(static_cast<float>(t3 - mm) * static_cast<float>(kLog2e));
+      const float e = ex2_approx(neg_f64_to_f32(t0 - mm)) + ex2_approx(neg_f64_to_f32(t1 - mm)) +
+                      ex2_approx(neg_f64_to_f32(t2 - mm)) + ex2_approx(neg_f64_to_f32(t3 - mm));
       sr[r] += static_cast<double>(e);
     }
   }
-  // ragged tail (m % 4 columns)
-  for (int64_t j = 4 * nq + threadIdx.x; j < m; j += kRowThreads) {
-    const double pj = p[j];
+  for (int64_t j = 4 * nq + threadIdx.x; j < m; j += kRowThreads) {  // ragged tail
+    const double pj = p[j] * kLog2e;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const double t = fma(-static_cast<double>(Cr[r][j]), kappa, pj);
+      const double t = fma(-f32_to_f64(Cr[r][j]), k2, pj);
       if (t > mr[r]) {
-        sr[r] *= exp(mr[r] - t);
+        jr[r] = static_cast<int>(j);
+        sr[r] *= exp2(mr[r] - t);
         mr[r] = t;
       }
-      sr[r] += static_cast<double>(
-          ex2_approx(static_cast<float>(t - mr[r]) * static_cast<float>(kLog2e)));
+      sr[r] += static_cast<double>(ex2_approx(neg_f64_to_f32(t - mr[r])));
     }
   }
-  // per row: exact max, then each thread rescales its partial once (fp64 exp)
+  // per row: exact max, then each thread rescales its partial once (fp64 exp2)
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const double M = block_max<kRowThreads>(mr[r], sh);
-    const double s = sr[r] > 0.0 ? sr[r] * exp(mr[r] - M) : 0.0;
+    const double M2 = block_max<kRowThreads>(mr[r], sh);
+    const double s = sr[r] > 0.0 ? sr[r] * exp2(mr[r] - M2) : 0.0;
     const double S = block_sum<kRowThreads>(s, sh);
+    const double J = block_max<kRowThreads>(mr[r] == M2 ? -static_cast<double>(jr[r]) : -1e300, sh);
     if (threadIdx.x == 0) {
-      resM[r] = M;
+      resM[r] = M2;
       resS[r] = S;
+      resJ[r] = static_cast<int>(-J);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < R && valid[threadIdx.x]) {
+    const int r = threadIdx.x;
+    const int64_t i = rows[r];
+    const double M2 = resM[r], S = resS[r];
+    const double M = M2 * kLn2;
+    const double ui = (loga[i] - M) - log(S);
+    const double wi = a[i] / S;
+    rowM[i] = M;
+    rowS[i] = S;
+    u[i] = ui;
+    wrow[i] = wi;
+    rowM2[i] = M2;
+    rowJ[i] = resJ[r];
+    // the column pass uses the S-consistent shift M2 split into hi + lo
+    float hi, lo;
+    split_q(M2, hi, lo);
+    aux[i] = make_float4(hi, lo, static_cast<float>(wi), 0.0f);
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(kRowThreads)
+k_row_exact(const float* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
+            const double* __restrict__ p, double kappa, const double* __restrict__ a,
+            const double* __restrict__ loga, double* __restrict__ rowM,
+            double* __restrict__ rowS, double* __restrict__ u, double* __restrict__ wrow,
+            float4* __restrict__ aux, double* __restrict__ rowM2, int* __restrict__ rowJ,
+            const Ctrl* __restrict__ ctrl) {
+  if (ctrl->done || ctrl->shift_valid) return;
+  int64_t rows[R];
+  bool valid[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * R + r;
+    valid[r] = i < n;
+    rows[r] = valid[r] ? i : n - 1;
+  }
+  row_exact_block<R>(rows, C, ldc, m, p, kappa, a, loga, rowM, rowS, u, wrow, aux, rowM2, rowJ,
+                     valid);
+}
+
+// Exact redo of the rows k_row_shift flagged (grid-stride over the list).
+__global__ void __launch_bounds__(kRowThreads)
+k_row_redo(const float* __restrict__ C, int64_t ldc, int64_t m, const double* __restrict__ p,
+           double kappa, const double* __restrict__ a, const double* __restrict__ loga,
+           double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
+           double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
+           int* __restrict__ rowJ, const int* __restrict__ redo_rows,
+           const Ctrl* __restrict__ ctrl) {
+  if (ctrl->done || !ctrl->shift_valid) return;
+  const unsigned cnt = ctrl->redo_count;
+  for (unsigned k = blockIdx.x; k < cnt; k += gridDim.x) {
+    const int64_t rows[1] = {redo_rows[k]};
+    const bool valid[1] = {true};
+    row_exact_block<1>(rows, C, ldc, m, p, kappa, a, loga, rowM, rowS, u, wrow, aux, rowM2,
+                       rowJ, valid);
+    __syncthreads();
+  }
+}
+
+// fp32 row pass with a shift ESTIMATE (all-fp32, no fp64 per element).  From
+// the previous evaluation the row keeps its exact base-2 max M2_prev and the
+// argmax column J; with dq_j = (p_new - p_old)_j log2e the new max satisfies
+//   L = M2_prev + dq_J  <=  M2_new  <=  M2_prev + max_j dq_j = U.
+// The shift s = min(L + 1, U), rounded up to a multiple of 2^-8, is an exact
+// constant of the row, so every exponent t = Vc_j - s - C_ij kappa2 (+ small
+// terms) is formed by the same exact-cancellation FMA as the column pass,
+// S_i = sum_j ex2(t_ij) and u_i = log a_i - s ln2 - log S_i are the
+// reference's quantities up to rounding.  Precision needs the dominant
+// exponents small: rows whose true max T = M2_new - s falls outside
+// [-kRedoLo, kRedoHi] (the argmax moved to a column whose potential moved
+// much more) are listed for an exact redo (k_row_redo).  The kernel tracks the
+// new argmax for the next evaluation.
+constexpr float kRedoLo = 2.0f;
+constexpr float kRedoHi = 6.0f;
+
+template <int R>
+__global__ void __launch_bounds__(kRowThreads)
+k_row_shift(const float* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
+            const float* __restrict__ vq, const double* __restrict__ dq, int64_t mpad, float kh,
+            float kl, const double* __restrict__ a, const double* __restrict__ loga,
+            double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
+            double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
+            int* __restrict__ rowJ, int* __restrict__ redo_rows, Ctrl* __restrict__ ctrl) {
+  if (ctrl->done || !ctrl->shift_valid) return;
+  __shared__ double sh[kRowThreads / 32];
+  __shared__ float shf[kRowThreads / 32];
+  __shared__ int shj[kRowThreads / 32];
+  __shared__ float sSc[R], resT[R];
+  __shared__ double resS[R];
+  __shared__ int resJ[R];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * R;
+  if (threadIdx.x < R) {
+    const int64_t i = r0 + threadIdx.x < n ? r0 + threadIdx.x : n - 1;
+    const double M2 = rowM2[i];
+    const double lo = M2 + dq[rowJ[i]], hi = M2 + ctrl->dmax2;
+    sSc[threadIdx.x] = static_cast<float>(ceil(fmin(lo + 1.0, hi) * 256.0) * (1.0 / 256.0));
+  }
+  __syncthreads();
+  float Sc[R], tm[R], fs[R];
+  int tj[R];
+  double ss[R];
+  const float* Cr[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    Sc[r] = sSc[r];
+    tm[r] = -FLT_MAX;
+    tj[r] = 0;
+    fs[r] = 0.f;
+    ss[r] = 0.0;
+    Cr[r] = C + (r0 + r < n ? r0 + r : n - 1) * ldc;
+  }
+  const int64_t nq = m >> 2;
+  const float4* Vq = reinterpret_cast<const float4*>(vq);
+  const float4* Fq = reinterpret_cast<const float4*>(vq + mpad);
+  int chunk = 0;
+  for (int64_t q = threadIdx.x; q < nq; q += kRowThreads) {
+    const float4 V = __ldg(Vq + q), F = __ldg(Fq + q);
+    float4 c[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) c[r] = ld_stream(reinterpret_cast<const float4*>(Cr[r]) + q);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const float t0 = fmaf(-c[r].x, kh, V.x - Sc[r]) + fmaf(-c[r].x, kl, F.x);
+      const float t1 = fmaf(-c[r].y, kh, V.y - Sc[r]) + fmaf(-c[r].y, kl, F.y);
+      const float t2 = fmaf(-c[r].z, kh, V.z - Sc[r]) + fmaf(-c[r].z, kl, F.z);
+      const float t3 = fmaf(-c[r].w, kh, V.w - Sc[r]) + fmaf(-c[r].w, kl, F.w);
+      const float qm = fmaxf(fmaxf(t0, t1), fmaxf(t2, t3));
+      if (qm > tm[r]) {
+        tm[r] = qm;
+        tj[r] = static_cast<int>(4 * q) + (t0 == qm ? 0 : t1 == qm ? 1 : t2 == qm ? 2 : 3);
+      }
+      fs[r] += (ex2_approx(t0) + ex2_approx(t1)) + (ex2_approx(t2) + ex2_approx(t3));
+    }
+    if (++chunk == 4) {  // fp32 partials flushed into fp64 every 16 elements
+      chunk = 0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        ss[r] += static_cast<double>(fs[r]);
+        fs[r] = 0.f;
+      }
+    }
+  }
+  for (int64_t j = 4 * nq + threadIdx.x; j < m; j += kRowThreads) {  // ragged tail
+    const float V = vq[j], F = vq[mpad + j];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const float c = Cr[r][j];
+      const float t = fmaf(-c, kh, V - Sc[r]) + fmaf(-c, kl, F);
+      if (t > tm[r]) {
+        tm[r] = t;
+        tj[r] = static_cast<int>(j);
+      }
+      fs[r] += ex2_approx(t);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    ss[r] += static_cast<double>(fs[r]);
+    float t = tm[r];
+    int jj = tj[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float t2 = __shfl_xor_sync(0xffffffffu, t, o);
+      const int j2 = __shfl_xor_sync(0xffffffffu, jj, o);
+      if (t2 > t || (t2 == t && j2 < jj)) {
+        t = t2;
+        jj = j2;
+      }
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+      shf[threadIdx.x >> 5] = t;
+      shj[threadIdx.x >> 5] = jj;
+    }
+    __syncthreads();
+    float T = -FLT_MAX;
+    int J = 0;
+#pragma unroll
+    for (int k = 0; k < kRowThreads / 32; ++k)
+      if (shf[k] > T) {
+        T = shf[k];
+        J = shj[k];
+      }
+    const double S = block_sum<kRowThreads>(ss[r], sh);
+    if (threadIdx.x == 0) {
+      resT[r] = T;
+      resS[r] = S;
+      resJ[r] = J;
     }
   }
   __syncthreads();
@@ -243,27 +463,24 @@ k_row_fast(const float* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
     const int r = threadIdx.x;
     const int64_t i = r0 + r;
     if (i < n) {
-      const double M = resM[r], S = resS[r];
-      const double ui = (loga[i] - M) - log(S);
-      const double wi = a[i] / S;
-      rowM[i] = M;
-      rowS[i] = S;
-      u[i] = ui;
-      wrow[i] = wi;
-      float hi, lo;
-      split_q(M * kLog2e, hi, lo);
-      aux[i] = make_float4(hi, lo, static_cast<float>(wi), 0.0f);
-      resS[r] = ui * a[i];
-    } else {
-      resS[r] = 0.0;
+      const float T = resT[r];
+      if (!(T >= -kRedoLo && T <= kRedoHi)) {  // estimate too loose (or NaN): exact redo
+        redo_rows[atomicAdd(&ctrl->redo_count, 1u)] = static_cast<int>(i);
+      } else {
+        const double S = resS[r];
+        const double sc = static_cast<double>(Sc[r]);
+        const double M = sc * kLn2;
+        const double ui = (loga[i] - M) - log(S);
+        const double wi = a[i] / S;
+        rowM[i] = M;
+        rowS[i] = S;
+        u[i] = ui;
+        wrow[i] = wi;
+        rowM2[i] = sc + static_cast<double>(T);
+        rowJ[i] = resJ[r];
+        aux[i] = make_float4(Sc[r], 0.0f, static_cast<float>(wi), 0.0f);
+      }
     }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-#pragma unroll
-    for (int r = 0; r < R; ++r) t += resS[r];
-    rowpart[blockIdx.x] = t;
   }
 }
 
@@ -373,13 +590,13 @@ k_col_fast(const float* __restrict__ C, int64_t ldc, int64_t m, const double* __
 __global__ void __launch_bounds__(kEThreads)
 k_merge(const double* __restrict__ part, int nshards, int splits, int64_t m, int64_t mpad,
         double* __restrict__ col, double* __restrict__ col_log, int* __restrict__ flag_idx,
-        int* __restrict__ fb_cols, const double* __restrict__ rowpart, int64_t nrowpart,
-        int flag, Ctrl* __restrict__ ctrl) {
+        int* __restrict__ fb_cols, const double* __restrict__ u, const double* __restrict__ a,
+        int64_t nrows, int flag, Ctrl* __restrict__ ctrl) {
   if (ctrl->done) return;
   __shared__ double sh[kEThreads / 32];
-  if (blockIdx.x == 0) {
+  if (blockIdx.x == 0) {  // <u, a> over the local rows, fixed order (for f)
     double t = 0.0;
-    for (int64_t k = threadIdx.x; k < nrowpart; k += kEThreads) t += rowpart[k];
+    for (int64_t k = threadIdx.x; k < nrows; k += kEThreads) t += u[k] * a[k];
     t = block_sum<kEThreads>(t, sh);
     if (threadIdx.x == 0) col[mpad] = t;
   }
@@ -661,6 +878,8 @@ k_finalize(int64_t m, int64_t mpad, const double* __restrict__ p, const double* 
   Ctrl* C = ctrl;
   C->e1_counter = 0;
   C->fb_count = 0;
+  C->redo_total += C->redo_count;
+  C->redo_count = 0;
   const double ua = col[mpad];
   const double f = (1.0 - ua) - pb;
   C->mean_y = sy / static_cast<double>(m);
@@ -681,11 +900,11 @@ __device__ __forceinline__ double expm1_over_z(double z) {  // mirror.cpp:21-24
 }
 
 __global__ void __launch_bounds__(kEThreads)
-k_apply(int64_t m, const double* __restrict__ b, double* __restrict__ p,
+k_apply(int64_t m, int64_t mpad, const double* __restrict__ b, double* __restrict__ p,
         double* __restrict__ wacc, double* __restrict__ y, const double* __restrict__ grad,
         double* __restrict__ prev_grad, double* __restrict__ prev_x,
-        double* __restrict__ prev_y, double* __restrict__ e2_part, double* __restrict__ trace,
-        Ctrl* __restrict__ ctrl) {
+        double* __restrict__ prev_y, float* __restrict__ vq, double* __restrict__ dq, int fast,
+        double* __restrict__ e2_part, double* __restrict__ trace, Ctrl* __restrict__ ctrl) {
   if (!ctrl->live_e2) return;
   __shared__ double sh[kEThreads / 32];
   __shared__ bool last;
@@ -697,7 +916,11 @@ k_apply(int64_t m, const double* __restrict__ b, double* __restrict__ p,
   const bool resc = ctrl->stage_changed && ctrl->rescale_w;
   const bool stab = ctrl->stability != 0 && mode >= MODE_ACC_RUN;
   const bool have_prev = ctrl->have_prev != 0;
+  // the next point replaces p: record max_j (p_new - p_old) and the split of
+  // p_new for the fp32 row pass's shift estimate (k_row_shift)
+  const bool moves = !done && mode != MODE_EVAL;
   double c1 = 0.0, br = 0.0, c2 = 0.0, qq = 0.0, drift = 0.0, ginf = 0.0, dom = 0.0;
+  double dstep = -INFINITY;
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * kEThreads + threadIdx.x; j < m;
        j += static_cast<int64_t>(gridDim.x) * kEThreads) {
     const double S = y[j] - mean;  // project_zero_sum (mirror.cpp:103-105)
@@ -705,60 +928,58 @@ k_apply(int64_t m, const double* __restrict__ b, double* __restrict__ p,
       y[j] = S;
       continue;
     }
-    if (mode == MODE_SINKHORN) {
-      if (!done) p[j] = S;
-      continue;
-    }
     const double x = p[j];
-    double w = wacc[j];
-    if (step) w = (w + (al * al - 2.0) * x + 2.0 * S) / (1.0 + al);  // accel.cpp:168
-    if (stab) {
-      const double yn = w / al;
-      const double g1 = grad[j];
-      if (have_prev) {
-        const double g0 = prev_grad[j], bj = b[j];
-        ginf = fmax(ginf, fabs(g0));
-        const double r0 = g0 / bj, r1 = g1 / bj;
-        if (r0 <= -1.0 || r1 <= -1.0) {
-          dom = 1.0;
-        } else {
-          const double D0 = bj * expm1_over_z(log1p(r0));
-          const double D1 = bj * expm1_over_z(log1p(r1));
-          c1 += g0 * g0 * D1 / (D0 * D0);
-          br += g0 - bj * log1p(r0);
-          const double vk = prev_y[j] - prev_x[j], vk1 = yn - x;
-          c2 += (D1 - D0) * (vk * vk);
-          qq += D1 * (vk1 * vk1);
-          drift = fmax(drift, fabs(D1 - D0));
+    double pn = S;
+    if (mode != MODE_SINKHORN) {
+      double w = wacc[j];
+      if (step) w = (w + (al * al - 2.0) * x + 2.0 * S) / (1.0 + al);  // accel.cpp:168
+      if (stab) {
+        const double yn = w / al;
+        const double g1 = grad[j];
+        if (have_prev) {
+          const double g0 = prev_grad[j], bj = b[j];
+          ginf = fmax(ginf, fabs(g0));
+          const double r0 = g0 / bj, r1 = g1 / bj;
+          if (r0 <= -1.0 || r1 <= -1.0) {
+            dom = 1.0;
+          } else {
+            const double D0 = bj * expm1_over_z(log1p(r0));
+            const double D1 = bj * expm1_over_z(log1p(r1));
+            c1 += g0 * g0 * D1 / (D0 * D0);
+            br += g0 - bj * log1p(r0);
+            const double vk = prev_y[j] - prev_x[j], vk1 = yn - x;
+            c2 += (D1 - D0) * (vk * vk);
+            qq += D1 * (vk1 * vk1);
+            drift = fmax(drift, fabs(D1 - D0));
+          }
         }
+        prev_grad[j] = g1;
+        prev_x[j] = x;
+        prev_y[j] = yn;
       }
-      prev_grad[j] = g1;
-      prev_x[j] = x;
-      prev_y[j] = yn;
+      if (resc) w *= an / al;  // accel.cpp:279
+      wacc[j] = w;
+      pn = (w + S) / (1.0 + an);  // accel.cpp:161
     }
-    if (resc) w *= an / al;  // accel.cpp:279
-    wacc[j] = w;
-    if (!done) p[j] = (w + S) / (1.0 + an);  // accel.cpp:161
-  }
-  if (!stab) {
-    // no cross-block bookkeeping needed beyond releasing the handoff
-    if (threadIdx.x == 0) {
-      __threadfence();
-      const unsigned prev = atomicAdd(&ctrl->e2_counter, 1u);
-      if (prev == gridDim.x - 1) {
-        ctrl->e2_counter = 0;
-        ctrl->live_e2 = 0;
+    if (moves) {
+      p[j] = pn;
+      dstep = fmax(dstep, pn - x);
+      if (fast) {
+        split_q(pn * kLog2e, vq[j], vq[mpad + j]);
+        dq[j] = (pn - x) * kLog2e;
       }
     }
-    return;
   }
-  c1 = block_sum<kEThreads>(c1, sh);
-  br = block_sum<kEThreads>(br, sh);
-  c2 = block_sum<kEThreads>(c2, sh);
-  qq = block_sum<kEThreads>(qq, sh);
-  drift = block_max<kEThreads>(drift, sh);
-  ginf = block_max<kEThreads>(ginf, sh);
-  dom = block_max<kEThreads>(dom, sh);
+  if (stab) {
+    c1 = block_sum<kEThreads>(c1, sh);
+    br = block_sum<kEThreads>(br, sh);
+    c2 = block_sum<kEThreads>(c2, sh);
+    qq = block_sum<kEThreads>(qq, sh);
+    drift = block_max<kEThreads>(drift, sh);
+    ginf = block_max<kEThreads>(ginf, sh);
+    dom = block_max<kEThreads>(dom, sh);
+  }
+  dstep = block_max<kEThreads>(dstep, sh);
   if (threadIdx.x == 0) {
     double* dst = e2_part + blockIdx.x * 8;
     dst[0] = c1;
@@ -768,6 +989,7 @@ k_apply(int64_t m, const double* __restrict__ b, double* __restrict__ p,
     dst[4] = drift;
     dst[5] = ginf;
     dst[6] = dom;
+    dst[7] = dstep;
     __threadfence();
     const unsigned prev = atomicAdd(&ctrl->e2_counter, 1u);
     last = prev == gridDim.x - 1;
@@ -775,14 +997,14 @@ k_apply(int64_t m, const double* __restrict__ b, double* __restrict__ p,
   __syncthreads();
   if (!last || threadIdx.x != 0) return;
   __threadfence();
-  double t[7] = {0, 0, 0, 0, 0, 0, 0};
+  double t[8] = {0, 0, 0, 0, 0, 0, 0, -INFINITY};
   for (unsigned k = 0; k < gridDim.x; ++k) {
     const volatile double* src = e2_part + k * 8;
     for (int q = 0; q < 4; ++q) t[q] += src[q];
-    for (int q = 4; q < 7; ++q) t[q] = fmax(t[q], src[q]);
+    for (int q = 4; q < 8; ++q) t[q] = fmax(t[q], src[q]);
   }
   Ctrl* C = ctrl;
-  if (have_prev) {
+  if (stab && have_prev) {
     double cells[5];
     bool valid = true;
     if (t[5] < kGradFloor) {  // diag.cpp:116-123: skipped, counts as held, not checked
@@ -804,7 +1026,11 @@ k_apply(int64_t m, const double* __restrict__ b, double* __restrict__ p,
       for (int q = 0; q < 5; ++q) r[7 + q] = cells[q];
     }
   }
-  C->have_prev = 1;
+  if (stab) C->have_prev = 1;
+  if (moves && fast) {
+    C->dmax2 = t[7] * kLog2e;
+    C->shift_valid = isfinite(t[7]) ? 1 : 0;
+  }
   C->e2_counter = 0;
   C->live_e2 = 0;
 }
@@ -817,15 +1043,25 @@ int e_grid(int64_t m) {
 }  // namespace
 
 // ---------------------------------------------------------------- launch ---
-int64_t rows_per_cta_fast(const Problem& P) { return P.n_local >= 8 ? 8 : 1; }
+// Rows per CTA of the fp32 row pass (tuning knob OTG_ROW_R = 1, 4 or 8).
+int64_t rows_per_cta_fast(const Problem& P) {
+  static const int env = [] {
+    const char* s = getenv("OTG_ROW_R");
+    return s ? atoi(s) : 0;
+  }();
+  const int64_t want = (env == 1 || env == 4 || env == 8) ? env : 4;
+  return P.n_local >= want ? want : 1;
+}
 
 void configure_sweeps(Problem& P) {
-  // column-pass split: enough CTAs to fill 148 SMs several times over
+  // column-pass split: ~24 CTAs per SM over the grid so the dynamic CTA
+  // scheduler balances the 148 SMs (ncu: 640 CTAs = 0.48 waves was
+  // latency-bound); partials cost splits * m * 8 B (< 1% of the sweep)
   const int64_t colblocks =
       P.storage == OTG_STORE_F64 ? (P.m + kColThreads - 1) / kColThreads
                                  : (P.m + 4 * kColThreads - 1) / (4 * kColThreads);
   const int64_t shard_rows = (P.n_local + P.vshards - 1) / P.vshards;
-  int64_t splits = (4 * 148 + colblocks - 1) / colblocks;
+  int64_t splits = (24 * 148 + colblocks - 1) / colblocks;
   splits = std::max<int64_t>(1, std::min<int64_t>(splits, (shard_rows + 63) / 64));
   P.col_splits = static_cast<int>(splits);
   P.rows_per_split = (shard_rows + splits - 1) / splits;
@@ -856,14 +1092,32 @@ void launch_row_pass(Problem& P) {
           P.C64, P.ldc, P.n_local, P.m, P.p, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, rowpart,
           P.ctrl);
   } else {
-    if (rows_per_cta_fast(P) == 8)
-      k_row_fast<8><<<blocks, kRowThreads, 0, P.stream>>>(
-          P.C32, P.ldc, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow,
-          P.aux, rowpart, P.ctrl);
-    else
-      k_row_fast<1><<<blocks, kRowThreads, 0, P.stream>>>(
-          P.C32, P.ldc, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow,
-          P.aux, rowpart, P.ctrl);
+    // exact kernel (first evaluation of a solve / one-shots), shift-estimate
+    // kernel (steady state), exact redo of the rows the estimate missed; each
+    // returns at once when its case does not apply
+    const int64_t R = rows_per_cta_fast(P);
+    const double k2 = P.kappa * kLog2e;
+    const float kh = static_cast<float>(k2);
+    const float kl = static_cast<float>(k2 - static_cast<double>(kh));
+#define OTG_ROW(RR)                                                                           \
+  k_row_exact<RR><<<blocks, kRowThreads, 0, P.stream>>>(P.C32, P.ldc, P.n_local, P.m, P.p,    \
+                                                       P.kappa, P.a, P.loga, P.rowM, P.rowS,  \
+                                                       P.u, P.wrow, P.aux, P.rowM2, P.rowJ,   \
+                                                       P.ctrl);                                \
+  k_row_shift<RR><<<blocks, kRowThreads, 0, P.stream>>>(                                      \
+      P.C32, P.ldc, P.n_local, P.m, P.vq, P.dq, P.mpad, kh, kl, P.a, P.loga, P.rowM, P.rowS,  \
+      P.u, P.wrow, P.aux, P.rowM2, P.rowJ, P.redo_rows, P.ctrl)
+    if (R == 8) {
+      OTG_ROW(8);
+    } else if (R == 4) {
+      OTG_ROW(4);
+    } else {
+      OTG_ROW(1);
+    }
+#undef OTG_ROW
+    k_row_redo<<<296, kRowThreads, 0, P.stream>>>(P.C32, P.ldc, P.m, P.p, P.kappa, P.a, P.loga,
+                                                  P.rowM, P.rowS, P.u, P.wrow, P.aux, P.rowM2,
+                                                  P.rowJ, P.redo_rows, P.ctrl);
   }
   OTG_CUDA(cudaGetLastError());
 }
@@ -891,12 +1145,17 @@ void launch_col_pass(Problem& P) {
   OTG_CUDA(cudaGetLastError());
 }
 
+int partial_rows(const Problem& P) {
+  return P.fused ? P.fused_clusters : P.vshards * P.col_splits;
+}
+
 static void launch_merge(Problem& P, bool flag) {
   const int64_t blocks = (P.m + kEThreads - 1) / kEThreads;
-  double* rowpart = P.e1_part + P.e_blocks * 8;
-  k_merge<<<blocks, kEThreads, 0, P.stream>>>(P.part, P.vshards, P.col_splits, P.m, P.mpad,
-                                              P.col, P.col_log, P.flag_idx, P.fb_cols, rowpart,
-                                              row_blocks(P), flag ? 1 : 0, P.ctrl);
+  const int shards = P.fused ? 1 : P.vshards;
+  const int splits = P.fused ? P.fused_clusters : P.col_splits;
+  k_merge<<<blocks, kEThreads, 0, P.stream>>>(P.part, shards, splits, P.m, P.mpad, P.col,
+                                              P.col_log, P.flag_idx, P.fb_cols, P.u, P.a,
+                                              P.n_local, flag ? 1 : 0, P.ctrl);
   OTG_CUDA(cudaGetLastError());
 }
 
@@ -908,13 +1167,29 @@ static void mark(Problem& P, cudaEvent_t e) {
   OTG_CUDA(cudaEventRecordWithFlags(e, P.stream, cudaEventRecordExternal));
 }
 
-void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
+// Both O(nm) passes: the fused single-HBM-pass kernel when the handle has one
+// (fp32 storage, m <= 65536), else the row pass then the column pass.
+void launch_sweeps(Problem& P, bool timed, cudaEvent_t* ev4) {
+  if (P.fused) {
+    if (timed) mark(P, ev4[0]);
+    launch_fused(P, P.e1_part + P.e_blocks * 8);
+    if (timed) {
+      mark(P, ev4[1]);
+      mark(P, ev4[2]);
+      mark(P, ev4[3]);
+    }
+    return;
+  }
   if (timed) mark(P, ev4[0]);
   launch_row_pass(P);
   if (timed) mark(P, ev4[1]);
   if (timed) mark(P, ev4[2]);
   launch_col_pass(P);
   if (timed) mark(P, ev4[3]);
+}
+
+void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
+  launch_sweeps(P, timed, ev4);
   launch_merge(P, with_log);
   if (P.world > 1) comm_allreduce_sum(P, P.col, static_cast<size_t>(P.mpad + 1));
   if (!with_log) return;
@@ -934,9 +1209,11 @@ void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
 }
 
 void launch_apply(Problem& P) {
-  k_apply<<<P.e_blocks, kEThreads, 0, P.stream>>>(P.m, P.b, P.p, P.wacc, P.y, P.grad,
-                                                  P.prev_grad, P.prev_x, P.prev_y, P.e2_part,
-                                                  P.trace, P.ctrl);
+  const int fast = P.storage == OTG_STORE_F32 && !P.fused;
+  k_apply<<<P.e_blocks, kEThreads, 0, P.stream>>>(P.m, P.mpad, P.b, P.p, P.wacc, P.y, P.grad,
+                                                  P.prev_grad, P.prev_x, P.prev_y, P.vq, P.dq,
+                                                  fast,
+                                                  P.e2_part, P.trace, P.ctrl);
   OTG_CUDA(cudaGetLastError());
 }
 

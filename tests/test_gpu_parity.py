@@ -326,3 +326,51 @@ def test_config1_full_size_fp64_both_solvers():
     os_ = O.sinkhorn_solve(q, np.zeros(1000), tol_l1=1e-8, max_iters=10000)
     assert gs.iterations == os_.iterations and gs.converged == os_.converged
     assert rel(gs.potentials.v, os_.v) <= REL64
+
+
+# ------------------------------------------- fused single-pass sweep ----
+
+def _points_problem(n, m, seed, eps, fused):
+    import os
+    x, y = ot.gen_config(3, n, m, seed)
+    old = os.environ.get("OTG_FUSED")
+    os.environ["OTG_FUSED"] = "1" if fused else "0"
+    try:
+        p = ot.TransportProblem.from_points(np.full(n, 1 / n), np.full(m, 1 / m), x, y, eps)
+    finally:
+        if old is None:
+            del os.environ["OTG_FUSED"]
+        else:
+            os.environ["OTG_FUSED"] = old
+    return p
+
+
+@pytest.mark.parametrize("n,m", [(512, 8192), (300, 4100), (1000, 1024), (257, 65536)])
+def test_fused_eval_matches_oracle_and_two_pass(n, m):
+    pf = _points_problem(n, m, 5, 1e-3, True)
+    p2 = _points_problem(n, m, 5, 1e-3, False)
+    assert np.array_equal(pf.stored_cost(), p2.stored_cost())
+    q = O.Problem(np.full(n, 1 / n), np.full(m, 1 / m), pf.stored_cost(), cost_div=1e-3)
+    rng = O.Rng(7)
+    v = O.random_zero_sum(rng, m, 30.0)
+    ef = ot.eval_normalized_step(pf, v)
+    e2 = ot.eval_normalized_step(p2, v)
+    r = O.eval_normalized_step(q, v)
+    for e in (ef, e2):
+        assert rel(e.u, r["u"]) <= 2e-6
+        assert rel(e.v_next, r["v_next"]) <= 2e-6
+        assert abs(e.grad_l1 - r["grad_l1"]) <= 2e-6 * max(r["grad_l1"], 1e-3)
+        assert abs(e.f_value - r["f_value"]) <= 1e-6 * max(1.0, abs(r["f_value"]))
+
+
+def test_fused_homotopy_cost_and_iterations():
+    n, m, eps, tol = 512, 2048, 5e-3, 1e-6
+    pf = _points_problem(n, m, 9, eps, True)
+    q = O.Problem(np.full(n, 1 / n), np.full(m, 1 / m), pf.stored_cost(), cost_div=eps)
+    g = ot.homotopy_solve(pf, ot.HomotopyConfig(tol_l1=tol))
+    o = O.homotopy_solve(q, tol_l1=tol)
+    assert g.converged and o.converged
+    assert abs(g.iterations - o.iterations) <= max(1, int(0.01 * o.iterations))
+    cg = ot.plan_stats(pf, g.potentials.u, g.potentials.v).primal_cost
+    co = O.plan_stats(q, o.u, o.v, eps)["primal_cost"]
+    assert abs(cg - co) <= REL32 * abs(co)
