@@ -800,3 +800,94 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(_lib().otg_nccl_get_unique_id(buf))
     return buf.raw
+
+
+# ------------------------------------------------------------- batched ---
+
+
+@dataclass
+class BatchResult:
+    converged: np.ndarray
+    iterations: np.ndarray
+    final_violation: np.ndarray
+    final_reduced_f: np.ndarray
+    u: List[np.ndarray]
+    v: List[np.ndarray]
+    device_seconds: float
+    total_iterations: int
+
+
+class BatchProblem:
+    """Many small independent (rescaled) problems, n, m <= 64 each, solved one
+    CTA per problem (BASELINE config 4).  a_list / b_list: per-problem
+    marginals; costs either dense fp32 (C_list) or built on the device as
+    1 - <x, y> from unit embeddings (``cosine``)."""
+
+    def __init__(self, raw, n, m):
+        self.raw = raw
+        self.n = np.asarray(n, dtype=np.int32)
+        self.m = np.asarray(m, dtype=np.int32)
+
+    @classmethod
+    def dense(cls, a_list, b_list, C_list, epsilon, device=0):
+        n = np.array([len(a) for a in a_list], dtype=np.int32)
+        m = np.array([len(b) for b in b_list], dtype=np.int32)
+        a = _f64(np.concatenate(a_list))
+        b = _f64(np.concatenate(b_list))
+        Cc = np.ascontiguousarray(np.concatenate([np.asarray(c, np.float32).ravel() for c in C_list]))
+        h = C.c_void_p()
+        opts = _device_opts(device, 1, 0, 0, 0, None, 1)
+        _check(_lib().otg_batch_create_dense(len(n), _ptr(n), _ptr(m), _ptr(a), _ptr(b), _ptr(Cc),
+                                             float(epsilon), C.byref(opts), C.byref(h)))
+        return cls(h, n, m)
+
+    @classmethod
+    def cosine(cls, n, m, x_cat, y_cat, epsilon, a_cat=None, b_cat=None, norm="none", device=0):
+        n = np.ascontiguousarray(n, dtype=np.int32)
+        m = np.ascontiguousarray(m, dtype=np.int32)
+        x = np.ascontiguousarray(x_cat, dtype=np.float32)
+        y = np.ascontiguousarray(y_cat, dtype=np.float32)
+        a = _f64(a_cat) if a_cat is not None else np.concatenate([np.full(k, 1.0 / k) for k in n])
+        b = _f64(b_cat) if b_cat is not None else np.concatenate([np.full(k, 1.0 / k) for k in m])
+        h = C.c_void_p()
+        opts = _device_opts(device, 1, 0, 0, 0, None, 1)
+        _check(_lib().otg_batch_create_cosine(len(n), _ptr(n), _ptr(m), x.shape[1], _ptr(a), _ptr(b),
+                                              _ptr(x), _ptr(y), NORM[norm], float(epsilon),
+                                              C.byref(opts), C.byref(h)))
+        return cls(h, n, m)
+
+    def stored_cost(self):
+        out = np.empty(int((self.n.astype(np.int64) * self.m).sum()), dtype=np.float32)
+        _check(_lib().otg_batch_get_cost(self.raw, _ptr(out)))
+        res, off = [], 0
+        for k in range(len(self.n)):
+            sz = int(self.n[k]) * int(self.m[k])
+            res.append(out[off:off + sz].reshape(self.n[k], self.m[k]))
+            off += sz
+        return res
+
+    def homotopy_solve(self, cfg: HomotopyConfig = HomotopyConfig()) -> BatchResult:
+        cnt = len(self.n)
+        conv = np.empty(cnt, dtype=np.int32)
+        it = np.empty(cnt, dtype=np.int64)
+        fv, ff = np.empty(cnt), np.empty(cnt)
+        u, v = np.empty(int(self.n.sum())), np.empty(int(self.m.sum()))
+        r = _capi.BatchResultC(_ptr(conv), _ptr(it), _ptr(fv), _ptr(ff), _ptr(u), _ptr(v), 0.0, 0)
+        c = _capi.HomotopyConfigC(cfg.mu0, cfg.m0, cfg.max_outer, cfg.tol_l1, cfg.max_total_inner,
+                                  int(cfg.rescale_w_across_stages), 0, 1)
+        _check(_lib().otg_batch_homotopy_solve(self.raw, C.byref(c), C.byref(r)))
+        us = np.split(u, np.cumsum(self.n)[:-1])
+        vs = np.split(v, np.cumsum(self.m)[:-1])
+        return BatchResult(conv.astype(bool), it, fv, ff, us, vs, r.device_seconds,
+                           r.total_iterations)
+
+    def close(self):
+        if self.raw:
+            _lib().otg_batch_destroy(self.raw)
+            self.raw = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
