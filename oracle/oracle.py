@@ -430,6 +430,16 @@ def sweep_rows_mt(p: Problem, v, row0, row1, nthreads):
     return u, col
 
 
+def cost_sqeuclid_f32(x, y):
+    """fp32 on-the-fly cost (config 5 definition, otoracle.h)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    y = np.ascontiguousarray(y, dtype=np.float32)
+    Cm = np.empty((x.shape[0], y.shape[0]), dtype=np.float32)
+    lib().orc_cost_sqeuclid_f32(_p(x), _p(y), C.c_int64(x.shape[0]), C.c_int64(y.shape[0]),
+                                C.c_int64(x.shape[1]), _p(Cm))
+    return Cm
+
+
 def sqeuclid_max(x, y, threads=1) -> float:
     x, y = _f64(x), _f64(y)
     return lib().orc_sqeuclid_max(_p(x), _p(y), x.shape[0], y.shape[0], x.shape[1], threads)

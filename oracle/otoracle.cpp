@@ -924,6 +924,17 @@ int orc_sweep_rows_mt(const orc_problem* pp, const double* v, int64_t row0, int6
   });
 }
 
+void orc_cost_sqeuclid_f32(const float* x, const float* y, int64_t n, int64_t m, int64_t d,
+                           float* C) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < m; ++j) {
+      float dv[3] = {0.f, 0.f, 0.f};
+      for (int64_t k = 0; k < d && k < 3; ++k) dv[k] = x[i * d + k] - y[j * d + k];
+      const float dx2 = dv[0] * dv[0];
+      C[i * m + j] = std::fmaf(dv[2], dv[2], std::fmaf(dv[1], dv[1], dx2));
+    }
+}
+
 double orc_sqeuclid_max(const double* x, const double* y, int64_t n, int64_t m, int64_t d,
                         int nthreads) {
   const int T = std::max(1, nthreads);

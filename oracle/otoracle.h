@@ -177,6 +177,13 @@ double orc_homotopy_rate_constant(double mu0, double r_hat, double l_f);
 int orc_sweep_rows_mt(const orc_problem* p, const double* v, int64_t row0, int64_t row1,
                       int nthreads, double* u, double* col_partial);
 
+/* On-the-fly cost of the B200 path's config 5 (OTG_STORE_ON_THE_FLY): fp32
+ * coordinates (d <= 3, missing coordinates 0), C_ij = fmaf(dz, dz, fmaf(dy,
+ * dy, dx * dx)) in fp32 with d = x_i - y_j — data.cpp:75-77's squared norm
+ * evaluated in this exact fp32 operation order, which defines that instance. */
+void orc_cost_sqeuclid_f32(const float* x, const float* y, int64_t n, int64_t m, int64_t d,
+                           float* C);
+
 /* max_ij ||x_i - y_j||^2 (the cost_sqeuclidean normaliser, data.cpp:78-80),
  * nthreads workers. */
 double orc_sqeuclid_max(const double* x, const double* y, int64_t n, int64_t m, int64_t d,

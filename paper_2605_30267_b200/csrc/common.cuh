@@ -52,6 +52,16 @@ constexpr double kTinyPrecise = 1e-280;      // dual.cpp:53 (fp64 path: same thr
 constexpr double kTinyFast = 1e-30;          // fp32 ex2.ftz path: flushed mass <= 1.2e-38
 constexpr float kQuant = 256.0f;             // 2^8 quantum of the split shifts
 
+// On-the-fly squared-Euclidean cost of fp32 points (x, y, z, 0): the
+// definition of the instance for OTG_STORE_ON_THE_FLY (the oracle evaluates
+// the same fp32 operations in the same order).
+#ifdef __CUDACC__
+__device__ __forceinline__ float otf_sqeuclid(const float4& x, const float4& y) {
+  const float dx = __fsub_rn(x.x, y.x), dy = __fsub_rn(x.y, y.y), dz = __fsub_rn(x.z, y.z);
+  return __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+}
+#endif
+
 // ------------------------------------------------------------ loop control --
 enum Mode : int {
   MODE_EVAL = 0,       // one eval_normalized_step

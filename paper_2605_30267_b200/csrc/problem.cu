@@ -126,6 +126,14 @@ __global__ void k_cost_store(const double* __restrict__ X, const double* __restr
   }
 }
 
+__global__ void k_otf_rows(const float4* __restrict__ X, const float4* __restrict__ Y,
+                           int64_t row0, int64_t nrows, int64_t m, float* __restrict__ out) {
+  const int64_t i = blockIdx.x;
+  if (i >= nrows) return;
+  for (int64_t j = threadIdx.x; j < m; j += blockDim.x)
+    out[i * m + j] = otf_sqeuclid(X[row0 + i], Y[j]);
+}
+
 }  // namespace
 
 void problem_free(Problem& P) {
@@ -318,9 +326,13 @@ otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const doub
     validate_eps(epsilon);
     if (d < 1 || !x || !y) fail(OTG_E_DIMENSION, "point clouds need d >= 1 and data");
     if (cost != OTG_COST_SQEUCLID && cost != OTG_COST_COSINE) fail(OTG_E_OT, "unknown cost");
-    if (storage == OTG_STORE_ON_THE_FLY)
-      fail(OTG_E_UNSUPPORTED, "on-the-fly storage is not built in this version");
-    if (storage != OTG_STORE_F64 && storage != OTG_STORE_F32) fail(OTG_E_OT, "unknown storage");
+    if (storage == OTG_STORE_ON_THE_FLY &&
+        (cost != OTG_COST_SQEUCLID || norm != OTG_NORM_NONE || d > 3))
+      fail(OTG_E_UNSUPPORTED,
+           "on-the-fly storage recomputes raw squared-Euclidean costs of d <= 3 points "
+           "(cost SQEUCLID, norm NONE)");
+    if (storage != OTG_STORE_F64 && storage != OTG_STORE_F32 && storage != OTG_STORE_ON_THE_FLY)
+      fail(OTG_E_OT, "unknown storage");
     begin(P, n, m, opts);
     const int64_t nl = P.n_local;
     const double* xl = x + P.row_begin * d;
@@ -328,6 +340,26 @@ otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const doub
       if (!std::isfinite(xl[t])) fail(OTG_E_OT, "point coordinates must be finite");
     for (int64_t t = 0; t < m * d; ++t)
       if (!std::isfinite(y[t])) fail(OTG_E_OT, "point coordinates must be finite");
+    if (storage == OTG_STORE_ON_THE_FLY) {
+      // fp32 coordinates padded to float4; the cost is recomputed per tile in
+      // the sweeps (sweep.cu: otf_cost) and never stored
+      P.storage = OTG_STORE_ON_THE_FLY;
+      P.epsilon = epsilon;
+      P.kappa = 1.0 / epsilon;
+      upload_marginals(P, a, b);
+      std::vector<float> hx(nl * 4, 0.f), hy(P.mpad * 4, 0.f);
+      for (int64_t i = 0; i < nl; ++i)
+        for (int64_t k = 0; k < d; ++k) hx[i * 4 + k] = static_cast<float>(xl[i * d + k]);
+      for (int64_t j = 0; j < m; ++j)
+        for (int64_t k = 0; k < d; ++k) hy[j * 4 + k] = static_cast<float>(y[j * d + k]);
+      P.X = dalloc<float>(P, hx.size());
+      P.Y = dalloc<float>(P, hy.size());
+      OTG_CUDA(cudaMemcpyAsync(P.X, hx.data(), hx.size() * 4, cudaMemcpyHostToDevice, P.stream));
+      OTG_CUDA(cudaMemcpyAsync(P.Y, hy.data(), hy.size() * 4, cudaMemcpyHostToDevice, P.stream));
+      OTG_CUDA(cudaStreamSynchronize(P.stream));
+      finish_create(P, opts, out);
+      return;
+    }
     if (cost == OTG_COST_COSINE) {  // data.cpp:89-96 unit-row check
       for (int side = 0; side < 2; ++side) {
         const double* Z = side ? y : xl;
@@ -463,6 +495,17 @@ otg_status otg_problem_get_cost(otg_problem h, int64_t row0, int64_t nrows, void
       OTG_CUDA(cudaStreamSynchronize(P.stream));
       double* o = static_cast<double*>(outp);
       for (size_t k = 0; k < tmp.size(); ++k) o[k] = P.epsilon == 1.0 ? tmp[k] : tmp[k] * P.epsilon;
+    } else if (P.storage == OTG_STORE_ON_THE_FLY) {  // evaluate the recomputed cost
+      float* d = nullptr;
+      OTG_CUDA(cudaMalloc(&d, std::max<int64_t>(nrows * P.m, 1) * sizeof(float)));
+      k_otf_rows<<<static_cast<unsigned>(std::max<int64_t>(nrows, 1)), kT, 0, P.stream>>>(
+          reinterpret_cast<const float4*>(P.X), reinterpret_cast<const float4*>(P.Y), row0,
+          nrows, P.m, d);
+      OTG_CUDA(cudaGetLastError());
+      OTG_CUDA(cudaMemcpyAsync(outp, d, nrows * P.m * sizeof(float), cudaMemcpyDeviceToHost,
+                               P.stream));
+      OTG_CUDA(cudaStreamSynchronize(P.stream));
+      cudaFree(d);
     } else {
       OTG_CUDA(cudaMemcpy2DAsync(outp, P.m * sizeof(float), P.C32 + row0 * P.ldc,
                                  P.ldc * sizeof(float), P.m * sizeof(float), nrows,

@@ -212,7 +212,20 @@ void one_eval(Problem& P, const double* v, bool with_log) {
   raise_device_error(*P.ctrl_host);
 }
 
+// C'_ij of any storage: fp64 C' (stored divided), fp32 C x 1/eps, or the
+// on-the-fly fp32 cost of the points x 1/eps.
+__device__ __forceinline__ double cost_at(const double* __restrict__ C64,
+                                          const float* __restrict__ C32,
+                                          const float4* __restrict__ X,
+                                          const float4* __restrict__ Y, int64_t ldc, double kappa,
+                                          int64_t i, int64_t j) {
+  if (C64) return C64[i * ldc + j];
+  if (C32) return static_cast<double>(C32[i * ldc + j]) * kappa;
+  return static_cast<double>(otf_sqeuclid(X[i], Y[j])) * kappa;
+}
+
 __global__ void k_plan_rows(const double* __restrict__ C64, const float* __restrict__ C32,
+                            const float4* __restrict__ X, const float4* __restrict__ Y,
                             int64_t ldc, int64_t n, int64_t m, double kappa,
                             const double* __restrict__ u, const double* __restrict__ v,
                             double* __restrict__ rowsum, double* __restrict__ rowcost,
@@ -221,7 +234,7 @@ __global__ void k_plan_rows(const double* __restrict__ C64, const float* __restr
   const int64_t i = blockIdx.x;
   double rs = 0.0, cs = 0.0, mx = -DBL_MAX;
   for (int64_t j = threadIdx.x; j < m; j += kT) {
-    const double c = C64 ? C64[i * ldc + j] : static_cast<double>(C32[i * ldc + j]) * kappa;
+    const double c = cost_at(C64, C32, X, Y, ldc, kappa, i, j);
     const double e = ((-c) + u[i]) + v[j];  // core.cpp:63-65
     const double P = exp(e);
     mx = fmax(mx, e);
@@ -248,6 +261,7 @@ __global__ void k_plan_rows(const double* __restrict__ C64, const float* __restr
 }
 
 __global__ void k_plan_cols(const double* __restrict__ C64, const float* __restrict__ C32,
+                            const float4* __restrict__ X, const float4* __restrict__ Y,
                             int64_t ldc, int64_t n, int64_t m, double kappa,
                             const double* __restrict__ u, const double* __restrict__ v,
                             double* __restrict__ colsum) {
@@ -255,7 +269,7 @@ __global__ void k_plan_cols(const double* __restrict__ C64, const float* __restr
   if (j >= m) return;
   double s = 0.0;
   for (int64_t i = 0; i < n; ++i) {
-    const double c = C64 ? C64[i * ldc + j] : static_cast<double>(C32[i * ldc + j]) * kappa;
+    const double c = cost_at(C64, C32, X, Y, ldc, kappa, i, j);
     s += exp(((-c) + u[i]) + v[j]);
   }
   colsum[j] = s;
@@ -441,10 +455,12 @@ otg_status otg_plan_stats(otg_problem h, const double* u, const double* v, otg_p
     OTG_CUDA(cudaMalloc(&cs, m * sizeof(double)));
     h2d(P, du, u, n);
     h2d(P, dv, v, m);
-    k_plan_rows<<<static_cast<unsigned>(n), kT, 0, P.stream>>>(P.C64, P.C32, P.ldc, n, m, P.kappa,
-                                                               du, dv, rs, rc, rm);
+    const float4* X4 = reinterpret_cast<const float4*>(P.X);
+    const float4* Y4 = reinterpret_cast<const float4*>(P.Y);
+    k_plan_rows<<<static_cast<unsigned>(n), kT, 0, P.stream>>>(P.C64, P.C32, X4, Y4, P.ldc, n, m,
+                                                               P.kappa, du, dv, rs, rc, rm);
     k_plan_cols<<<static_cast<unsigned>((m + kT - 1) / kT), kT, 0, P.stream>>>(
-        P.C64, P.C32, P.ldc, n, m, P.kappa, du, dv, cs);
+        P.C64, P.C32, X4, Y4, P.ldc, n, m, P.kappa, du, dv, cs);
     OTG_CUDA(cudaGetLastError());
     std::vector<double> hrs(n), hrc(n), hrm(n), hcs(m);
     d2h(P, hrs.data(), rs, n);

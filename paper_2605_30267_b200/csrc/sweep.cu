@@ -183,13 +183,58 @@ k_row_precise(const double* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
   }
 }
 
+// ---------------------------------------------------------- cost sources ----
+// The fp32 kernels read the cost either from the stored matrix (C, ldc) or
+// recompute it per tile from fp32 points (BASELINE config 5, C never stored):
+//   C_ij = fl32(fl32(dz^2 + fl32(dy^2 + fl32(dx^2))))  with d = x_i - y_j,
+// the squared-Euclidean cost of data.cpp:69-82 evaluated in fp32 with this
+// exact operation order, which is the definition the oracle reproduces.
+struct CostSrc {
+  const float* C;    // stored: n x ldc
+  int64_t ldc;
+  const float4* X;   // on-the-fly: n points (x, y, z, 0)
+  const float4* Y;   // on-the-fly: m points
+};
+
+__device__ __forceinline__ float otf_cost(const float4& x, const float4& y) {
+  return otf_sqeuclid(x, y);
+}
+
+// One quad of row `i` (columns 4q .. 4q+3).  Stored: a 128-bit streaming load.
+// On the fly: xi = X[i] (row-invariant), y4 = Y[4q .. 4q+3] (shared by rows).
+template <bool OTF>
+__device__ __forceinline__ float4 cost_quad(const CostSrc& s, int64_t i, int64_t q,
+                                            const float4& xi, const float4* y4) {
+  if constexpr (OTF) {
+    return make_float4(otf_cost(xi, y4[0]), otf_cost(xi, y4[1]), otf_cost(xi, y4[2]),
+                       otf_cost(xi, y4[3]));
+  } else {
+    return ld_stream(reinterpret_cast<const float4*>(s.C + i * s.ldc) + q);
+  }
+}
+template <bool OTF>
+__device__ __forceinline__ float cost_one(const CostSrc& s, int64_t i, int64_t j) {
+  if constexpr (OTF) {
+    return otf_cost(s.X[i], s.Y[j]);
+  } else {
+    return s.C[i * s.ldc + j];
+  }
+}
+template <bool OTF>
+__device__ __forceinline__ void load_y4(const CostSrc& s, int64_t q, float4* y4) {
+  if constexpr (OTF) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) y4[k] = __ldg(s.Y + 4 * q + k);
+  }
+}
+
 // fp32 storage, exact row statistics for R rows (fp64 exponent argument with an
 // online max).  Every thread streams float4 columns of the R rows; the column
 // potential is loaded once per column chunk and reused across the R rows.
 // Used for the first evaluation of a solve (no shift estimate yet) and, in
 // LIST mode, to redo the rows whose shift estimate failed (k_row_shift).
-template <int R>
-__device__ void row_exact_block(const int64_t* rows, const float* __restrict__ C, int64_t ldc,
+template <int R, bool OTF>
+__device__ void row_exact_block(const int64_t* rows, const CostSrc src,
                                 int64_t m, const double* __restrict__ p, double kappa,
                                 const double* __restrict__ a, const double* __restrict__ loga,
                                 double* __restrict__ rowM, double* __restrict__ rowS,
@@ -199,9 +244,9 @@ __device__ void row_exact_block(const int64_t* rows, const float* __restrict__ C
   __shared__ double sh[kRowThreads / 32];
   __shared__ double resM[R], resS[R];
   __shared__ int resJ[R];
-  const float* Cr[R];
+  float4 xr[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) Cr[r] = C + rows[r] * ldc;
+  for (int r = 0; r < R; ++r) xr[r] = OTF ? src.X[rows[r]] : make_float4(0.f, 0.f, 0.f, 0.f);
   double mr[R], sr[R];
   int jr[R];  // argmax column of the running max (next evaluation's shift estimate)
 #pragma unroll
@@ -219,9 +264,11 @@ __device__ void row_exact_block(const int64_t* rows, const float* __restrict__ C
   for (int64_t q = threadIdx.x; q < nq; q += kRowThreads) {
     const double2 pa = __ldg(p2 + 2 * q), pb = __ldg(p2 + 2 * q + 1);
     const double q0 = pa.x * kLog2e, q1 = pa.y * kLog2e, q2 = pb.x * kLog2e, q3 = pb.y * kLog2e;
+    float4 y4[4];
+    load_y4<OTF>(src, q, y4);
     float4 c[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) c[r] = ld_stream(reinterpret_cast<const float4*>(Cr[r]) + q);
+    for (int r = 0; r < R; ++r) c[r] = cost_quad<OTF>(src, rows[r], q, xr[r], y4);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const double t0 = fma(-f32_to_f64(c[r].x), k2, q0);
@@ -244,7 +291,7 @@ __device__ void row_exact_block(const int64_t* rows, const float* __restrict__ C
     const double pj = p[j] * kLog2e;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const double t = fma(-f32_to_f64(Cr[r][j]), k2, pj);
+      const double t = fma(-f32_to_f64(cost_one<OTF>(src, rows[r], j)), k2, pj);
       if (t > mr[r]) {
         jr[r] = static_cast<int>(j);
         sr[r] *= exp2(mr[r] - t);
@@ -287,9 +334,9 @@ __device__ void row_exact_block(const int64_t* rows, const float* __restrict__ C
   }
 }
 
-template <int R>
+template <int R, bool OTF>
 __global__ void __launch_bounds__(kRowThreads)
-k_row_exact(const float* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
+k_row_exact(const CostSrc src, int64_t n, int64_t m,
             const double* __restrict__ p, double kappa, const double* __restrict__ a,
             const double* __restrict__ loga, double* __restrict__ rowM,
             double* __restrict__ rowS, double* __restrict__ u, double* __restrict__ wrow,
@@ -304,13 +351,14 @@ k_row_exact(const float* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
     valid[r] = i < n;
     rows[r] = valid[r] ? i : n - 1;
   }
-  row_exact_block<R>(rows, C, ldc, m, p, kappa, a, loga, rowM, rowS, u, wrow, aux, rowM2, rowJ,
-                     valid);
+  row_exact_block<R, OTF>(rows, src, m, p, kappa, a, loga, rowM, rowS, u, wrow, aux, rowM2, rowJ,
+                          valid);
 }
 
 // Exact redo of the rows k_row_shift flagged (grid-stride over the list).
+template <bool OTF>
 __global__ void __launch_bounds__(kRowThreads)
-k_row_redo(const float* __restrict__ C, int64_t ldc, int64_t m, const double* __restrict__ p,
+k_row_redo(const CostSrc src, int64_t m, const double* __restrict__ p,
            double kappa, const double* __restrict__ a, const double* __restrict__ loga,
            double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
            double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
@@ -321,8 +369,8 @@ k_row_redo(const float* __restrict__ C, int64_t ldc, int64_t m, const double* __
   for (unsigned k = blockIdx.x; k < cnt; k += gridDim.x) {
     const int64_t rows[1] = {redo_rows[k]};
     const bool valid[1] = {true};
-    row_exact_block<1>(rows, C, ldc, m, p, kappa, a, loga, rowM, rowS, u, wrow, aux, rowM2,
-                       rowJ, valid);
+    row_exact_block<1, OTF>(rows, src, m, p, kappa, a, loga, rowM, rowS, u, wrow, aux, rowM2,
+                            rowJ, valid);
     __syncthreads();
   }
 }
@@ -343,9 +391,9 @@ k_row_redo(const float* __restrict__ C, int64_t ldc, int64_t m, const double* __
 constexpr float kRedoLo = 2.0f;
 constexpr float kRedoHi = 6.0f;
 
-template <int R>
+template <int R, bool OTF>
 __global__ void __launch_bounds__(kRowThreads)
-k_row_shift(const float* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
+k_row_shift(const CostSrc src, int64_t n, int64_t m,
             const float* __restrict__ vq, const double* __restrict__ dq, int64_t mpad, float kh,
             float kl, const double* __restrict__ a, const double* __restrict__ loga,
             double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
@@ -369,7 +417,8 @@ k_row_shift(const float* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
   float Sc[R], tm[R], fs[R];
   int tj[R];
   double ss[R];
-  const float* Cr[R];
+  int64_t rr[R];
+  float4 xr[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     Sc[r] = sSc[r];
@@ -377,7 +426,8 @@ k_row_shift(const float* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
     tj[r] = 0;
     fs[r] = 0.f;
     ss[r] = 0.0;
-    Cr[r] = C + (r0 + r < n ? r0 + r : n - 1) * ldc;
+    rr[r] = r0 + r < n ? r0 + r : n - 1;
+    xr[r] = OTF ? src.X[rr[r]] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const int64_t nq = m >> 2;
   const float4* Vq = reinterpret_cast<const float4*>(vq);
@@ -385,9 +435,11 @@ k_row_shift(const float* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
   int chunk = 0;
   for (int64_t q = threadIdx.x; q < nq; q += kRowThreads) {
     const float4 V = __ldg(Vq + q), F = __ldg(Fq + q);
+    float4 y4[4];
+    load_y4<OTF>(src, q, y4);
     float4 c[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) c[r] = ld_stream(reinterpret_cast<const float4*>(Cr[r]) + q);
+    for (int r = 0; r < R; ++r) c[r] = cost_quad<OTF>(src, rr[r], q, xr[r], y4);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const float t0 = fmaf(-c[r].x, kh, V.x - Sc[r]) + fmaf(-c[r].x, kl, F.x);
@@ -414,7 +466,7 @@ k_row_shift(const float* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
     const float V = vq[j], F = vq[mpad + j];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const float c = Cr[r][j];
+      const float c = cost_one<OTF>(src, rr[r], j);
       const float t = fmaf(-c, kh, V - Sc[r]) + fmaf(-c, kl, F);
       if (t > tm[r]) {
         tm[r] = t;
@@ -504,40 +556,48 @@ k_col_precise(const double* __restrict__ C, int64_t ldc, int64_t m,
   }
 }
 
-// fp32: thread owns 4 consecutive columns, loops over the split's rows.
+// fp32: thread owns 4 consecutive columns, loops over the split's rows.  The
+// rows' shift / weight (aux) -- and, on the fly, the rows' points -- are
+// staged in shared memory per 256-row tile and read as broadcasts.
+template <bool OTF>
 __global__ void __launch_bounds__(kColThreads)
-k_col_fast(const float* __restrict__ C, int64_t ldc, int64_t m, const double* __restrict__ p,
-           float kh, float kl, const float4* __restrict__ aux, int64_t row_lo, int64_t row_hi,
+k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh, float kl,
+           const float4* __restrict__ aux, int64_t row_lo, int64_t row_hi,
            int64_t rows_per_split, double* __restrict__ part, int64_t mpad,
            const Ctrl* __restrict__ ctrl) {
   if (ctrl->done) return;
   __shared__ float4 sh_aux[kAuxTile];
+  __shared__ float4 sh_x[OTF ? kAuxTile : 1];
   const int64_t q = static_cast<int64_t>(blockIdx.x) * kColThreads + threadIdx.x;
   const int64_t j0 = 4 * q;
   const int64_t i0 = row_lo + static_cast<int64_t>(blockIdx.y) * rows_per_split;
   const int64_t i1 = min(i0 + rows_per_split, row_hi);
   float Vc[4], vf[4];
+  float4 y4[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const double pj = (j0 + k < m) ? p[j0 + k] : 0.0;
     split_q(pj * kLog2e, Vc[k], vf[k]);
+    if (OTF) y4[k] = src.Y[(j0 + k < m) ? j0 + k : 0];
   }
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
   double acc64[4] = {0.0, 0.0, 0.0, 0.0};
   const bool active = j0 < m;
-  const float4* Cq = reinterpret_cast<const float4*>(C + (active ? j0 : 0));
-  const int64_t ldq = ldc >> 2;
   for (int64_t t0 = i0; t0 < i1; t0 += kAuxTile) {
     const int64_t tn = min(static_cast<int64_t>(kAuxTile), i1 - t0);
     __syncthreads();
-    for (int k = threadIdx.x; k < tn; k += kColThreads) sh_aux[k] = aux[t0 + k];
+    for (int k = threadIdx.x; k < tn; k += kColThreads) {
+      sh_aux[k] = aux[t0 + k];
+      if (OTF) sh_x[k] = src.X[t0 + k];
+    }
     __syncthreads();
     if (!active) continue;
     int k = 0;
     for (; k + kColUnroll <= tn; k += kColUnroll) {
       float4 c[kColUnroll];
 #pragma unroll
-      for (int r = 0; r < kColUnroll; ++r) c[r] = ld_stream(Cq + (t0 + k + r) * ldq);
+      for (int r = 0; r < kColUnroll; ++r)
+        c[r] = cost_quad<OTF>(src, t0 + k + r, q, OTF ? sh_x[k + r] : y4[0], y4);
 #pragma unroll
       for (int r = 0; r < kColUnroll; ++r) {
         const float4 ax = sh_aux[k + r];
@@ -559,7 +619,7 @@ k_col_fast(const float* __restrict__ C, int64_t ldc, int64_t m, const double* __
       }
     }
     for (; k < tn; ++k) {
-      const float4 cv = ld_stream(Cq + (t0 + k) * ldq);
+      const float4 cv = cost_quad<OTF>(src, t0 + k, q, OTF ? sh_x[k] : y4[0], y4);
       const float4 ax = sh_aux[k];
       const float cc[4] = {cv.x, cv.y, cv.z, cv.w};
 #pragma unroll
@@ -624,10 +684,10 @@ k_merge(const double* __restrict__ part, int nshards, int splits, int64_t m, int
 // ------------------------------------------------------------------ K5 ----
 // Exact column log-sum-exp (dual.cpp:54-69) for flagged columns, split over
 // row chunks: fb_part[f][chunk] = (max_i t_ij, sum_i exp(t_ij - max)).
-template <bool PRECISE>
+template <bool PRECISE, bool OTF>
 __global__ void __launch_bounds__(kEThreads)
-k_fallback(const double* __restrict__ C64, const float* __restrict__ C32, int64_t ldc,
-           int64_t n, double kappa, const double* __restrict__ u, const double* __restrict__ p,
+k_fallback(const double* __restrict__ C64, const CostSrc src, int64_t ldc, int64_t n,
+           double kappa, const double* __restrict__ u, const double* __restrict__ p,
            const int* __restrict__ fb_cols, double2* __restrict__ fb_part,
            const Ctrl* __restrict__ ctrl) {
   if (ctrl->done) return;
@@ -644,7 +704,7 @@ k_fallback(const double* __restrict__ C64, const float* __restrict__ C32, int64_
     double top = -INFINITY;
     for (int64_t i = i0 + threadIdx.x; i < i1; i += kEThreads) {
       const double t = PRECISE ? (u[i] + vj) - C64[i * ldc + j]
-                               : fma(-static_cast<double>(C32[i * ldc + j]), kappa, u[i] + vj);
+                               : fma(-static_cast<double>(cost_one<OTF>(src, i, j)), kappa, u[i] + vj);
       top = fmax(top, t);
     }
     top = block_max<kEThreads>(top, sh);
@@ -652,7 +712,7 @@ k_fallback(const double* __restrict__ C64, const float* __restrict__ C32, int64_
     if (top > -INFINITY)
       for (int64_t i = i0 + threadIdx.x; i < i1; i += kEThreads) {
         const double t = PRECISE ? (u[i] + vj) - C64[i * ldc + j]
-                                 : fma(-static_cast<double>(C32[i * ldc + j]), kappa, u[i] + vj);
+                                 : fma(-static_cast<double>(cost_one<OTF>(src, i, j)), kappa, u[i] + vj);
         s += exp(t - top);
       }
     s = block_sum<kEThreads>(s, sh);
@@ -1068,6 +1128,15 @@ void configure_sweeps(Problem& P) {
   P.e_blocks = e_grid(P.m);
 }
 
+static CostSrc cost_src(const Problem& P) {
+  CostSrc s;
+  s.C = P.C32;
+  s.ldc = P.ldc;
+  s.X = reinterpret_cast<const float4*>(P.X);
+  s.Y = reinterpret_cast<const float4*>(P.Y);
+  return s;
+}
+
 int64_t row_blocks(const Problem& P) {
   if (P.storage == OTG_STORE_F64) {
     const int G = P.m <= 2048 ? 32 : kRowThreads;
@@ -1099,25 +1168,26 @@ void launch_row_pass(Problem& P) {
     const double k2 = P.kappa * kLog2e;
     const float kh = static_cast<float>(k2);
     const float kl = static_cast<float>(k2 - static_cast<double>(kh));
-#define OTG_ROW(RR)                                                                           \
-  k_row_exact<RR><<<blocks, kRowThreads, 0, P.stream>>>(P.C32, P.ldc, P.n_local, P.m, P.p,    \
-                                                       P.kappa, P.a, P.loga, P.rowM, P.rowS,  \
-                                                       P.u, P.wrow, P.aux, P.rowM2, P.rowJ,   \
-                                                       P.ctrl);                                \
-  k_row_shift<RR><<<blocks, kRowThreads, 0, P.stream>>>(                                      \
-      P.C32, P.ldc, P.n_local, P.m, P.vq, P.dq, P.mpad, kh, kl, P.a, P.loga, P.rowM, P.rowS,  \
-      P.u, P.wrow, P.aux, P.rowM2, P.rowJ, P.redo_rows, P.ctrl)
+    const CostSrc src = cost_src(P);
+#define OTG_ROW(RR, OTF)                                                                      \
+  k_row_exact<RR, OTF><<<blocks, kRowThreads, 0, P.stream>>>(                                 \
+      src, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,     \
+      P.rowM2, P.rowJ, P.ctrl);                                                               \
+  k_row_shift<RR, OTF><<<blocks, kRowThreads, 0, P.stream>>>(                                 \
+      src, P.n_local, P.m, P.vq, P.dq, P.mpad, kh, kl, P.a, P.loga, P.rowM, P.rowS, P.u,      \
+      P.wrow, P.aux, P.rowM2, P.rowJ, P.redo_rows, P.ctrl);                                   \
+  k_row_redo<OTF><<<296, kRowThreads, 0, P.stream>>>(src, P.m, P.p, P.kappa, P.a, P.loga,     \
+                                                     P.rowM, P.rowS, P.u, P.wrow, P.aux,      \
+                                                     P.rowM2, P.rowJ, P.redo_rows, P.ctrl)
+    const bool otf = P.storage == OTG_STORE_ON_THE_FLY;
     if (R == 8) {
-      OTG_ROW(8);
+      if (otf) { OTG_ROW(8, true); } else { OTG_ROW(8, false); }
     } else if (R == 4) {
-      OTG_ROW(4);
+      if (otf) { OTG_ROW(4, true); } else { OTG_ROW(4, false); }
     } else {
-      OTG_ROW(1);
+      if (otf) { OTG_ROW(1, true); } else { OTG_ROW(1, false); }
     }
 #undef OTG_ROW
-    k_row_redo<<<296, kRowThreads, 0, P.stream>>>(P.C32, P.ldc, P.m, P.p, P.kappa, P.a, P.loga,
-                                                  P.rowM, P.rowS, P.u, P.wrow, P.aux, P.rowM2,
-                                                  P.rowJ, P.redo_rows, P.ctrl);
   }
   OTG_CUDA(cudaGetLastError());
 }
@@ -1138,8 +1208,12 @@ void launch_col_pass(Problem& P) {
     } else {
       dim3 grid(static_cast<unsigned>((P.m + 4 * kColThreads - 1) / (4 * kColThreads)),
                 P.col_splits);
-      k_col_fast<<<grid, kColThreads, 0, P.stream>>>(P.C32, P.ldc, P.m, P.p, kh, kl, P.aux, lo,
-                                                     hi, P.rows_per_split, part, P.mpad, P.ctrl);
+      if (P.storage == OTG_STORE_ON_THE_FLY)
+        k_col_fast<true><<<grid, kColThreads, 0, P.stream>>>(
+            cost_src(P), P.m, P.p, kh, kl, P.aux, lo, hi, P.rows_per_split, part, P.mpad, P.ctrl);
+      else
+        k_col_fast<false><<<grid, kColThreads, 0, P.stream>>>(
+            cost_src(P), P.m, P.p, kh, kl, P.aux, lo, hi, P.rows_per_split, part, P.mpad, P.ctrl);
     }
   }
   OTG_CUDA(cudaGetLastError());
@@ -1194,12 +1268,14 @@ void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
   if (P.world > 1) comm_allreduce_sum(P, P.col, static_cast<size_t>(P.mpad + 1));
   if (!with_log) return;
   if (P.storage == OTG_STORE_F64)
-    k_fallback<true><<<296, kEThreads, 0, P.stream>>>(P.C64, nullptr, P.ldc, P.n_local, P.kappa,
-                                                      P.u, P.p, P.fb_cols, P.fb_part, P.ctrl);
+    k_fallback<true, false><<<296, kEThreads, 0, P.stream>>>(
+        P.C64, cost_src(P), P.ldc, P.n_local, P.kappa, P.u, P.p, P.fb_cols, P.fb_part, P.ctrl);
+  else if (P.storage == OTG_STORE_ON_THE_FLY)
+    k_fallback<false, true><<<296, kEThreads, 0, P.stream>>>(
+        nullptr, cost_src(P), P.ldc, P.n_local, P.kappa, P.u, P.p, P.fb_cols, P.fb_part, P.ctrl);
   else
-    k_fallback<false><<<296, kEThreads, 0, P.stream>>>(nullptr, P.C32, P.ldc, P.n_local,
-                                                       P.kappa, P.u, P.p, P.fb_cols, P.fb_part,
-                                                       P.ctrl);
+    k_fallback<false, false><<<296, kEThreads, 0, P.stream>>>(
+        nullptr, cost_src(P), P.ldc, P.n_local, P.kappa, P.u, P.p, P.fb_cols, P.fb_part, P.ctrl);
   OTG_CUDA(cudaGetLastError());
   k_finalize<<<P.e_blocks, kEThreads, 0, P.stream>>>(P.m, P.mpad, P.p, P.b, P.logb, P.col,
                                                      P.col_log, P.flag_idx, P.fb_part, P.y,
@@ -1209,7 +1285,7 @@ void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
 }
 
 void launch_apply(Problem& P) {
-  const int fast = P.storage == OTG_STORE_F32 && !P.fused;
+  const int fast = P.storage != OTG_STORE_F64 && !P.fused;  // fp32 stored or on the fly
   k_apply<<<P.e_blocks, kEThreads, 0, P.stream>>>(P.m, P.mpad, P.b, P.p, P.wacc, P.y, P.grad,
                                                   P.prev_grad, P.prev_x, P.prev_y, P.vq, P.dq,
                                                   fast,
