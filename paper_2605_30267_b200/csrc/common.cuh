@@ -138,6 +138,10 @@ struct Problem {
   double raw_min = 0.0, raw_max = 0.0;
   int device = 0;
   int world = 1, rank = 0;
+  int sharded = 0;  // rows split across ranks; column sums all-reduced over NCCL
+  double* fbA = nullptr;  // sharded fallback: per-column global top (MAX all-reduce)
+  double* fbS = nullptr;  //                   per-column rescaled sums (SUM all-reduce)
+  double* fbT = nullptr;  //                   per-column local top
   int vshards = 1;
 
   cudaStream_t stream = nullptr;

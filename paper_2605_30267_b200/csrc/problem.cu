@@ -142,7 +142,7 @@ void problem_free(Problem& P) {
                   P.col_log,
                   P.y, P.grad, P.prev_grad,
                   P.prev_x, P.prev_y, P.flag_idx, P.fb_cols, P.fb_part, P.part, P.e1_part,
-                  P.e2_part, P.ctrl, P.trace, P.bounds};
+                  P.e2_part, P.ctrl, P.trace, P.bounds, P.fbA, P.fbS, P.fbT};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (P.ctrl_host) cudaFreeHost(P.ctrl_host);
@@ -180,6 +180,11 @@ void problem_alloc_state(Problem& P) {
   P.flag_idx = dalloc<int>(P, mp);
   P.fb_cols = dalloc<int>(P, mp);
   P.fb_part = dalloc<double2>(P, mp * kFbChunks);
+  if (P.sharded) {
+    P.fbA = dalloc<double>(P, mp);
+    P.fbS = dalloc<double>(P, mp);
+    P.fbT = dalloc<double>(P, mp);
+  }
   const size_t prow = std::max<size_t>(static_cast<size_t>(P.vshards) * P.col_splits,
                                        static_cast<size_t>(P.fused_clusters));
   P.part = dalloc<double>(P, prow * mp);
@@ -207,15 +212,19 @@ static void begin(Problem& P, int64_t n, int64_t m, const otg_device_opts* opts)
   P.m = m;
   P.n_local = n;
   P.row_begin = 0;
-  if (opts && opts->world_size > 1) {
-    if (opts->rank < 0 || opts->rank >= opts->world_size)
+  // Sharded (NCCL) when world_size > 1, or when an id is given for a 1-rank
+  // communicator (exercises the collective path on one GPU).
+  if (opts && (opts->world_size > 1 || opts->nccl_unique_id)) {
+    if (opts->world_size < 1 || opts->rank < 0 || opts->rank >= opts->world_size)
       fail(OTG_E_DIMENSION, "rank outside [0, world_size)");
     if (opts->row_begin < 0 || opts->row_end > n || opts->row_begin >= opts->row_end)
       fail(OTG_E_DIMENSION, "row shard [row_begin, row_end) outside [0, n)");
+    if (!opts->nccl_unique_id) fail(OTG_E_NCCL, "world_size > 1 needs nccl_unique_id");
     P.world = opts->world_size;
     P.rank = opts->rank;
     P.row_begin = opts->row_begin;
     P.n_local = opts->row_end - opts->row_begin;
+    P.sharded = 1;
   }
   P.vshards = (opts && opts->virtual_shards > 1) ? opts->virtual_shards : 1;
   if (P.vshards > P.n_local) P.vshards = static_cast<int>(P.n_local);
@@ -241,7 +250,7 @@ static void upload_marginals(Problem& P, const double* a, const double* b) {
 }
 
 static void finish_create(Problem& P, const otg_device_opts* opts, otg_problem* out) {
-  if (P.world > 1) comm_init(P, opts->nccl_unique_id);
+  if (P.sharded) comm_init(P, opts->nccl_unique_id);
   problem_alloc_state(P);
   OTG_CUDA(cudaStreamSynchronize(P.stream));
   auto* h = new otg_problem_s;
@@ -397,7 +406,7 @@ otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const doub
         mn = std::min(mn, v.x);
         mx = std::max(mx, v.y);
       }
-      if (P.world > 1) {
+      if (P.sharded) {
         comm_init(P, opts->nccl_unique_id);
         double buf[2] = {-mn, mx};
         double* dbuf = nullptr;
@@ -432,7 +441,7 @@ otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const doub
     OTG_CUDA(cudaStreamSynchronize(P.stream));
     cudaFree(dX);
     cudaFree(dY);
-    if (P.world > 1 && P.nccl_comm) {
+    if (P.sharded && P.nccl_comm) {
       // communicator already built for the normaliser; finish_create must not re-init
       problem_alloc_state(P);
       OTG_CUDA(cudaStreamSynchronize(P.stream));

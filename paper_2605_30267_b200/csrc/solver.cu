@@ -292,7 +292,7 @@ otg_status otg_row_solve_marginals(otg_problem h, const double* v, double* u, do
     h2d(P, P.p, v, P.m);
     launch_sweeps(P, false, nullptr);
     launch_merge_nolog(P);
-    if (P.world > 1) comm_allreduce_sum(P, P.col, static_cast<size_t>(P.mpad + 1));
+    if (P.sharded) comm_allreduce_sum(P, P.col, static_cast<size_t>(P.mpad + 1));
     d2h(P, u, P.u, P.n_local);
     d2h(P, col, P.col, P.m);
     OTG_CUDA(cudaStreamSynchronize(P.stream));
@@ -449,7 +449,7 @@ otg_status otg_plan_stats(otg_problem h, const double* u, const double* v, otg_p
     double *du = nullptr, *dv = nullptr, *rs = nullptr, *rc = nullptr, *rm = nullptr, *cs = nullptr;
     OTG_CUDA(cudaMalloc(&du, n * sizeof(double)));
     OTG_CUDA(cudaMalloc(&dv, m * sizeof(double)));
-    OTG_CUDA(cudaMalloc(&rs, n * sizeof(double)));
+    OTG_CUDA(cudaMalloc(&rs, std::max<int64_t>(n, 2) * sizeof(double)));
     OTG_CUDA(cudaMalloc(&rc, n * sizeof(double)));
     OTG_CUDA(cudaMalloc(&rm, n * sizeof(double)));
     OTG_CUDA(cudaMalloc(&cs, m * sizeof(double)));
@@ -462,17 +462,15 @@ otg_status otg_plan_stats(otg_problem h, const double* u, const double* v, otg_p
     k_plan_cols<<<static_cast<unsigned>((m + kT - 1) / kT), kT, 0, P.stream>>>(
         P.C64, P.C32, X4, Y4, P.ldc, n, m, P.kappa, du, dv, cs);
     OTG_CUDA(cudaGetLastError());
+    if (P.sharded) comm_allreduce_sum(P, cs, static_cast<size_t>(m));  // global column sums
     std::vector<double> hrs(n), hrc(n), hrm(n), hcs(m);
     d2h(P, hrs.data(), rs, n);
     d2h(P, hrc.data(), rc, n);
     d2h(P, hrm.data(), rm, n);
     d2h(P, hcs.data(), cs, m);
     OTG_CUDA(cudaStreamSynchronize(P.stream));
-    for (double* q : {du, dv, rs, rc, rm, cs}) cudaFree(q);
     double top = -DBL_MAX, cost = 0.0, viol = 0.0, vc = 0.0;
     for (int64_t i = 0; i < n; ++i) top = std::max(top, hrm[i]);
-    out->max_exponent = top;
-    if (top > kExpOverflowBound) fail(OTG_E_OVERFLOW, "plan exponent exceeds bound");
     std::vector<double> hb(m), ha(n);
     OTG_CUDA(cudaMemcpy(hb.data(), P.b, m * sizeof(double), cudaMemcpyDeviceToHost));
     OTG_CUDA(cudaMemcpy(ha.data(), P.a, n * sizeof(double), cudaMemcpyDeviceToHost));
@@ -480,6 +478,22 @@ otg_status otg_plan_stats(otg_problem h, const double* u, const double* v, otg_p
       cost += hrc[i];
       viol += std::abs(hrs[i] - ha[i]);
     }
+    if (P.sharded) {  // row-local scalars: sum the cost and the row violation, max the exponent
+      double hsum[2] = {cost, viol}, hmax[1] = {top};
+      OTG_CUDA(cudaMemcpyAsync(rs, hsum, sizeof hsum, cudaMemcpyHostToDevice, P.stream));
+      OTG_CUDA(cudaMemcpyAsync(rm, hmax, sizeof hmax, cudaMemcpyHostToDevice, P.stream));
+      comm_allreduce_sum(P, rs, 2);
+      comm_allreduce_max(P, rm, 1);
+      OTG_CUDA(cudaMemcpyAsync(hsum, rs, sizeof hsum, cudaMemcpyDeviceToHost, P.stream));
+      OTG_CUDA(cudaMemcpyAsync(hmax, rm, sizeof hmax, cudaMemcpyDeviceToHost, P.stream));
+      OTG_CUDA(cudaStreamSynchronize(P.stream));
+      cost = hsum[0];
+      viol = hsum[1];
+      top = hmax[0];
+    }
+    for (double* q : {du, dv, rs, rc, rm, cs}) cudaFree(q);
+    out->max_exponent = top;
+    if (top > kExpOverflowBound) fail(OTG_E_OVERFLOW, "plan exponent exceeds bound");
     for (int64_t j = 0; j < m; ++j) vc += std::abs(hcs[j] - hb[j]);
     out->marginal_violation_l1 = viol + vc;
     out->primal_cost = cost * P.epsilon;  // (eps_original / eps) with eps = 1 (core.cpp:77-79)

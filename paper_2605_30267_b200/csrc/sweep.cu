@@ -651,10 +651,10 @@ __global__ void __launch_bounds__(kEThreads)
 k_merge(const double* __restrict__ part, int nshards, int splits, int64_t m, int64_t mpad,
         double* __restrict__ col, double* __restrict__ col_log, int* __restrict__ flag_idx,
         int* __restrict__ fb_cols, const double* __restrict__ u, const double* __restrict__ a,
-        int64_t nrows, int flag, Ctrl* __restrict__ ctrl) {
+        int64_t nrows, int do_merge, int flag, Ctrl* __restrict__ ctrl) {
   if (ctrl->done) return;
   __shared__ double sh[kEThreads / 32];
-  if (blockIdx.x == 0) {  // <u, a> over the local rows, fixed order (for f)
+  if (do_merge && blockIdx.x == 0) {  // <u, a> over the local rows, fixed order (for f)
     double t = 0.0;
     for (int64_t k = threadIdx.x; k < nrows; k += kEThreads) t += u[k] * a[k];
     t = block_sum<kEThreads>(t, sh);
@@ -663,12 +663,16 @@ k_merge(const double* __restrict__ part, int nshards, int splits, int64_t m, int
   const int64_t j = static_cast<int64_t>(blockIdx.x) * kEThreads + threadIdx.x;
   if (j >= m) return;
   double c = 0.0;
-  for (int s = 0; s < nshards; ++s) {
-    double loc = 0.0;
-    for (int k = 0; k < splits; ++k) loc += part[(static_cast<int64_t>(s) * splits + k) * mpad + j];
-    c += loc;
+  if (do_merge) {
+    for (int s = 0; s < nshards; ++s) {
+      double loc = 0.0;
+      for (int k = 0; k < splits; ++k) loc += part[(static_cast<int64_t>(s) * splits + k) * mpad + j];
+      c += loc;
+    }
+    col[j] = c;
+  } else {
+    c = col[j];  // already merged (and all-reduced across ranks)
   }
-  col[j] = c;
   if (flag) {
     if (c >= ctrl->tiny) {
       col_log[j] = log(c);
@@ -718,6 +722,40 @@ k_fallback(const double* __restrict__ C64, const CostSrc src, int64_t ldc, int64
     s = block_sum<kEThreads>(s, sh);
     if (threadIdx.x == 0) fb_part[f * kFbChunks + ch] = make_double2(top, s);
   }
+}
+
+// Sharded fallback: this rank's (top, sum) of each flagged column over its
+// rows, laid out densely by column so every rank's buffers line up for the
+// MAX / SUM all-reduces (the slot order of fb_cols is rank-local).
+__global__ void __launch_bounds__(kEThreads)
+k_fb_local(int64_t m, const int* __restrict__ flag_idx, const double2* __restrict__ fb_part,
+           double* __restrict__ fbA, double* __restrict__ fbS, double* __restrict__ fbT,
+           const Ctrl* __restrict__ ctrl) {
+  if (ctrl->done) return;
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * kEThreads + threadIdx.x;
+  if (j >= m) return;
+  const int slot = flag_idx[j];
+  double top = -DBL_MAX, s = 0.0;
+  if (slot >= 0) {
+    for (int k = 0; k < kFbChunks; ++k) top = fmax(top, fb_part[slot * kFbChunks + k].x);
+    for (int k = 0; k < kFbChunks; ++k) {
+      const double2 fp = fb_part[slot * kFbChunks + k];
+      if (fp.y > 0.0) s += fp.y * exp(fp.x - top);
+    }
+  }
+  fbA[j] = top;
+  fbT[j] = top;
+  fbS[j] = s;
+}
+
+__global__ void __launch_bounds__(kEThreads)
+k_fb_rescale(int64_t m, const int* __restrict__ flag_idx, const double* __restrict__ fbA,
+             double* __restrict__ fbS, const double* __restrict__ fbT,
+             const Ctrl* __restrict__ ctrl) {
+  if (ctrl->done) return;
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * kEThreads + threadIdx.x;
+  if (j >= m || flag_idx[j] < 0) return;
+  if (fbS[j] > 0.0) fbS[j] *= exp(fbT[j] - fbA[j]);
 }
 
 // --------------------------------------------------------------- control --
@@ -870,7 +908,8 @@ __global__ void __launch_bounds__(kEThreads)
 k_finalize(int64_t m, int64_t mpad, const double* __restrict__ p, const double* __restrict__ b,
            const double* __restrict__ logb, double* __restrict__ col,
            double* __restrict__ col_log, const int* __restrict__ flag_idx,
-           const double2* __restrict__ fb_part, double* __restrict__ y,
+           const double2* __restrict__ fb_part, const double* __restrict__ fbA,
+           const double* __restrict__ fbS, int sharded, double* __restrict__ y,
            double* __restrict__ grad, double* __restrict__ e1_part, double* __restrict__ trace,
            double* __restrict__ bounds, Ctrl* __restrict__ ctrl) {
   if (ctrl->done) return;
@@ -882,12 +921,18 @@ k_finalize(int64_t m, int64_t mpad, const double* __restrict__ p, const double* 
     double c = col[j], cl;
     const int slot = flag_idx[j];
     if (slot >= 0) {
-      double top = -INFINITY;
-      for (int k = 0; k < kFbChunks; ++k) top = fmax(top, fb_part[slot * kFbChunks + k].x);
-      double s = 0.0;
-      for (int k = 0; k < kFbChunks; ++k) {
-        const double2 fp = fb_part[slot * kFbChunks + k];
-        if (fp.y > 0.0) s += fp.y * exp(fp.x - top);
+      double top, s;
+      if (sharded) {  // combined across ranks (k_fb_local / k_fb_rescale + all-reduces)
+        top = fbA[j];
+        s = fbS[j];
+      } else {
+        top = -INFINITY;
+        for (int k = 0; k < kFbChunks; ++k) top = fmax(top, fb_part[slot * kFbChunks + k].x);
+        s = 0.0;
+        for (int k = 0; k < kFbChunks; ++k) {
+          const double2 fp = fb_part[slot * kFbChunks + k];
+          if (fp.y > 0.0) s += fp.y * exp(fp.x - top);
+        }
       }
       cl = top + log(s);
       c = exp(cl);
@@ -1223,17 +1268,17 @@ int partial_rows(const Problem& P) {
   return P.fused ? P.fused_clusters : P.vshards * P.col_splits;
 }
 
-static void launch_merge(Problem& P, bool flag) {
+static void launch_merge(Problem& P, bool merge, bool flag) {
   const int64_t blocks = (P.m + kEThreads - 1) / kEThreads;
   const int shards = P.fused ? 1 : P.vshards;
   const int splits = P.fused ? P.fused_clusters : P.col_splits;
   k_merge<<<blocks, kEThreads, 0, P.stream>>>(P.part, shards, splits, P.m, P.mpad, P.col,
                                               P.col_log, P.flag_idx, P.fb_cols, P.u, P.a,
-                                              P.n_local, flag ? 1 : 0, P.ctrl);
+                                              P.n_local, merge ? 1 : 0, flag ? 1 : 0, P.ctrl);
   OTG_CUDA(cudaGetLastError());
 }
 
-void launch_merge_nolog(Problem& P) { launch_merge(P, false); }
+void launch_merge_nolog(Problem& P) { launch_merge(P, true, false); }
 
 // Event records are "external" so that, under stream capture, they become
 // event-record nodes of the chunk graph (timestamps readable after replay).
@@ -1264,8 +1309,15 @@ void launch_sweeps(Problem& P, bool timed, cudaEvent_t* ev4) {
 
 void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
   launch_sweeps(P, timed, ev4);
-  launch_merge(P, with_log);
-  if (P.world > 1) comm_allreduce_sum(P, P.col, static_cast<size_t>(P.mpad + 1));
+  if (P.sharded) {
+    // local merge, then one all-reduce of the m column sums + <u, a>; the
+    // underflow test needs the global sums, so flagging follows the reduce
+    launch_merge(P, true, false);
+    comm_allreduce_sum(P, P.col, static_cast<size_t>(P.mpad + 1));
+    if (with_log) launch_merge(P, false, true);
+  } else {
+    launch_merge(P, true, with_log);
+  }
   if (!with_log) return;
   if (P.storage == OTG_STORE_F64)
     k_fallback<true, false><<<296, kEThreads, 0, P.stream>>>(
@@ -1277,10 +1329,21 @@ void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
     k_fallback<false, false><<<296, kEThreads, 0, P.stream>>>(
         nullptr, cost_src(P), P.ldc, P.n_local, P.kappa, P.u, P.p, P.fb_cols, P.fb_part, P.ctrl);
   OTG_CUDA(cudaGetLastError());
+  if (P.sharded) {
+    // exact column LSE across ranks: local (top, sum) per flagged column,
+    // MAX all-reduce of the tops, rescale, SUM all-reduce of the sums
+    const unsigned g = static_cast<unsigned>((P.m + kEThreads - 1) / kEThreads);
+    k_fb_local<<<g, kEThreads, 0, P.stream>>>(P.m, P.flag_idx, P.fb_part, P.fbA, P.fbS, P.fbT,
+                                              P.ctrl);
+    comm_allreduce_max(P, P.fbA, static_cast<size_t>(P.m));
+    k_fb_rescale<<<g, kEThreads, 0, P.stream>>>(P.m, P.flag_idx, P.fbA, P.fbS, P.fbT, P.ctrl);
+    comm_allreduce_sum(P, P.fbS, static_cast<size_t>(P.m));
+    OTG_CUDA(cudaGetLastError());
+  }
   k_finalize<<<P.e_blocks, kEThreads, 0, P.stream>>>(P.m, P.mpad, P.p, P.b, P.logb, P.col,
-                                                     P.col_log, P.flag_idx, P.fb_part, P.y,
-                                                     P.grad, P.e1_part, P.trace, P.bounds,
-                                                     P.ctrl);
+                                                     P.col_log, P.flag_idx, P.fb_part, P.fbA,
+                                                     P.fbS, P.sharded, P.y, P.grad, P.e1_part,
+                                                     P.trace, P.bounds, P.ctrl);
   OTG_CUDA(cudaGetLastError());
 }
 
