@@ -59,53 +59,78 @@ def peaks():
 
 # ------------------------------------------------------------ clocks ----
 class ClockSampler:
-    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled DURING the timed region
+    (B200_PROFILING.md clocks line) through NVML every 10 ms on a thread;
+    nvidia-smi (-lms 100) when NVML is unavailable."""
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4),
+               ("hw_power_brake_slowdown", 0x80))
 
-    def __init__(self, index=0):
+    def __init__(self, index=0, period_s=0.01):
         self.index = index
-        self.samples = []
-        self.proc = None
+        self.period = period_s
+        self.samples = []  # (sm_mhz, max_mhz, reasons_mask)
+        self._stop = threading.Event()
+        self._nv = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except FileNotFoundError:
-            self.proc = None
+            import pynvml as nv
+            nv.nvmlInit()
+            self._nv = nv
+            self._h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self._max = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
+    def _run(self):
+        if self._nv is not None:
+            nv = self._nv
+            while not self._stop.is_set():
+                try:
+                    sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                    self.samples.append((float(sm), float(self._max), int(rs)))
+                except Exception:
+                    pass
+                self._stop.wait(self.period)
+            return
+        try:
+            proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            return
+        for line in proc.stdout:
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                self.samples.append(parts)
+            try:
+                self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+            except (ValueError, IndexError):
+                pass
+            if self._stop.is_set():
+                break
+        proc.terminate()
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        self._t.join(timeout=5)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4)
-                          if s[2 + k].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        mask = 0
+        for s in self.samples:
+            mask |= s[2]
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": [n for n, bit in self.REASONS if mask & bit],
+                "samples": len(self.samples),
+                "source": "nvml" if self._nv is not None else "nvidia-smi"}
 
 
 # ------------------------------------------------------- CPU baseline ----
@@ -244,7 +269,8 @@ def main():
     barrier()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e_iters = r_e2e.iterations
-    h2d = (x.nbytes * (1 if world == 1 else 1) + y.nbytes + a.nbytes + b.nbytes)
+    rows = (shard["row_end"] - shard["row_begin"]) if shard else N
+    h2d = (x[:rows].nbytes + y.nbytes + a.nbytes + b.nbytes)
     d2h = u_host.nbytes + v_host.nbytes
 
     # ---- device-timed throughput: W warm-up iterations, then K timed ----
@@ -252,12 +278,16 @@ def main():
     barrier()
     with ClockSampler(local_rank) as clk:
         barrier()
-        r = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=args.steps),
-                              time_sweeps=True)
+        r = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=args.steps))
         barrier()
     dev_s = max_over_ranks(r.device_seconds)
     iters = r.iterations
     value = iters / dev_s
+    launches = r.kernel_launches
+
+    # per-kernel CUDA events (separate run so they do not perturb `value`)
+    r = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=args.steps),
+                          time_sweeps=True)
     evals = r.evaluations
 
     # dominant kernel roofline (CUDA events around every launch inside the solve)
@@ -316,7 +346,7 @@ def main():
                          "avg_launch_ms": dom_ms, "row_pass_ms": row_ms, "col_pass_ms": col_ms,
                          "isolated_ms": {"row": ms_sw[0], "col": ms_sw[1], "merge": ms_sw[2]}},
             "cpu_baseline": cpu,
-            "gpu_launches": int(evals * 6),
+            "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -179,9 +179,11 @@ typedef struct {
   double device_seconds; /* device time of the whole solve (CUDA events)    */
   double row_pass_seconds; /* summed row-pass launch times (time_sweeps)    */
   double col_pass_seconds; /* summed column-pass launch times (time_sweeps) */
-  int64_t kernel_launches; /* live (non-skipped) kernels launched           */
+  int64_t kernel_launches; /* kernel nodes replayed by the solve loop        */
   int64_t row_redos;     /* fp32 row pass: rows recomputed exactly because
                             the shift estimate was loose (diagnostic)       */
+  double epilogue_seconds; /* summed merge + fallback + finalize + apply
+                              times (time_sweeps)                           */
 } otg_solve_result;
 
 /* plan_from_potentials + marginal_violation_l1 + primal_cost

@@ -62,7 +62,8 @@ class SolveResultC(C.Structure):
                 ("boundaries", C.c_void_p), ("boundaries_cap", C.c_int64),
                 ("time_sweeps", C.c_int), ("device_seconds", C.c_double),
                 ("row_pass_seconds", C.c_double), ("col_pass_seconds", C.c_double),
-                ("kernel_launches", C.c_int64), ("row_redos", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("row_redos", C.c_int64),
+                ("epilogue_seconds", C.c_double)]
 
 
 class PlanSummaryC(C.Structure):

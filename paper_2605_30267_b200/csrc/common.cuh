@@ -178,6 +178,7 @@ struct Problem {
 
   // column-pass partials
   int col_splits = 1;
+  int col_threads = 128;  // fp32 column pass CTA width (4 columns per thread)
   int64_t rows_per_split = 0;
   double* part = nullptr;  // (vshards * col_splits) x mpad
 
@@ -197,7 +198,8 @@ struct Problem {
   cudaGraphExec_t chunk_exec = nullptr;
   cudaGraphExec_t chunk_exec_timed = nullptr;
   int chunk_len = 0;
-  std::vector<cudaEvent_t> chunk_events;  // 4 per iteration (timed graph)
+  int chunk_kernels = 0, chunk_kernels_timed = 0;  // kernel nodes per chunk graph
+  std::vector<cudaEvent_t> chunk_events;  // 5 per iteration (timed graph)
 
   // NCCL (sharded)
   void* nccl_comm = nullptr;

@@ -8,6 +8,8 @@
 #include <cstdio>
 #include <cstring>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace otg {
@@ -170,7 +172,7 @@ void problem_alloc_state(Problem& P) {
   P.vq = dalloc<float>(P, 2 * mp);
   P.p = dalloc<double>(P, mp);
   P.wacc = dalloc<double>(P, mp);
-  P.col = dalloc<double>(P, mp + 8);
+  P.col = dalloc<double>(P, mp + 8 + (P.m + 255) / 256);  // + <u, a> slices (k_merge)
   P.col_log = dalloc<double>(P, mp);
   P.y = dalloc<double>(P, mp);
   P.grad = dalloc<double>(P, mp);
@@ -230,7 +232,11 @@ static void begin(Problem& P, int64_t n, int64_t m, const otg_device_opts* opts)
   if (P.vshards > P.n_local) P.vshards = static_cast<int>(P.n_local);
   P.mpad = round_up(m, 4);
   // rows padded to whole 8-CTA-cluster slices of 16-byte multiples (fused.cu)
-  P.ldc = round_up(m, 32);
+  static const int64_t ldc_pad = [] {  // tuning knob: extra floats per cost row
+    const char* s = getenv("OTG_LDC_PAD");
+    return s ? static_cast<int64_t>(atoi(s)) : int64_t{0};
+  }();
+  P.ldc = round_up(m, 32) + round_up(ldc_pad, 32);
   OTG_CUDA(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
 }
 

@@ -86,15 +86,18 @@ void build_graph(Problem& P, bool timed) {
   cudaGraphExec_t& exec = timed ? P.chunk_exec_timed : P.chunk_exec;
   if (exec) return;
   if (timed && P.chunk_events.empty()) {
-    P.chunk_events.resize(4 * kChunk);
+    P.chunk_events.resize(5 * kChunk);
     for (auto& e : P.chunk_events) OTG_CUDA(cudaEventCreate(&e));
   }
   cudaGraph_t g = nullptr;
   OTG_CUDA(cudaStreamBeginCapture(P.stream, cudaStreamCaptureModeThreadLocal));
   try {
     for (int k = 0; k < kChunk; ++k) {
-      launch_eval(P, true, timed, timed ? &P.chunk_events[4 * k] : nullptr);
+      launch_eval(P, true, timed, timed ? &P.chunk_events[5 * k] : nullptr);
       launch_apply(P);
+      if (timed)
+        OTG_CUDA(cudaEventRecordWithFlags(P.chunk_events[5 * k + 4], P.stream,
+                                          cudaEventRecordExternal));
     }
   } catch (...) {
     cudaStreamEndCapture(P.stream, &g);
@@ -102,14 +105,26 @@ void build_graph(Problem& P, bool timed) {
     throw;
   }
   OTG_CUDA(cudaStreamEndCapture(P.stream, &g));
+  size_t nn = 0;
+  OTG_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  OTG_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+  int kernels = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    OTG_CUDA(cudaGraphNodeGetType(nd, &t));
+    kernels += (t == cudaGraphNodeTypeKernel);
+  }
+  (timed ? P.chunk_kernels_timed : P.chunk_kernels) = kernels;
   OTG_CUDA(cudaGraphInstantiate(&exec, g, 0));
   cudaGraphDestroy(g);
   P.chunk_len = kChunk;
 }
 
 struct LoopOut {
-  double device_s = 0.0, row_s = 0.0, col_s = 0.0;
+  double device_s = 0.0, row_s = 0.0, col_s = 0.0, epi_s = 0.0;
   int64_t trace_len = 0;
+  int64_t launches = 0;  // kernel nodes executed (every replayed chunk)
 };
 
 // Replays the chunk graph until the device control block says done; drains
@@ -125,16 +140,20 @@ LoopOut run_loop(Problem& P, otg_solve_result* res, bool timed) {
   OTG_CUDA(cudaEventRecord(t0, P.stream));
   for (;;) {
     OTG_CUDA(cudaGraphLaunch(timed ? P.chunk_exec_timed : P.chunk_exec, P.stream));
+    lo.launches += timed ? P.chunk_kernels_timed : P.chunk_kernels;
     get_ctrl(P);
     const Ctrl& c = *P.ctrl_host;
     if (timed) {
       const long long live = c.evaluations - ev_before;
       for (long long k = 0; k < live && k < kChunk; ++k) {
-        float a = 0.f, b = 0.f;
-        OTG_CUDA(cudaEventElapsedTime(&a, P.chunk_events[4 * k], P.chunk_events[4 * k + 1]));
-        OTG_CUDA(cudaEventElapsedTime(&b, P.chunk_events[4 * k + 2], P.chunk_events[4 * k + 3]));
+        float a = 0.f, b = 0.f, e = 0.f;
+        const cudaEvent_t* ev = &P.chunk_events[5 * k];
+        OTG_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+        OTG_CUDA(cudaEventElapsedTime(&b, ev[2], ev[3]));
+        OTG_CUDA(cudaEventElapsedTime(&e, ev[3], ev[4]));
         lo.row_s += a * 1e-3;
         lo.col_s += b * 1e-3;
+        lo.epi_s += e * 1e-3;
       }
       ev_before = c.evaluations;
     }
@@ -181,7 +200,8 @@ void fill_result(Problem& P, otg_solve_result* res, const LoopOut& lo) {
   res->device_seconds = lo.device_s;
   res->row_pass_seconds = lo.row_s;
   res->col_pass_seconds = lo.col_s;
-  res->kernel_launches = c.evaluations * 7;
+  res->epilogue_seconds = lo.epi_s;
+  res->kernel_launches = lo.launches;
   res->row_redos = c.redo_total;
   d2h(P, res->u, P.u, P.n_local);
   d2h(P, res->v, P.p, P.m);

@@ -66,6 +66,17 @@ __device__ __forceinline__ float4 ld_stream(const float4* ptr) {
   return r;
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* ptr) {
+  asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(ptr));
+}
+__device__ __forceinline__ float4 ld_stream256(const float4* ptr) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(ptr));
+  return r;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -334,27 +345,6 @@ __device__ void row_exact_block(const int64_t* rows, const CostSrc src,
   }
 }
 
-template <int R, bool OTF>
-__global__ void __launch_bounds__(kRowThreads)
-k_row_exact(const CostSrc src, int64_t n, int64_t m,
-            const double* __restrict__ p, double kappa, const double* __restrict__ a,
-            const double* __restrict__ loga, double* __restrict__ rowM,
-            double* __restrict__ rowS, double* __restrict__ u, double* __restrict__ wrow,
-            float4* __restrict__ aux, double* __restrict__ rowM2, int* __restrict__ rowJ,
-            const Ctrl* __restrict__ ctrl) {
-  if (ctrl->done || ctrl->shift_valid) return;
-  int64_t rows[R];
-  bool valid[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * R + r;
-    valid[r] = i < n;
-    rows[r] = valid[r] ? i : n - 1;
-  }
-  row_exact_block<R, OTF>(rows, src, m, p, kappa, a, loga, rowM, rowS, u, wrow, aux, rowM2, rowJ,
-                          valid);
-}
-
 // Exact redo of the rows k_row_shift flagged (grid-stride over the list).
 template <bool OTF>
 __global__ void __launch_bounds__(kRowThreads)
@@ -391,15 +381,14 @@ k_row_redo(const CostSrc src, int64_t m, const double* __restrict__ p,
 constexpr float kRedoLo = 2.0f;
 constexpr float kRedoHi = 6.0f;
 
-template <int R, bool OTF>
-__global__ void __launch_bounds__(kRowThreads)
-k_row_shift(const CostSrc src, int64_t n, int64_t m,
-            const float* __restrict__ vq, const double* __restrict__ dq, int64_t mpad, float kh,
-            float kl, const double* __restrict__ a, const double* __restrict__ loga,
-            double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
-            double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
-            int* __restrict__ rowJ, int* __restrict__ redo_rows, Ctrl* __restrict__ ctrl) {
-  if (ctrl->done || !ctrl->shift_valid) return;
+template <int R, bool OTF, int PF>
+__device__ __forceinline__ void row_shift_block(
+    const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
+    const double* __restrict__ dq, int64_t mpad, float kh, float kl, const double* __restrict__ a,
+    const double* __restrict__ loga, double* __restrict__ rowM, double* __restrict__ rowS,
+    double* __restrict__ u, double* __restrict__ wrow, float4* __restrict__ aux,
+    double* __restrict__ rowM2, int* __restrict__ rowJ, int* __restrict__ redo_rows,
+    Ctrl* __restrict__ ctrl) {
   __shared__ double sh[kRowThreads / 32];
   __shared__ float shf[kRowThreads / 32];
   __shared__ int shj[kRowThreads / 32];
@@ -438,8 +427,22 @@ k_row_shift(const CostSrc src, int64_t n, int64_t m,
     float4 y4[4];
     load_y4<OTF>(src, q, y4);
     float4 c[R];
+    if constexpr (!OTF && PF == 1) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) c[r] = cost_quad<OTF>(src, rr[r], q, xr[r], y4);
+      for (int r = 0; r < R; ++r)
+        c[r] = ld_stream256(reinterpret_cast<const float4*>(src.C + rr[r] * src.ldc) + q);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) c[r] = cost_quad<OTF>(src, rr[r], q, xr[r], y4);
+    }
+    if constexpr (!OTF && PF >= 2) {
+      const int64_t qp = q + static_cast<int64_t>(PF - 1) * kRowThreads;
+      if (qp < nq) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          prefetch_l2(reinterpret_cast<const float4*>(src.C + rr[r] * src.ldc) + qp);
+      }
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const float t0 = fmaf(-c[r].x, kh, V.x - Sc[r]) + fmaf(-c[r].x, kl, F.x);
@@ -536,6 +539,43 @@ k_row_shift(const CostSrc src, int64_t n, int64_t m,
   }
 }
 
+// fp32 row pass kernels: the exact body on the first evaluation of a solve
+// (no previous point), the shift-estimate body after; each returns at once
+// when its case does not apply.  (Kept as two kernels: one kernel holding both
+// bodies needs 76 registers and drops the shift pass to 3 CTAs per SM.)
+template <int R, bool OTF>
+__global__ void __launch_bounds__(kRowThreads)
+k_row_exact(const CostSrc src, int64_t n, int64_t m, const double* __restrict__ p, double kappa,
+            const double* __restrict__ a, const double* __restrict__ loga,
+            double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
+            double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
+            int* __restrict__ rowJ, const Ctrl* __restrict__ ctrl) {
+  if (ctrl->done || ctrl->shift_valid) return;
+  int64_t rows[R];
+  bool valid[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * R + r;
+    valid[r] = i < n;
+    rows[r] = valid[r] ? i : n - 1;
+  }
+  row_exact_block<R, OTF>(rows, src, m, p, kappa, a, loga, rowM, rowS, u, wrow, aux, rowM2, rowJ,
+                          valid);
+}
+
+template <int R, bool OTF, int PF>
+__global__ void __launch_bounds__(kRowThreads)
+k_row_shift(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
+            const double* __restrict__ dq, int64_t mpad, float kh, float kl,
+            const double* __restrict__ a, const double* __restrict__ loga,
+            double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
+            double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
+            int* __restrict__ rowJ, int* __restrict__ redo_rows, Ctrl* __restrict__ ctrl) {
+  if (ctrl->done || !ctrl->shift_valid) return;
+  row_shift_block<R, OTF, PF>(src, n, m, vq, dq, mpad, kh, kl, a, loga, rowM, rowS, u, wrow, aux,
+                              rowM2, rowJ, redo_rows, ctrl);
+}
+
 // ------------------------------------------------------------------ K2 ----
 // fp64: partial c_j = sum_i exp(((-C'_ij) + p_j) - M_i) * w_i  (dual.cpp:36,41)
 __global__ void __launch_bounds__(kColThreads)
@@ -559,8 +599,8 @@ k_col_precise(const double* __restrict__ C, int64_t ldc, int64_t m,
 // fp32: thread owns 4 consecutive columns, loops over the split's rows.  The
 // rows' shift / weight (aux) -- and, on the fly, the rows' points -- are
 // staged in shared memory per 256-row tile and read as broadcasts.
-template <bool OTF>
-__global__ void __launch_bounds__(kColThreads)
+template <bool OTF, int NT>
+__global__ void __launch_bounds__(NT)
 k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh, float kl,
            const float4* __restrict__ aux, int64_t row_lo, int64_t row_hi,
            int64_t rows_per_split, double* __restrict__ part, int64_t mpad,
@@ -568,7 +608,7 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
   if (ctrl->done) return;
   __shared__ float4 sh_aux[kAuxTile];
   __shared__ float4 sh_x[OTF ? kAuxTile : 1];
-  const int64_t q = static_cast<int64_t>(blockIdx.x) * kColThreads + threadIdx.x;
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x;
   const int64_t j0 = 4 * q;
   const int64_t i0 = row_lo + static_cast<int64_t>(blockIdx.y) * rows_per_split;
   const int64_t i1 = min(i0 + rows_per_split, row_hi);
@@ -586,7 +626,7 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
   for (int64_t t0 = i0; t0 < i1; t0 += kAuxTile) {
     const int64_t tn = min(static_cast<int64_t>(kAuxTile), i1 - t0);
     __syncthreads();
-    for (int k = threadIdx.x; k < tn; k += kColThreads) {
+    for (int k = threadIdx.x; k < tn; k += NT) {
       sh_aux[k] = aux[t0 + k];
       if (OTF) sh_x[k] = src.X[t0 + k];
     }
@@ -646,7 +686,8 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
 // ----------------------------------------------------------------- E1a ----
 // c_j = sum over shards of (sum over the shard's splits of the partials); the
 // inner sum is what one rank holds, the outer sum stands in for the allreduce.
-// Block 0 also folds the row-pass partials of <u, a> into col[mpad].
+// CTA k also folds <u, a> over row slice k into col[mpad + 1 + k] (the
+// sharded all-reduce covers col[0, mpad + 1 + gridDim.x); finalize sums them).
 __global__ void __launch_bounds__(kEThreads)
 k_merge(const double* __restrict__ part, int nshards, int splits, int64_t m, int64_t mpad,
         double* __restrict__ col, double* __restrict__ col_log, int* __restrict__ flag_idx,
@@ -654,11 +695,12 @@ k_merge(const double* __restrict__ part, int nshards, int splits, int64_t m, int
         int64_t nrows, int do_merge, int flag, Ctrl* __restrict__ ctrl) {
   if (ctrl->done) return;
   __shared__ double sh[kEThreads / 32];
-  if (do_merge && blockIdx.x == 0) {  // <u, a> over the local rows, fixed order (for f)
+  if (do_merge) {  // <u, a> over the local rows: CTA k folds row slice k (for f)
+    const int64_t r0 = nrows * blockIdx.x / gridDim.x, r1 = nrows * (blockIdx.x + 1) / gridDim.x;
     double t = 0.0;
-    for (int64_t k = threadIdx.x; k < nrows; k += kEThreads) t += u[k] * a[k];
+    for (int64_t k = r0 + threadIdx.x; k < r1; k += kEThreads) t += u[k] * a[k];
     t = block_sum<kEThreads>(t, sh);
-    if (threadIdx.x == 0) col[mpad] = t;
+    if (threadIdx.x == 0) col[mpad + 1 + blockIdx.x] = t;
   }
   const int64_t j = static_cast<int64_t>(blockIdx.x) * kEThreads + threadIdx.x;
   if (j >= m) return;
@@ -909,7 +951,7 @@ k_finalize(int64_t m, int64_t mpad, const double* __restrict__ p, const double* 
            const double* __restrict__ logb, double* __restrict__ col,
            double* __restrict__ col_log, const int* __restrict__ flag_idx,
            const double2* __restrict__ fb_part, const double* __restrict__ fbA,
-           const double* __restrict__ fbS, int sharded, double* __restrict__ y,
+           const double* __restrict__ fbS, int sharded, int ua_slices, double* __restrict__ y,
            double* __restrict__ grad, double* __restrict__ e1_part, double* __restrict__ trace,
            double* __restrict__ bounds, Ctrl* __restrict__ ctrl) {
   if (ctrl->done) return;
@@ -969,10 +1011,11 @@ k_finalize(int64_t m, int64_t mpad, const double* __restrict__ p, const double* 
     last = prev == gridDim.x - 1;
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last) return;
   __threadfence();
+  // the last CTA folds the per-CTA partials with all its threads (fixed order)
   double gl = 0.0, sy = 0.0, pb = 0.0, mp = 0.0, bd = 0.0;
-  for (unsigned k = 0; k < gridDim.x; ++k) {
+  for (unsigned k = threadIdx.x; k < gridDim.x; k += kEThreads) {
     const volatile double* src = e1_part + k * 8;
     gl += src[0];
     sy += src[1];
@@ -980,12 +1023,20 @@ k_finalize(int64_t m, int64_t mpad, const double* __restrict__ p, const double* 
     mp = fmax(mp, src[3]);
     bd = fmax(bd, src[4]);
   }
+  gl = block_sum<kEThreads>(gl, sh);
+  sy = block_sum<kEThreads>(sy, sh);
+  pb = block_sum<kEThreads>(pb, sh);
+  mp = block_max<kEThreads>(mp, sh);
+  bd = block_max<kEThreads>(bd, sh);
+  double ua = 0.0;  // <u, a> partials of the merge CTAs (col[mpad + 1 + k])
+  for (int k = threadIdx.x; k < ua_slices; k += kEThreads) ua += col[mpad + 1 + k];
+  ua = block_sum<kEThreads>(ua, sh);
+  if (threadIdx.x != 0) return;
   Ctrl* C = ctrl;
   C->e1_counter = 0;
   C->fb_count = 0;
   C->redo_total += C->redo_count;
   C->redo_count = 0;
-  const double ua = col[mpad];
   const double f = (1.0 - ua) - pb;
   C->mean_y = sy / static_cast<double>(m);
   C->max_v_inf = fmax(C->max_v_inf, mp);
@@ -1100,14 +1151,20 @@ k_apply(int64_t m, int64_t mpad, const double* __restrict__ b, double* __restric
     last = prev == gridDim.x - 1;
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last) return;
   __threadfence();
   double t[8] = {0, 0, 0, 0, 0, 0, 0, -INFINITY};
-  for (unsigned k = 0; k < gridDim.x; ++k) {
+  for (unsigned k = threadIdx.x; k < gridDim.x; k += kEThreads) {
     const volatile double* src = e2_part + k * 8;
     for (int q = 0; q < 4; ++q) t[q] += src[q];
     for (int q = 4; q < 8; ++q) t[q] = fmax(t[q], src[q]);
   }
+  if (stab) {
+    for (int q = 0; q < 4; ++q) t[q] = block_sum<kEThreads>(t[q], sh);
+    for (int q = 4; q < 7; ++q) t[q] = block_max<kEThreads>(t[q], sh);
+  }
+  t[7] = block_max<kEThreads>(t[7], sh);
+  if (threadIdx.x != 0) return;
   Ctrl* C = ctrl;
   if (stab && have_prev) {
     double cells[5];
@@ -1158,16 +1215,64 @@ int64_t rows_per_cta_fast(const Problem& P) {
   return P.n_local >= want ? want : 1;
 }
 
+// Resident CTAs of the fp32 column pass over the whole GPU.
+static int64_t col_slots(const Problem& P) {
+  const void* fn = nullptr;
+  const bool otf = P.storage == OTG_STORE_ON_THE_FLY;
+  switch (P.col_threads) {
+    case 512: fn = otf ? (const void*)k_col_fast<true, 512> : (const void*)k_col_fast<false, 512>; break;
+    case 256: fn = otf ? (const void*)k_col_fast<true, 256> : (const void*)k_col_fast<false, 256>; break;
+    default: fn = otf ? (const void*)k_col_fast<true, 128> : (const void*)k_col_fast<false, 128>;
+  }
+  int occ = 0, sms = 0;
+  OTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, P.col_threads, 0));
+  OTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.device));
+  return std::max<int64_t>(1, static_cast<int64_t>(occ) * sms);
+}
+
 void configure_sweeps(Problem& P) {
   // column-pass split: ~24 CTAs per SM over the grid so the dynamic CTA
   // scheduler balances the 148 SMs (ncu: 640 CTAs = 0.48 waves was
   // latency-bound); partials cost splits * m * 8 B (< 1% of the sweep)
+  static const int env_t = [] {
+    const char* s = getenv("OTG_COL_T");
+    return s ? atoi(s) : 0;
+  }();
+  static const int env_s = [] {
+    const char* s = getenv("OTG_COL_SPLITS");
+    return s ? atoi(s) : 0;
+  }();
+  // 256 threads x 4 columns = 4 KB of each cost row per CTA, ~9 CTAs per SM
+  // in one wave (tools/col_sweep.py on B200: 2.77 ms = 95% of HBM at
+  // 65536^2, vs 3.53 ms for 128-thread CTAs in 2.7 waves)
+  P.col_threads = (env_t == 128 || env_t == 256 || env_t == 512) ? env_t : 256;
   const int64_t colblocks =
       P.storage == OTG_STORE_F64 ? (P.m + kColThreads - 1) / kColThreads
-                                 : (P.m + 4 * kColThreads - 1) / (4 * kColThreads);
+                                 : (P.m + 4 * P.col_threads - 1) / (4 * P.col_threads);
   const int64_t shard_rows = (P.n_local + P.vshards - 1) / P.vshards;
-  int64_t splits = (24 * 148 + colblocks - 1) / colblocks;
-  splits = std::max<int64_t>(1, std::min<int64_t>(splits, (shard_rows + 63) / 64));
+  const int64_t max_splits = std::max<int64_t>(1, (shard_rows + 63) / 64);
+  int64_t splits = 1;
+  if (env_s > 0) {
+    splits = env_s;
+  } else if (P.storage == OTG_STORE_F64) {
+    splits = (24 * 148 + colblocks - 1) / colblocks;
+  } else {
+    // fp32: the CTA count is a near-integer number of waves of the resident
+    // slots (B200, 65536^2: 1.04 waves 4.19 ms, 1.38 w 3.27 ms, 2.08 w
+    // 3.27 ms, 1.99 w 2.59 ms): maximise the fill of the last wave, <= 4 waves
+    const int64_t slots = col_slots(P);
+    double best = -1.0;
+    for (int64_t S = 1; S <= max_splits; ++S) {
+      const double waves = static_cast<double>(colblocks * S) / static_cast<double>(slots);
+      if (waves > 4.0 && S > 1) break;
+      const double fill = waves / std::ceil(waves);
+      if (fill > best + 1e-3) {
+        best = fill;
+        splits = S;
+      }
+    }
+  }
+  splits = std::max<int64_t>(1, std::min<int64_t>(splits, max_splits));
   P.col_splits = static_cast<int>(splits);
   P.rows_per_split = (shard_rows + splits - 1) / splits;
   P.e_blocks = e_grid(P.m);
@@ -1214,13 +1319,28 @@ void launch_row_pass(Problem& P) {
     const float kh = static_cast<float>(k2);
     const float kl = static_cast<float>(k2 - static_cast<double>(kh));
     const CostSrc src = cost_src(P);
+    // L2 prefetch of the cost two column chunks ahead (OTG_ROW_PF: 0 off,
+    // 1 = L2::256B loads, 3 / 5 = prefetch 2 / 4 chunks ahead).  B200, 65536^2:
+    // 3.19 ms (off) -> 2.95 ms (3), although it costs 76 registers (3 CTAs/SM)
+    static const int row_pf = [] {
+      const char* s = getenv("OTG_ROW_PF");
+      return s ? atoi(s) : 3;
+    }();
+#define OTG_SHIFT_ARGS                                                                        \
+  src, P.n_local, P.m, P.vq, P.dq, P.mpad, kh, kl, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow,  \
+      P.aux, P.rowM2, P.rowJ, P.redo_rows, P.ctrl
 #define OTG_ROW(RR, OTF)                                                                      \
   k_row_exact<RR, OTF><<<blocks, kRowThreads, 0, P.stream>>>(                                 \
       src, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,     \
       P.rowM2, P.rowJ, P.ctrl);                                                               \
-  k_row_shift<RR, OTF><<<blocks, kRowThreads, 0, P.stream>>>(                                 \
-      src, P.n_local, P.m, P.vq, P.dq, P.mpad, kh, kl, P.a, P.loga, P.rowM, P.rowS, P.u,      \
-      P.wrow, P.aux, P.rowM2, P.rowJ, P.redo_rows, P.ctrl);                                   \
+  if (RR == 4 && !OTF && row_pf == 1)                                                         \
+    k_row_shift<RR, OTF, 1><<<blocks, kRowThreads, 0, P.stream>>>(OTG_SHIFT_ARGS);            \
+  else if (RR == 4 && !OTF && row_pf == 3)                                                    \
+    k_row_shift<RR, OTF, 3><<<blocks, kRowThreads, 0, P.stream>>>(OTG_SHIFT_ARGS);            \
+  else if (RR == 4 && !OTF && row_pf == 5)                                                    \
+    k_row_shift<RR, OTF, 5><<<blocks, kRowThreads, 0, P.stream>>>(OTG_SHIFT_ARGS);            \
+  else                                                                                        \
+    k_row_shift<RR, OTF, 0><<<blocks, kRowThreads, 0, P.stream>>>(OTG_SHIFT_ARGS);            \
   k_row_redo<OTF><<<296, kRowThreads, 0, P.stream>>>(src, P.m, P.p, P.kappa, P.a, P.loga,     \
                                                      P.rowM, P.rowS, P.u, P.wrow, P.aux,      \
                                                      P.rowM2, P.rowJ, P.redo_rows, P.ctrl)
@@ -1233,6 +1353,7 @@ void launch_row_pass(Problem& P) {
       if (otf) { OTG_ROW(1, true); } else { OTG_ROW(1, false); }
     }
 #undef OTG_ROW
+#undef OTG_SHIFT_ARGS
   }
   OTG_CUDA(cudaGetLastError());
 }
@@ -1251,14 +1372,20 @@ void launch_col_pass(Problem& P) {
                                                         lo, hi, P.rows_per_split, part, P.mpad,
                                                         P.ctrl);
     } else {
-      dim3 grid(static_cast<unsigned>((P.m + 4 * kColThreads - 1) / (4 * kColThreads)),
-                P.col_splits);
-      if (P.storage == OTG_STORE_ON_THE_FLY)
-        k_col_fast<true><<<grid, kColThreads, 0, P.stream>>>(
-            cost_src(P), P.m, P.p, kh, kl, P.aux, lo, hi, P.rows_per_split, part, P.mpad, P.ctrl);
-      else
-        k_col_fast<false><<<grid, kColThreads, 0, P.stream>>>(
-            cost_src(P), P.m, P.p, kh, kl, P.aux, lo, hi, P.rows_per_split, part, P.mpad, P.ctrl);
+      const int NT = P.col_threads;
+      dim3 grid(static_cast<unsigned>((P.m + 4 * NT - 1) / (4 * NT)), P.col_splits);
+#define OTG_COL(OTF, T)                                                                      \
+  k_col_fast<OTF, T><<<grid, T, 0, P.stream>>>(cost_src(P), P.m, P.p, kh, kl, P.aux, lo, hi, \
+                                               P.rows_per_split, part, P.mpad, P.ctrl)
+      const bool otf = P.storage == OTG_STORE_ON_THE_FLY;
+      if (NT == 512) {
+        if (otf) { OTG_COL(true, 512); } else { OTG_COL(false, 512); }
+      } else if (NT == 256) {
+        if (otf) { OTG_COL(true, 256); } else { OTG_COL(false, 256); }
+      } else {
+        if (otf) { OTG_COL(true, 128); } else { OTG_COL(false, 128); }
+      }
+#undef OTG_COL
     }
   }
   OTG_CUDA(cudaGetLastError());
@@ -1268,8 +1395,10 @@ int partial_rows(const Problem& P) {
   return P.fused ? P.fused_clusters : P.vshards * P.col_splits;
 }
 
+int64_t merge_blocks(const Problem& P) { return (P.m + kEThreads - 1) / kEThreads; }
+
 static void launch_merge(Problem& P, bool merge, bool flag) {
-  const int64_t blocks = (P.m + kEThreads - 1) / kEThreads;
+  const int64_t blocks = merge_blocks(P);
   const int shards = P.fused ? 1 : P.vshards;
   const int splits = P.fused ? P.fused_clusters : P.col_splits;
   k_merge<<<blocks, kEThreads, 0, P.stream>>>(P.part, shards, splits, P.m, P.mpad, P.col,
@@ -1313,7 +1442,7 @@ void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
     // local merge, then one all-reduce of the m column sums + <u, a>; the
     // underflow test needs the global sums, so flagging follows the reduce
     launch_merge(P, true, false);
-    comm_allreduce_sum(P, P.col, static_cast<size_t>(P.mpad + 1));
+    comm_allreduce_sum(P, P.col, static_cast<size_t>(P.mpad + 1 + merge_blocks(P)));
     if (with_log) launch_merge(P, false, true);
   } else {
     launch_merge(P, true, with_log);
@@ -1342,7 +1471,9 @@ void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
   }
   k_finalize<<<P.e_blocks, kEThreads, 0, P.stream>>>(P.m, P.mpad, P.p, P.b, P.logb, P.col,
                                                      P.col_log, P.flag_idx, P.fb_part, P.fbA,
-                                                     P.fbS, P.sharded, P.y, P.grad, P.e1_part,
+                                                     P.fbS, P.sharded,
+                                                     static_cast<int>(merge_blocks(P)), P.y,
+                                                     P.grad, P.e1_part,
                                                      P.trace, P.bounds, P.ctrl);
   OTG_CUDA(cudaGetLastError());
 }

@@ -419,6 +419,7 @@ class SolveResult:  # sinkhorn.hpp:44-54
     col_pass_seconds: float = 0.0
     kernel_launches: int = 0
     row_redos: int = 0
+    epilogue_seconds: float = 0.0
 
 
 @dataclass
@@ -489,7 +490,8 @@ class _Res:
         return SolveResult(DualPotentials(self.u, self.v), bool(r.converged), r.iterations,
                            r.evaluations, r.outer_stages, r.final_violation, r.final_reduced_f,
                            r.max_v_inf, tr, r.device_seconds, r.row_pass_seconds,
-                           r.col_pass_seconds, r.kernel_launches, r.row_redos)
+                           r.col_pass_seconds, r.kernel_launches, r.row_redos,
+                           r.epilogue_seconds)
 
 
 def _trace_cap(max_iters, stride):

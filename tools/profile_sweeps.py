@@ -10,7 +10,7 @@ m = 65536
 x, y = ot.gen_config(3, rows, m, 3)
 p = ot.TransportProblem.from_points(np.full(rows, 1.0 / rows), np.full(m, 1.0 / m), x, y, 1e-3)
 r = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=3))
-ms, by = ot.time_sweeps(p, r.potentials.v, reps=3)
+ms, by = ot.time_sweeps(p, r.potentials.v, reps=6)
 info = p.handle.info
 print("rows", rows, "mode", info.sweep_mode, "clusters", info.sweep_clusters, "splits",
       info.col_splits, "ms", [round(x, 4) for x in ms], "GB/s pass1",
