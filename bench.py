@@ -66,7 +66,7 @@ class ClockSampler:
                ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4),
                ("hw_power_brake_slowdown", 0x80))
 
-    def __init__(self, index=0, period_s=0.01):
+    def __init__(self, index=0, period_s=0.002):
         self.index = index
         self.period = period_s
         self.samples = []  # (sm_mhz, max_mhz, reasons_mask)
@@ -84,6 +84,8 @@ class ClockSampler:
             self._nv = None
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        while self._nv is not None and not self.samples and self._t.is_alive():
+            time.sleep(0.0005)  # first sample taken before the timed region starts
         return self
 
     def _run(self):
@@ -312,11 +314,12 @@ def main():
     ttt = None
     if not args.no_tol:
         barrier()
-        rt = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=TOL, max_total_inner=args.max_tol_iters))
-        barrier()
+        with ClockSampler(local_rank, period_s=0.02) as clk_tol:
+            rt = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=TOL, max_total_inner=args.max_tol_iters))
+            barrier()
         ttt = {"seconds": max_over_ranks(rt.device_seconds), "iterations": rt.iterations,
                "converged": bool(rt.converged), "final_violation": rt.final_violation,
-               "tol_l1": TOL}
+               "tol_l1": TOL, "clocks": clk_tol.summary()}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

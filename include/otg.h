@@ -184,6 +184,9 @@ typedef struct {
                             the shift estimate was loose (diagnostic)       */
   double epilogue_seconds; /* summed merge + fallback + finalize + apply
                               times (time_sweeps)                           */
+  int64_t fallback_columns; /* columns whose mass underflowed and took the
+                               exact log-sum-exp (dual.cpp:54-69), summed
+                               over the evaluations (diagnostic)            */
 } otg_solve_result;
 
 /* plan_from_potentials + marginal_violation_l1 + primal_cost

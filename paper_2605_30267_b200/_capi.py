@@ -63,7 +63,7 @@ class SolveResultC(C.Structure):
                 ("time_sweeps", C.c_int), ("device_seconds", C.c_double),
                 ("row_pass_seconds", C.c_double), ("col_pass_seconds", C.c_double),
                 ("kernel_launches", C.c_int64), ("row_redos", C.c_int64),
-                ("epilogue_seconds", C.c_double)]
+                ("epilogue_seconds", C.c_double), ("fallback_columns", C.c_int64)]
 
 
 class PlanSummaryC(C.Structure):

@@ -97,11 +97,13 @@ struct Ctrl {
   long long cond_checked, cond_held;
   long long live_kernels;
   unsigned int e1_counter, e2_counter, fb_count, redo_count;
+  unsigned int bar_count, bar_gen;  // software grid barrier of k_epilogue
   // fp32 row pass: shift estimate from the previous evaluation (sweep.cu)
   int shift_valid;    // rowM2 / vq describe the previous point, dmax2 the step
   int pad1;
   double dmax2;       // max_j (p_new - p_old)_j * log2(e)
   long long redo_total;  // rows redone exactly over the solve (diagnostic)
+  long long fb_total;    // columns that took the exact LSE fallback (diagnostic)
   // --- configuration (host-written) ---
   int mode;
   int record_trace;
@@ -121,6 +123,7 @@ struct Ctrl {
 };
 
 constexpr int kTraceCols = OTG_TRACE_COLS;
+constexpr int kEpiMaxGrid = 296;  // CTAs of the single-kernel epilogue, at most
 
 // ---------------------------------------------------------------- problem --
 struct Shard {
@@ -179,6 +182,8 @@ struct Problem {
   // column-pass partials
   int col_splits = 1;
   int col_threads = 128;  // fp32 column pass CTA width (4 columns per thread)
+  int epi_grid = 0;       // single-kernel epilogue CTAs (0 = unset, -1 = unavailable)
+  int apply_pending = 0;  // launch_eval left the vector update to launch_apply
   int64_t rows_per_split = 0;
   double* part = nullptr;  // (vshards * col_splits) x mpad
 
@@ -186,6 +191,7 @@ struct Problem {
   int e_blocks = 1;
   double* e1_part = nullptr;  // e_blocks x 8
   double* e2_part = nullptr;  // e_blocks x 8
+  double* epi_part = nullptr; // single-kernel epilogue: 2 x kEpiMaxGrid x 8
   Ctrl* ctrl = nullptr;
   Ctrl* ctrl_host = nullptr;  // pinned mirror
   double* trace = nullptr;    // ring: trace_cap x kTraceCols

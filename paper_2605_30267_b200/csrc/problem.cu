@@ -144,7 +144,7 @@ void problem_free(Problem& P) {
                   P.col_log,
                   P.y, P.grad, P.prev_grad,
                   P.prev_x, P.prev_y, P.flag_idx, P.fb_cols, P.fb_part, P.part, P.e1_part,
-                  P.e2_part, P.ctrl, P.trace, P.bounds, P.fbA, P.fbS, P.fbT};
+                  P.e2_part, P.epi_part, P.ctrl, P.trace, P.bounds, P.fbA, P.fbS, P.fbT};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (P.ctrl_host) cudaFreeHost(P.ctrl_host);
@@ -172,7 +172,7 @@ void problem_alloc_state(Problem& P) {
   P.vq = dalloc<float>(P, 2 * mp);
   P.p = dalloc<double>(P, mp);
   P.wacc = dalloc<double>(P, mp);
-  P.col = dalloc<double>(P, mp + 8 + (P.m + 255) / 256);  // + <u, a> slices (k_merge)
+  P.col = dalloc<double>(P, mp + 8 + std::max<int64_t>((P.m + 255) / 256, kEpiMaxGrid));  // + <u, a> slices
   P.col_log = dalloc<double>(P, mp);
   P.y = dalloc<double>(P, mp);
   P.grad = dalloc<double>(P, mp);
@@ -192,6 +192,7 @@ void problem_alloc_state(Problem& P) {
   P.part = dalloc<double>(P, prow * mp);
   P.e1_part = dalloc<double>(P, P.e_blocks * 8 + row_blocks(P) + 8);
   P.e2_part = dalloc<double>(P, P.e_blocks * 8);
+  P.epi_part = dalloc<double>(P, 2 * kEpiMaxGrid * 8);
   P.ctrl = dalloc<Ctrl>(P, 1);
   P.trace = dalloc<double>(P, kTraceCap * kTraceCols);
   P.bounds = dalloc<double>(P, kBoundaryCap * 4);

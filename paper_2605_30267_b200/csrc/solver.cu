@@ -203,6 +203,7 @@ void fill_result(Problem& P, otg_solve_result* res, const LoopOut& lo) {
   res->epilogue_seconds = lo.epi_s;
   res->kernel_launches = lo.launches;
   res->row_redos = c.redo_total;
+  res->fallback_columns = c.fb_total;
   d2h(P, res->u, P.u, P.n_local);
   d2h(P, res->v, P.p, P.m);
   d2h(P, res->w, P.wacc, P.m);

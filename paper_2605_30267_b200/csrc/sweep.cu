@@ -50,6 +50,7 @@ constexpr int kColUnroll = 8;
 constexpr int kAuxTile = 256;
 constexpr int kEThreads = 256;
 constexpr int kFbChunks = 32;
+constexpr int kFbUnroll = 8;
 constexpr int kFlushRows = 16;
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -378,6 +379,14 @@ k_row_redo(const CostSrc src, int64_t m, const double* __restrict__ p,
 // [-kRedoLo, kRedoHi] (the argmax moved to a column whose potential moved
 // much more) are listed for an exact redo (k_row_redo).  The kernel tracks the
 // new argmax for the next evaluation.
+__device__ __forceinline__ void quad_exponents(const float4& c, float2 V01, float2 V23, float2 F01,
+                                               float2 F23, float2 nSc2, float2 nkh2, float2 nkl2,
+                                               float2& t01, float2& t23) {
+  const float2 c01 = make_float2(c.x, c.y), c23 = make_float2(c.z, c.w);
+  t01 = __fadd2_rn(__ffma2_rn(c01, nkh2, __fadd2_rn(V01, nSc2)), __ffma2_rn(c01, nkl2, F01));
+  t23 = __fadd2_rn(__ffma2_rn(c23, nkh2, __fadd2_rn(V23, nSc2)), __ffma2_rn(c23, nkl2, F23));
+}
+
 constexpr float kRedoLo = 2.0f;
 constexpr float kRedoHi = 6.0f;
 
@@ -388,14 +397,16 @@ __device__ __forceinline__ void row_shift_block(
     const double* __restrict__ loga, double* __restrict__ rowM, double* __restrict__ rowS,
     double* __restrict__ u, double* __restrict__ wrow, float4* __restrict__ aux,
     double* __restrict__ rowM2, int* __restrict__ rowJ, int* __restrict__ redo_rows,
-    Ctrl* __restrict__ ctrl) {
+    Ctrl* __restrict__ ctrl, int64_t r0, const double* __restrict__ p, double kappa) {
+  // redo_rows == nullptr: rows whose estimate failed are redone here, exactly,
+  // by the whole CTA (the single-pass sweep, whose column step follows at once)
   __shared__ double sh[kRowThreads / 32];
   __shared__ float shf[kRowThreads / 32];
   __shared__ int shj[kRowThreads / 32];
   __shared__ float sSc[R], resT[R];
   __shared__ double resS[R];
   __shared__ int resJ[R];
-  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * R;
+  __shared__ int bad[R];
   if (threadIdx.x < R) {
     const int64_t i = r0 + threadIdx.x < n ? r0 + threadIdx.x : n - 1;
     const double M2 = rowM2[i];
@@ -403,21 +414,30 @@ __device__ __forceinline__ void row_shift_block(
     sSc[threadIdx.x] = static_cast<float>(ceil(fmin(lo + 1.0, hi) * 256.0) * (1.0 / 256.0));
   }
   __syncthreads();
-  float Sc[R], tm[R], fs[R];
-  int tj[R];
+  // Inner loop on packed f32x2 arithmetic (FADD2 / FFMA2): the exponents are
+  // bitwise those of the scalar form  t = fmaf(-c, kh, V - Sc) + fmaf(-c, kl, F)
+  // at half the FP32 issue slots.  The argmax is tracked per thread as the
+  // quad index only (one compare + select per quad); the column inside the
+  // winning quad is resolved once at the end.
+  float Sc[R], tm[R];
+  int tq[R];       // column code of the running max: 4q (quad) or j (ragged tail)
+  float2 fs2[R];   // fp32 partial sums, flushed to fp64 every 16 columns
+  float2 nSc2[R];
   double ss[R];
   int64_t rr[R];
   float4 xr[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     Sc[r] = sSc[r];
+    nSc2[r] = make_float2(-Sc[r], -Sc[r]);
     tm[r] = -FLT_MAX;
-    tj[r] = 0;
-    fs[r] = 0.f;
+    tq[r] = 0;
+    fs2[r] = make_float2(0.f, 0.f);
     ss[r] = 0.0;
     rr[r] = r0 + r < n ? r0 + r : n - 1;
     xr[r] = OTF ? src.X[rr[r]] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  const float2 nkh2 = make_float2(-kh, -kh), nkl2 = make_float2(-kl, -kl);
   const int64_t nq = m >> 2;
   const float4* Vq = reinterpret_cast<const float4*>(vq);
   const float4* Fq = reinterpret_cast<const float4*>(vq + mpad);
@@ -443,25 +463,25 @@ __device__ __forceinline__ void row_shift_block(
           prefetch_l2(reinterpret_cast<const float4*>(src.C + rr[r] * src.ldc) + qp);
       }
     }
+    const float2 V01 = make_float2(V.x, V.y), V23 = make_float2(V.z, V.w);
+    const float2 F01 = make_float2(F.x, F.y), F23 = make_float2(F.z, F.w);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const float t0 = fmaf(-c[r].x, kh, V.x - Sc[r]) + fmaf(-c[r].x, kl, F.x);
-      const float t1 = fmaf(-c[r].y, kh, V.y - Sc[r]) + fmaf(-c[r].y, kl, F.y);
-      const float t2 = fmaf(-c[r].z, kh, V.z - Sc[r]) + fmaf(-c[r].z, kl, F.z);
-      const float t3 = fmaf(-c[r].w, kh, V.w - Sc[r]) + fmaf(-c[r].w, kl, F.w);
-      const float qm = fmaxf(fmaxf(t0, t1), fmaxf(t2, t3));
-      if (qm > tm[r]) {
-        tm[r] = qm;
-        tj[r] = static_cast<int>(4 * q) + (t0 == qm ? 0 : t1 == qm ? 1 : t2 == qm ? 2 : 3);
-      }
-      fs[r] += (ex2_approx(t0) + ex2_approx(t1)) + (ex2_approx(t2) + ex2_approx(t3));
+      float2 t01, t23;
+      quad_exponents(c[r], V01, V23, F01, F23, nSc2[r], nkh2, nkl2, t01, t23);
+      const float mx = fmaxf(fmaxf(fmaxf(tm[r], t01.x), t01.y), fmaxf(t23.x, t23.y));
+      tq[r] = mx > tm[r] ? static_cast<int>(4 * q) : tq[r];
+      tm[r] = mx;
+      const float2 e = __fadd2_rn(make_float2(ex2_approx(t01.x), ex2_approx(t23.x)),
+                                  make_float2(ex2_approx(t01.y), ex2_approx(t23.y)));
+      fs2[r] = __fadd2_rn(fs2[r], e);
     }
     if (++chunk == 4) {  // fp32 partials flushed into fp64 every 16 elements
       chunk = 0;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        ss[r] += static_cast<double>(fs[r]);
-        fs[r] = 0.f;
+        ss[r] += static_cast<double>(fs2[r].x) + static_cast<double>(fs2[r].y);
+        fs2[r] = make_float2(0.f, 0.f);
       }
     }
   }
@@ -473,16 +493,16 @@ __device__ __forceinline__ void row_shift_block(
       const float t = fmaf(-c, kh, V - Sc[r]) + fmaf(-c, kl, F);
       if (t > tm[r]) {
         tm[r] = t;
-        tj[r] = static_cast<int>(j);
+        tq[r] = static_cast<int>(j);
       }
-      fs[r] += ex2_approx(t);
+      fs2[r].x += ex2_approx(t);
     }
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    ss[r] += static_cast<double>(fs[r]);
+    ss[r] += static_cast<double>(fs2[r].x) + static_cast<double>(fs2[r].y);
     float t = tm[r];
-    int jj = tj[r];
+    int jj = tq[r];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const float t2 = __shfl_xor_sync(0xffffffffu, t, o);
@@ -502,7 +522,7 @@ __device__ __forceinline__ void row_shift_block(
     int J = 0;
 #pragma unroll
     for (int k = 0; k < kRowThreads / 32; ++k)
-      if (shf[k] > T) {
+      if (shf[k] > T || (shf[k] == T && shj[k] < J)) {
         T = shf[k];
         J = shj[k];
       }
@@ -514,13 +534,38 @@ __device__ __forceinline__ void row_shift_block(
     }
   }
   __syncthreads();
+  if (threadIdx.x < R) {  // column of the max inside the winning quad
+    const int r = threadIdx.x;
+    const int code = resJ[r];
+    if (code < 4 * nq) {
+      const int64_t q = code >> 2;
+      const int64_t ir = r0 + r < n ? r0 + r : n - 1;  // (no register-array indexing by r)
+      float4 y4[4];
+      load_y4<OTF>(src, q, y4);
+      const float4 xi = OTF ? src.X[ir] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 cq = cost_quad<OTF>(src, ir, q, xi, y4);
+      const float4 V = __ldg(Vq + q), F = __ldg(Fq + q);
+      const float nsc = -sSc[r];
+      float2 t01, t23;
+      quad_exponents(cq, make_float2(V.x, V.y), make_float2(V.z, V.w), make_float2(F.x, F.y),
+                     make_float2(F.z, F.w), make_float2(nsc, nsc), nkh2, nkl2, t01, t23);
+      const float T = resT[r];
+      resJ[r] = code + (t01.x == T ? 0 : t01.y == T ? 1 : t23.x == T ? 2 : t23.y == T ? 3 : 0);
+    }
+  }
+  __syncthreads();
   if (threadIdx.x < R) {
     const int r = threadIdx.x;
     const int64_t i = r0 + r;
     if (i < n) {
       const float T = resT[r];
+      bad[r] = 0;
       if (!(T >= -kRedoLo && T <= kRedoHi)) {  // estimate too loose (or NaN): exact redo
-        redo_rows[atomicAdd(&ctrl->redo_count, 1u)] = static_cast<int>(i);
+        const unsigned slot = atomicAdd(&ctrl->redo_count, 1u);
+        if (redo_rows)
+          redo_rows[slot] = static_cast<int>(i);
+        else
+          bad[r] = 1;
       } else {
         const double S = resS[r];
         const double sc = static_cast<double>(Sc[r]);
@@ -534,6 +579,20 @@ __device__ __forceinline__ void row_shift_block(
         rowM2[i] = sc + static_cast<double>(T);
         rowJ[i] = resJ[r];
         aux[i] = make_float4(Sc[r], 0.0f, static_cast<float>(wi), 0.0f);
+      }
+    } else {
+      bad[r] = 0;
+    }
+  }
+  if (redo_rows == nullptr) {
+    __syncthreads();
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+      if (bad[r]) {  // uniform over the CTA
+        const int64_t rows[1] = {r0 + r};
+        const bool valid[1] = {true};
+        row_exact_block<1, OTF>(rows, src, m, p, kappa, a, loga, rowM, rowS, u, wrow, aux, rowM2,
+                                rowJ, valid);
       }
     }
   }
@@ -573,7 +632,8 @@ k_row_shift(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ v
             int* __restrict__ rowJ, int* __restrict__ redo_rows, Ctrl* __restrict__ ctrl) {
   if (ctrl->done || !ctrl->shift_valid) return;
   row_shift_block<R, OTF, PF>(src, n, m, vq, dq, mpad, kh, kl, a, loga, rowM, rowS, u, wrow, aux,
-                              rowM2, rowJ, redo_rows, ctrl);
+                              rowM2, rowJ, redo_rows, ctrl, static_cast<int64_t>(blockIdx.x) * R,
+                              nullptr, 0.0);
 }
 
 // ------------------------------------------------------------------ K2 ----
@@ -594,6 +654,31 @@ k_col_precise(const double* __restrict__ C, int64_t ldc, int64_t m,
     for (int64_t i = i0; i < i1; ++i) acc += exp(((-C[i * ldc + j]) + pj) - rowM[i]) * wrow[i];
     part[static_cast<int64_t>(blockIdx.y) * mpad + j] = acc;
   }
+}
+
+// One row of a thread's 4 columns: A = Vc - Mc (exact: both multiples of
+// 2^-8), g = fmaf(-c, kl, vf - mf), t = fmaf(-c, kh, A) + g, acc += w ex2(t).
+__device__ __forceinline__ void col_quad_step(const float4& c, const float4& ax, float2 Vc01,
+                                              float2 Vc23, float2 vf01, float2 vf23, float2 nkh2,
+                                              float2 nkl2, float2& acc01, float2& acc23) {
+  const float2 nM = make_float2(-ax.x, -ax.x), nm = make_float2(-ax.y, -ax.y);
+  const float2 w2 = make_float2(ax.z, ax.z);
+  const float2 c01 = make_float2(c.x, c.y), c23 = make_float2(c.z, c.w);
+  const float2 t01 = __fadd2_rn(__ffma2_rn(c01, nkh2, __fadd2_rn(Vc01, nM)),
+                                __ffma2_rn(c01, nkl2, __fadd2_rn(vf01, nm)));
+  const float2 t23 = __fadd2_rn(__ffma2_rn(c23, nkh2, __fadd2_rn(Vc23, nM)),
+                                __ffma2_rn(c23, nkl2, __fadd2_rn(vf23, nm)));
+  acc01 = __ffma2_rn(w2, make_float2(ex2_approx(t01.x), ex2_approx(t01.y)), acc01);
+  acc23 = __ffma2_rn(w2, make_float2(ex2_approx(t23.x), ex2_approx(t23.y)), acc23);
+}
+
+__device__ __forceinline__ void flush_acc(float2& acc01, float2& acc23, double* acc64) {
+  acc64[0] += static_cast<double>(acc01.x);
+  acc64[1] += static_cast<double>(acc01.y);
+  acc64[2] += static_cast<double>(acc23.x);
+  acc64[3] += static_cast<double>(acc23.y);
+  acc01 = make_float2(0.f, 0.f);
+  acc23 = make_float2(0.f, 0.f);
 }
 
 // fp32: thread owns 4 consecutive columns, loops over the split's rows.  The
@@ -620,7 +705,12 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
     split_q(pj * kLog2e, Vc[k], vf[k]);
     if (OTF) y4[k] = src.Y[(j0 + k < m) ? j0 + k : 0];
   }
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  // packed f32x2 form of  acc += w * ex2((Vc - Mc) - c kh + ((vf - mf) - c kl)):
+  // bitwise the scalar expression, half the FP32 issue slots
+  const float2 Vc01 = make_float2(Vc[0], Vc[1]), Vc23 = make_float2(Vc[2], Vc[3]);
+  const float2 vf01 = make_float2(vf[0], vf[1]), vf23 = make_float2(vf[2], vf[3]);
+  const float2 nkh2 = make_float2(-kh, -kh), nkl2 = make_float2(-kl, -kl);
+  float2 acc01 = make_float2(0.f, 0.f), acc23 = make_float2(0.f, 0.f);
   double acc64[4] = {0.0, 0.0, 0.0, 0.0};
   const bool active = j0 < m;
   for (int64_t t0 = i0; t0 < i1; t0 += kAuxTile) {
@@ -639,42 +729,15 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
       for (int r = 0; r < kColUnroll; ++r)
         c[r] = cost_quad<OTF>(src, t0 + k + r, q, OTF ? sh_x[k + r] : y4[0], y4);
 #pragma unroll
-      for (int r = 0; r < kColUnroll; ++r) {
-        const float4 ax = sh_aux[k + r];
-        const float cc[4] = {c[r].x, c[r].y, c[r].z, c[r].w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float A = Vc[e] - ax.x;  // exact: both multiples of 2^-8
-          const float g = fmaf(-cc[e], kl, vf[e] - ax.y);
-          const float t = fmaf(-cc[e], kh, A) + g;
-          acc[e] = fmaf(ax.z, ex2_approx(t), acc[e]);
-        }
-      }
-      if (((k + kColUnroll) % kFlushRows) == 0) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          acc64[e] += static_cast<double>(acc[e]);
-          acc[e] = 0.f;
-        }
-      }
+      for (int r = 0; r < kColUnroll; ++r) col_quad_step(c[r], sh_aux[k + r], Vc01, Vc23, vf01,
+                                                          vf23, nkh2, nkl2, acc01, acc23);
+      if (((k + kColUnroll) % kFlushRows) == 0) flush_acc(acc01, acc23, acc64);
     }
     for (; k < tn; ++k) {
       const float4 cv = cost_quad<OTF>(src, t0 + k, q, OTF ? sh_x[k] : y4[0], y4);
-      const float4 ax = sh_aux[k];
-      const float cc[4] = {cv.x, cv.y, cv.z, cv.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float A = Vc[e] - ax.x;
-        const float g = fmaf(-cc[e], kl, vf[e] - ax.y);
-        const float t = fmaf(-cc[e], kh, A) + g;
-        acc[e] = fmaf(ax.z, ex2_approx(t), acc[e]);
-      }
+      col_quad_step(cv, sh_aux[k], Vc01, Vc23, vf01, vf23, nkh2, nkl2, acc01, acc23);
     }
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      acc64[e] += static_cast<double>(acc[e]);
-      acc[e] = 0.f;
-    }
+    flush_acc(acc01, acc23, acc64);
   }
   if (active) {
     double* dst = part + static_cast<int64_t>(blockIdx.y) * mpad + j0;
@@ -686,8 +749,52 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
 // ----------------------------------------------------------------- E1a ----
 // c_j = sum over shards of (sum over the shard's splits of the partials); the
 // inner sum is what one rank holds, the outer sum stands in for the allreduce.
-// CTA k also folds <u, a> over row slice k into col[mpad + 1 + k] (the
-// sharded all-reduce covers col[0, mpad + 1 + gridDim.x); finalize sums them).
+// Work unit `blk` of `nblk` also folds <u, a> over row slice blk into
+// col[mpad + 1 + blk] (the sharded all-reduce covers col[0, mpad + 1 + nblk);
+// finalize sums them).
+__device__ __forceinline__ void merge_body(const double* __restrict__ part, int nshards, int splits,
+                                           int64_t m, int64_t mpad, double* __restrict__ col,
+                                           double* __restrict__ col_log,
+                                           int* __restrict__ flag_idx, int* __restrict__ fb_cols,
+                                           const double* __restrict__ u,
+                                           const double* __restrict__ a, int64_t nrows,
+                                           int do_merge, int flag, Ctrl* __restrict__ ctrl,
+                                           int blk, int nblk, double* sh) {
+  if (do_merge) {  // <u, a> over the local rows (for f)
+    const int64_t r0 = nrows * blk / nblk, r1 = nrows * (blk + 1) / nblk;
+    double t = 0.0;
+    for (int64_t k = r0 + threadIdx.x; k < r1; k += kEThreads) t += u[k] * a[k];
+    t = block_sum<kEThreads>(t, sh);
+    if (threadIdx.x == 0) col[mpad + 1 + blk] = t;
+  }
+  const double tiny = ctrl->tiny;
+  for (int64_t j = static_cast<int64_t>(blk) * kEThreads + threadIdx.x; j < m;
+       j += static_cast<int64_t>(nblk) * kEThreads) {
+    double c = 0.0;
+    if (do_merge) {
+      for (int s = 0; s < nshards; ++s) {
+        double loc = 0.0;
+        for (int k = 0; k < splits; ++k)
+          loc += part[(static_cast<int64_t>(s) * splits + k) * mpad + j];
+        c += loc;
+      }
+      col[j] = c;
+    } else {
+      c = col[j];  // already merged (and all-reduced across ranks)
+    }
+    if (flag) {
+      if (c >= tiny) {
+        col_log[j] = log(c);
+        flag_idx[j] = -1;
+      } else {
+        const unsigned slot = atomicAdd(&ctrl->fb_count, 1u);
+        fb_cols[slot] = static_cast<int>(j);
+        flag_idx[j] = static_cast<int>(slot);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kEThreads)
 k_merge(const double* __restrict__ part, int nshards, int splits, int64_t m, int64_t mpad,
         double* __restrict__ col, double* __restrict__ col_log, int* __restrict__ flag_idx,
@@ -695,41 +802,64 @@ k_merge(const double* __restrict__ part, int nshards, int splits, int64_t m, int
         int64_t nrows, int do_merge, int flag, Ctrl* __restrict__ ctrl) {
   if (ctrl->done) return;
   __shared__ double sh[kEThreads / 32];
-  if (do_merge) {  // <u, a> over the local rows: CTA k folds row slice k (for f)
-    const int64_t r0 = nrows * blockIdx.x / gridDim.x, r1 = nrows * (blockIdx.x + 1) / gridDim.x;
-    double t = 0.0;
-    for (int64_t k = r0 + threadIdx.x; k < r1; k += kEThreads) t += u[k] * a[k];
-    t = block_sum<kEThreads>(t, sh);
-    if (threadIdx.x == 0) col[mpad + 1 + blockIdx.x] = t;
-  }
-  const int64_t j = static_cast<int64_t>(blockIdx.x) * kEThreads + threadIdx.x;
-  if (j >= m) return;
-  double c = 0.0;
-  if (do_merge) {
-    for (int s = 0; s < nshards; ++s) {
-      double loc = 0.0;
-      for (int k = 0; k < splits; ++k) loc += part[(static_cast<int64_t>(s) * splits + k) * mpad + j];
-      c += loc;
-    }
-    col[j] = c;
-  } else {
-    c = col[j];  // already merged (and all-reduced across ranks)
-  }
-  if (flag) {
-    if (c >= ctrl->tiny) {
-      col_log[j] = log(c);
-      flag_idx[j] = -1;
-    } else {
-      const unsigned slot = atomicAdd(&ctrl->fb_count, 1u);
-      fb_cols[slot] = static_cast<int>(j);
-      flag_idx[j] = static_cast<int>(slot);
-    }
-  }
+  merge_body(part, nshards, splits, m, mpad, col, col_log, flag_idx, fb_cols, u, a, nrows,
+             do_merge, flag, ctrl, blockIdx.x, gridDim.x, sh);
 }
 
 // ------------------------------------------------------------------ K5 ----
 // Exact column log-sum-exp (dual.cpp:54-69) for flagged columns, split over
 // row chunks: fb_part[f][chunk] = (max_i t_ij, sum_i exp(t_ij - max)).
+// One pass per work item: every thread gathers kFbUnroll exponents with all
+// loads in flight (the column is strided in memory, so the item is latency-
+// bound, not bandwidth-bound), keeps an online (max, sum) and the CTA merges
+// the per-thread pairs.  Same value as the two-pass LSE up to rounding.
+template <bool PRECISE, bool OTF>
+__device__ __forceinline__ void fallback_body(const double* __restrict__ C64, const CostSrc& src,
+                                              int64_t ldc, int64_t n, double kappa,
+                                              const double* __restrict__ u,
+                                              const double* __restrict__ p,
+                                              const int* __restrict__ fb_cols,
+                                              double2* __restrict__ fb_part, unsigned nf, int blk,
+                                              int nblk, double* sh) {
+  const int64_t rpc = (n + kFbChunks - 1) / kFbChunks;
+  const int64_t items = static_cast<int64_t>(nf) * kFbChunks;
+  for (int64_t it = blk; it < items; it += nblk) {
+    const int64_t f = it / kFbChunks, ch = it % kFbChunks;
+    const int64_t j = fb_cols[f];
+    const double vj = p[j];
+    const int64_t i0 = ch * rpc, i1 = min(n, i0 + rpc);
+    double top = -INFINITY, sum = 0.0;
+    for (int64_t base = i0 + threadIdx.x; base < i1; base += kEThreads * kFbUnroll) {
+      double t[kFbUnroll];
+#pragma unroll
+      for (int k = 0; k < kFbUnroll; ++k) {
+        const int64_t i = base + static_cast<int64_t>(k) * kEThreads;
+        if (i < i1) {
+          t[k] = PRECISE ? (u[i] + vj) - C64[i * ldc + j]
+                         : fma(-static_cast<double>(cost_one<OTF>(src, i, j)), kappa, u[i] + vj);
+        } else {
+          t[k] = -INFINITY;
+        }
+      }
+      double mx = t[0];
+#pragma unroll
+      for (int k = 1; k < kFbUnroll; ++k) mx = fmax(mx, t[k]);
+      if (mx > -INFINITY) {
+        if (mx > top) {
+          sum = (top > -INFINITY) ? sum * exp(top - mx) : 0.0;
+          top = mx;
+        }
+#pragma unroll
+        for (int k = 0; k < kFbUnroll; ++k) sum += exp(t[k] - top);
+      }
+    }
+    const double T = block_max<kEThreads>(top, sh);
+    const double part = (top > -INFINITY) ? sum * exp(top - T) : 0.0;
+    const double S = block_sum<kEThreads>(part, sh);
+    if (threadIdx.x == 0) fb_part[f * kFbChunks + ch] = make_double2(T, S);
+  }
+}
+
 template <bool PRECISE, bool OTF>
 __global__ void __launch_bounds__(kEThreads)
 k_fallback(const double* __restrict__ C64, const CostSrc src, int64_t ldc, int64_t n,
@@ -740,30 +870,8 @@ k_fallback(const double* __restrict__ C64, const CostSrc src, int64_t ldc, int64
   const unsigned nf = ctrl->fb_count;
   if (nf == 0) return;
   __shared__ double sh[kEThreads / 32];
-  const int64_t rpc = (n + kFbChunks - 1) / kFbChunks;
-  const int64_t items = static_cast<int64_t>(nf) * kFbChunks;
-  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-    const int64_t f = it / kFbChunks, ch = it % kFbChunks;
-    const int64_t j = fb_cols[f];
-    const double vj = p[j];
-    const int64_t i0 = ch * rpc, i1 = min(n, i0 + rpc);
-    double top = -INFINITY;
-    for (int64_t i = i0 + threadIdx.x; i < i1; i += kEThreads) {
-      const double t = PRECISE ? (u[i] + vj) - C64[i * ldc + j]
-                               : fma(-static_cast<double>(cost_one<OTF>(src, i, j)), kappa, u[i] + vj);
-      top = fmax(top, t);
-    }
-    top = block_max<kEThreads>(top, sh);
-    double s = 0.0;
-    if (top > -INFINITY)
-      for (int64_t i = i0 + threadIdx.x; i < i1; i += kEThreads) {
-        const double t = PRECISE ? (u[i] + vj) - C64[i * ldc + j]
-                                 : fma(-static_cast<double>(cost_one<OTF>(src, i, j)), kappa, u[i] + vj);
-        s += exp(t - top);
-      }
-    s = block_sum<kEThreads>(s, sh);
-    if (threadIdx.x == 0) fb_part[f * kFbChunks + ch] = make_double2(top, s);
-  }
+  fallback_body<PRECISE, OTF>(C64, src, ldc, n, kappa, u, p, fb_cols, fb_part, nf, blockIdx.x,
+                              gridDim.x, sh);
 }
 
 // Sharded fallback: this rank's (top, sum) of each flagged column over its
@@ -946,52 +1054,63 @@ __device__ void control_step(Ctrl* C, double* trace, double* bounds, double gl, 
 }
 
 // ----------------------------------------------------------------- E1b ----
-__global__ void __launch_bounds__(kEThreads)
-k_finalize(int64_t m, int64_t mpad, const double* __restrict__ p, const double* __restrict__ b,
-           const double* __restrict__ logb, double* __restrict__ col,
-           double* __restrict__ col_log, const int* __restrict__ flag_idx,
-           const double2* __restrict__ fb_part, const double* __restrict__ fbA,
-           const double* __restrict__ fbS, int sharded, int ua_slices, double* __restrict__ y,
-           double* __restrict__ grad, double* __restrict__ e1_part, double* __restrict__ trace,
-           double* __restrict__ bounds, Ctrl* __restrict__ ctrl) {
-  if (ctrl->done) return;
-  __shared__ double sh[kEThreads / 32];
-  __shared__ bool last;
+struct FinArgs {
+  int64_t m, mpad;
+  const double* p;
+  const double* b;
+  const double* logb;
+  double* col;
+  double* col_log;
+  const int* flag_idx;
+  const double2* fb_part;
+  const double* fbA;
+  const double* fbS;
+  int sharded;
+  int ua_slices;
+  double* y;
+  double* grad;
+  double* e1_part;
+  double* trace;
+  double* bounds;
+};
+
+// Per-column finalize of work unit blk of nblk; its partials -> e1_part[blk].
+__device__ __forceinline__ void finalize_cols(const FinArgs& A, int blk, int nblk, double* sh) {
   double s_abs = 0.0, s_y = 0.0, s_pb = 0.0, mx_p = 0.0, bad = 0.0;
-  for (int64_t j = static_cast<int64_t>(blockIdx.x) * kEThreads + threadIdx.x; j < m;
-       j += static_cast<int64_t>(gridDim.x) * kEThreads) {
-    double c = col[j], cl;
-    const int slot = flag_idx[j];
+  for (int64_t j = static_cast<int64_t>(blk) * kEThreads + threadIdx.x; j < A.m;
+       j += static_cast<int64_t>(nblk) * kEThreads) {
+    double c = A.col[j], cl;
+    const int slot = A.flag_idx[j];
     if (slot >= 0) {
       double top, s;
-      if (sharded) {  // combined across ranks (k_fb_local / k_fb_rescale + all-reduces)
-        top = fbA[j];
-        s = fbS[j];
+      if (A.sharded) {  // combined across ranks (k_fb_local / k_fb_rescale + all-reduces)
+        top = A.fbA[j];
+        s = A.fbS[j];
       } else {
         top = -INFINITY;
-        for (int k = 0; k < kFbChunks; ++k) top = fmax(top, fb_part[slot * kFbChunks + k].x);
+        for (int k = 0; k < kFbChunks; ++k) top = fmax(top, A.fb_part[slot * kFbChunks + k].x);
         s = 0.0;
         for (int k = 0; k < kFbChunks; ++k) {
-          const double2 fp = fb_part[slot * kFbChunks + k];
+          const double2 fp = A.fb_part[slot * kFbChunks + k];
           if (fp.y > 0.0) s += fp.y * exp(fp.x - top);
         }
       }
       cl = top + log(s);
       c = exp(cl);
-      col[j] = c;
-      col_log[j] = cl;
+      A.col[j] = c;
+      A.col_log[j] = cl;
     } else {
-      cl = col_log[j];
+      cl = A.col_log[j];
     }
     if (!isfinite(cl)) bad = 1.0;
-    const double g = c - b[j];
-    grad[j] = g;
-    const double pj = p[j];
-    const double yj = pj + (logb[j] - cl);
-    y[j] = yj;
+    const double g = c - A.b[j];
+    A.grad[j] = g;
+    const double pj = A.p[j];
+    const double yj = pj + (A.logb[j] - cl);
+    A.y[j] = yj;
     s_abs += fabs(g);
     s_y += yj;
-    s_pb += pj * b[j];
+    s_pb += pj * A.b[j];
     mx_p = fmax(mx_p, fabs(pj));
   }
   s_abs = block_sum<kEThreads>(s_abs, sh);
@@ -1000,23 +1119,22 @@ k_finalize(int64_t m, int64_t mpad, const double* __restrict__ p, const double* 
   mx_p = block_max<kEThreads>(mx_p, sh);
   bad = block_max<kEThreads>(bad, sh);
   if (threadIdx.x == 0) {
-    double* dst = e1_part + blockIdx.x * 8;
+    double* dst = A.e1_part + blk * 8;
     dst[0] = s_abs;
     dst[1] = s_y;
     dst[2] = s_pb;
     dst[3] = mx_p;
     dst[4] = bad;
-    __threadfence();
-    const unsigned prev = atomicAdd(&ctrl->e1_counter, 1u);
-    last = prev == gridDim.x - 1;
   }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  // the last CTA folds the per-CTA partials with all its threads (fixed order)
+}
+
+// One CTA folds the nparts partials (all threads, fixed order) and its thread
+// 0 runs the solver's scalar control flow.
+__device__ __forceinline__ void finalize_tail(const FinArgs& A, int nparts, double* sh,
+                                              Ctrl* __restrict__ ctrl) {
   double gl = 0.0, sy = 0.0, pb = 0.0, mp = 0.0, bd = 0.0;
-  for (unsigned k = threadIdx.x; k < gridDim.x; k += kEThreads) {
-    const volatile double* src = e1_part + k * 8;
+  for (int k = threadIdx.x; k < nparts; k += kEThreads) {
+    const volatile double* src = A.e1_part + k * 8;
     gl += src[0];
     sy += src[1];
     pb += src[2];
@@ -1028,17 +1146,18 @@ k_finalize(int64_t m, int64_t mpad, const double* __restrict__ p, const double* 
   pb = block_sum<kEThreads>(pb, sh);
   mp = block_max<kEThreads>(mp, sh);
   bd = block_max<kEThreads>(bd, sh);
-  double ua = 0.0;  // <u, a> partials of the merge CTAs (col[mpad + 1 + k])
-  for (int k = threadIdx.x; k < ua_slices; k += kEThreads) ua += col[mpad + 1 + k];
+  double ua = 0.0;  // <u, a> partials of the merge work units (col[mpad + 1 + k])
+  for (int k = threadIdx.x; k < A.ua_slices; k += kEThreads) ua += A.col[A.mpad + 1 + k];
   ua = block_sum<kEThreads>(ua, sh);
   if (threadIdx.x != 0) return;
   Ctrl* C = ctrl;
   C->e1_counter = 0;
+  C->fb_total += C->fb_count;
   C->fb_count = 0;
   C->redo_total += C->redo_count;
   C->redo_count = 0;
   const double f = (1.0 - ua) - pb;
-  C->mean_y = sy / static_cast<double>(m);
+  C->mean_y = sy / static_cast<double>(A.m);
   C->max_v_inf = fmax(C->max_v_inf, mp);
   if (bd > 0.0) {  // check_col_log_finite (sinkhorn.cpp:20-25)
     C->error = OTG_E_DOMAIN;
@@ -1046,7 +1165,24 @@ k_finalize(int64_t m, int64_t mpad, const double* __restrict__ p, const double* 
     C->live_e2 = 0;
     return;
   }
-  control_step(C, trace, bounds, gl, f);
+  control_step(C, A.trace, A.bounds, gl, f);
+}
+
+__global__ void __launch_bounds__(kEThreads)
+k_finalize(const FinArgs A, Ctrl* __restrict__ ctrl) {
+  if (ctrl->done) return;
+  __shared__ double sh[kEThreads / 32];
+  __shared__ bool last;
+  finalize_cols(A, blockIdx.x, gridDim.x, sh);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&ctrl->e1_counter, 1u);
+    last = prev == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  finalize_tail(A, gridDim.x, sh, ctrl);
 }
 
 // ------------------------------------------------------------------ E2 ----
@@ -1055,15 +1191,30 @@ __device__ __forceinline__ double expm1_over_z(double z) {  // mirror.cpp:21-24
   return expm1(z) / z;
 }
 
-__global__ void __launch_bounds__(kEThreads)
-k_apply(int64_t m, int64_t mpad, const double* __restrict__ b, double* __restrict__ p,
-        double* __restrict__ wacc, double* __restrict__ y, const double* __restrict__ grad,
-        double* __restrict__ prev_grad, double* __restrict__ prev_x,
-        double* __restrict__ prev_y, float* __restrict__ vq, double* __restrict__ dq, int fast,
-        double* __restrict__ e2_part, double* __restrict__ trace, Ctrl* __restrict__ ctrl) {
-  if (!ctrl->live_e2) return;
-  __shared__ double sh[kEThreads / 32];
-  __shared__ bool last;
+struct AppArgs {
+  int64_t m, mpad;
+  const double* b;
+  double* p;
+  double* wacc;
+  double* y;
+  const double* grad;
+  double* prev_grad;
+  double* prev_x;
+  double* prev_y;
+  float* vq;
+  double* dq;
+  int fast;
+  double* e2_part;
+  double* trace;
+};
+
+// The solver's vector update for work unit blk of nblk (accel.cpp:161-168,
+// 279; stability sums of diag.cpp); partials -> e2_part[blk].  The control
+// fields are read through a volatile view: inside the single-kernel
+// epilogue they were written by another CTA before a grid barrier.
+__device__ __forceinline__ void apply_cols(const AppArgs& A, const Ctrl* ctrl_in, int blk, int nblk,
+                                           double* sh) {
+  const volatile Ctrl* ctrl = ctrl_in;
   const int mode = ctrl->mode;
   const bool done = ctrl->done != 0;
   const double mean = ctrl->mean_y;
@@ -1077,23 +1228,23 @@ k_apply(int64_t m, int64_t mpad, const double* __restrict__ b, double* __restric
   const bool moves = !done && mode != MODE_EVAL;
   double c1 = 0.0, br = 0.0, c2 = 0.0, qq = 0.0, drift = 0.0, ginf = 0.0, dom = 0.0;
   double dstep = -INFINITY;
-  for (int64_t j = static_cast<int64_t>(blockIdx.x) * kEThreads + threadIdx.x; j < m;
-       j += static_cast<int64_t>(gridDim.x) * kEThreads) {
-    const double S = y[j] - mean;  // project_zero_sum (mirror.cpp:103-105)
+  for (int64_t j = static_cast<int64_t>(blk) * kEThreads + threadIdx.x; j < A.m;
+       j += static_cast<int64_t>(nblk) * kEThreads) {
+    const double S = A.y[j] - mean;  // project_zero_sum (mirror.cpp:103-105)
     if (mode == MODE_EVAL) {
-      y[j] = S;
+      A.y[j] = S;
       continue;
     }
-    const double x = p[j];
+    const double x = A.p[j];
     double pn = S;
     if (mode != MODE_SINKHORN) {
-      double w = wacc[j];
+      double w = A.wacc[j];
       if (step) w = (w + (al * al - 2.0) * x + 2.0 * S) / (1.0 + al);  // accel.cpp:168
       if (stab) {
         const double yn = w / al;
-        const double g1 = grad[j];
+        const double g1 = A.grad[j];
         if (have_prev) {
-          const double g0 = prev_grad[j], bj = b[j];
+          const double g0 = A.prev_grad[j], bj = A.b[j];
           ginf = fmax(ginf, fabs(g0));
           const double r0 = g0 / bj, r1 = g1 / bj;
           if (r0 <= -1.0 || r1 <= -1.0) {
@@ -1103,26 +1254,26 @@ k_apply(int64_t m, int64_t mpad, const double* __restrict__ b, double* __restric
             const double D1 = bj * expm1_over_z(log1p(r1));
             c1 += g0 * g0 * D1 / (D0 * D0);
             br += g0 - bj * log1p(r0);
-            const double vk = prev_y[j] - prev_x[j], vk1 = yn - x;
+            const double vk = A.prev_y[j] - A.prev_x[j], vk1 = yn - x;
             c2 += (D1 - D0) * (vk * vk);
             qq += D1 * (vk1 * vk1);
             drift = fmax(drift, fabs(D1 - D0));
           }
         }
-        prev_grad[j] = g1;
-        prev_x[j] = x;
-        prev_y[j] = yn;
+        A.prev_grad[j] = g1;
+        A.prev_x[j] = x;
+        A.prev_y[j] = yn;
       }
       if (resc) w *= an / al;  // accel.cpp:279
-      wacc[j] = w;
+      A.wacc[j] = w;
       pn = (w + S) / (1.0 + an);  // accel.cpp:161
     }
     if (moves) {
-      p[j] = pn;
+      A.p[j] = pn;
       dstep = fmax(dstep, pn - x);
-      if (fast) {
-        split_q(pn * kLog2e, vq[j], vq[mpad + j]);
-        dq[j] = (pn - x) * kLog2e;
+      if (A.fast) {
+        split_q(pn * kLog2e, A.vq[j], A.vq[A.mpad + j]);
+        A.dq[j] = (pn - x) * kLog2e;
       }
     }
   }
@@ -1137,7 +1288,7 @@ k_apply(int64_t m, int64_t mpad, const double* __restrict__ b, double* __restric
   }
   dstep = block_max<kEThreads>(dstep, sh);
   if (threadIdx.x == 0) {
-    double* dst = e2_part + blockIdx.x * 8;
+    double* dst = A.e2_part + blk * 8;
     dst[0] = c1;
     dst[1] = br;
     dst[2] = c2;
@@ -1146,16 +1297,21 @@ k_apply(int64_t m, int64_t mpad, const double* __restrict__ b, double* __restric
     dst[5] = ginf;
     dst[6] = dom;
     dst[7] = dstep;
-    __threadfence();
-    const unsigned prev = atomicAdd(&ctrl->e2_counter, 1u);
-    last = prev == gridDim.x - 1;
   }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
+}
+
+__device__ __forceinline__ void apply_tail(const AppArgs& A, int nparts, double* sh,
+                                           Ctrl* __restrict__ ctrl) {
+  const volatile Ctrl* cv = ctrl;
+  const int mode = cv->mode;
+  const bool done = cv->done != 0;
+  const bool stab = cv->stability != 0 && mode >= MODE_ACC_RUN;
+  const bool have_prev = cv->have_prev != 0;
+  const double al = cv->alpha_step;
+  const bool moves = !done && mode != MODE_EVAL;
   double t[8] = {0, 0, 0, 0, 0, 0, 0, -INFINITY};
-  for (unsigned k = threadIdx.x; k < gridDim.x; k += kEThreads) {
-    const volatile double* src = e2_part + k * 8;
+  for (int k = threadIdx.x; k < nparts; k += kEThreads) {
+    const volatile double* src = A.e2_part + k * 8;
     for (int q = 0; q < 4; ++q) t[q] += src[q];
     for (int q = 4; q < 8; ++q) t[q] = fmax(t[q], src[q]);
   }
@@ -1184,17 +1340,108 @@ k_apply(int64_t m, int64_t mpad, const double* __restrict__ b, double* __restric
       C->cond_held += (cells[0] < cells[1] && cells[2] < cells[3]) ? 1 : 0;
     }
     if (valid && C->trace_row >= 0) {
-      double* r = trace + C->trace_row * kTraceCols;
+      double* r = A.trace + C->trace_row * kTraceCols;
       for (int q = 0; q < 5; ++q) r[7 + q] = cells[q];
     }
   }
   if (stab) C->have_prev = 1;
-  if (moves && fast) {
+  if (moves && A.fast) {
     C->dmax2 = t[7] * kLog2e;
     C->shift_valid = isfinite(t[7]) ? 1 : 0;
   }
   C->e2_counter = 0;
   C->live_e2 = 0;
+}
+
+__global__ void __launch_bounds__(kEThreads)
+k_apply(const AppArgs A, Ctrl* __restrict__ ctrl) {
+  if (!ctrl->live_e2) return;
+  __shared__ double sh[kEThreads / 32];
+  __shared__ bool last;
+  apply_cols(A, ctrl, blockIdx.x, gridDim.x, sh);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&ctrl->e2_counter, 1u);
+    last = prev == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  apply_tail(A, gridDim.x, sh, ctrl);
+}
+
+// ------------------------------------------------------ fused epilogue ----
+// Merge + flag, exact fallback, finalize + control step and the vector update
+// of one evaluation in ONE launch: a cooperative grid (one CTA per SM) with
+// software grid barriers instead of four kernel boundaries.  Opt-in
+// (OTG_EPI_FUSED=1): measured on B200 it is SLOWER than the four launches
+// (256^2: 30 vs 20 us per evaluation; 65536^2: 108 vs 98 us) -- five grid
+// barriers cost more than three graph kernel boundaries.  Unsharded only.
+__device__ __forceinline__ void grid_sync(Ctrl* ctrl) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = &ctrl->bar_gen;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(&ctrl->bar_count, 1u) == gridDim.x - 1) {
+      ctrl->bar_count = 0;
+      __threadfence();
+      atomicAdd(&ctrl->bar_gen, 1u);
+    } else {
+      while (*gen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+struct EpiArgs {
+  const double* part;
+  int nshards, splits;
+  int64_t nrows;
+  int* fb_cols;
+  const double* u;
+  const double* a;
+  const double* C64;
+  CostSrc src;
+  int64_t ldc;
+  double kappa;
+  double2* fb_part;
+  int storage;
+  FinArgs F;
+  AppArgs P;
+};
+
+__global__ void __launch_bounds__(kEThreads)
+k_epilogue(const EpiArgs E, Ctrl* __restrict__ ctrl) {
+  if (ctrl->done) return;  // uniform: written by an earlier launch
+  __shared__ double sh[kEThreads / 32];
+  const int blk = blockIdx.x, nblk = gridDim.x;
+  merge_body(E.part, E.nshards, E.splits, E.F.m, E.F.mpad, E.F.col, E.F.col_log,
+             const_cast<int*>(E.F.flag_idx), E.fb_cols, E.u, E.a, E.nrows, 1, 1, ctrl, blk, nblk,
+             sh);
+  grid_sync(ctrl);
+  const unsigned nf = *static_cast<volatile unsigned*>(&ctrl->fb_count);
+  if (nf > 0) {
+    if (E.storage == OTG_STORE_F64)
+      fallback_body<true, false>(E.C64, E.src, E.ldc, E.nrows, E.kappa, E.u, E.F.p, E.fb_cols,
+                                 E.fb_part, nf, blk, nblk, sh);
+    else if (E.storage == OTG_STORE_ON_THE_FLY)
+      fallback_body<false, true>(E.C64, E.src, E.ldc, E.nrows, E.kappa, E.u, E.F.p, E.fb_cols,
+                                 E.fb_part, nf, blk, nblk, sh);
+    else
+      fallback_body<false, false>(E.C64, E.src, E.ldc, E.nrows, E.kappa, E.u, E.F.p, E.fb_cols,
+                                  E.fb_part, nf, blk, nblk, sh);
+    grid_sync(ctrl);
+  }
+  finalize_cols(E.F, blk, nblk, sh);
+  grid_sync(ctrl);
+  if (blk == 0) finalize_tail(E.F, nblk, sh, ctrl);
+  grid_sync(ctrl);
+  if (!*static_cast<volatile int*>(&ctrl->live_e2)) return;  // uniform after the barrier
+  apply_cols(E.P, ctrl, blk, nblk, sh);
+  grid_sync(ctrl);
+  if (blk == 0) apply_tail(E.P, nblk, sh, ctrl);
 }
 
 int e_grid(int64_t m) {
@@ -1436,8 +1683,106 @@ void launch_sweeps(Problem& P, bool timed, cudaEvent_t* ev4) {
   if (timed) mark(P, ev4[3]);
 }
 
+static FinArgs fin_args(const Problem& P, int64_t ua_slices) {
+  FinArgs A;
+  A.m = P.m;
+  A.mpad = P.mpad;
+  A.p = P.p;
+  A.b = P.b;
+  A.logb = P.logb;
+  A.col = P.col;
+  A.col_log = P.col_log;
+  A.flag_idx = P.flag_idx;
+  A.fb_part = P.fb_part;
+  A.fbA = P.fbA;
+  A.fbS = P.fbS;
+  A.sharded = P.sharded;
+  A.ua_slices = static_cast<int>(ua_slices);
+  A.y = P.y;
+  A.grad = P.grad;
+  A.e1_part = P.e1_part;
+  A.trace = P.trace;
+  A.bounds = P.bounds;
+  return A;
+}
+
+static AppArgs app_args(const Problem& P) {
+  AppArgs A;
+  A.m = P.m;
+  A.mpad = P.mpad;
+  A.b = P.b;
+  A.p = P.p;
+  A.wacc = P.wacc;
+  A.y = P.y;
+  A.grad = P.grad;
+  A.prev_grad = P.prev_grad;
+  A.prev_x = P.prev_x;
+  A.prev_y = P.prev_y;
+  A.vq = P.vq;
+  A.dq = P.dq;
+  A.fast = P.storage != OTG_STORE_F64 && !P.fused;  // fp32 stored or on the fly
+  A.e2_part = P.e2_part;
+  A.trace = P.trace;
+  return A;
+}
+
+// CTAs of the single-kernel epilogue (co-resident: <= one per SM), 0 = off.
+static int epilogue_grid(Problem& P) {
+  static const int env = [] {
+    const char* s = getenv("OTG_EPI_FUSED");
+    return s ? atoi(s) : 0;
+  }();
+  if (!env || P.sharded) return 0;
+  if (P.epi_grid == 0) {
+    int sms = 0, occ = 0;
+    OTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.device));
+    OTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_epilogue, kEThreads, 0));
+    P.epi_grid = occ >= 1 ? std::min(sms, kEpiMaxGrid) : -1;
+  }
+  return std::max(P.epi_grid, 0);
+}
+
+static void launch_epilogue(Problem& P, int grid) {
+  EpiArgs E;
+  E.part = P.part;
+  E.nshards = P.fused ? 1 : P.vshards;
+  E.splits = P.fused ? P.fused_clusters : P.col_splits;
+  E.nrows = P.n_local;
+  E.fb_cols = P.fb_cols;
+  E.u = P.u;
+  E.a = P.a;
+  E.C64 = P.C64;
+  E.src = cost_src(P);
+  E.ldc = P.ldc;
+  E.kappa = P.kappa;
+  E.fb_part = P.fb_part;
+  E.storage = P.storage;
+  E.F = fin_args(P, grid);
+  E.F.e1_part = P.epi_part;
+  E.P = app_args(P);
+  E.P.e2_part = P.epi_part + kEpiMaxGrid * 8;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kEThreads);
+  cfg.stream = P.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  OTG_CUDA(cudaLaunchKernelEx(&cfg, k_epilogue, E, P.ctrl));
+}
+
 void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
+  P.apply_pending = 0;
   launch_sweeps(P, timed, ev4);
+  if (with_log) {
+    const int grid = epilogue_grid(P);
+    if (grid > 0) {
+      launch_epilogue(P, grid);
+      return;
+    }
+  }
   if (P.sharded) {
     // local merge, then one all-reduce of the m column sums + <u, a>; the
     // underflow test needs the global sums, so flagging follows the reduce
@@ -1469,21 +1814,14 @@ void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
     comm_allreduce_sum(P, P.fbS, static_cast<size_t>(P.m));
     OTG_CUDA(cudaGetLastError());
   }
-  k_finalize<<<P.e_blocks, kEThreads, 0, P.stream>>>(P.m, P.mpad, P.p, P.b, P.logb, P.col,
-                                                     P.col_log, P.flag_idx, P.fb_part, P.fbA,
-                                                     P.fbS, P.sharded,
-                                                     static_cast<int>(merge_blocks(P)), P.y,
-                                                     P.grad, P.e1_part,
-                                                     P.trace, P.bounds, P.ctrl);
+  k_finalize<<<P.e_blocks, kEThreads, 0, P.stream>>>(fin_args(P, merge_blocks(P)), P.ctrl);
   OTG_CUDA(cudaGetLastError());
+  P.apply_pending = 1;
 }
 
 void launch_apply(Problem& P) {
-  const int fast = P.storage != OTG_STORE_F64 && !P.fused;  // fp32 stored or on the fly
-  k_apply<<<P.e_blocks, kEThreads, 0, P.stream>>>(P.m, P.mpad, P.b, P.p, P.wacc, P.y, P.grad,
-                                                  P.prev_grad, P.prev_x, P.prev_y, P.vq, P.dq,
-                                                  fast,
-                                                  P.e2_part, P.trace, P.ctrl);
+  if (!P.apply_pending) return;  // done inside the single-kernel epilogue
+  k_apply<<<P.e_blocks, kEThreads, 0, P.stream>>>(app_args(P), P.ctrl);
   OTG_CUDA(cudaGetLastError());
 }
 

@@ -420,6 +420,7 @@ class SolveResult:  # sinkhorn.hpp:44-54
     kernel_launches: int = 0
     row_redos: int = 0
     epilogue_seconds: float = 0.0
+    fallback_columns: int = 0
 
 
 @dataclass
@@ -491,7 +492,7 @@ class _Res:
                            r.evaluations, r.outer_stages, r.final_violation, r.final_reduced_f,
                            r.max_v_inf, tr, r.device_seconds, r.row_pass_seconds,
                            r.col_pass_seconds, r.kernel_launches, r.row_redos,
-                           r.epilogue_seconds)
+                           r.epilogue_seconds, r.fallback_columns)
 
 
 def _trace_cap(max_iters, stride):

@@ -13,8 +13,8 @@ BIN = os.path.join(ROOT, "tests", "cpp", "build", "test_kat")
 def build_cpp_tests() -> str:
     os.makedirs(os.path.dirname(BIN), exist_ok=True)
     lib_dir = os.path.join(ROOT, "paper_2605_30267_b200")
-    if (not os.path.exists(BIN) or os.path.getmtime(BIN) < os.path.getmtime(SRC)
-            or os.path.getmtime(BIN) < os.path.getmtime(os.path.join(ROOT, "include", "otg.hpp"))):
+    deps = [SRC] + [os.path.join(ROOT, "include", h) for h in ("otg.hpp", "otg.h")]
+    if not os.path.exists(BIN) or os.path.getmtime(BIN) < max(os.path.getmtime(d) for d in deps):
         subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", "-o", BIN, SRC,
                         f"-L{lib_dir}", "-lotg", f"-Wl,-rpath,{lib_dir}"], check=True)
     return BIN

@@ -15,7 +15,8 @@ r2 = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=30))
 e = r.evaluations
 print(f"row {r.row_pass_seconds / e * 1e3:.4f} ms  col {r.col_pass_seconds / e * 1e3:.4f} ms  "
       f"epi {r.epilogue_seconds / e * 1e3:.4f} ms  step(ev) {r.device_seconds / r.iterations * 1e3:.4f} "
-      f"step {r2.device_seconds / r2.iterations * 1e3:.4f} ms  redos {r.row_redos}")
+      f"step {r2.device_seconds / r2.iterations * 1e3:.4f} ms  redos {r.row_redos}  "
+      f"fallback cols {r.fallback_columns}")
 ''' % ROOT
 for spec in sys.argv[1:] or [""]:
     env = dict(os.environ)
