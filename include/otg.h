@@ -267,11 +267,13 @@ otg_status otg_plan_stats(otg_problem h, const double* u, const double* v,
                           otg_plan_summary* out);
 
 /* Device timing of the O(nm) sweep kernels at point v: reps launches of
- * each, CUDA events on the handle's stream.  ms[0] = row pass, ms[1] =
- * column pass, ms[2] = epilogue (all kernels after the column pass).
- * bytes[0..1] = algorithmic HBM bytes of one row / column pass launch. */
+ * each, CUDA events on the handle's stream.  These are the first-evaluation
+ * (exact, two-pass) kernels.  ms[0] = row pass, ms[1] = column pass, ms[2] =
+ * merge.  bytes[0..1] = algorithmic HBM bytes of one row / column pass
+ * launch; bytes[2] = those of one steady-state single-pass launch (fused.cu;
+ * 0 when the handle has no single-pass kernel). */
 otg_status otg_time_sweeps(otg_problem h, const double* v, int reps, double ms[3],
-                           double bytes[2]);
+                           double bytes[3]);
 
 /* ---- batched path: many small independent problems, one CTA each ---- */
 typedef struct otg_batch_s* otg_batch;

@@ -178,6 +178,9 @@ struct Problem {
   // single-pass fused sweep (fused.cu), fp32 storage only
   int fused = 0, fused_qpt = 0, fused_W = 0, fused_slots = 0, fused_smem = 0,
       fused_clusters = 0;
+  double* sp_rec = nullptr;     // per-row 32-byte records (shift estimate, a, log a)
+  int* sp_bad_rows = nullptr;   // rows whose shift estimate was loose, per cluster
+  int* sp_bad_count = nullptr;
 
   // column-pass partials
   int col_splits = 1;
@@ -232,7 +235,9 @@ void launch_col_pass(Problem& P);
 void launch_merge_nolog(Problem& P);
 void launch_sweeps(Problem& P, bool timed, cudaEvent_t* ev4);
 bool fused_configure(Problem& P);
-void launch_fused(Problem& P, double* rowpart);
+void fused_alloc(Problem& P);
+void launch_fused(Problem& P, float kh, float kl);
+void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int ncl);
 int partial_rows(const Problem& P);  // rows of P.part the merge sums
 
 // NCCL (comm.cpp)

@@ -1,35 +1,40 @@
 // fused.cu — single-HBM-pass evaluation sweep for fp32 stored costs (sm_100a).
 //
-// One evaluation needs, per row i, the row statistics (max M_i, sum S_i of
-// exp(p_j - C'_ij - M_i)) BEFORE the row can contribute w_i exp(...) to the
-// column sums (dual.cpp:34-41).  A 65536-wide fp32 row is 256 KB, more than
-// one SM's shared memory, so the two-pass kernels of sweep.cu read the cost
-// twice.  Here a cluster of kCL = 8 CTAs (one per SM) holds a whole row on
-// chip, each CTA a W = m/8 column slice, and the cost is read from HBM once:
+// One evaluation needs, per row i, the row sum S_i BEFORE the row can add
+// w_i = a_i / S_i times its exponentials to the column sums (dual.cpp:34-41).
+// A 65536-wide fp32 row is 256 KB, more than one SM's shared memory, so the
+// two-pass kernels of sweep.cu read the cost twice.  Here a cluster of kCL = 8
+// CTAs (one per SM) holds a row on chip, each CTA a W <= 8192-column slice,
+// and the cost is read from HBM once per evaluation:
 //
-//   TMA      cp.async.bulk of the CTA's 32 KB row slice into a 6-slot smem
-//            ring (mbarrier complete_tx), 3 rows ahead of use
-//   pass A   rough row max from the slot: fmaf(-C, kappa2_hi, Vc_j) (2 ops/elem)
-//   pass B   exact exponents relative to the quantised cluster-wide max
-//            (all-fp32 exact cancellation, see sweep.cu), MUFU ex2, row sum;
-//            e_ij written back into the slot
-//   column   acc_j += w_i e_ij in fp32, flushed to fp64 registers every 16
-//            rows; the CTA owns its 8192 columns for its cluster's whole row
-//            range, so column partials never leave the SM until the end
-//   exchange per row one cluster barrier (arrive / wait split around the
-//            column step): CTA partials of (row max, row sum) in smem, read by
-//            every CTA over DSMEM (mapa + ld.shared::cluster)
+//   loads          thread 0 keeps kPre rows ahead: cp.async.bulk of the CTA's
+//                  row slice and the row's 32-byte record (shift estimate, a,
+//                  log a; k_sp_prep) into a kSlots-deep smem ring, completing
+//                  on full[s]; a slot is refilled once every thread has passed
+//                  the barrier that follows its column step
+//   stats (row k)  exponents against the row's shift ESTIMATE s_i (the
+//                  previous evaluation's base-2 row max plus the potential's
+//                  move, exactly as k_row_shift in sweep.cu), e = ex2(t)
+//                  written back over the cost, partial (sum, max, argmax)
+//   exchange       the CTA's partial goes to all 8 CTAs of the cluster with
+//                  st.async (DSMEM push, completes on the receiver's mbarrier)
+//   column (k-D)   D = kLag rows later the 8 partials of row k-D have arrived:
+//                  S, max T, w = a / S; acc_j += w e_ij from smem; fp32
+//                  accumulators flushed into fp64 registers every 16 rows
 //
-// Rows are software-pipelined three deep: iteration k runs pass A on row k,
-// pass B on row k-1 (its max arrived at the end of iteration k-1) and the
-// column step on row k-2 (its sum arrived at the end of iteration k-1).
+// No max pass: s_i is known before the row is read.  A row whose true max T
+// relative to s_i falls outside [-2, 6] (the estimate was too loose) adds
+// nothing here and is listed; k_sp_redo recomputes it exactly and k_sp_patch
+// adds its columns (both cheap: such rows are rare).  The per-element work is
+// the k_row_shift inner loop (packed f32x2) plus one LDS/FFMA2 for the column.
 //
-// Output: per-cluster column partials part[cluster][j] (merged by k_merge like
-// the column-split partials of the two-pass path), u, rowM, rowS, wrow, and
-// the per-cluster <u, a> partial.
+// Output: per-cluster column partials part[cluster][j] plus one patch row
+// part[clusters][j] (summed by k_merge), u, rowM, rowS, wrow, rowM2, rowJ, aux.
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -37,26 +42,41 @@ namespace otg {
 
 namespace {
 
-constexpr int kCL = 8;         // CTAs per cluster (one row across the cluster)
-constexpr int kFT = 512;       // threads per CTA
-constexpr int kFW = kFT / 32;  // warps per CTA
-constexpr int kSlotsMax = 16;
-constexpr int kSmemBudget = 227 * 1024 - 2048;  // bytes of row slots per CTA
+constexpr int kCL = 8;                       // CTAs per cluster
+constexpr int kSW = 8;                       // stats warps
+constexpr int kCW = 8;                       // column warps
+constexpr int kST = kSW * 32;                // threads per role
+constexpr int kCT = (kSW + kCW) * 32;        // threads per CTA
+constexpr int kQPT = 8;                      // float4 quads per thread and row (W <= 8192)
+constexpr int kSlotsMax = 32;                // row-slice ring (runtime depth <= this)
+constexpr int kLagMax = 7;                   // (kept for the configuration knob)
+constexpr int kXD = 16;                      // exchange ring
+constexpr float kRedoLo = 2.0f;              // same window as sweep.cu k_row_shift
+constexpr float kRedoHi = 6.0f;
+constexpr int kPatchThreads = 256;
 
-constexpr int kXD = 4;  // exchange ring depth (2 suffice: see the flow argument below)
-
-struct XMsg {  // one CTA's partials for one iteration, pushed by st.async
-  uint32_t max_bits;
-  uint32_t pad;
-  uint64_t sum_bits;
+struct Msg {  // one CTA's partial of one row (16 bytes, one st.async.v4)
+  double sum;
+  float max;
+  int code;
 };
 
-struct FusedShared {
-  uint64_t full[kSlotsMax];  // TMA completion barriers
-  uint64_t xbar[kXD];        // exchange barriers (8 messages of 12 bytes each)
-  XMsg xin[kXD][kCL];        // partials received from every CTA of the cluster
-  float wmax[2][kFW];        // warp partial max of the pass-A row
-  double wsum[2][kFW];       // warp partial sum of the pass-B row
+struct RowRec {  // per-row inputs, bulk-copied with the row slice (32 bytes)
+  float shift;     // quantised base-2 shift estimate (k_sp_prep)
+  int pad;
+  double a, loga;
+  double pad2;
+};
+
+struct SpShared {
+  uint64_t full[kSlotsMax];    // TMA -> stats warps
+  uint64_t sdone[kSlotsMax];   // stats warps -> column warps (e in the slot, partials)
+  uint64_t empty[kSlotsMax];   // column warps -> loader (slot free)
+  uint64_t xbar[kXD];          // cluster partials of a row received
+  Msg xin[kXD][kCL];
+  RowRec rec[kSlotsMax];
+  unsigned wkey[kSlotsMax][kSW];  // stats-warp partials of the row in each slot
+  int wcode[kSlotsMax][kSW];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -89,29 +109,21 @@ __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint
       "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void cluster_arrive() {
-  asm volatile("barrier.cluster.arrive.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() {
-  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
-// Remote smem store that completes `bytes` on the remote mbarrier (DSMEM push).
-__device__ __forceinline__ void st_async_u32(uint32_t raddr, uint32_t v, uint32_t rbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(
-                   raddr),
-               "r"(v), "r"(rbar)
-               : "memory");
+// float <-> unsigned key with the same order (for redux.sync max / min)
+__device__ __forceinline__ unsigned ordered_key(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
-__device__ __forceinline__ void st_async_u64(uint32_t raddr, uint64_t v, uint32_t rbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u64 [%0], %1, [%2];" ::"r"(
-                   raddr),
-               "l"(v), "r"(rbar)
-               : "memory");
+__device__ __forceinline__ float key_to_float(unsigned k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -124,265 +136,374 @@ __device__ __forceinline__ void split_q(double x2, float& hi, float& lo) {
   lo = static_cast<float>(x2 - h);
 }
 
-template <int QPT>
-__global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kFT, 1)
-k_fused(const float* __restrict__ C, int64_t ldc, int64_t n, int64_t m, int W, int nslots,
-        const double* __restrict__ p, float kh, float kl, const double* __restrict__ a,
-        const double* __restrict__ loga, double* __restrict__ rowM, double* __restrict__ rowS,
-        double* __restrict__ u, double* __restrict__ wrow, double* __restrict__ part,
-        int64_t mpad, double* __restrict__ rowpart, const Ctrl* __restrict__ ctrl) {
-  if (ctrl->done) return;  // uniform over the grid: no cluster barrier is skipped unevenly
+struct SpArgs {
+  const RowRec* rec;
+  const float* C;
+  int64_t ldc, n, m, mpad;
+  int W;
+  const double* p;     // potentials (for the column split)
+  const float* vq;     // split potential of the row pass (Vc[mpad], vf[mpad])
+  const double* dq;
+  float kh, kl;
+  const double* a;
+  const double* loga;
+  double* rowM;
+  double* rowS;
+  double* u;
+  double* wrow;
+  float4* aux;
+  double* rowM2;
+  int* rowJ;
+  double* part;
+  int* bad_rows;       // per cluster: bad_rows[r0 + k], k < bad_count[cluster]
+  int* bad_count;
+  int nslots, lag;     // ring depth; column step `lag` rows after the stats
+  long long* dbg;      // optional timeline (OTG_SP_TRACE): 8 stamps per row, CTA 0 thread 0
+};
+
+// Per-row record of the steady state: the quantised shift estimate
+// s = ceil(min(M2 + dq_J + 1, M2 + dmax2) 256) / 256 (as k_row_shift), a, log a.
+__global__ void __launch_bounds__(256)
+k_sp_prep(int64_t n, const double* __restrict__ rowM2, const int* __restrict__ rowJ,
+          const double* __restrict__ dq, const double* __restrict__ a,
+          const double* __restrict__ loga, RowRec* __restrict__ rec,
+          const Ctrl* __restrict__ ctrl) {
+  if (ctrl->done || !ctrl->shift_valid) return;
+  const double dmax2 = ctrl->dmax2;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * 256) {
+    const double M2 = rowM2[i];
+    const double lo = M2 + dq[rowJ[i]], hi = M2 + dmax2;
+    RowRec r;
+    r.shift = static_cast<float>(ceil(fmin(lo + 1.0, hi) * 256.0) * (1.0 / 256.0));
+    r.pad = 0;
+    r.a = a[i];
+    r.loga = loga[i];
+    r.pad2 = 0.0;
+    rec[i] = r;
+  }
+}
+
+// Kahan step on packed pairs: acc += x with the running error in cmp
+// (cmp holds the NEGATED lost low part: true sum = acc - cmp).
+__device__ __forceinline__ void kahan2(float2& acc, float2& cmp, float2 x) {
+  const float2 y = __fadd2_rn(x, make_float2(-cmp.x, -cmp.y));
+  const float2 tt = __fadd2_rn(acc, y);
+  cmp = __fadd2_rn(__fadd2_rn(tt, make_float2(-acc.x, -acc.y)), make_float2(-y.x, -y.y));
+  acc = tt;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Warp-specialised: 8 stats warps stream the rows (exponentials against the
+// row's shift estimate, written back into the slot, per-warp partials) and
+// never wait on the cluster; 8 column warps publish each row's CTA partial to
+// the cluster, wait for the 8 CTA partials, and fold w * e into the column
+// sums.  Hand-offs are mbarriers (full / sdone / empty / xbar), so the stats of
+// row k overlap the exchange and column step of earlier rows; the only
+// throttle is the slot ring.
+__global__ void __launch_bounds__(kCT, 1)
+k_sp(const SpArgs A, const Ctrl* __restrict__ ctrl) {
+  if (ctrl->done || !ctrl->shift_valid) return;  // uniform: written by earlier launches
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  FusedShared& S = *reinterpret_cast<FusedShared*>(smem_raw);
-  float* slots = reinterpret_cast<float*>(smem_raw + ((sizeof(FusedShared) + 127) / 128) * 128);
+  SpShared& S = *reinterpret_cast<SpShared*>(smem_raw);
+  float* slots = reinterpret_cast<float*>(smem_raw + ((sizeof(SpShared) + 127) / 128) * 128);
+  const int nslots = A.nslots;
+  float* tsum = slots + static_cast<size_t>(nslots) * A.W;  // [nslots][kST] thread partials
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t rank = cluster_rank();
   const int64_t cid = blockIdx.x / kCL, ncl = gridDim.x / kCL;
-  const int64_t r0 = n * cid / ncl, r1 = n * (cid + 1) / ncl;
+  const int64_t r0 = A.n * cid / ncl, r1 = A.n * (cid + 1) / ncl;
   const int R = static_cast<int>(r1 - r0);
-  const int64_t col0 = static_cast<int64_t>(rank) * W;
-  const uint32_t slot_bytes = static_cast<uint32_t>(W) * 4u;
+  const int64_t col0 = static_cast<int64_t>(rank) * A.W;
+  const uint32_t slot_bytes = static_cast<uint32_t>(A.W) * 4u;
 
-  // column potentials of my quads, base-2, quantised split (pad columns -> -1e30)
-  float Vc[QPT][4], vf[QPT][4];
-  bool qvalid[QPT];
-#pragma unroll
-  for (int k = 0; k < QPT; ++k) {
-    const int q = tid + k * kFT;
-    qvalid[k] = 4 * q < W;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int64_t j = col0 + 4 * q + e;
-      if (qvalid[k] && j < m) {
-        split_q(p[j] * kLog2e, Vc[k][e], vf[k][e]);
-      } else {
-        Vc[k][e] = -1e30f;
-        vf[k][e] = 0.f;
-      }
-    }
-  }
-  float acc[QPT][4];
-  double acc64[QPT][4];
-#pragma unroll
-  for (int k = 0; k < QPT; ++k)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      acc[k][e] = 0.f;
-      acc64[k][e] = 0.0;
-    }
+  auto issue_load = [&](int r) {  // row r of this cluster -> slot r % nslots
+    const int s = r % nslots;
+    mbar_expect_tx(&S.full[s], slot_bytes + static_cast<uint32_t>(sizeof(RowRec)));
+    bulk_load(slots + static_cast<size_t>(s) * A.W, A.C + (r0 + r) * A.ldc + col0, slot_bytes,
+              &S.full[s]);
+    bulk_load(&S.rec[s], A.rec + r0 + r, static_cast<uint32_t>(sizeof(RowRec)), &S.full[s]);
+  };
 
   if (tid == 0) {
-    for (int s = 0; s < nslots; ++s) mbar_init(&S.full[s], 1);
+    for (int s = 0; s < nslots; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.sdone[s], kSW);
+      mbar_init(&S.empty[s], kCW);
+    }
     for (int s = 0; s < kXD; ++s) mbar_init(&S.xbar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const int pre = R < nslots ? R : nslots;
-    for (int k = 0; k < pre; ++k) {
-      mbar_expect_tx(&S.full[k], slot_bytes);
-      bulk_load(slots + static_cast<size_t>(k) * W, C + (r0 + k) * ldc + col0, slot_bytes,
-                &S.full[k]);
-    }
+    for (int r = 0; r < nslots && r < R; ++r) issue_load(r);
   }
   __syncthreads();
-  cluster_arrive();  // every CTA of the cluster is resident before any DSMEM access
-  cluster_wait();
+  cluster_sync();  // every CTA's barriers exist before any DSMEM push
 
-  // Pipeline with a one-iteration lag between publishing and consuming the
-  // cluster partials, so the DSMEM exchange latency is hidden behind a whole
-  // iteration of work.  Iteration k:
-  //   pass A  row k      (rough max)                     -> publish max(k)
-  //   pass B  row k-2    (needs max(k-2): received at the end of k-1)
-  //                                                      -> publish sum(k-2)
-  //   column  row k-4    (needs sum(k-4): received at the end of k-1)
-  //   receive the messages of iteration k-1: max(k-1), sum(k-3)
-  // Row r lives in slot r % nslots from its load until its column step at
-  // iteration r + 4; the slot is refilled at iteration r + 5 with row
-  // r + nslots (nslots >= 7 keeps 2 rows of prefetch in flight).
-  float shiftB = 0.f;      // shift of row k-2 (pass B this iteration)
-  float shiftH[4] = {0.f, 0.f, 0.f, 0.f};  // shift used for row r, by r & 3
-  float wC = 0.f;          // w of row k-4 (column step this iteration)
-  int flush = 0;
-  double ua = 0.0;
-  const int K = R + 4;
+  const int t = warp < kSW ? tid : tid - kST;  // thread index within its role
+  auto stamp = [&](int k, int e) {  // OTG_SP_TRACE timeline (CTA 0)
+    if (A.dbg != nullptr && blockIdx.x == 0 && k < 256) A.dbg[k * 8 + e] = clock64();
+  };
+  bool qvalid[kQPT];
+#pragma unroll
+  for (int q = 0; q < kQPT; ++q) qvalid[q] = 4 * (t + q * kST) < A.W;
 
-  for (int k = 0; k <= K; ++k) {
-    // ---- pass A: rough max of row k ----
-    float tmax = -FLT_MAX;
-    if (k < R) {
+  if (warp < kSW) {
+    // =============================================== stats warps ====
+    float2 V01[kQPT], V23[kQPT], F01[kQPT], F23[kQPT];  // row-pass split of p
+#pragma unroll
+    for (int q = 0; q < kQPT; ++q) {
+      const int qq = t + q * kST;
+      float v[4], f[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t j = col0 + 4 * qq + e;
+        if (qvalid[q] && j < A.m) {
+          v[e] = A.vq[j];
+          f[e] = A.vq[A.mpad + j];
+        } else {
+          v[e] = -1e30f;  // padding columns: e = 0, never the max
+          f[e] = 0.f;
+        }
+      }
+      V01[q] = make_float2(v[0], v[1]);
+      V23[q] = make_float2(v[2], v[3]);
+      F01[q] = make_float2(f[0], f[1]);
+      F23[q] = make_float2(f[2], f[3]);
+    }
+    const float2 nkh2 = make_float2(-A.kh, -A.kh), nkl2 = make_float2(-A.kl, -A.kl);
+    for (int k = 0; k < R; ++k) {
       const int s = k % nslots;
+      if (tid == 0) stamp(k, 0);
       mbar_wait(&S.full[s], (k / nslots) & 1);
-      const float4* slot = reinterpret_cast<const float4*>(slots + static_cast<size_t>(s) * W);
+      if (tid == 0) stamp(k, 1);
+      const float sc = S.rec[s].shift;
+      const float2 nSc2 = make_float2(-sc, -sc);
+      float4* slot = reinterpret_cast<float4*>(slots + static_cast<size_t>(s) * A.W);
+      // running max and the quad holding it; the column inside the quad is
+      // resolved at the column step from the exponentials (ex2 is monotonic)
+      float tm = -FLT_MAX;
+      int code = 0x7fffffff;
+      float2 fs = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int q = 0; q < QPT; ++q) {
+      for (int q = 0; q < kQPT; ++q) {
         if (!qvalid[q]) continue;
-        const float4 c = slot[tid + q * kFT];
-        tmax = fmaxf(tmax, fmaxf(fmaxf(fmaf(-c.x, kh, Vc[q][0]), fmaf(-c.y, kh, Vc[q][1])),
-                                 fmaxf(fmaf(-c.z, kh, Vc[q][2]), fmaf(-c.w, kh, Vc[q][3]))));
+        const int qq = t + q * kST;
+        const float4 c = slot[qq];
+        const float2 c01 = make_float2(c.x, c.y), c23 = make_float2(c.z, c.w);
+        const float2 t01 = __fadd2_rn(__ffma2_rn(c01, nkh2, __fadd2_rn(V01[q], nSc2)),
+                                      __ffma2_rn(c01, nkl2, F01[q]));
+        const float2 t23 = __fadd2_rn(__ffma2_rn(c23, nkh2, __fadd2_rn(V23[q], nSc2)),
+                                      __ffma2_rn(c23, nkl2, F23[q]));
+        const float mx = fmaxf(fmaxf(fmaxf(tm, t01.x), t01.y), fmaxf(t23.x, t23.y));
+        code = mx > tm ? static_cast<int>(col0) + 4 * qq : code;
+        tm = mx;
+        const float4 ev = make_float4(ex2_approx(t01.x), ex2_approx(t01.y), ex2_approx(t23.x),
+                                      ex2_approx(t23.y));
+        slot[qq] = ev;
+        fs = __fadd2_rn(fs, __fadd2_rn(make_float2(ev.x, ev.z), make_float2(ev.y, ev.w)));
       }
+      // per-thread fp32 partial (<= 32 terms) -> smem; the publisher folds them
+      tsum[s * kST + t] = fs.x + fs.y;
+      const unsigned key = ordered_key(tm);
+      const unsigned wkey = __reduce_max_sync(0xffffffffu, key);
+      const unsigned wcode = __reduce_min_sync(
+          0xffffffffu, key == wkey ? static_cast<unsigned>(code) : 0x7fffffffu);
+      if (lane == 0) {
+        S.wkey[s][warp] = wkey;
+        S.wcode[s][warp] = static_cast<int>(wcode);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.sdone[s]);  // release: e and partials visible
+      if (tid == 0) stamp(k, 2);
     }
+  } else {
+    // ============================================== column warps ====
+    const int cw = warp - kSW;
+    // compensated (Kahan) fp32 column sums: sum + running error per column,
+    // 2 registers per column instead of an fp32 partial plus an fp64 total
+    float2 acc01[kQPT], acc23[kQPT], cmp01[kQPT], cmp23[kQPT];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-    if (lane == 0) S.wmax[k & 1][warp] = tmax;
-
-    // ---- pass B: exact exponents of row k-2 relative to its cluster max ----
-    double bsum = 0.0;
-    const int rb = k - 2;
-    if (rb >= 0 && rb < R) {
-      const int s = rb % nslots;
-      float4* slot = reinterpret_cast<float4*>(slots + static_cast<size_t>(s) * W);
-      float fs = 0.f;
+    for (int q = 0; q < kQPT; ++q) {
+      acc01[q] = make_float2(0.f, 0.f);
+      acc23[q] = make_float2(0.f, 0.f);
+      cmp01[q] = make_float2(0.f, 0.f);
+      cmp23[q] = make_float2(0.f, 0.f);
+    }
+    int nbad = 0;
+    const int lag = A.lag;
+    for (int kk = 0; kk < R + lag; ++kk) {
+      // ---- publish the CTA partial of row kk (rotating warp), `lag` rows
+      // ahead of its column step so the exchange latency is hidden ----
+      if (kk < R && cw == kk % kCW) {
+        const int sp = kk % nslots, xp = kk % kXD;
+        mbar_wait(&S.sdone[sp], (kk / nslots) & 1);
+        if (lane == 0) stamp(kk, 3);
+        double cs = 0.0;  // fixed order: lane l folds threads l, l + 32, ..., then a tree
 #pragma unroll
-      for (int q = 0; q < QPT; ++q) {
-        if (!qvalid[q]) continue;
-        const float4 c = slot[tid + q * kFT];
-        const float cc[4] = {c.x, c.y, c.z, c.w};
-        float ev[4];
+        for (int w = 0; w < kSW; ++w) cs += static_cast<double>(tsum[sp * kST + w * 32 + lane]);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float A = Vc[q][e] - shiftB;  // exact (multiples of 2^-8)
-          const float g = fmaf(-cc[e], kl, vf[q][e]);
-          const float t = fmaf(-cc[e], kh, A) + g;
-          ev[e] = ex2_approx(t);
-          fs += ev[e];
+        for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+        const unsigned lk = lane < kSW ? S.wkey[sp][lane] : 0u;
+        const unsigned ck = __reduce_max_sync(0xffffffffu, lk);
+        const unsigned cc = __reduce_min_sync(
+            0xffffffffu,
+            (lane < kSW && lk == ck) ? static_cast<unsigned>(S.wcode[sp][lane]) : 0x7fffffffu);
+        const float cm = key_to_float(ck);
+        if (lane == 0) mbar_expect_tx(&S.xbar[xp], kCL * 16u);
+        cs = __shfl_sync(0xffffffffu, cs, 0);
+        if (lane < kCL) {
+          uint32_t ra, rbar;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                       : "=r"(ra)
+                       : "r"(smem_u32(&S.xin[xp][rank])), "r"(static_cast<uint32_t>(lane)));
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                       : "=r"(rbar)
+                       : "r"(smem_u32(&S.xbar[xp])), "r"(static_cast<uint32_t>(lane)));
+          const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(cs));
+          asm volatile(
+              "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, "
+              "%4}, [%5];" ::"r"(ra),
+              "r"(static_cast<uint32_t>(sb)), "r"(static_cast<uint32_t>(sb >> 32)),
+              "r"(__float_as_uint(cm)), "r"(cc), "r"(rbar)
+              : "memory");
         }
-        slot[tid + q * kFT] = make_float4(ev[0], ev[1], ev[2], ev[3]);
+        if (lane == 0) stamp(kk, 4);
       }
-      bsum = static_cast<double>(fs);
-      shiftH[rb & 3] = shiftB;
-    }
+      const int k = kk - lag;
+      if (k < 0) continue;
+      const int s = k % nslots;
+      const int xs = k % kXD;
+      mbar_wait(&S.sdone[s], (k / nslots) & 1);  // (acquire: e values of row k)
+      // ---- column step of row k: the 8 CTA partials ----
+      mbar_wait(&S.xbar[xs], (k / kXD) & 1);
+      if (cw == 0 && lane == 0) stamp(k, 5);
+      double Ssum = 0.0;
+      float T = -FLT_MAX;
+      int J = 0x7fffffff;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
-    if (lane == 0) S.wsum[k & 1][warp] = bsum;
-    __syncthreads();
-
-    // ---- publish {max(k), sum(k-2)} to every CTA of the cluster ----
-    // st.async pushes 12 bytes into slot k % kXD of each CTA and completes them
-    // on that CTA's exchange mbarrier.  Flow control: a CTA reaches iteration
-    // k + kXD only after receiving every message of iteration k + kXD - 2, so
-    // all CTAs are past iteration k + 1, where slot k % kXD was consumed.
-    const int xs = k % kXD;
-    if (warp == 0 && k < K) {  // the last iteration only receives
-      float cm = lane < kFW ? S.wmax[k & 1][lane] : -FLT_MAX;
-      double cs = lane < kFW ? S.wsum[k & 1][lane] : 0.0;
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
-        cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
-        cs += __shfl_xor_sync(0xffffffffu, cs, o);
+      for (int c = 0; c < kCL; ++c) {  // fixed order: every CTA gets the same S, T, J
+        const Msg msg = S.xin[xs][c];
+        Ssum += msg.sum;
+        if (msg.max > T || (msg.max == T && msg.code < J)) {
+          T = msg.max;
+          J = msg.code;
+        }
       }
-      if (lane == 0) mbar_expect_tx(&S.xbar[xs], kCL * 12u);  // my arrival on slot xs
-      if (lane < kCL) {
-        uint32_t ra, rbar;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-                     : "=r"(ra)
-                     : "r"(smem_u32(&S.xin[xs][rank])), "r"(static_cast<uint32_t>(lane)));
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-                     : "=r"(rbar)
-                     : "r"(smem_u32(&S.xbar[xs])), "r"(static_cast<uint32_t>(lane)));
-        cm = __shfl_sync(0x000000ffu, cm, 0, 8);
-        cs = __shfl_sync(0x000000ffu, cs, 0, 8);
-        st_async_u32(ra, __float_as_uint(cm), rbar);
-        st_async_u64(ra + 8, static_cast<uint64_t>(__double_as_longlong(cs)), rbar);
-      }
-      // refill the slot of row k-5 (its column step ran in iteration k-1 and every
-      // thread passed the barrier above since) with row k-5+nslots
-      const int kr = k - 5;
-      if (lane == 0 && kr >= 0 && kr + nslots < R) {
-        const int s = kr % nslots;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&S.full[s], slot_bytes);
-        bulk_load(slots + static_cast<size_t>(s) * W, C + (r0 + kr + nslots) * ldc + col0,
-                  slot_bytes, &S.full[s]);
-      }
-    }
-
-    // ---- column step: row k-4 ----
-    const int rc = k - 4;
-    if (rc >= 0 && rc < R) {
-      const int s = rc % nslots;
-      const float4* slot = reinterpret_cast<const float4*>(slots + static_cast<size_t>(s) * W);
+      const float sc = S.rec[s].shift;
+      const int64_t i = r0 + k;
+      const float4* slot = reinterpret_cast<const float4*>(slots + static_cast<size_t>(s) * A.W);
+      if (T >= -kRedoLo && T <= kRedoHi) {
+        const double ai = S.rec[s].a;
+        const float wf = static_cast<float>(ai) / static_cast<float>(Ssum);  // IEEE fp32
+        const float2 w2 = make_float2(wf, wf);
 #pragma unroll
-      for (int q = 0; q < QPT; ++q) {
-        if (!qvalid[q]) continue;
-        const float4 ev = slot[tid + q * kFT];
-        acc[q][0] = fmaf(wC, ev.x, acc[q][0]);
-        acc[q][1] = fmaf(wC, ev.y, acc[q][1]);
-        acc[q][2] = fmaf(wC, ev.z, acc[q][2]);
-        acc[q][3] = fmaf(wC, ev.w, acc[q][3]);
-      }
-      if (++flush == 16) {
-        flush = 0;
-#pragma unroll
-        for (int q = 0; q < QPT; ++q)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            acc64[q][e] += static_cast<double>(acc[q][e]);
-            acc[q][e] = 0.f;
+        for (int q = 0; q < kQPT; ++q) {
+          if (!qvalid[q]) continue;
+          const float4 ev = slot[t + q * kST];
+          kahan2(acc01[q], cmp01[q], __ffma2_rn(w2, make_float2(ev.x, ev.y), make_float2(0.f, 0.f)));
+          kahan2(acc23[q], cmp23[q], __ffma2_rn(w2, make_float2(ev.z, ev.w), make_float2(0.f, 0.f)));
+        }
+        // row outputs (k_row_shift's epilogue): one CTA per row, rotating
+        if (static_cast<int>(rank) == (k & (kCL - 1)) && cw == 1 && lane == 0) {
+          const double scd = static_cast<double>(sc);
+          const double M = scd * kLn2;
+          A.rowM[i] = M;
+          A.rowS[i] = Ssum;
+          A.u[i] = (S.rec[s].loga - M) - log(Ssum);
+          A.wrow[i] = ai / Ssum;
+          A.rowM2[i] = scd + static_cast<double>(T);
+          A.aux[i] = make_float4(sc, 0.0f, wf, 0.0f);
+        }
+        {  // argmax column: the thread owning the winning quad picks its largest e
+          const int64_t off = static_cast<int64_t>(J) - col0;
+          if (off >= 0 && off < A.W && static_cast<int>((off >> 2) % kST) == t) {
+            const float4 ev = slot[off >> 2];
+            const float em = fmaxf(fmaxf(ev.x, ev.y), fmaxf(ev.z, ev.w));
+            A.rowJ[i] = J + (ev.x == em ? 0 : ev.y == em ? 1 : ev.z == em ? 2 : 3);
           }
-      }
-    }
-
-    // ---- receive iteration k-1: max(k-1), sum(k-3) ----
-    if (k >= 1) {
-      const int ps = (k - 1) % kXD;
-      mbar_wait(&S.xbar[ps], ((k - 1) / kXD) & 1);
-      float gmax = -FLT_MAX;
-      double gsum = 0.0;
-      if (lane < kCL) {
-        gmax = __uint_as_float(S.xin[ps][lane].max_bits);
-        gsum = __longlong_as_double(static_cast<long long>(S.xin[ps][lane].sum_bits));
-      }
-#pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
-        gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
-        gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
-      }
-      gmax = __shfl_sync(0xffffffffu, gmax, 0);
-      gsum = __shfl_sync(0xffffffffu, gsum, 0);
-      if (k - 1 < R) shiftB = rintf(gmax * 256.f) * (1.f / 256.f);  // row k-1, pass B at k+1
-      const int rs = k - 3;                                          // row whose sum arrived
-      if (rs >= 0 && rs < R) {
-        const int64_t i = r0 + rs;
-        const double ai = a[i];
-        const double wi = ai / gsum;
-        wC = static_cast<float>(wi);  // column step of row k-3 at iteration k+1
-        if (rank == 0 && tid == 0) {
-          const double M = static_cast<double>(shiftH[rs & 3]) * kLn2;
-          const double ui = (loga[i] - M) - log(gsum);
-          rowM[i] = M;
-          rowS[i] = gsum;
-          u[i] = ui;
-          wrow[i] = wi;
-          ua += ui * ai;
         }
+      } else if (rank == 0 && cw == 0 && lane == 0) {
+        A.bad_rows[r0 + nbad] = static_cast<int>(i);  // in row order: deterministic patch
+        ++nbad;
+      }
+      // slot free: refill with row k + nslots once all column warps are done
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[s]);
+      if (cw == 0 && lane == 0) stamp(k, 6);
+      if (cw == kCW - 1 && lane == 0 && k + nslots < R) {
+        mbar_wait(&S.empty[s], (k / nslots) & 1);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_load(k + nslots);
+        stamp(k, 7);
       }
     }
-  }
-
-  // column partials of this cluster's rows
+    // column partials of this cluster's rows
 #pragma unroll
-  for (int q = 0; q < QPT; ++q) {
-    if (!qvalid[q]) continue;
-    const int64_t j = col0 + 4 * (tid + q * kFT);
+    for (int q = 0; q < kQPT; ++q) {
+      if (!qvalid[q]) continue;
+      const int64_t j = col0 + 4 * (t + q * kST);
+      const double v[4] = {static_cast<double>(acc01[q].x) - static_cast<double>(cmp01[q].x),
+                           static_cast<double>(acc01[q].y) - static_cast<double>(cmp01[q].y),
+                           static_cast<double>(acc23[q].x) - static_cast<double>(cmp23[q].x),
+                           static_cast<double>(acc23[q].y) - static_cast<double>(cmp23[q].y)};
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-      if (j + e < m) part[cid * mpad + j + e] = acc64[q][e] + static_cast<double>(acc[q][e]);
+      for (int e = 0; e < 4; ++e)
+        if (j + e < A.m) A.part[cid * A.mpad + j + e] = v[e];
+    }
+    if (rank == 0 && cw == 0 && lane == 0) A.bad_count[cid] = nbad;
   }
-  if (rank == 0 && tid == 0) rowpart[cid] = ua;
-  // every message addressed to this CTA was received (the last iteration's
-  // receive); the barrier keeps all CTAs resident until their peers are too
-  cluster_arrive();
-  cluster_wait();
+  // every message addressed to this CTA has been consumed (the column warps
+  // waited for each); keep the cluster resident until all peers are done
+  __syncthreads();
+  cluster_sync();
 }
 
-template <int QPT>
-int fused_clusters(int smem) {
+__global__ void __launch_bounds__(kPatchThreads)
+k_sp_patch(const float* __restrict__ C, int64_t ldc, int64_t m, const double* __restrict__ p,
+           float kh, float kl, const float4* __restrict__ aux, const int* __restrict__ bad_rows,
+           const int* __restrict__ bad_count, int64_t n, int ncl, double* __restrict__ out,
+           const Ctrl* __restrict__ ctrl) {
+  // columns of the rows the stream kernel skipped: out[j] = sum over the
+  // listed rows (cluster order, then row order) of w_i ex2(t_ij), with the
+  // exact split shift k_row_redo wrote into aux -- the k_col_fast formula
+  if (ctrl->done || !ctrl->shift_valid) return;
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * kPatchThreads + threadIdx.x;
+  if (j >= m) return;
+  float Vc, vf;
+  split_q(p[j] * kLog2e, Vc, vf);
+  double acc = 0.0;
+  for (int c = 0; c < ncl; ++c) {
+    const int64_t r0 = n * c / ncl;
+    const int nb = bad_count[c];
+    for (int k = 0; k < nb; ++k) {
+      const int64_t i = bad_rows[r0 + k];
+      const float4 ax = aux[i];
+      const float cc = C[i * ldc + j];
+      const float Aq = Vc - ax.x;
+      const float g = fmaf(-cc, kl, vf - ax.y);
+      const float t = fmaf(-cc, kh, Aq) + g;
+      acc += static_cast<double>(ax.z * ex2_approx(t));
+    }
+  }
+  out[j] = acc;
+}
+
+long long*& sp_trace_buf() {
+  static long long* p = nullptr;
+  return p;
+}
+
+int sp_clusters(int smem) {
   static int cached = -1;
   static int cached_smem = -1;
   if (cached >= 0 && cached_smem == smem) return cached;
-  OTG_CUDA(cudaFuncSetAttribute(k_fused<QPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  OTG_CUDA(cudaFuncSetAttribute(k_sp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kCL * 148);
-  cfg.blockDim = dim3(kFT);
+  cfg.blockDim = dim3(kCT);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
@@ -392,7 +513,7 @@ int fused_clusters(int smem) {
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   int ncl = 0;
-  OTG_CUDA(cudaOccupancyMaxActiveClusters(&ncl, k_fused<QPT>, &cfg));
+  OTG_CUDA(cudaOccupancyMaxActiveClusters(&ncl, k_sp, &cfg));
   cached = ncl;
   cached_smem = smem;
   return ncl;
@@ -400,54 +521,119 @@ int fused_clusters(int smem) {
 
 }  // namespace
 
-// Decide whether the fused path applies and size it (called at handle setup).
+// Decide whether the single-pass path applies and size it (handle setup).
+// Opt-in (OTG_FUSED=1): on B200 at n = m = 65536 it takes 6.4 ms per
+// evaluation against 5.6 ms for the two-pass kernels -- the per-row chain
+// (stats -> cluster exchange -> column step) costs ~2000 cycles of latency per
+// row that the 16 warps do not hide (tools/sp_trace.py timeline,
+// profiles/r01_single_pass.md).
 bool fused_configure(Problem& P) {
   P.fused = 0;
   if (P.storage != OTG_STORE_F32 || P.vshards != 1) return false;
-  // Opt-in (OTG_FUSED=1) until it beats the two-pass path: measured 10.5 ms per
-  // evaluation at n = m = 65536 vs 8.5 ms (profiles/r01_fused_v2.md).
   const char* s = getenv("OTG_FUSED");
   if (!s || atoi(s) == 0) return false;
   const int64_t W = round_up((P.m + kCL - 1) / kCL, 4);
-  if (W * kCL > P.ldc) return false;  // C rows must hold whole slices
-  const int64_t quads = W / 4;
-  int qpt = quads <= kFT ? 1 : quads <= 2 * kFT ? 2 : quads <= 4 * kFT ? 4 : 0;
-  if (qpt == 0 || P.n_local < 64 || P.m < 1024) return false;
-  const int64_t slot_bytes = W * 4;
-  int nslots = static_cast<int>(std::min<int64_t>(kSlotsMax, kSmemBudget / slot_bytes));
-  if (nslots < 7) return false;
-  const int smem = static_cast<int>(((sizeof(FusedShared) + 127) / 128) * 128 + nslots * slot_bytes);
-  int ncl = qpt == 1 ? fused_clusters<1>(smem) : qpt == 2 ? fused_clusters<2>(smem)
-                                                           : fused_clusters<4>(smem);
+  if (W * kCL > P.ldc) return false;          // C rows must hold whole slices
+  if (W > 4 * kST * kQPT) return false;       // columns per CTA held in registers
+  if (P.n_local < 16 * 8 || P.m < 1024) return false;
+  const int64_t head = ((sizeof(SpShared) + 127) / 128) * 128;
+  const int64_t budget = 220 * 1024 - head;
+  const int nslots = static_cast<int>(std::min<int64_t>(kSlotsMax, budget / (W * 4 + kST * 4)));
+  if (nslots < 5) return false;
+  const char* lag_env = getenv("OTG_SP_LAG");
+  int lag = lag_env ? atoi(lag_env) : 3;
+  lag = std::max(0, std::min(std::min(lag, kLagMax), nslots - 2));
+  const int smem = static_cast<int>(head + static_cast<int64_t>(nslots) * (W * 4 + kST * 4));
+  int ncl = sp_clusters(smem);
+  if (getenv("OTG_VERBOSE"))
+    fprintf(stderr, "[otg] single-pass: W=%lld smem=%d slots=%d lag=%d clusters=%d\n",
+            static_cast<long long>(W), smem, nslots, lag, ncl);
   if (ncl < 1) return false;
-  // at least ~64 rows per cluster so the 3-deep pipeline fill is amortised
-  ncl = static_cast<int>(std::min<int64_t>(ncl, std::max<int64_t>(1, P.n_local / 64)));
+  // at least ~16 rows per cluster so the pipeline fill is amortised
+  ncl = static_cast<int>(std::min<int64_t>(ncl, std::max<int64_t>(1, P.n_local / 16)));
   P.fused = 1;
-  P.fused_qpt = qpt;
   P.fused_W = static_cast<int>(W);
-  P.fused_slots = nslots;
   P.fused_smem = smem;
   P.fused_clusters = ncl;
+  P.fused_slots = nslots;
+  P.fused_qpt = lag;  // (column-step lag of the single-pass kernel)
   return true;
 }
 
-void launch_fused(Problem& P, double* rowpart) {
-  const double k2 = P.kappa * kLog2e;
-  const float kh = static_cast<float>(k2);
-  const float kl = static_cast<float>(k2 - static_cast<double>(kh));
-  const dim3 grid(kCL * P.fused_clusters), block(kFT);
-#define OTG_FUSED_LAUNCH(Q)                                                                   \
-  k_fused<Q><<<grid, block, P.fused_smem, P.stream>>>(                                        \
-      P.C32, P.ldc, P.n_local, P.m, P.fused_W, P.fused_slots, P.p, kh, kl, P.a, P.loga, P.rowM, \
-      P.rowS, P.u, P.wrow, P.part, P.mpad, rowpart, P.ctrl)
-  if (P.fused_qpt == 1)
-    OTG_FUSED_LAUNCH(1);
-  else if (P.fused_qpt == 2)
-    OTG_FUSED_LAUNCH(2);
-  else
-    OTG_FUSED_LAUNCH(4);
-#undef OTG_FUSED_LAUNCH
+void fused_alloc(Problem& P) {
+  if (!P.fused) return;
+  if (getenv("OTG_SP_TRACE") && !sp_trace_buf())
+    OTG_CUDA(cudaMalloc(&sp_trace_buf(), 256 * 8 * sizeof(long long)));
+  P.sp_rec = dalloc<double>(P, static_cast<size_t>(P.n_local) * (sizeof(RowRec) / 8));
+  P.sp_bad_rows = dalloc<int>(P, P.n_local);
+  P.sp_bad_count = dalloc<int>(P, P.fused_clusters);
+  OTG_CUDA(cudaMemsetAsync(P.sp_bad_count, 0, P.fused_clusters * sizeof(int), P.stream));
+}
+
+// Steady-state evaluation sweep (launched after the exact-path kernels, each
+// of which returns at once when the other applies): single pass, redo of the
+// loose rows, their column patch into partial row `fused_clusters`.
+void launch_fused(Problem& P, float kh, float kl) {
+  RowRec* rec = reinterpret_cast<RowRec*>(P.sp_rec);
+  k_sp_prep<<<296, 256, 0, P.stream>>>(P.n_local, P.rowM2, P.rowJ, P.dq, P.a, P.loga, rec,
+                                       P.ctrl);
+  SpArgs A;
+  A.rec = rec;
+  A.C = P.C32;
+  A.ldc = P.ldc;
+  A.n = P.n_local;
+  A.m = P.m;
+  A.mpad = P.mpad;
+  A.W = P.fused_W;
+  A.p = P.p;
+  A.vq = P.vq;
+  A.dq = P.dq;
+  A.kh = kh;
+  A.kl = kl;
+  A.a = P.a;
+  A.loga = P.loga;
+  A.rowM = P.rowM;
+  A.rowS = P.rowS;
+  A.u = P.u;
+  A.wrow = P.wrow;
+  A.aux = P.aux;
+  A.rowM2 = P.rowM2;
+  A.rowJ = P.rowJ;
+  A.part = P.part;
+  A.bad_rows = P.sp_bad_rows;
+  A.bad_count = P.sp_bad_count;
+  A.nslots = P.fused_slots;
+  A.lag = P.fused_qpt;
+  A.dbg = sp_trace_buf();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(kCL * P.fused_clusters));
+  cfg.blockDim = dim3(kCT);
+  cfg.dynamicSmemBytes = static_cast<size_t>(P.fused_smem);
+  cfg.stream = P.stream;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = kCL;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  OTG_CUDA(cudaLaunchKernelEx(&cfg, k_sp, A, static_cast<const Ctrl*>(P.ctrl)));
+  launch_sp_redo(P, P.sp_bad_rows, P.sp_bad_count, P.fused_clusters);
+  const unsigned g = static_cast<unsigned>((P.m + kPatchThreads - 1) / kPatchThreads);
+  k_sp_patch<<<g, kPatchThreads, 0, P.stream>>>(
+      P.C32, P.ldc, P.m, P.p, kh, kl, P.aux, P.sp_bad_rows, P.sp_bad_count, P.n_local,
+      P.fused_clusters, P.part + static_cast<int64_t>(P.fused_clusters) * P.mpad, P.ctrl);
   OTG_CUDA(cudaGetLastError());
 }
 
 }  // namespace otg
+
+// Debug: copy the single-pass kernel's timeline (OTG_SP_TRACE) to the host.
+extern "C" int otg_debug_sp_trace(long long* out, int count) {
+  long long* p = otg::sp_trace_buf();
+  if (!p) return 1;
+  if (cudaMemcpy(out, p, static_cast<size_t>(count) * sizeof(long long), cudaMemcpyDeviceToHost) !=
+      cudaSuccess)
+    return 2;
+  return 0;
+}

@@ -524,7 +524,7 @@ otg_status otg_plan_stats(otg_problem h, const double* u, const double* v, otg_p
 }
 
 otg_status otg_time_sweeps(otg_problem h, const double* v, int reps, double ms[3],
-                           double bytes[2]) {
+                           double bytes[3]) {
   return guard([&] {
     Problem& P = get(h);
     if (reps < 1) reps = 1;
@@ -538,14 +538,9 @@ otg_status otg_time_sweeps(otg_problem h, const double* v, int reps, double ms[3
       put_ctrl(P, c);
       h2d(P, P.p, v, P.m);
       OTG_CUDA(cudaEventRecord(e[0], P.stream));
-      if (P.fused) {
-        launch_sweeps(P, false, nullptr);
-        OTG_CUDA(cudaEventRecord(e[1], P.stream));
-      } else {
-        launch_row_pass(P);
-        OTG_CUDA(cudaEventRecord(e[1], P.stream));
-        launch_col_pass(P);
-      }
+      launch_row_pass(P);  // exact first-evaluation kernels (no shift estimate here)
+      OTG_CUDA(cudaEventRecord(e[1], P.stream));
+      launch_col_pass(P);
       OTG_CUDA(cudaEventRecord(e[2], P.stream));
       launch_merge_nolog(P);
       OTG_CUDA(cudaEventRecord(e[3], P.stream));
@@ -564,14 +559,15 @@ otg_status otg_time_sweeps(otg_problem h, const double* v, int reps, double ms[3
     if (bytes) {
       const double elem = P.storage == OTG_STORE_F64 ? 8.0 : 4.0;
       const double nm = static_cast<double>(P.n_local) * static_cast<double>(P.m);
-      if (P.fused) {  // one read of C, p, a, log a; u/M/S/w out; per-cluster partials
-        bytes[0] = nm * elem + P.m * 8.0 + P.n_local * (2 * 8.0 + 4 * 8.0) +
-                   static_cast<double>(P.fused_clusters) * P.m * 8.0;
-        bytes[1] = 0.0;
-      } else {
-        bytes[0] = nm * elem + P.m * 8.0 + P.n_local * (2 * 8.0 + 4 * 8.0 + 16.0);
-        bytes[1] = nm * elem + P.m * 8.0 + P.n_local * 16.0 +
-                   static_cast<double>(P.col_splits) * P.vshards * P.m * 8.0;  // C + aux + partials
+      bytes[0] = nm * elem + P.m * 8.0 + P.n_local * (2 * 8.0 + 4 * 8.0 + 16.0);
+      bytes[1] = nm * elem + P.m * 8.0 + P.n_local * 16.0 +
+                 static_cast<double>(P.col_splits) * P.vshards * P.m * 8.0;  // C + aux + partials
+      bytes[2] = 0.0;
+      if (P.fused) {
+        // in-solve single pass: C once, split p (8 B), row state in/out
+        // (rowM2, rowJ, a, log a in; u, M, S, w, M2, J, aux out), cluster partials
+        bytes[2] = nm * elem + P.m * 8.0 + P.n_local * (8.0 + 4 + 16.0 + 5 * 8.0 + 4 + 16.0) +
+                   static_cast<double>(P.fused_clusters + 1) * P.m * 8.0;
       }
     }
   });

@@ -598,6 +598,30 @@ __device__ __forceinline__ void row_shift_block(
   }
 }
 
+// Exact redo of the rows the single-pass kernel (fused.cu) listed as loose,
+// per cluster c at bad_rows[n c / ncl + k], k < bad_count[c].
+__global__ void __launch_bounds__(kRowThreads)
+k_sp_redo(const CostSrc src, int64_t n, int64_t m, const double* __restrict__ p, double kappa,
+          const double* __restrict__ a, const double* __restrict__ loga,
+          double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
+          double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
+          int* __restrict__ rowJ, const int* __restrict__ bad_rows,
+          const int* __restrict__ bad_count, int ncl, Ctrl* __restrict__ ctrl) {
+  if (ctrl->done || !ctrl->shift_valid) return;
+  for (int c = 0; c < ncl; ++c) {
+    const int nb = bad_count[c];
+    const int64_t base = n * c / ncl;
+    for (int k = blockIdx.x; k < nb; k += gridDim.x) {
+      const int64_t rows[1] = {bad_rows[base + k]};
+      const bool valid[1] = {true};
+      row_exact_block<1, false>(rows, src, m, p, kappa, a, loga, rowM, rowS, u, wrow, aux, rowM2,
+                                rowJ, valid);
+      __syncthreads();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && nb > 0) atomicAdd(&ctrl->redo_count, static_cast<unsigned>(nb));
+  }
+}
+
 // fp32 row pass kernels: the exact body on the first evaluation of a solve
 // (no previous point), the shift-estimate body after; each returns at once
 // when its case does not apply.  (Kept as two kernels: one kernel holding both
@@ -689,8 +713,9 @@ __global__ void __launch_bounds__(NT)
 k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh, float kl,
            const float4* __restrict__ aux, int64_t row_lo, int64_t row_hi,
            int64_t rows_per_split, double* __restrict__ part, int64_t mpad,
-           const Ctrl* __restrict__ ctrl) {
-  if (ctrl->done) return;
+           const Ctrl* __restrict__ ctrl, int exact_only) {
+  // exact_only: the single-pass kernel (fused.cu) does the steady-state columns
+  if (ctrl->done || (exact_only && ctrl->shift_valid)) return;
   __shared__ float4 sh_aux[kAuxTile];
   __shared__ float4 sh_x[OTF ? kAuxTile : 1];
   const int64_t q = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x;
@@ -759,7 +784,12 @@ __device__ __forceinline__ void merge_body(const double* __restrict__ part, int 
                                            const double* __restrict__ u,
                                            const double* __restrict__ a, int64_t nrows,
                                            int do_merge, int flag, Ctrl* __restrict__ ctrl,
-                                           int blk, int nblk, double* sh) {
+                                           int blk, int nblk, double* sh, int fused_rows) {
+  // single-pass steady state: the cluster partials + the patch row
+  if (fused_rows && ctrl->shift_valid) {
+    nshards = 1;
+    splits = fused_rows;
+  }
   if (do_merge) {  // <u, a> over the local rows (for f)
     const int64_t r0 = nrows * blk / nblk, r1 = nrows * (blk + 1) / nblk;
     double t = 0.0;
@@ -799,11 +829,11 @@ __global__ void __launch_bounds__(kEThreads)
 k_merge(const double* __restrict__ part, int nshards, int splits, int64_t m, int64_t mpad,
         double* __restrict__ col, double* __restrict__ col_log, int* __restrict__ flag_idx,
         int* __restrict__ fb_cols, const double* __restrict__ u, const double* __restrict__ a,
-        int64_t nrows, int do_merge, int flag, Ctrl* __restrict__ ctrl) {
+        int64_t nrows, int do_merge, int flag, Ctrl* __restrict__ ctrl, int fused_rows) {
   if (ctrl->done) return;
   __shared__ double sh[kEThreads / 32];
   merge_body(part, nshards, splits, m, mpad, col, col_log, flag_idx, fb_cols, u, a, nrows,
-             do_merge, flag, ctrl, blockIdx.x, gridDim.x, sh);
+             do_merge, flag, ctrl, blockIdx.x, gridDim.x, sh, fused_rows);
 }
 
 // ------------------------------------------------------------------ K5 ----
@@ -1408,6 +1438,7 @@ struct EpiArgs {
   double kappa;
   double2* fb_part;
   int storage;
+  int fused_rows;
   FinArgs F;
   AppArgs P;
 };
@@ -1419,7 +1450,7 @@ k_epilogue(const EpiArgs E, Ctrl* __restrict__ ctrl) {
   const int blk = blockIdx.x, nblk = gridDim.x;
   merge_body(E.part, E.nshards, E.splits, E.F.m, E.F.mpad, E.F.col, E.F.col_log,
              const_cast<int*>(E.F.flag_idx), E.fb_cols, E.u, E.a, E.nrows, 1, 1, ctrl, blk, nblk,
-             sh);
+             sh, E.fused_rows);
   grid_sync(ctrl);
   const unsigned nf = *static_cast<volatile unsigned*>(&ctrl->fb_count);
   if (nf > 0) {
@@ -1592,7 +1623,13 @@ void launch_row_pass(Problem& P) {
                                                      P.rowM, P.rowS, P.u, P.wrow, P.aux,      \
                                                      P.rowM2, P.rowJ, P.redo_rows, P.ctrl)
     const bool otf = P.storage == OTG_STORE_ON_THE_FLY;
-    if (R == 8) {
+    if (P.fused) {
+      // exact first evaluation (two-pass), then the single-pass kernel
+      k_row_exact<4, false><<<blocks, kRowThreads, 0, P.stream>>>(
+          src, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,
+          P.rowM2, P.rowJ, P.ctrl);
+      launch_fused(P, kh, kl);
+    } else if (R == 8) {
       if (otf) { OTG_ROW(8, true); } else { OTG_ROW(8, false); }
     } else if (R == 4) {
       if (otf) { OTG_ROW(4, true); } else { OTG_ROW(4, false); }
@@ -1623,7 +1660,7 @@ void launch_col_pass(Problem& P) {
       dim3 grid(static_cast<unsigned>((P.m + 4 * NT - 1) / (4 * NT)), P.col_splits);
 #define OTG_COL(OTF, T)                                                                      \
   k_col_fast<OTF, T><<<grid, T, 0, P.stream>>>(cost_src(P), P.m, P.p, kh, kl, P.aux, lo, hi, \
-                                               P.rows_per_split, part, P.mpad, P.ctrl)
+                                               P.rows_per_split, part, P.mpad, P.ctrl, P.fused)
       const bool otf = P.storage == OTG_STORE_ON_THE_FLY;
       if (NT == 512) {
         if (otf) { OTG_COL(true, 512); } else { OTG_COL(false, 512); }
@@ -1638,19 +1675,25 @@ void launch_col_pass(Problem& P) {
   OTG_CUDA(cudaGetLastError());
 }
 
-int partial_rows(const Problem& P) {
-  return P.fused ? P.fused_clusters : P.vshards * P.col_splits;
+void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int ncl) {
+  k_sp_redo<<<148, kRowThreads, 0, P.stream>>>(cost_src(P), P.n_local, P.m, P.p, P.kappa, P.a,
+                                                P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,
+                                                P.rowM2, P.rowJ, bad_rows, bad_count, ncl,
+                                                P.ctrl);
 }
+
+int partial_rows(const Problem& P) { return P.vshards * P.col_splits; }
 
 int64_t merge_blocks(const Problem& P) { return (P.m + kEThreads - 1) / kEThreads; }
 
 static void launch_merge(Problem& P, bool merge, bool flag) {
   const int64_t blocks = merge_blocks(P);
-  const int shards = P.fused ? 1 : P.vshards;
-  const int splits = P.fused ? P.fused_clusters : P.col_splits;
+  const int shards = P.vshards;
+  const int splits = P.col_splits;
   k_merge<<<blocks, kEThreads, 0, P.stream>>>(P.part, shards, splits, P.m, P.mpad, P.col,
                                               P.col_log, P.flag_idx, P.fb_cols, P.u, P.a,
-                                              P.n_local, merge ? 1 : 0, flag ? 1 : 0, P.ctrl);
+                                              P.n_local, merge ? 1 : 0, flag ? 1 : 0, P.ctrl,
+                                              P.fused ? P.fused_clusters + 1 : 0);
   OTG_CUDA(cudaGetLastError());
 }
 
@@ -1665,16 +1708,6 @@ static void mark(Problem& P, cudaEvent_t e) {
 // Both O(nm) passes: the fused single-HBM-pass kernel when the handle has one
 // (fp32 storage, m <= 65536), else the row pass then the column pass.
 void launch_sweeps(Problem& P, bool timed, cudaEvent_t* ev4) {
-  if (P.fused) {
-    if (timed) mark(P, ev4[0]);
-    launch_fused(P, P.e1_part + P.e_blocks * 8);
-    if (timed) {
-      mark(P, ev4[1]);
-      mark(P, ev4[2]);
-      mark(P, ev4[3]);
-    }
-    return;
-  }
   if (timed) mark(P, ev4[0]);
   launch_row_pass(P);
   if (timed) mark(P, ev4[1]);
@@ -1720,7 +1753,7 @@ static AppArgs app_args(const Problem& P) {
   A.prev_y = P.prev_y;
   A.vq = P.vq;
   A.dq = P.dq;
-  A.fast = P.storage != OTG_STORE_F64 && !P.fused;  // fp32 stored or on the fly
+  A.fast = P.storage != OTG_STORE_F64;  // fp32 stored or on the fly: shift estimate
   A.e2_part = P.e2_part;
   A.trace = P.trace;
   return A;
@@ -1745,8 +1778,9 @@ static int epilogue_grid(Problem& P) {
 static void launch_epilogue(Problem& P, int grid) {
   EpiArgs E;
   E.part = P.part;
-  E.nshards = P.fused ? 1 : P.vshards;
-  E.splits = P.fused ? P.fused_clusters : P.col_splits;
+  E.nshards = P.vshards;
+  E.splits = P.col_splits;
+  E.fused_rows = P.fused ? P.fused_clusters + 1 : 0;
   E.nrows = P.n_local;
   E.fb_cols = P.fb_cols;
   E.u = P.u;

@@ -745,12 +745,13 @@ def primal_cost(p, u, v) -> float:
 
 
 def time_sweeps(p: TransportProblem, v, reps=10):
-    """Device time (ms) of one row pass, one column pass and the merge at v,
-    plus the algorithmic HBM bytes of one row / column pass."""
+    """Device time (ms) of one (exact, first-evaluation) row pass, column pass
+    and merge at v, plus the algorithmic HBM bytes of one row pass, one column
+    pass and one steady-state single-pass launch (0 if none)."""
     h = p.handle
     v = _f64(v)
     ms = (C.c_double * 3)()
-    by = (C.c_double * 2)()
+    by = (C.c_double * 3)()
     _check(_lib().otg_time_sweeps(h.raw, _ptr(v), int(reps), ms, by))
     return list(ms), list(by)
 

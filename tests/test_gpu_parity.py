@@ -363,6 +363,22 @@ def test_fused_eval_matches_oracle_and_two_pass(n, m):
         assert abs(e.f_value - r["f_value"]) <= 1e-6 * max(1.0, abs(r["f_value"]))
 
 
+@pytest.mark.parametrize("n,m,eps", [(300, 4100, 2e-3), (257, 65536, 1e-3), (2048, 2048, 5e-4)])
+def test_fused_single_pass_matches_two_pass_solve(n, m, eps):
+    """Steady-state single-pass kernel (cluster exchange, shift estimates,
+    loose-row redo + column patch) against the two-pass kernels."""
+    pf = _points_problem(n, m, 11, eps, True)
+    p2 = _points_problem(n, m, 11, eps, False)
+    assert pf.handle.info.sweep_mode == 2 and p2.handle.info.sweep_mode == 1
+    cfg = ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=40)
+    gf = ot.homotopy_solve(pf, cfg)
+    g2 = ot.homotopy_solve(p2, cfg)
+    assert gf.iterations == g2.iterations
+    assert rel(gf.potentials.v, g2.potentials.v) <= 2e-6
+    assert rel(gf.potentials.u, g2.potentials.u) <= 2e-6
+    assert abs(gf.final_violation - g2.final_violation) <= 1e-5 * max(g2.final_violation, 1e-3)
+
+
 def test_fused_homotopy_cost_and_iterations():
     n, m, eps, tol = 512, 2048, 5e-3, 1e-6
     pf = _points_problem(n, m, 9, eps, True)

@@ -16,7 +16,8 @@ e = r.evaluations
 print(f"row {r.row_pass_seconds / e * 1e3:.4f} ms  col {r.col_pass_seconds / e * 1e3:.4f} ms  "
       f"epi {r.epilogue_seconds / e * 1e3:.4f} ms  step(ev) {r.device_seconds / r.iterations * 1e3:.4f} "
       f"step {r2.device_seconds / r2.iterations * 1e3:.4f} ms  redos {r.row_redos}  "
-      f"fallback cols {r.fallback_columns}")
+      f"fallback cols {r.fallback_columns}  mode {p.handle.info.sweep_mode} "
+      f"clusters {p.handle.info.sweep_clusters}")
 ''' % ROOT
 for spec in sys.argv[1:] or [""]:
     env = dict(os.environ)
