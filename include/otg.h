@@ -50,6 +50,7 @@ typedef enum {
   OTG_E_NONPOSITIVE = 6,       /* NonPositiveEntry                            */
   OTG_E_DIMENSION = 7,         /* DimensionMismatch                           */
   OTG_E_TOO_LARGE = 8,         /* DimensionTooLarge                           */
+  OTG_E_DEGENERATE = 9,        /* DegenerateColumn                            */
   OTG_E_CUDA = 20,             /* CUDA runtime / launch failure               */
   OTG_E_NCCL = 21,             /* NCCL failure (sharded handles)              */
   OTG_E_OOM = 22,              /* device allocation failed                    */
@@ -274,6 +275,35 @@ otg_status otg_plan_stats(otg_problem h, const double* u, const double* v,
  * 0 when the handle has no single-pass kernel). */
 otg_status otg_time_sweeps(otg_problem h, const double* v, int reps, double ms[3],
                            double bytes[3]);
+
+/* ---- plan consumers over the implicit plan P = exp(u + v - C') ----
+ * (SURVEY §8f row 1).  P is never materialised: each call streams the cost
+ * once and rebuilds P_ij = exp(((-C'_ij) + u_i) + v_j) (core.cpp:63-70) in
+ * fp64; PotentialOverflow if an exponent exceeds 700 (core.cpp:66-69).  u is
+ * the handle's local rows (row shard), v all m columns. */
+
+/* barycentric_projection (pipelines.cpp:58-71): out[j][k] = sum_i P_ij src[i][k]
+ * / sum_i P_ij, src is n_local x d row-major (1 <= d <= 8), out m x d;
+ * DegenerateColumn (OTG_E_DEGENERATE) if a column has zero mass.  col_mass
+ * (optional, m) receives sum_i P_ij.  Sharded handles all-reduce the sums. */
+otg_status otg_plan_barycentric(otg_problem h, const double* u, const double* v,
+                                const double* src, int d, double* out, double* col_mass);
+
+/* predict_translations (pipelines.cpp:101-111): out[i] = argmax_j P_ij,
+ * ties to the lowest index (n_local entries). */
+otg_status otg_plan_row_argmax(otg_problem h, const double* u, const double* v, int* out);
+
+/* The per-source ranking of topk_accuracy (pipelines.cpp:113-145): for each
+ * row rows[b], the k columns with the largest P (value descending, index
+ * ascending on ties) into out[b * k + r]; -1 past m.  OtError if k < 1. */
+otg_status otg_plan_topk(otg_problem h, const double* u, const double* v, const int* rows,
+                         int64_t nrows, int k, int* out);
+
+/* The nearest-sample search of nn_propagate (pipelines.cpp:80-92): out[p] =
+ * argmin_s ||queries[p] - refs[s]||^2 in fp64, strict < so ties go to the
+ * lowest index; d in 1..4, row-major. */
+otg_status otg_nn_assign(const double* queries, int64_t nq, const double* refs, int64_t nref,
+                         int d, int device, int* out);
 
 /* ---- batched path: many small independent problems, one CTA each ---- */
 typedef struct otg_batch_s* otg_batch;

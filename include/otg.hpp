@@ -34,6 +34,7 @@ struct InvalidMarginals : OtError { using OtError::OtError; };
 struct NonPositiveEntry : OtError { using OtError::OtError; };
 struct DimensionMismatch : OtError { using OtError::OtError; };
 struct DimensionTooLarge : OtError { using OtError::OtError; };
+struct DegenerateColumn : OtError { using OtError::OtError; };
 struct DeviceError : OtError { using OtError::OtError; };  // CUDA / NCCL / OOM / no device
 
 inline void check(otg_status s) {
@@ -47,6 +48,7 @@ inline void check(otg_status s) {
     case OTG_E_NONPOSITIVE: throw NonPositiveEntry(m);
     case OTG_E_DIMENSION: throw DimensionMismatch(m);
     case OTG_E_TOO_LARGE: throw DimensionTooLarge(m);
+    case OTG_E_DEGENERATE: throw DegenerateColumn(m);
     case OTG_E_CUDA:
     case OTG_E_NCCL:
     case OTG_E_OOM:
@@ -370,6 +372,31 @@ inline PlanStats plan_stats(const TransportProblem& p, const Vec& u, const Vec& 
   s.primal_cost = out.primal_cost;
   s.max_exponent = out.max_exponent;
   return s;
+}
+
+// ------------------------------------------------------------ pipelines.hpp plan consumers
+// Over the implicit plan of the potentials (the reference takes a PlanDense).
+// src is n x d row-major; the result m x d row-major.
+inline Vec barycentric_projection(const TransportProblem& p, const Vec& u, const Vec& v,
+                                  const Vec& src, int d) {  // pipelines.cpp:58-71
+  if (static_cast<long>(src.size()) != p.info().n_local * d)
+    throw DimensionMismatch("plan rows and source colors disagree");
+  Vec out(static_cast<size_t>(p.m()) * d);
+  check(otg_plan_barycentric(p.handle(), u.data(), v.data(), src.data(), d, out.data(), nullptr));
+  return out;
+}
+inline std::vector<int> predict_translations(const TransportProblem& p, const Vec& u,
+                                             const Vec& v) {  // pipelines.cpp:101-111
+  std::vector<int> out(static_cast<size_t>(p.info().n_local));
+  check(otg_plan_row_argmax(p.handle(), u.data(), v.data(), out.data()));
+  return out;
+}
+inline std::vector<int> plan_topk(const TransportProblem& p, const Vec& u, const Vec& v,
+                                  const std::vector<int>& rows, int k) {
+  std::vector<int> out(rows.size() * static_cast<size_t>(k > 0 ? k : 1));
+  check(otg_plan_topk(p.handle(), u.data(), v.data(), rows.data(),
+                      static_cast<int64_t>(rows.size()), k, out.data()));
+  return out;
 }
 
 // ------------------------------------------------------------ pipelines.hpp run_solver

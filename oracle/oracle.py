@@ -27,7 +27,7 @@ TRACE_FIELDS = ("iter", "wall_time_s", "marginal_violation_l1", "grad_f_l1", "re
 
 _ERR_NAMES = {1: "OtError", 2: "PotentialOverflow", 3: "DomainViolation", 4: "GaugeViolation",
               5: "InvalidMarginals", 6: "NonPositiveEntry", 7: "DimensionMismatch",
-              8: "DimensionTooLarge", 9: "OracleUnavailable"}
+              8: "DimensionTooLarge", 9: "OracleUnavailable", 10: "DegenerateColumn"}
 
 
 class OracleError(RuntimeError):
@@ -443,6 +443,39 @@ def cost_sqeuclid_f32(x, y):
 def sqeuclid_max(x, y, threads=1) -> float:
     x, y = _f64(x), _f64(y)
     return lib().orc_sqeuclid_max(_p(x), _p(y), x.shape[0], y.shape[0], x.shape[1], threads)
+
+
+# plan consumers (pipelines.cpp:58-145) on the plan of plan_from_potentials ---
+def barycentric_projection(p: Problem, u, v, src):
+    src = np.ascontiguousarray(src, dtype=np.float64)
+    d = src.shape[1]
+    out = np.empty((p.m, d))
+    _check(lib().orc_barycentric_projection(p.ref, _p(_f64(u)), _p(_f64(v)), _p(src), C.c_int(d),
+                                            _p(out)))
+    return out
+
+
+def predict_translations(p: Problem, u, v):
+    out = np.empty(p.n, dtype=np.int32)
+    _check(lib().orc_predict_translations(p.ref, _p(_f64(u)), _p(_f64(v)), _p(out)))
+    return out
+
+
+def plan_topk(p: Problem, u, v, rows, k):
+    rows = np.ascontiguousarray(rows, dtype=np.int32)
+    out = np.empty((len(rows), k), dtype=np.int32)
+    _check(lib().orc_plan_topk(p.ref, _p(_f64(u)), _p(_f64(v)), _p(rows), C.c_int64(len(rows)),
+                               C.c_int(k), _p(out)))
+    return out
+
+
+def nn_assign(q, ref):
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    ref = np.ascontiguousarray(ref, dtype=np.float64)
+    out = np.empty(q.shape[0], dtype=np.int32)
+    lib().orc_nn_assign(_p(q), C.c_int64(q.shape[0]), _p(ref), C.c_int64(ref.shape[0]),
+                        C.c_int(q.shape[1]), _p(out))
+    return out
 
 
 # fixtures (helpers.hpp:14-27) ----------------------------------------------

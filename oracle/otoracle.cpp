@@ -553,6 +553,97 @@ int orc_plan_stats(const orc_problem* pp, const double* u, const double* v, doub
   });
 }
 
+// ---- plan consumers (pipelines.cpp) on the plan of plan_from_potentials ----
+// P_ij = exp(((-C'_ij) + u_i) + v_j) with the 700 overflow guard (core.cpp:59-71).
+static Vec plan_dense(const Prob& p, const double* u, const double* v) {
+  double top = -std::numeric_limits<double>::infinity();
+  for (int64_t i = 0; i < p.n; ++i)
+    for (int64_t j = 0; j < p.m; ++j) top = std::max(top, ((-p.C(i, j)) + u[i]) + v[j]);
+  if (top > kExpOverflowBound) fail(ORC_E_OVERFLOW, "plan exponent exceeds bound");
+  Vec P(static_cast<size_t>(p.n * p.m));
+  for (int64_t i = 0; i < p.n; ++i)
+    for (int64_t j = 0; j < p.m; ++j) P[i * p.m + j] = std::exp(((-p.C(i, j)) + u[i]) + v[j]);
+  return P;
+}
+
+// pipelines.cpp:58-71
+int orc_barycentric_projection(const orc_problem* pp, const double* u, const double* v,
+                               const double* src, int d, double* out) {
+  return guard([&] {
+    Prob p = wrap(pp);
+    const Vec P = plan_dense(p, u, v);
+    Vec col(p.m, 0.0);  // make_plan: column sums
+    for (int64_t i = 0; i < p.n; ++i)
+      for (int64_t j = 0; j < p.m; ++j) col[j] += P[i * p.m + j];
+    for (int64_t j = 0; j < p.m; ++j)
+      if (!(col[j] > 0.0)) fail(ORC_E_DEGENERATE, "plan column has zero mass");
+    for (int64_t j = 0; j < p.m; ++j)
+      for (int k = 0; k < d; ++k) {
+        double t = 0.0;  // (P^T src)(j, k)
+        for (int64_t i = 0; i < p.n; ++i) t += P[i * p.m + j] * src[i * d + k];
+        out[j * d + k] = t / col[j];
+      }
+  });
+}
+
+// pipelines.cpp:101-111
+int orc_predict_translations(const orc_problem* pp, const double* u, const double* v,
+                             int* out) {
+  return guard([&] {
+    Prob p = wrap(pp);
+    const Vec P = plan_dense(p, u, v);
+    for (int64_t i = 0; i < p.n; ++i) {
+      int64_t best = 0;
+      for (int64_t j = 1; j < p.m; ++j)
+        if (P[i * p.m + j] > P[i * p.m + best]) best = j;
+      out[i] = static_cast<int>(best);
+    }
+  });
+}
+
+// pipelines.cpp:113-145: per-row top-k (value descending, index ascending)
+int orc_plan_topk(const orc_problem* pp, const double* u, const double* v, const int* rows,
+                  int64_t nrows, int k, int* out) {
+  return guard([&] {
+    Prob p = wrap(pp);
+    if (k < 1) fail(ORC_E_OT, "topk_accuracy needs k >= 1");
+    const Vec P = plan_dense(p, u, v);
+    std::vector<int> order(static_cast<size_t>(p.m));
+    const int64_t kk = std::min<int64_t>(k, p.m);
+    for (int64_t b = 0; b < nrows; ++b) {
+      const int64_t s = rows[b];
+      if (s < 0 || s >= p.n) fail(ORC_E_DIMENSION, "dictionary index outside the plan");
+      for (size_t j = 0; j < order.size(); ++j) order[j] = static_cast<int>(j);
+      std::partial_sort(order.begin(), order.begin() + kk, order.end(), [&](int x, int y) {
+        const double px = P[s * p.m + x], py = P[s * p.m + y];
+        return px > py || (px == py && x < y);
+      });
+      for (int64_t r = 0; r < k; ++r) out[b * k + r] = r < kk ? order[r] : -1;
+    }
+  });
+}
+
+// pipelines.cpp:80-92: nearest sample, squared distance, strict < (lowest index)
+void orc_nn_assign(const double* q, int64_t nq, const double* ref, int64_t nref, int d,
+                   int* out) {
+  for (int64_t a = 0; a < nq; ++a) {
+    int64_t best = 0;
+    double best_d2 = 0.0;
+    for (int64_t s = 0; s < nref; ++s) {
+      double d2 = 0.0;
+      for (int k = 0; k < d; ++k) {
+        const double dd = q[a * d + k] - ref[s * d + k];
+        d2 += dd * dd;
+      }
+      if (s == 0 || d2 < best_d2) {
+        best_d2 = d2;
+        best = s;
+      }
+    }
+    out[a] = static_cast<int>(best);
+  }
+}
+
 // core.cpp:81-93
 int orc_entropic_objective(const orc_problem* pp, const double* u, const double* v,
                            double epsilon, double* out) {

@@ -42,7 +42,8 @@ enum {
   ORC_E_NONPOSITIVE = 6,        /* NonPositiveEntry                         */
   ORC_E_DIMENSION = 7,          /* DimensionMismatch                        */
   ORC_E_TOO_LARGE = 8,          /* DimensionTooLarge                        */
-  ORC_E_ORACLE_UNAVAILABLE = 9  /* OracleUnavailable                        */
+  ORC_E_ORACLE_UNAVAILABLE = 9, /* OracleUnavailable                        */
+  ORC_E_DEGENERATE = 10         /* DegenerateColumn                         */
 };
 
 typedef struct {
@@ -115,6 +116,15 @@ int orc_cost_cosine(const double* x, const double* y, int64_t n, int64_t m, int6
 int orc_plan_stats(const orc_problem* p, const double* u, const double* v, double eps_ratio,
                    double* row_sums, double* col_sums, double* violation_l1,
                    double* primal_cost);
+/* Plan consumers on the plan of plan_from_potentials (pipelines.cpp:58-145). */
+int orc_barycentric_projection(const orc_problem* p, const double* u, const double* v,
+                               const double* src, int d, double* out);
+int orc_predict_translations(const orc_problem* p, const double* u, const double* v, int* out);
+int orc_plan_topk(const orc_problem* p, const double* u, const double* v, const int* rows,
+                  int64_t nrows, int k, int* out);
+void orc_nn_assign(const double* q, int64_t nq, const double* ref, int64_t nref, int d,
+                   int* out);
+
 int orc_entropic_objective(const orc_problem* p, const double* u, const double* v,
                            double epsilon, double* out);
 

@@ -103,6 +103,10 @@ SIGNATURES = {
     "otg_homotopy_solve": (C.c_int, [H, VP, VP, VP]),
     "otg_plan_stats": (C.c_int, [H, VP, VP, VP]),
     "otg_time_sweeps": (C.c_int, [H, VP, C.c_int, VP, VP]),
+    "otg_plan_barycentric": (C.c_int, [H, VP, VP, VP, C.c_int, VP, VP]),
+    "otg_plan_row_argmax": (C.c_int, [H, VP, VP, VP]),
+    "otg_plan_topk": (C.c_int, [H, VP, VP, VP, C.c_int64, C.c_int, VP]),
+    "otg_nn_assign": (C.c_int, [VP, C.c_int64, VP, C.c_int64, C.c_int, C.c_int, VP]),
     "otg_batch_create_dense": (C.c_int, [I64, VP, VP, VP, VP, VP, C.c_double, VP, VP]),
     "otg_batch_create_cosine": (C.c_int, [I64, VP, VP, I64, VP, VP, VP, VP, C.c_int,
                                           C.c_double, VP, VP]),

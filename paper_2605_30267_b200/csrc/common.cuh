@@ -60,6 +60,18 @@ __device__ __forceinline__ float otf_sqeuclid(const float4& x, const float4& y) 
   const float dx = __fsub_rn(x.x, y.x), dy = __fsub_rn(x.y, y.y), dz = __fsub_rn(x.z, y.z);
   return __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
 }
+
+// C'_ij of any storage, in fp64: fp64 C' (stored divided), fp32 C x 1/eps, or
+// the on-the-fly fp32 cost of the points x 1/eps (plan statistics, consumers).
+__device__ __forceinline__ double cost_at(const double* __restrict__ C64,
+                                          const float* __restrict__ C32,
+                                          const float4* __restrict__ X,
+                                          const float4* __restrict__ Y, int64_t ldc, double kappa,
+                                          int64_t i, int64_t j) {
+  if (C64) return C64[i * ldc + j];
+  if (C32) return static_cast<double>(C32[i * ldc + j]) * kappa;
+  return static_cast<double>(otf_sqeuclid(X[i], Y[j])) * kappa;
+}
 #endif
 
 // ------------------------------------------------------------ loop control --
@@ -225,6 +237,7 @@ T* dalloc(Problem& P, size_t count) {
 }
 
 void problem_free(Problem& P);
+Problem& problem_of(otg_problem h);  // handle -> problem (sets the device)
 void problem_alloc_state(Problem& P);
 
 // sweeps / epilogue (sweep.cu)

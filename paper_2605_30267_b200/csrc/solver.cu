@@ -233,18 +233,6 @@ void one_eval(Problem& P, const double* v, bool with_log) {
   raise_device_error(*P.ctrl_host);
 }
 
-// C'_ij of any storage: fp64 C' (stored divided), fp32 C x 1/eps, or the
-// on-the-fly fp32 cost of the points x 1/eps.
-__device__ __forceinline__ double cost_at(const double* __restrict__ C64,
-                                          const float* __restrict__ C32,
-                                          const float4* __restrict__ X,
-                                          const float4* __restrict__ Y, int64_t ldc, double kappa,
-                                          int64_t i, int64_t j) {
-  if (C64) return C64[i * ldc + j];
-  if (C32) return static_cast<double>(C32[i * ldc + j]) * kappa;
-  return static_cast<double>(otf_sqeuclid(X[i], Y[j])) * kappa;
-}
-
 __global__ void k_plan_rows(const double* __restrict__ C64, const float* __restrict__ C32,
                             const float4* __restrict__ X, const float4* __restrict__ Y,
                             int64_t ldc, int64_t n, int64_t m, double kappa,
@@ -297,6 +285,9 @@ __global__ void k_plan_cols(const double* __restrict__ C64, const float* __restr
 }
 
 }  // namespace
+
+Problem& problem_of(otg_problem h) { return get(h); }
+
 }  // namespace otg
 
 using namespace otg;

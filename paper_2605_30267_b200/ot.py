@@ -60,6 +60,10 @@ class DimensionTooLarge(OtError):
     pass
 
 
+class DegenerateColumn(OtError):
+    pass
+
+
 class DeviceError(OtError):
     """CUDA / NCCL / allocation failures of the device path (no reference analogue)."""
 
@@ -70,7 +74,7 @@ class Unsupported(DeviceError):
 
 _ERRORS = {1: OtError, 2: PotentialOverflow, 3: DomainViolation, 4: GaugeViolation,
            5: InvalidMarginals, 6: NonPositiveEntry, 7: DimensionMismatch,
-           8: DimensionTooLarge, 20: DeviceError, 21: DeviceError, 22: DeviceError,
+           8: DimensionTooLarge, 9: DegenerateColumn, 20: DeviceError, 21: DeviceError, 22: DeviceError,
            23: Unsupported}
 
 
@@ -734,6 +738,98 @@ def plan_stats(p: TransportProblem, u, v) -> PlanStats:
     # <C, P> * (epsilon_original / epsilon) with C the stored (scaled) cost.
     scale = (p.epsilon_original / p.epsilon) / p.cost_div
     return PlanStats(out.marginal_violation_l1, out.primal_cost * scale, out.max_exponent, rs, cs)
+
+
+# ------------------------------------------ plan consumers (pipelines.hpp) ----
+# The reference consumes a materialised PlanDense; these take the potentials
+# and stream the cost once on the device (P is never stored).
+
+def _uv(p: TransportProblem, u, v):
+    h = p.handle
+    u, v = _f64(u), _f64(v)
+    if u.size != h.n_local or v.size != p.m():
+        raise DimensionMismatch("potential sizes do not match the instance")
+    return h, u, v
+
+
+def barycentric_projection(p: TransportProblem, u, v, src_colors) -> np.ndarray:
+    """pipelines.cpp:58-71 on the implicit plan: (P^T src) / column mass, m x d.
+    DimensionMismatch if src rows != n; DegenerateColumn on a zero-mass column."""
+    h, u, v = _uv(p, u, v)
+    src = np.ascontiguousarray(src_colors, dtype=np.float64)
+    if src.ndim != 2 or src.shape[0] != h.n_local:
+        raise DimensionMismatch("plan rows and source colors disagree")
+    out = np.empty((p.m(), src.shape[1]))
+    _check(_lib().otg_plan_barycentric(h.raw, _ptr(u), _ptr(v), _ptr(src), src.shape[1],
+                                       _ptr(out), None))
+    return out
+
+
+def predict_translations(p: TransportProblem, u, v) -> List[int]:
+    """pipelines.cpp:101-111: row argmax of the plan, ties to the lowest index."""
+    h, u, v = _uv(p, u, v)
+    out = np.empty(h.n_local, dtype=np.int32)
+    _check(_lib().otg_plan_row_argmax(h.raw, _ptr(u), _ptr(v), _ptr(out)))
+    return [int(x) for x in out]
+
+
+def plan_topk(p: TransportProblem, u, v, rows, k: int) -> np.ndarray:
+    """Top-k columns of the given rows (value descending, index ascending);
+    -1 past m."""
+    h, u, v = _uv(p, u, v)
+    rows = np.ascontiguousarray(rows, dtype=np.int32)
+    out = np.empty((len(rows), max(int(k), 1)), dtype=np.int32)
+    _check(_lib().otg_plan_topk(h.raw, _ptr(u), _ptr(v), _ptr(rows), len(rows), int(k),
+                                _ptr(out)))
+    return out
+
+
+def topk_accuracy(p: TransportProblem, u, v, pairs, k: int) -> Optional[float]:
+    """pipelines.cpp:113-145: fraction of dictionary source words whose
+    top-k plan columns contain one of their targets; None for an empty
+    dictionary; OtError for k < 1; DimensionMismatch for indices outside."""
+    if k < 1:
+        raise OtError("topk_accuracy needs k >= 1")
+    pairs = list(pairs)
+    if not pairs:
+        return None
+    n, m = p.handle.n_local, p.m()
+    targets = {}
+    for s_, t_ in pairs:
+        if s_ < 0 or s_ >= n or t_ < 0 or t_ >= m:
+            raise DimensionMismatch("dictionary index outside the plan")
+        targets.setdefault(int(s_), set()).add(int(t_))
+    srcs = sorted(targets)
+    top = plan_topk(p, u, v, srcs, k)
+    correct = sum(1 for b, s_ in enumerate(srcs) if any(int(j) in targets[s_] for j in top[b] if j >= 0))
+    return correct / len(srcs)
+
+
+def nn_assign(queries, refs, device: int = 0) -> np.ndarray:
+    """Nearest reference point of every query (squared distance in fp64,
+    strict <: ties to the lowest index) -- the search of nn_propagate."""
+    q = np.ascontiguousarray(queries, dtype=np.float64)
+    r = np.ascontiguousarray(refs, dtype=np.float64)
+    if q.ndim != 2 or r.ndim != 2 or q.shape[1] != r.shape[1]:
+        raise DimensionMismatch("query and reference dimensions disagree")
+    out = np.empty(q.shape[0], dtype=np.int32)
+    _check(_lib().otg_nn_assign(_ptr(q), q.shape[0], _ptr(r), r.shape[0], q.shape[1], device,
+                                _ptr(out)))
+    return out
+
+
+def nn_propagate(target_pixels, sampled_tgt_colors, transferred, device: int = 0) -> np.ndarray:
+    """pipelines.cpp:73-99 on raw pixels: target_pixels (npix x 3 uint8) are
+    matched to their nearest sampled target colour (values in [0, 1]) and take
+    that sample's transferred colour, clipped to [0, 1] and rounded to uint8."""
+    sampled = np.asarray(sampled_tgt_colors, dtype=np.float64)
+    tr = np.asarray(transferred, dtype=np.float64)
+    if sampled.shape[0] != tr.shape[0] or sampled.shape[1:] != (3,) or tr.shape[1:] != (3,):
+        raise DimensionMismatch("sampled colors and transferred colors disagree")
+    px = np.asarray(target_pixels, dtype=np.uint8).reshape(-1, 3)
+    best = nn_assign(px.astype(np.float64) / 255.0, sampled, device)
+    vals = np.clip(tr[best], 0.0, 1.0) * 255.0
+    return np.floor(vals + 0.5).astype(np.uint8)  # std::lround of a non-negative value
 
 
 def marginal_violation_l1(p, u, v) -> float:

@@ -17,7 +17,10 @@ REF_TESTS = "/root/reference/proj/tests"
 
 # Derived values that the reference states as an expression, not a literal.
 DERIVED_OK = {"0.7071067811865476", "0.5", "0.25", "0.125", "1.0", "-0.5", "500.0", "2", "1",
-              "19", "3", "0", "4", "10", "-600.0", "600.0", "0.1"}
+              "19", "3", "0", "4", "10", "-600.0", "600.0", "0.1",
+              # integer / exponent literals of test_pipelines.cpp (Rng(23), 1e-15,
+              # uint8 channel values) that the decimal-literal scan below skips
+              "23", "1e-15", "128", "255", "64"}
 
 
 def literals(obj):
