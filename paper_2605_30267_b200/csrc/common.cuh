@@ -166,6 +166,7 @@ struct Problem {
   float* C32 = nullptr;   // fp32: raw C
   float* X = nullptr;     // on-the-fly: x (n_local x 4 padded), y (m x 4)
   float* Y = nullptr;
+  float* Yn = nullptr;    // on-the-fly: -y as SoA [x | y | z], stride mpad (packed kernels)
 
   // marginals (fp64)
   double *a = nullptr, *loga = nullptr, *b = nullptr, *logb = nullptr;

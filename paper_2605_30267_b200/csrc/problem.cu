@@ -139,7 +139,7 @@ __global__ void k_otf_rows(const float4* __restrict__ X, const float4* __restric
 }  // namespace
 
 void problem_free(Problem& P) {
-  void* ptrs[] = {P.C64, P.C32, P.X, P.Y, P.a, P.loga, P.b, P.logb, P.rowM, P.rowS, P.u,
+  void* ptrs[] = {P.C64, P.C32, P.X, P.Y, P.Yn, P.a, P.loga, P.b, P.logb, P.rowM, P.rowS, P.u,
                   P.wrow, P.aux, P.rowM2, P.rowJ, P.dq, P.redo_rows, P.vq, P.p, P.wacc, P.col,
                   P.col_log,
                   P.y, P.grad, P.prev_grad,
@@ -369,10 +369,16 @@ otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const doub
         for (int64_t k = 0; k < d; ++k) hx[i * 4 + k] = static_cast<float>(xl[i * d + k]);
       for (int64_t j = 0; j < m; ++j)
         for (int64_t k = 0; k < d; ++k) hy[j * 4 + k] = static_cast<float>(y[j * d + k]);
+      std::vector<float> hyn(P.mpad * 3, 0.f);  // negated SoA copy for the packed kernels
+      for (int64_t j = 0; j < m; ++j)
+        for (int64_t k = 0; k < d; ++k) hyn[k * P.mpad + j] = -hy[j * 4 + k];
       P.X = dalloc<float>(P, hx.size());
       P.Y = dalloc<float>(P, hy.size());
+      P.Yn = dalloc<float>(P, hyn.size());
       OTG_CUDA(cudaMemcpyAsync(P.X, hx.data(), hx.size() * 4, cudaMemcpyHostToDevice, P.stream));
       OTG_CUDA(cudaMemcpyAsync(P.Y, hy.data(), hy.size() * 4, cudaMemcpyHostToDevice, P.stream));
+      OTG_CUDA(cudaMemcpyAsync(P.Yn, hyn.data(), hyn.size() * 4, cudaMemcpyHostToDevice,
+                               P.stream));
       OTG_CUDA(cudaStreamSynchronize(P.stream));
       finish_create(P, opts, out);
       return;

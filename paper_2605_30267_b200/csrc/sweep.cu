@@ -205,21 +205,39 @@ struct CostSrc {
   const float* C;    // stored: n x ldc
   int64_t ldc;
   const float4* X;   // on-the-fly: n points (x, y, z, 0)
-  const float4* Y;   // on-the-fly: m points
+  const float4* Y;   // on-the-fly: m points (x, y, z, 0)
+  const float* Yn;   // on-the-fly: the same points negated, SoA [-x | -y | -z], stride ypad
+  int64_t ypad;
 };
 
 __device__ __forceinline__ float otf_cost(const float4& x, const float4& y) {
   return otf_sqeuclid(x, y);
 }
 
+// The 4 columns 4q .. 4q+3 of an on-the-fly quad: negated coordinates, SoA,
+// so that each coordinate pair is a packed f32x2 operand.
+struct YQ {
+  float4 x, y, z;
+};
+
 // One quad of row `i` (columns 4q .. 4q+3).  Stored: a 128-bit streaming load.
-// On the fly: xi = X[i] (row-invariant), y4 = Y[4q .. 4q+3] (shared by rows).
+// On the fly: packed f32x2 form of otf_sqeuclid -- d = x_i + (-y_j) (exactly
+// x_i - y_j), c = fma(dz, dz, fma(dy, dy, dx * dx)): bitwise the scalar cost.
 template <bool OTF>
 __device__ __forceinline__ float4 cost_quad(const CostSrc& s, int64_t i, int64_t q,
-                                            const float4& xi, const float4* y4) {
+                                            const float4& xi, const YQ& yq) {
   if constexpr (OTF) {
-    return make_float4(otf_cost(xi, y4[0]), otf_cost(xi, y4[1]), otf_cost(xi, y4[2]),
-                       otf_cost(xi, y4[3]));
+    const float2 bx = make_float2(xi.x, xi.x), by = make_float2(xi.y, xi.y),
+                 bz = make_float2(xi.z, xi.z);
+    const float2 dx01 = __fadd2_rn(bx, make_float2(yq.x.x, yq.x.y));
+    const float2 dx23 = __fadd2_rn(bx, make_float2(yq.x.z, yq.x.w));
+    const float2 dy01 = __fadd2_rn(by, make_float2(yq.y.x, yq.y.y));
+    const float2 dy23 = __fadd2_rn(by, make_float2(yq.y.z, yq.y.w));
+    const float2 dz01 = __fadd2_rn(bz, make_float2(yq.z.x, yq.z.y));
+    const float2 dz23 = __fadd2_rn(bz, make_float2(yq.z.z, yq.z.w));
+    const float2 c01 = __ffma2_rn(dz01, dz01, __ffma2_rn(dy01, dy01, __fmul2_rn(dx01, dx01)));
+    const float2 c23 = __ffma2_rn(dz23, dz23, __ffma2_rn(dy23, dy23, __fmul2_rn(dx23, dx23)));
+    return make_float4(c01.x, c01.y, c23.x, c23.y);
   } else {
     return ld_stream(reinterpret_cast<const float4*>(s.C + i * s.ldc) + q);
   }
@@ -233,10 +251,13 @@ __device__ __forceinline__ float cost_one(const CostSrc& s, int64_t i, int64_t j
   }
 }
 template <bool OTF>
-__device__ __forceinline__ void load_y4(const CostSrc& s, int64_t q, float4* y4) {
+__device__ __forceinline__ void load_y4(const CostSrc& s, int64_t q, YQ& yq) {
   if constexpr (OTF) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) y4[k] = __ldg(s.Y + 4 * q + k);
+    const float4* Yn = reinterpret_cast<const float4*>(s.Yn);
+    const int64_t st = s.ypad >> 2;
+    yq.x = __ldg(Yn + q);
+    yq.y = __ldg(Yn + st + q);
+    yq.z = __ldg(Yn + 2 * st + q);
   }
 }
 
@@ -276,7 +297,7 @@ __device__ void row_exact_block(const int64_t* rows, const CostSrc src,
   for (int64_t q = threadIdx.x; q < nq; q += kRowThreads) {
     const double2 pa = __ldg(p2 + 2 * q), pb = __ldg(p2 + 2 * q + 1);
     const double q0 = pa.x * kLog2e, q1 = pa.y * kLog2e, q2 = pb.x * kLog2e, q3 = pb.y * kLog2e;
-    float4 y4[4];
+    YQ y4;
     load_y4<OTF>(src, q, y4);
     float4 c[R];
 #pragma unroll
@@ -444,7 +465,7 @@ __device__ __forceinline__ void row_shift_block(
   int chunk = 0;
   for (int64_t q = threadIdx.x; q < nq; q += kRowThreads) {
     const float4 V = __ldg(Vq + q), F = __ldg(Fq + q);
-    float4 y4[4];
+    YQ y4;
     load_y4<OTF>(src, q, y4);
     float4 c[R];
     if constexpr (!OTF && PF == 1) {
@@ -540,7 +561,7 @@ __device__ __forceinline__ void row_shift_block(
     if (code < 4 * nq) {
       const int64_t q = code >> 2;
       const int64_t ir = r0 + r < n ? r0 + r : n - 1;  // (no register-array indexing by r)
-      float4 y4[4];
+      YQ y4;
       load_y4<OTF>(src, q, y4);
       const float4 xi = OTF ? src.X[ir] : make_float4(0.f, 0.f, 0.f, 0.f);
       const float4 cq = cost_quad<OTF>(src, ir, q, xi, y4);
@@ -723,13 +744,13 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
   const int64_t i0 = row_lo + static_cast<int64_t>(blockIdx.y) * rows_per_split;
   const int64_t i1 = min(i0 + rows_per_split, row_hi);
   float Vc[4], vf[4];
-  float4 y4[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const double pj = (j0 + k < m) ? p[j0 + k] : 0.0;
     split_q(pj * kLog2e, Vc[k], vf[k]);
-    if (OTF) y4[k] = src.Y[(j0 + k < m) ? j0 + k : 0];
   }
+  YQ y4;
+  if (j0 < m) load_y4<OTF>(src, q, y4);
   // packed f32x2 form of  acc += w * ex2((Vc - Mc) - c kh + ((vf - mf) - c kl)):
   // bitwise the scalar expression, half the FP32 issue slots
   const float2 Vc01 = make_float2(Vc[0], Vc[1]), Vc23 = make_float2(Vc[2], Vc[3]);
@@ -752,14 +773,14 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
       float4 c[kColUnroll];
 #pragma unroll
       for (int r = 0; r < kColUnroll; ++r)
-        c[r] = cost_quad<OTF>(src, t0 + k + r, q, OTF ? sh_x[k + r] : y4[0], y4);
+        c[r] = cost_quad<OTF>(src, t0 + k + r, q, sh_x[OTF ? k + r : 0], y4);
 #pragma unroll
       for (int r = 0; r < kColUnroll; ++r) col_quad_step(c[r], sh_aux[k + r], Vc01, Vc23, vf01,
                                                           vf23, nkh2, nkl2, acc01, acc23);
       if (((k + kColUnroll) % kFlushRows) == 0) flush_acc(acc01, acc23, acc64);
     }
     for (; k < tn; ++k) {
-      const float4 cv = cost_quad<OTF>(src, t0 + k, q, OTF ? sh_x[k] : y4[0], y4);
+      const float4 cv = cost_quad<OTF>(src, t0 + k, q, sh_x[OTF ? k : 0], y4);
       col_quad_step(cv, sh_aux[k], Vc01, Vc23, vf01, vf23, nkh2, nkl2, acc01, acc23);
     }
     flush_acc(acc01, acc23, acc64);
@@ -1562,6 +1583,8 @@ static CostSrc cost_src(const Problem& P) {
   s.ldc = P.ldc;
   s.X = reinterpret_cast<const float4*>(P.X);
   s.Y = reinterpret_cast<const float4*>(P.Y);
+  s.Yn = P.Yn;
+  s.ypad = P.mpad;
   return s;
 }
 
