@@ -1620,12 +1620,13 @@ void launch_row_pass(Problem& P) {
     const float kh = static_cast<float>(k2);
     const float kl = static_cast<float>(k2 - static_cast<double>(kh));
     const CostSrc src = cost_src(P);
-    // L2 prefetch of the cost two column chunks ahead (OTG_ROW_PF: 0 off,
-    // 1 = L2::256B loads, 3 / 5 = prefetch 2 / 4 chunks ahead).  B200, 65536^2:
-    // 3.19 ms (off) -> 2.95 ms (3), although it costs 76 registers (3 CTAs/SM)
+    // L2 prefetch of the cost ahead of the loads (OTG_ROW_PF: 0 off, 1 =
+    // L2::256B loads, 3 / 5 = prefetch 2 / 4 chunks ahead).  B200, 65536^2:
+    // with the scalar inner loop 3.19 ms (off) -> 2.95 ms (3); with the packed
+    // f32x2 loop both take ~2.92 ms (3 CTAs/SM either way), so it is off
     static const int row_pf = [] {
       const char* s = getenv("OTG_ROW_PF");
-      return s ? atoi(s) : 3;
+      return s ? atoi(s) : 0;
     }();
 #define OTG_SHIFT_ARGS                                                                        \
   src, P.n_local, P.m, P.vq, P.dq, P.mpad, kh, kl, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow,  \
