@@ -1,6 +1,7 @@
 // capi.cpp — ABI-level helpers: thread-local last error, version, devices.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -10,6 +11,13 @@ namespace {
 thread_local std::string g_last_error;
 }
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* s = getenv("OTG_PDL");
+    return !s || atoi(s) != 0;
+  }();
+  return on;
+}
 }  // namespace otg
 
 extern "C" {

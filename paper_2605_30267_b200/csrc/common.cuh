@@ -74,6 +74,34 @@ __device__ __forceinline__ double cost_at(const double* __restrict__ C64,
 }
 #endif
 
+// -------------------------------------------- programmatic dependent launch --
+// Every graph kernel is launched with programmatic stream serialization and
+// starts with griddepcontrol.wait: the next kernel's grid is set up while the
+// previous one drains (no early trigger, so no resource contention), then it
+// waits for the previous grid's completion and memory flush before touching
+// its outputs.  OTG_PDL=0 turns the attribute off (plain stream order).
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#endif
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  OTG_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 // ------------------------------------------------------------ loop control --
 enum Mode : int {
   MODE_EVAL = 0,       // one eval_normalized_step

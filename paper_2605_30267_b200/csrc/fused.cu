@@ -168,6 +168,7 @@ k_sp_prep(int64_t n, const double* __restrict__ rowM2, const int* __restrict__ r
           const double* __restrict__ dq, const double* __restrict__ a,
           const double* __restrict__ loga, RowRec* __restrict__ rec,
           const Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done || !ctrl->shift_valid) return;
   const double dmax2 = ctrl->dmax2;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; i < n;
@@ -206,6 +207,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // throttle is the slot ring.
 __global__ void __launch_bounds__(kCT, 1)
 k_sp(const SpArgs A, const Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done || !ctrl->shift_valid) return;  // uniform: written by earlier launches
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SpShared& S = *reinterpret_cast<SpShared*>(smem_raw);
@@ -466,6 +468,7 @@ k_sp_patch(const float* __restrict__ C, int64_t ldc, int64_t m, const double* __
            float kh, float kl, const float4* __restrict__ aux, const int* __restrict__ bad_rows,
            const int* __restrict__ bad_count, int64_t n, int ncl, double* __restrict__ out,
            const Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   // columns of the rows the stream kernel skipped: out[j] = sum over the
   // listed rows (cluster order, then row order) of w_i ex2(t_ij), with the
   // exact split shift k_row_redo wrote into aux -- the k_col_fast formula
@@ -575,7 +578,7 @@ void fused_alloc(Problem& P) {
 // loose rows, their column patch into partial row `fused_clusters`.
 void launch_fused(Problem& P, float kh, float kl) {
   RowRec* rec = reinterpret_cast<RowRec*>(P.sp_rec);
-  k_sp_prep<<<296, 256, 0, P.stream>>>(P.n_local, P.rowM2, P.rowJ, P.dq, P.a, P.loga, rec,
+  launch_k(k_sp_prep, 296, 256, 0, P.stream, P.n_local, P.rowM2, P.rowJ, P.dq, P.a, P.loga, rec,
                                        P.ctrl);
   SpArgs A;
   A.rec = rec;
@@ -620,7 +623,7 @@ void launch_fused(Problem& P, float kh, float kl) {
   OTG_CUDA(cudaLaunchKernelEx(&cfg, k_sp, A, static_cast<const Ctrl*>(P.ctrl)));
   launch_sp_redo(P, P.sp_bad_rows, P.sp_bad_count, P.fused_clusters);
   const unsigned g = static_cast<unsigned>((P.m + kPatchThreads - 1) / kPatchThreads);
-  k_sp_patch<<<g, kPatchThreads, 0, P.stream>>>(
+  launch_k(k_sp_patch, g, kPatchThreads, 0, P.stream, 
       P.C32, P.ldc, P.m, P.p, kh, kl, P.aux, P.sp_bad_rows, P.sp_bad_count, P.n_local,
       P.fused_clusters, P.part + static_cast<int64_t>(P.fused_clusters) * P.mpad, P.ctrl);
   OTG_CUDA(cudaGetLastError());

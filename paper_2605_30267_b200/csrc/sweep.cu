@@ -153,6 +153,7 @@ k_row_precise(const double* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
               const double* __restrict__ loga, double* __restrict__ rowM,
               double* __restrict__ rowS, double* __restrict__ u, double* __restrict__ wrow,
               double* __restrict__ rowpart, const Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done) return;
   constexpr int RPB = kRowThreads / G;
   __shared__ double sh[kRowThreads / 32];
@@ -376,6 +377,7 @@ k_row_redo(const CostSrc src, int64_t m, const double* __restrict__ p,
            double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
            int* __restrict__ rowJ, const int* __restrict__ redo_rows,
            const Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done || !ctrl->shift_valid) return;
   const unsigned cnt = ctrl->redo_count;
   for (unsigned k = blockIdx.x; k < cnt; k += gridDim.x) {
@@ -628,6 +630,7 @@ k_sp_redo(const CostSrc src, int64_t n, int64_t m, const double* __restrict__ p,
           double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
           int* __restrict__ rowJ, const int* __restrict__ bad_rows,
           const int* __restrict__ bad_count, int ncl, Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done || !ctrl->shift_valid) return;
   for (int c = 0; c < ncl; ++c) {
     const int nb = bad_count[c];
@@ -654,6 +657,7 @@ k_row_exact(const CostSrc src, int64_t n, int64_t m, const double* __restrict__ 
             double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
             double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
             int* __restrict__ rowJ, const Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done || ctrl->shift_valid) return;
   int64_t rows[R];
   bool valid[R];
@@ -675,6 +679,7 @@ k_row_shift(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ v
             double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
             double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
             int* __restrict__ rowJ, int* __restrict__ redo_rows, Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done || !ctrl->shift_valid) return;
   row_shift_block<R, OTF, PF>(src, n, m, vq, dq, mpad, kh, kl, a, loga, rowM, rowS, u, wrow, aux,
                               rowM2, rowJ, redo_rows, ctrl, static_cast<int64_t>(blockIdx.x) * R,
@@ -689,6 +694,7 @@ k_col_precise(const double* __restrict__ C, int64_t ldc, int64_t m,
               const double* __restrict__ wrow, int64_t row_lo, int64_t row_hi,
               int64_t rows_per_split, double* __restrict__ part, int64_t mpad,
               const Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done) return;
   const int64_t j = static_cast<int64_t>(blockIdx.x) * kColThreads + threadIdx.x;
   const int64_t i0 = row_lo + static_cast<int64_t>(blockIdx.y) * rows_per_split;
@@ -735,6 +741,7 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
            const float4* __restrict__ aux, int64_t row_lo, int64_t row_hi,
            int64_t rows_per_split, double* __restrict__ part, int64_t mpad,
            const Ctrl* __restrict__ ctrl, int exact_only) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   // exact_only: the single-pass kernel (fused.cu) does the steady-state columns
   if (ctrl->done || (exact_only && ctrl->shift_valid)) return;
   __shared__ float4 sh_aux[kAuxTile];
@@ -851,6 +858,7 @@ k_merge(const double* __restrict__ part, int nshards, int splits, int64_t m, int
         double* __restrict__ col, double* __restrict__ col_log, int* __restrict__ flag_idx,
         int* __restrict__ fb_cols, const double* __restrict__ u, const double* __restrict__ a,
         int64_t nrows, int do_merge, int flag, Ctrl* __restrict__ ctrl, int fused_rows) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done) return;
   __shared__ double sh[kEThreads / 32];
   merge_body(part, nshards, splits, m, mpad, col, col_log, flag_idx, fb_cols, u, a, nrows,
@@ -917,6 +925,7 @@ k_fallback(const double* __restrict__ C64, const CostSrc src, int64_t ldc, int64
            double kappa, const double* __restrict__ u, const double* __restrict__ p,
            const int* __restrict__ fb_cols, double2* __restrict__ fb_part,
            const Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done) return;
   const unsigned nf = ctrl->fb_count;
   if (nf == 0) return;
@@ -932,6 +941,7 @@ __global__ void __launch_bounds__(kEThreads)
 k_fb_local(int64_t m, const int* __restrict__ flag_idx, const double2* __restrict__ fb_part,
            double* __restrict__ fbA, double* __restrict__ fbS, double* __restrict__ fbT,
            const Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done) return;
   const int64_t j = static_cast<int64_t>(blockIdx.x) * kEThreads + threadIdx.x;
   if (j >= m) return;
@@ -953,6 +963,7 @@ __global__ void __launch_bounds__(kEThreads)
 k_fb_rescale(int64_t m, const int* __restrict__ flag_idx, const double* __restrict__ fbA,
              double* __restrict__ fbS, const double* __restrict__ fbT,
              const Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done) return;
   const int64_t j = static_cast<int64_t>(blockIdx.x) * kEThreads + threadIdx.x;
   if (j >= m || flag_idx[j] < 0) return;
@@ -1221,6 +1232,7 @@ __device__ __forceinline__ void finalize_tail(const FinArgs& A, int nparts, doub
 
 __global__ void __launch_bounds__(kEThreads)
 k_finalize(const FinArgs A, Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done) return;
   __shared__ double sh[kEThreads / 32];
   __shared__ bool last;
@@ -1406,6 +1418,7 @@ __device__ __forceinline__ void apply_tail(const AppArgs& A, int nparts, double*
 
 __global__ void __launch_bounds__(kEThreads)
 k_apply(const AppArgs A, Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (!ctrl->live_e2) return;
   __shared__ double sh[kEThreads / 32];
   __shared__ bool last;
@@ -1466,6 +1479,7 @@ struct EpiArgs {
 
 __global__ void __launch_bounds__(kEThreads)
 k_epilogue(const EpiArgs E, Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done) return;  // uniform: written by an earlier launch
   __shared__ double sh[kEThreads / 32];
   const int blk = blockIdx.x, nblk = gridDim.x;
@@ -1604,11 +1618,11 @@ void launch_row_pass(Problem& P) {
   double* rowpart = P.e1_part + P.e_blocks * 8;  // scratch after the E1 partials
   if (P.storage == OTG_STORE_F64) {
     if (P.m <= 2048)
-      k_row_precise<32><<<blocks, kRowThreads, 0, P.stream>>>(
+      launch_k(k_row_precise<32>, blocks, kRowThreads, 0, P.stream, 
           P.C64, P.ldc, P.n_local, P.m, P.p, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, rowpart,
           P.ctrl);
     else
-      k_row_precise<kRowThreads><<<blocks, kRowThreads, 0, P.stream>>>(
+      launch_k(k_row_precise<kRowThreads>, blocks, kRowThreads, 0, P.stream, 
           P.C64, P.ldc, P.n_local, P.m, P.p, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, rowpart,
           P.ctrl);
   } else {
@@ -1632,24 +1646,24 @@ void launch_row_pass(Problem& P) {
   src, P.n_local, P.m, P.vq, P.dq, P.mpad, kh, kl, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow,  \
       P.aux, P.rowM2, P.rowJ, P.redo_rows, P.ctrl
 #define OTG_ROW(RR, OTF)                                                                      \
-  k_row_exact<RR, OTF><<<blocks, kRowThreads, 0, P.stream>>>(                                 \
+  launch_k(k_row_exact<RR, OTF>, blocks, kRowThreads, 0, P.stream,                                  \
       src, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,     \
       P.rowM2, P.rowJ, P.ctrl);                                                               \
   if (RR == 4 && !OTF && row_pf == 1)                                                         \
-    k_row_shift<RR, OTF, 1><<<blocks, kRowThreads, 0, P.stream>>>(OTG_SHIFT_ARGS);            \
+    launch_k(k_row_shift<RR, OTF, 1>, blocks, kRowThreads, 0, P.stream, OTG_SHIFT_ARGS);            \
   else if (RR == 4 && !OTF && row_pf == 3)                                                    \
-    k_row_shift<RR, OTF, 3><<<blocks, kRowThreads, 0, P.stream>>>(OTG_SHIFT_ARGS);            \
+    launch_k(k_row_shift<RR, OTF, 3>, blocks, kRowThreads, 0, P.stream, OTG_SHIFT_ARGS);            \
   else if (RR == 4 && !OTF && row_pf == 5)                                                    \
-    k_row_shift<RR, OTF, 5><<<blocks, kRowThreads, 0, P.stream>>>(OTG_SHIFT_ARGS);            \
+    launch_k(k_row_shift<RR, OTF, 5>, blocks, kRowThreads, 0, P.stream, OTG_SHIFT_ARGS);            \
   else                                                                                        \
-    k_row_shift<RR, OTF, 0><<<blocks, kRowThreads, 0, P.stream>>>(OTG_SHIFT_ARGS);            \
-  k_row_redo<OTF><<<296, kRowThreads, 0, P.stream>>>(src, P.m, P.p, P.kappa, P.a, P.loga,     \
+    launch_k(k_row_shift<RR, OTF, 0>, blocks, kRowThreads, 0, P.stream, OTG_SHIFT_ARGS);            \
+  launch_k(k_row_redo<OTF>, 296, kRowThreads, 0, P.stream, src, P.m, P.p, P.kappa, P.a, P.loga,     \
                                                      P.rowM, P.rowS, P.u, P.wrow, P.aux,      \
                                                      P.rowM2, P.rowJ, P.redo_rows, P.ctrl)
     const bool otf = P.storage == OTG_STORE_ON_THE_FLY;
     if (P.fused) {
       // exact first evaluation (two-pass), then the single-pass kernel
-      k_row_exact<4, false><<<blocks, kRowThreads, 0, P.stream>>>(
+      launch_k(k_row_exact<4, false>, blocks, kRowThreads, 0, P.stream, 
           src, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,
           P.rowM2, P.rowJ, P.ctrl);
       launch_fused(P, kh, kl);
@@ -1676,14 +1690,14 @@ void launch_col_pass(Problem& P) {
     double* part = P.part + static_cast<int64_t>(s) * P.col_splits * P.mpad;
     if (P.storage == OTG_STORE_F64) {
       dim3 grid(static_cast<unsigned>((P.m + kColThreads - 1) / kColThreads), P.col_splits);
-      k_col_precise<<<grid, kColThreads, 0, P.stream>>>(P.C64, P.ldc, P.m, P.p, P.rowM, P.wrow,
+      launch_k(k_col_precise, grid, kColThreads, 0, P.stream, P.C64, P.ldc, P.m, P.p, P.rowM, P.wrow,
                                                         lo, hi, P.rows_per_split, part, P.mpad,
                                                         P.ctrl);
     } else {
       const int NT = P.col_threads;
       dim3 grid(static_cast<unsigned>((P.m + 4 * NT - 1) / (4 * NT)), P.col_splits);
 #define OTG_COL(OTF, T)                                                                      \
-  k_col_fast<OTF, T><<<grid, T, 0, P.stream>>>(cost_src(P), P.m, P.p, kh, kl, P.aux, lo, hi, \
+  launch_k(k_col_fast<OTF, T>, grid, T, 0, P.stream, cost_src(P), P.m, P.p, kh, kl, P.aux, lo, hi, \
                                                P.rows_per_split, part, P.mpad, P.ctrl, P.fused)
       const bool otf = P.storage == OTG_STORE_ON_THE_FLY;
       if (NT == 512) {
@@ -1700,7 +1714,7 @@ void launch_col_pass(Problem& P) {
 }
 
 void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int ncl) {
-  k_sp_redo<<<148, kRowThreads, 0, P.stream>>>(cost_src(P), P.n_local, P.m, P.p, P.kappa, P.a,
+  launch_k(k_sp_redo, 148, kRowThreads, 0, P.stream, cost_src(P), P.n_local, P.m, P.p, P.kappa, P.a,
                                                 P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,
                                                 P.rowM2, P.rowJ, bad_rows, bad_count, ncl,
                                                 P.ctrl);
@@ -1714,7 +1728,7 @@ static void launch_merge(Problem& P, bool merge, bool flag) {
   const int64_t blocks = merge_blocks(P);
   const int shards = P.vshards;
   const int splits = P.col_splits;
-  k_merge<<<blocks, kEThreads, 0, P.stream>>>(P.part, shards, splits, P.m, P.mpad, P.col,
+  launch_k(k_merge, blocks, kEThreads, 0, P.stream, P.part, shards, splits, P.m, P.mpad, P.col,
                                               P.col_log, P.flag_idx, P.fb_cols, P.u, P.a,
                                               P.n_local, merge ? 1 : 0, flag ? 1 : 0, P.ctrl,
                                               P.fused ? P.fused_clusters + 1 : 0);
@@ -1852,34 +1866,34 @@ void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
   }
   if (!with_log) return;
   if (P.storage == OTG_STORE_F64)
-    k_fallback<true, false><<<296, kEThreads, 0, P.stream>>>(
+    launch_k(k_fallback<true, false>, 296, kEThreads, 0, P.stream, 
         P.C64, cost_src(P), P.ldc, P.n_local, P.kappa, P.u, P.p, P.fb_cols, P.fb_part, P.ctrl);
   else if (P.storage == OTG_STORE_ON_THE_FLY)
-    k_fallback<false, true><<<296, kEThreads, 0, P.stream>>>(
+    launch_k(k_fallback<false, true>, 296, kEThreads, 0, P.stream, 
         nullptr, cost_src(P), P.ldc, P.n_local, P.kappa, P.u, P.p, P.fb_cols, P.fb_part, P.ctrl);
   else
-    k_fallback<false, false><<<296, kEThreads, 0, P.stream>>>(
+    launch_k(k_fallback<false, false>, 296, kEThreads, 0, P.stream, 
         nullptr, cost_src(P), P.ldc, P.n_local, P.kappa, P.u, P.p, P.fb_cols, P.fb_part, P.ctrl);
   OTG_CUDA(cudaGetLastError());
   if (P.sharded) {
     // exact column LSE across ranks: local (top, sum) per flagged column,
     // MAX all-reduce of the tops, rescale, SUM all-reduce of the sums
     const unsigned g = static_cast<unsigned>((P.m + kEThreads - 1) / kEThreads);
-    k_fb_local<<<g, kEThreads, 0, P.stream>>>(P.m, P.flag_idx, P.fb_part, P.fbA, P.fbS, P.fbT,
+    launch_k(k_fb_local, g, kEThreads, 0, P.stream, P.m, P.flag_idx, P.fb_part, P.fbA, P.fbS, P.fbT,
                                               P.ctrl);
     comm_allreduce_max(P, P.fbA, static_cast<size_t>(P.m));
-    k_fb_rescale<<<g, kEThreads, 0, P.stream>>>(P.m, P.flag_idx, P.fbA, P.fbS, P.fbT, P.ctrl);
+    launch_k(k_fb_rescale, g, kEThreads, 0, P.stream, P.m, P.flag_idx, P.fbA, P.fbS, P.fbT, P.ctrl);
     comm_allreduce_sum(P, P.fbS, static_cast<size_t>(P.m));
     OTG_CUDA(cudaGetLastError());
   }
-  k_finalize<<<P.e_blocks, kEThreads, 0, P.stream>>>(fin_args(P, merge_blocks(P)), P.ctrl);
+  launch_k(k_finalize, P.e_blocks, kEThreads, 0, P.stream, fin_args(P, merge_blocks(P)), P.ctrl);
   OTG_CUDA(cudaGetLastError());
   P.apply_pending = 1;
 }
 
 void launch_apply(Problem& P) {
   if (!P.apply_pending) return;  // done inside the single-kernel epilogue
-  k_apply<<<P.e_blocks, kEThreads, 0, P.stream>>>(app_args(P), P.ctrl);
+  launch_k(k_apply, P.e_blocks, kEThreads, 0, P.stream, app_args(P), P.ctrl);
   OTG_CUDA(cudaGetLastError());
 }
 
