@@ -276,6 +276,7 @@ void launch_row_pass(Problem& P);
 void launch_col_pass(Problem& P);
 void launch_merge_nolog(Problem& P);
 void launch_sweeps(Problem& P, bool timed, cudaEvent_t* ev4);
+void launch_split_p(Problem& P);  // vq <- split of p (after the host sets p)
 bool fused_configure(Problem& P);
 void fused_alloc(Problem& P);
 void launch_fused(Problem& P, float kh, float kl);

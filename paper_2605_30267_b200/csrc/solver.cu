@@ -73,6 +73,11 @@ void get_ctrl(Problem& P) {
 void h2d(Problem& P, double* dst, const double* src, int64_t count) {
   OTG_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyHostToDevice, P.stream));
 }
+// New evaluation point from the host: p and its fp32 split (row pass input).
+void set_point(Problem& P, const double* v) {
+  h2d(P, P.p, v, P.m);
+  launch_split_p(P);
+}
 void d2h(Problem& P, double* dst, const double* src, int64_t count) {
   if (dst) OTG_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToHost, P.stream));
 }
@@ -226,7 +231,7 @@ void one_eval(Problem& P, const double* v, bool with_log) {
   Ctrl c = base_ctrl(P);
   c.mode = MODE_EVAL;
   put_ctrl(P, c);
-  h2d(P, P.p, v, P.m);
+  set_point(P, v);
   launch_eval(P, with_log, false, nullptr);
   if (with_log) launch_apply(P);
   get_ctrl(P);
@@ -301,7 +306,7 @@ otg_status otg_row_solve_marginals(otg_problem h, const double* v, double* u, do
     Ctrl c = base_ctrl(P);
     c.mode = MODE_EVAL;
     put_ctrl(P, c);
-    h2d(P, P.p, v, P.m);
+    set_point(P, v);
     launch_sweeps(P, false, nullptr);
     launch_merge_nolog(P);
     if (P.sharded) comm_allreduce_sum(P, P.col, static_cast<size_t>(P.mpad + 1));
@@ -357,7 +362,7 @@ otg_status otg_sinkhorn_solve(otg_problem h, const double* v0, const otg_solve_c
     c.record_trace = cfg->record_trace;
     c.trace_stride = cfg->trace_stride;
     put_ctrl(P, c);
-    h2d(P, P.p, v.data(), P.m);
+    set_point(P, v.data());
     const LoopOut lo = run_loop(P, res, res && res->time_sweeps);
     fill_result(P, res, lo);
   });
@@ -368,7 +373,7 @@ static void start_acc(Problem& P, Ctrl& c, const double* x0, const double* w0, d
   c.alpha_next = std::sqrt(2.0 * mu);  // accel.cpp:149
   c.alpha_step = c.alpha_next;
   put_ctrl(P, c);
-  h2d(P, P.p, x0, P.m);
+  set_point(P, x0);
   if (w0)
     h2d(P, P.wacc, w0, P.m);
   else
@@ -527,7 +532,7 @@ otg_status otg_time_sweeps(otg_problem h, const double* v, int reps, double ms[3
       Ctrl c = base_ctrl(P);
       c.mode = MODE_EVAL;
       put_ctrl(P, c);
-      h2d(P, P.p, v, P.m);
+      set_point(P, v);
       OTG_CUDA(cudaEventRecord(e[0], P.stream));
       launch_row_pass(P);  // exact first-evaluation kernels (no shift estimate here)
       OTG_CUDA(cudaEventRecord(e[1], P.stream));

@@ -646,19 +646,265 @@ k_sp_redo(const CostSrc src, int64_t n, int64_t m, const double* __restrict__ p,
   }
 }
 
-// fp32 row pass kernels: the exact body on the first evaluation of a solve
+// vq = quantised split of p * log2(e) (the row pass's column potential),
+// refreshed whenever the host sets a new evaluation point.
+__global__ void k_split_p(int64_t m, int64_t mpad, const double* __restrict__ p,
+                          float* __restrict__ vq) {
+  pdl_wait();
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    split_q(p[j] * kLog2e, vq[j], vq[mpad + j]);
+}
+
+__constant__ int c_online_first = 1;  // OTG_ONLINE_FIRST=0: fp64-argument first pass
+__device__ __forceinline__ bool online_first_pass() { return c_online_first != 0; }
+
+// fp32 storage, row statistics WITHOUT a shift estimate (first evaluation of
+// a solve): the k_row_shift inner loop with a per-thread RUNNING shift s (a
+// multiple of 2^-8, so V - s stays exact).  s starts at the thread's first
+// quad's (rounded-up) max; when a quad exceeds s by more than 8 the thread's
+// partial sums are rescaled by 2^-(delta) and s moves up (a handful of times
+// per row), so ex2 never overflows and the dominant terms keep full fp32
+// precision.  The CTA then folds the per-thread (s, sum, max) onto the
+// largest s.  Same arithmetic per element as the shift pass (~2x faster than
+// the fp64-argument row_exact_block it replaces on the first evaluation).
+template <int R, bool OTF>
+__device__ __forceinline__ void row_online_block(
+    const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq, int64_t mpad,
+    float kh, float kl,
+    const double* __restrict__ a, const double* __restrict__ loga, double* __restrict__ rowM,
+    double* __restrict__ rowS, double* __restrict__ u, double* __restrict__ wrow,
+    float4* __restrict__ aux, double* __restrict__ rowM2, int* __restrict__ rowJ, int64_t r0) {
+  __shared__ double sh[kRowThreads / 32];
+  __shared__ float shf[kRowThreads / 32];
+  __shared__ int shj[kRowThreads / 32];
+  __shared__ float resS0[R], resT[R];
+  __shared__ double resS[R];
+  __shared__ int resJ[R];
+  float s[R], tm[R];
+  int tq[R];
+  float2 fs2[R];
+  double ss[R];
+  int64_t rr[R];
+  float4 xr[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    s[r] = -FLT_MAX;  // no column seen yet
+    tm[r] = -FLT_MAX;
+    tq[r] = 0;
+    fs2[r] = make_float2(0.f, 0.f);
+    ss[r] = 0.0;
+    rr[r] = r0 + r < n ? r0 + r : n - 1;
+    xr[r] = OTF ? src.X[rr[r]] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const float2 nkh2 = make_float2(-kh, -kh), nkl2 = make_float2(-kl, -kl);
+  const int64_t nq = m >> 2;
+  const float4* Vq = reinterpret_cast<const float4*>(vq);
+  const float4* Fq = reinterpret_cast<const float4*>(vq + mpad);
+  {
+    // common starting shift per row: the max over the CTA's first 4 x 256
+    // columns (rounded up), so most threads never rescale
+    float rm[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) rm[r] = -FLT_MAX;
+    if (threadIdx.x < nq) {
+      const int64_t q = threadIdx.x;
+      const float4 V = __ldg(Vq + q), F = __ldg(Fq + q);
+      YQ y4;
+      load_y4<OTF>(src, q, y4);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float2 r01, r23;
+        quad_exponents(cost_quad<OTF>(src, rr[r], q, xr[r], y4), make_float2(V.x, V.y),
+                       make_float2(V.z, V.w), make_float2(F.x, F.y), make_float2(F.z, F.w),
+                       make_float2(0.f, 0.f), nkh2, nkl2, r01, r23);
+        rm[r] = fmaxf(fmaxf(r01.x, r01.y), fmaxf(r23.x, r23.y));
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float b = rm[r];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+      __syncthreads();
+      if ((threadIdx.x & 31) == 0) shf[threadIdx.x >> 5] = b;
+      __syncthreads();
+      float B = -FLT_MAX;
+#pragma unroll
+      for (int k = 0; k < kRowThreads / 32; ++k) B = fmaxf(B, shf[k]);
+      if (B > -FLT_MAX) s[r] = ceilf(B * 256.0f) * (1.0f / 256.0f);
+    }
+  }
+  int chunk = 0;
+  for (int64_t q = threadIdx.x; q < nq; q += kRowThreads) {
+    const float4 V = __ldg(Vq + q), F = __ldg(Fq + q);
+    YQ y4;
+    load_y4<OTF>(src, q, y4);
+    float4 c[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) c[r] = cost_quad<OTF>(src, rr[r], q, xr[r], y4);
+    const float2 V01 = make_float2(V.x, V.y), V23 = make_float2(V.z, V.w);
+    const float2 F01 = make_float2(F.x, F.y), F23 = make_float2(F.z, F.w);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float2 t01, t23;
+      quad_exponents(c[r], V01, V23, F01, F23, make_float2(-s[r], -s[r]), nkh2, nkl2, t01, t23);
+      float mx = fmaxf(fmaxf(t01.x, t01.y), fmaxf(t23.x, t23.y));
+      if (mx > 8.0f) {  // a max well above the running shift: move s up (rare)
+        const float d = ceilf(mx * 256.0f) * (1.0f / 256.0f) + 16.0f;  // 16 of headroom
+        s[r] += d;
+        const float sc = ex2_approx(-d);
+        fs2[r] = make_float2(fs2[r].x * sc, fs2[r].y * sc);
+        ss[r] *= exp2(-static_cast<double>(d));
+        tm[r] -= d;
+        quad_exponents(c[r], V01, V23, F01, F23, make_float2(-s[r], -s[r]), nkh2, nkl2, t01, t23);
+        mx = fmaxf(fmaxf(t01.x, t01.y), fmaxf(t23.x, t23.y));
+      }
+      tq[r] = mx > tm[r] ? static_cast<int>(4 * q) : tq[r];
+      tm[r] = fmaxf(tm[r], mx);
+      const float2 e = __fadd2_rn(make_float2(ex2_approx(t01.x), ex2_approx(t23.x)),
+                                  make_float2(ex2_approx(t01.y), ex2_approx(t23.y)));
+      fs2[r] = __fadd2_rn(fs2[r], e);
+    }
+    if (++chunk == 4) {
+      chunk = 0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        ss[r] += static_cast<double>(fs2[r].x) + static_cast<double>(fs2[r].y);
+        fs2[r] = make_float2(0.f, 0.f);
+      }
+    }
+  }
+  for (int64_t j = 4 * nq + threadIdx.x; j < m; j += kRowThreads) {  // ragged tail
+    const float V = vq[j], F = vq[mpad + j];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const float c = cost_one<OTF>(src, rr[r], j);
+      if (s[r] == -FLT_MAX) s[r] = ceilf((fmaf(-c, kh, V) + fmaf(-c, kl, F)) * 256.0f) * (1.0f / 256.0f);
+      float t = fmaf(-c, kh, V - s[r]) + fmaf(-c, kl, F);
+      if (t > 8.0f) {
+        const float d = ceilf(t * 256.0f) * (1.0f / 256.0f);
+        s[r] += d;
+        const float sc = ex2_approx(-d);
+        fs2[r] = make_float2(fs2[r].x * sc, fs2[r].y * sc);
+        ss[r] *= exp2(-static_cast<double>(d));
+        tm[r] -= d;
+        t = fmaf(-c, kh, V - s[r]) + fmaf(-c, kl, F);
+      }
+      if (t > tm[r]) {
+        tm[r] = t;
+        tq[r] = static_cast<int>(j);
+      }
+      fs2[r].x += ex2_approx(t);
+    }
+  }
+  // fold the threads onto the CTA's largest running shift
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    ss[r] += static_cast<double>(fs2[r].x) + static_cast<double>(fs2[r].y);
+    float sb = s[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sb = fmaxf(sb, __shfl_xor_sync(0xffffffffu, sb, o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) shf[threadIdx.x >> 5] = sb;
+    __syncthreads();
+    float S0 = -FLT_MAX;
+#pragma unroll
+    for (int k = 0; k < kRowThreads / 32; ++k) S0 = fmaxf(S0, shf[k]);
+    const bool seen = s[r] != -FLT_MAX;
+    const double part = seen ? ss[r] * exp2(static_cast<double>(s[r] - S0)) : 0.0;
+    float t = seen ? (s[r] - S0) + tm[r] : -FLT_MAX;  // max relative to S0
+    int jj = tq[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float t2 = __shfl_xor_sync(0xffffffffu, t, o);
+      const int j2 = __shfl_xor_sync(0xffffffffu, jj, o);
+      if (t2 > t || (t2 == t && j2 < jj)) {
+        t = t2;
+        jj = j2;
+      }
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+      shf[threadIdx.x >> 5] = t;
+      shj[threadIdx.x >> 5] = jj;
+    }
+    __syncthreads();
+    float T = -FLT_MAX;
+    int J = 0;
+#pragma unroll
+    for (int k = 0; k < kRowThreads / 32; ++k)
+      if (shf[k] > T || (shf[k] == T && shj[k] < J)) {
+        T = shf[k];
+        J = shj[k];
+      }
+    const double Ssum = block_sum<kRowThreads>(part, sh);
+    if (threadIdx.x == 0) {
+      resS0[r] = S0;
+      resT[r] = T;
+      resS[r] = Ssum;
+      resJ[r] = J;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < R) {
+    const int r = threadIdx.x;
+    const int64_t i = r0 + r;
+    const int code = resJ[r];
+    const float S0 = resS0[r];
+    int J = code;
+    if (code < 4 * nq) {  // column of the max inside the winning quad
+      const int64_t q = code >> 2;
+      const int64_t ir = i < n ? i : n - 1;
+      YQ y4;
+      load_y4<OTF>(src, q, y4);
+      const float4 xi = OTF ? src.X[ir] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 cq = cost_quad<OTF>(src, ir, q, xi, y4);
+      const float4 V = __ldg(Vq + q), F = __ldg(Fq + q);
+      float2 t01, t23;
+      quad_exponents(cq, make_float2(V.x, V.y), make_float2(V.z, V.w), make_float2(F.x, F.y),
+                     make_float2(F.z, F.w), make_float2(-S0, -S0), nkh2, nkl2, t01, t23);
+      const float em = fmaxf(fmaxf(t01.x, t01.y), fmaxf(t23.x, t23.y));
+      J = code + (t01.x == em ? 0 : t01.y == em ? 1 : t23.x == em ? 2 : 3);
+    }
+    if (i < n) {
+      const double S = resS[r];
+      const double sc = static_cast<double>(S0);
+      const double M = sc * kLn2;
+      const double wi = a[i] / S;
+      rowM[i] = M;
+      rowS[i] = S;
+      u[i] = (loga[i] - M) - log(S);
+      wrow[i] = wi;
+      rowM2[i] = sc + static_cast<double>(resT[r]);
+      rowJ[i] = J;
+      aux[i] = make_float4(S0, 0.0f, static_cast<float>(wi), 0.0f);
+    }
+  }
+}
+
+// fp32 row pass kernels: the exact body on the first evaluation of a solve// fp32 row pass kernels: the exact body on the first evaluation of a solve
 // (no previous point), the shift-estimate body after; each returns at once
 // when its case does not apply.  (Kept as two kernels: one kernel holding both
 // bodies needs 76 registers and drops the shift pass to 3 CTAs per SM.)
 template <int R, bool OTF>
-__global__ void __launch_bounds__(kRowThreads)
+__global__ void __launch_bounds__(kRowThreads, (R == 4 && !OTF) ? 3 : 1)
 k_row_exact(const CostSrc src, int64_t n, int64_t m, const double* __restrict__ p, double kappa,
             const double* __restrict__ a, const double* __restrict__ loga,
             double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
             double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
-            int* __restrict__ rowJ, const Ctrl* __restrict__ ctrl) {
+            int* __restrict__ rowJ, const Ctrl* __restrict__ ctrl, const float* __restrict__ vq,
+            int64_t mpad) {
   pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done || ctrl->shift_valid) return;
+  if (online_first_pass()) {
+    const double k2 = kappa * kLog2e;
+    const float kh = static_cast<float>(k2);
+    const float kl = static_cast<float>(k2 - static_cast<double>(kh));
+    row_online_block<R, OTF>(src, n, m, vq, mpad, kh, kl, a, loga, rowM, rowS, u, wrow, aux,
+                             rowM2, rowJ, static_cast<int64_t>(blockIdx.x) * R);
+    return;
+  }
   int64_t rows[R];
   bool valid[R];
 #pragma unroll
@@ -1544,6 +1790,11 @@ static int64_t col_slots(const Problem& P) {
 }
 
 void configure_sweeps(Problem& P) {
+  static const int online = [] {
+    const char* s = getenv("OTG_ONLINE_FIRST");
+    return s ? atoi(s) : 1;
+  }();
+  OTG_CUDA(cudaMemcpyToSymbol(c_online_first, &online, sizeof(int)));
   // column-pass split: ~24 CTAs per SM over the grid so the dynamic CTA
   // scheduler balances the 148 SMs (ncu: 640 CTAs = 0.48 waves was
   // latency-bound); partials cost splits * m * 8 B (< 1% of the sweep)
@@ -1648,7 +1899,7 @@ void launch_row_pass(Problem& P) {
 #define OTG_ROW(RR, OTF)                                                                      \
   launch_k(k_row_exact<RR, OTF>, blocks, kRowThreads, 0, P.stream,                                  \
       src, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,     \
-      P.rowM2, P.rowJ, P.ctrl);                                                               \
+      P.rowM2, P.rowJ, P.ctrl, P.vq, P.mpad);                                                 \
   if (RR == 4 && !OTF && row_pf == 1)                                                         \
     launch_k(k_row_shift<RR, OTF, 1>, blocks, kRowThreads, 0, P.stream, OTG_SHIFT_ARGS);            \
   else if (RR == 4 && !OTF && row_pf == 3)                                                    \
@@ -1665,7 +1916,7 @@ void launch_row_pass(Problem& P) {
       // exact first evaluation (two-pass), then the single-pass kernel
       launch_k(k_row_exact<4, false>, blocks, kRowThreads, 0, P.stream, 
           src, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,
-          P.rowM2, P.rowJ, P.ctrl);
+          P.rowM2, P.rowJ, P.ctrl, P.vq, P.mpad);
       launch_fused(P, kh, kl);
     } else if (R == 8) {
       if (otf) { OTG_ROW(8, true); } else { OTG_ROW(8, false); }
@@ -1711,6 +1962,12 @@ void launch_col_pass(Problem& P) {
     }
   }
   OTG_CUDA(cudaGetLastError());
+}
+
+void launch_split_p(Problem& P) {
+  if (P.storage == OTG_STORE_F64) return;
+  const unsigned g = static_cast<unsigned>(std::min<int64_t>((P.m + 255) / 256, 1184));
+  launch_k(k_split_p, g, 256, 0, P.stream, P.m, P.mpad, P.p, P.vq);
 }
 
 void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int ncl) {
