@@ -218,7 +218,7 @@ struct Problem {
 
   // single-pass fused sweep (fused.cu), fp32 storage only
   int fused = 0, fused_qpt = 0, fused_W = 0, fused_slots = 0, fused_smem = 0,
-      fused_clusters = 0;
+      fused_clusters = 0, fused_cl = 8;
   double* sp_rec = nullptr;     // per-row 32-byte records (shift estimate, a, log a)
   int* sp_bad_rows = nullptr;   // rows whose shift estimate was loose, per cluster
   int* sp_bad_count = nullptr;

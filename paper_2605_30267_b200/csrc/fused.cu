@@ -42,7 +42,8 @@ namespace otg {
 
 namespace {
 
-constexpr int kCL = 8;                       // CTAs per cluster
+constexpr int kCLMax = 8;                    // CTAs per cluster: 8 (row slices), or 1
+                                             // when a whole row fits one CTA (m <= 8192)
 constexpr int kSW = 8;                       // stats warps
 constexpr int kCW = 8;                       // column warps
 constexpr int kST = kSW * 32;                // threads per role
@@ -73,7 +74,7 @@ struct SpShared {
   uint64_t sdone[kSlotsMax];   // stats warps -> column warps (e in the slot, partials)
   uint64_t empty[kSlotsMax];   // column warps -> loader (slot free)
   uint64_t xbar[kXD];          // cluster partials of a row received
-  Msg xin[kXD][kCL];
+  Msg xin[kXD][kCLMax];
   RowRec rec[kSlotsMax];
   unsigned wkey[kSlotsMax][kSW];  // stats-warp partials of the row in each slot
   int wcode[kSlotsMax][kSW];
@@ -205,6 +206,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // sums.  Hand-offs are mbarriers (full / sdone / empty / xbar), so the stats of
 // row k overlap the exchange and column step of earlier rows; the only
 // throttle is the slot ring.
+template <int CL>
 __global__ void __launch_bounds__(kCT, 1)
 k_sp(const SpArgs A, const Ctrl* __restrict__ ctrl) {
   pdl_wait();  // programmatic dependent launch: after the previous kernel
@@ -217,7 +219,7 @@ k_sp(const SpArgs A, const Ctrl* __restrict__ ctrl) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t rank = cluster_rank();
-  const int64_t cid = blockIdx.x / kCL, ncl = gridDim.x / kCL;
+  const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   const int64_t r0 = A.n * cid / ncl, r1 = A.n * (cid + 1) / ncl;
   const int R = static_cast<int>(r1 - r0);
   const int64_t col0 = static_cast<int64_t>(rank) * A.W;
@@ -354,9 +356,9 @@ k_sp(const SpArgs A, const Ctrl* __restrict__ ctrl) {
             0xffffffffu,
             (lane < kSW && lk == ck) ? static_cast<unsigned>(S.wcode[sp][lane]) : 0x7fffffffu);
         const float cm = key_to_float(ck);
-        if (lane == 0) mbar_expect_tx(&S.xbar[xp], kCL * 16u);
+        if (lane == 0) mbar_expect_tx(&S.xbar[xp], CL * 16u);
         cs = __shfl_sync(0xffffffffu, cs, 0);
-        if (lane < kCL) {
+        if (lane < CL) {
           uint32_t ra, rbar;
           asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
                        : "=r"(ra)
@@ -386,7 +388,7 @@ k_sp(const SpArgs A, const Ctrl* __restrict__ ctrl) {
       float T = -FLT_MAX;
       int J = 0x7fffffff;
 #pragma unroll
-      for (int c = 0; c < kCL; ++c) {  // fixed order: every CTA gets the same S, T, J
+      for (int c = 0; c < CL; ++c) {  // fixed order: every CTA gets the same S, T, J
         const Msg msg = S.xin[xs][c];
         Ssum += msg.sum;
         if (msg.max > T || (msg.max == T && msg.code < J)) {
@@ -409,7 +411,7 @@ k_sp(const SpArgs A, const Ctrl* __restrict__ ctrl) {
           kahan2(acc23[q], cmp23[q], __ffma2_rn(w2, make_float2(ev.z, ev.w), make_float2(0.f, 0.f)));
         }
         // row outputs (k_row_shift's epilogue): one CTA per row, rotating
-        if (static_cast<int>(rank) == (k & (kCL - 1)) && cw == 1 && lane == 0) {
+        if (static_cast<int>(rank) == (k & (CL - 1)) && cw == 1 && lane == 0) {
           const double scd = static_cast<double>(sc);
           const double M = scd * kLn2;
           A.rowM[i] = M;
@@ -499,26 +501,30 @@ long long*& sp_trace_buf() {
   return p;
 }
 
-int sp_clusters(int smem) {
-  static int cached = -1;
-  static int cached_smem = -1;
-  if (cached >= 0 && cached_smem == smem) return cached;
-  OTG_CUDA(cudaFuncSetAttribute(k_sp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+template <int CL>
+cudaLaunchConfig_t sp_config(unsigned clusters, int smem, cudaStream_t stream,
+                             cudaLaunchAttribute* attr) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(kCL * 148);
+  cfg.gridDim = dim3(CL * clusters);
   cfg.blockDim = dim3(kCT);
   cfg.dynamicSmemBytes = smem;
-  cudaLaunchAttribute attr;
-  attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = kCL;
-  attr.val.clusterDim.y = 1;
-  attr.val.clusterDim.z = 1;
-  cfg.attrs = &attr;
+  cfg.stream = stream;
+  attr->id = cudaLaunchAttributeClusterDimension;
+  attr->val.clusterDim.x = CL;
+  attr->val.clusterDim.y = 1;
+  attr->val.clusterDim.z = 1;
+  cfg.attrs = attr;
   cfg.numAttrs = 1;
+  return cfg;
+}
+
+template <int CL>
+int sp_clusters(int smem) {
+  OTG_CUDA(cudaFuncSetAttribute(k_sp<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  cudaLaunchAttribute attr;
+  cudaLaunchConfig_t cfg = sp_config<CL>(148, smem, nullptr, &attr);
   int ncl = 0;
-  OTG_CUDA(cudaOccupancyMaxActiveClusters(&ncl, k_sp, &cfg));
-  cached = ncl;
-  cached_smem = smem;
+  OTG_CUDA(cudaOccupancyMaxActiveClusters(&ncl, k_sp<CL>, &cfg));
   return ncl;
 }
 
@@ -535,8 +541,9 @@ bool fused_configure(Problem& P) {
   if (P.storage != OTG_STORE_F32 || P.vshards != 1) return false;
   const char* s = getenv("OTG_FUSED");
   if (!s || atoi(s) == 0) return false;
-  const int64_t W = round_up((P.m + kCL - 1) / kCL, 4);
-  if (W * kCL > P.ldc) return false;          // C rows must hold whole slices
+  const int CL = P.m <= 4 * kST * kQPT ? 1 : kCLMax;  // whole rows per CTA when they fit
+  const int64_t W = round_up((P.m + CL - 1) / CL, 4);
+  if (W * CL > P.ldc) return false;           // C rows must hold whole slices
   if (W > 4 * kST * kQPT) return false;       // columns per CTA held in registers
   if (P.n_local < 16 * 8 || P.m < 1024) return false;
   const int64_t head = ((sizeof(SpShared) + 127) / 128) * 128;
@@ -547,10 +554,10 @@ bool fused_configure(Problem& P) {
   int lag = lag_env ? atoi(lag_env) : 3;
   lag = std::max(0, std::min(std::min(lag, kLagMax), nslots - 2));
   const int smem = static_cast<int>(head + static_cast<int64_t>(nslots) * (W * 4 + kST * 4));
-  int ncl = sp_clusters(smem);
+  int ncl = CL == 1 ? sp_clusters<1>(smem) : sp_clusters<kCLMax>(smem);
   if (getenv("OTG_VERBOSE"))
-    fprintf(stderr, "[otg] single-pass: W=%lld smem=%d slots=%d lag=%d clusters=%d\n",
-            static_cast<long long>(W), smem, nslots, lag, ncl);
+    fprintf(stderr, "[otg] single-pass: CL=%d W=%lld smem=%d slots=%d lag=%d clusters=%d\n",
+            CL, static_cast<long long>(W), smem, nslots, lag, ncl);
   if (ncl < 1) return false;
   // at least ~16 rows per cluster so the pipeline fill is amortised
   ncl = static_cast<int>(std::min<int64_t>(ncl, std::max<int64_t>(1, P.n_local / 16)));
@@ -560,6 +567,7 @@ bool fused_configure(Problem& P) {
   P.fused_clusters = ncl;
   P.fused_slots = nslots;
   P.fused_qpt = lag;  // (column-step lag of the single-pass kernel)
+  P.fused_cl = CL;
   return true;
 }
 
@@ -608,19 +616,14 @@ void launch_fused(Problem& P, float kh, float kl) {
   A.nslots = P.fused_slots;
   A.lag = P.fused_qpt;
   A.dbg = sp_trace_buf();
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(kCL * P.fused_clusters));
-  cfg.blockDim = dim3(kCT);
-  cfg.dynamicSmemBytes = static_cast<size_t>(P.fused_smem);
-  cfg.stream = P.stream;
   cudaLaunchAttribute attr;
-  attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = kCL;
-  attr.val.clusterDim.y = 1;
-  attr.val.clusterDim.z = 1;
-  cfg.attrs = &attr;
-  cfg.numAttrs = 1;
-  OTG_CUDA(cudaLaunchKernelEx(&cfg, k_sp, A, static_cast<const Ctrl*>(P.ctrl)));
+  if (P.fused_cl == 1) {
+    cudaLaunchConfig_t cfg = sp_config<1>(P.fused_clusters, P.fused_smem, P.stream, &attr);
+    OTG_CUDA(cudaLaunchKernelEx(&cfg, k_sp<1>, A, static_cast<const Ctrl*>(P.ctrl)));
+  } else {
+    cudaLaunchConfig_t cfg = sp_config<kCLMax>(P.fused_clusters, P.fused_smem, P.stream, &attr);
+    OTG_CUDA(cudaLaunchKernelEx(&cfg, k_sp<kCLMax>, A, static_cast<const Ctrl*>(P.ctrl)));
+  }
   launch_sp_redo(P, P.sp_bad_rows, P.sp_bad_count, P.fused_clusters);
   const unsigned g = static_cast<unsigned>((P.m + kPatchThreads - 1) / kPatchThreads);
   launch_k(k_sp_patch, g, kPatchThreads, 0, P.stream, 
