@@ -38,7 +38,7 @@ extern "C" {
 #endif
 
 #define OTG_ABI_VERSION 1
-#define OTG_TRACE_COLS 12 /* see otg_solve_result.trace */
+#define OTG_TRACE_COLS 15 /* see otg_solve_result.trace */
 
 typedef enum {
   OTG_OK = 0,
@@ -124,12 +124,16 @@ typedef struct {
   double f_value;
 } otg_step_eval;
 
-/* SolveConfig (sinkhorn.hpp:29-39). */
+/* SolveConfig (sinkhorn.hpp:29-39).  reference_v (m, or NULL) and
+ * reference_f form the optional ReferenceSolution (diag.hpp:46-49) that adds
+ * the energy / radius trace columns to acc_solve (accel.cpp:211-213). */
 typedef struct {
   double tol_l1;
   int64_t max_iters;
   int record_trace;
   int64_t trace_stride;
+  const double* reference_v;
+  double reference_f;
 } otg_solve_config;
 
 /* HomotopyConfig (accel.hpp:68-81). */
@@ -144,19 +148,25 @@ typedef struct {
   int64_t trace_stride;
 } otg_homotopy_config;
 
-/* AccelInstrumentation (accel.hpp:37-40): only the stability conditions
- * (diag.cpp:107-146), fused into the evaluation epilogue. */
+/* AccelInstrumentation (accel.hpp:37-40): the stability conditions
+ * (diag.cpp:107-146) and, with a ReferenceSolution (reference_v != NULL,
+ * diag.hpp:46-49), the Lyapunov energy and radii (diag.cpp:76-88, 206-215),
+ * all fused into the evaluation epilogue. */
 typedef struct {
   int stability;
+  const double* reference_v; /* m, or NULL */
+  double reference_f;
 } otg_instr;
 
 /* SolveResult (sinkhorn.hpp:44-54) + HomotopyResult (accel.hpp:92-99)
  * scalars.  Output buffers are caller-owned; set the ones you want.
  * trace rows hold OTG_TRACE_COLS doubles: iter, wall_time_s (always 0:
  * byte-stable traces), marginal_violation_l1, grad_f_l1, reduced_f, mu,
- * alpha, cond1_lhs, cond1_rhs, cond2_lhs, cond2_rhs, metric_drift_inf
- * (NaN marks an empty optional cell, diag.hpp:15-33).
- * boundaries rows hold (stage, mu, alpha, inner_before) (accel.hpp:84-90). */
+ * alpha, cond1_lhs, cond1_rhs, cond2_lhs, cond2_rhs, metric_drift_inf,
+ * energy, radius_x_d, radius_y (NaN marks an empty optional cell,
+ * diag.hpp:15-33).
+ * boundaries rows hold (stage, mu, alpha, inner_before, energy)
+ * (accel.hpp:84-90). */
 typedef struct {
   int converged;
   int64_t iterations;
@@ -188,6 +198,8 @@ typedef struct {
   int64_t fallback_columns; /* columns whose mass underflowed and took the
                                exact log-sum-exp (dual.cpp:54-69), summed
                                over the evaluations (diagnostic)            */
+  double radius_x_max;      /* RadiusTracker maxima (diag.hpp:120-135), with a */
+  double radius_y_max;      /* reference; r_hat = max of the two            */
 } otg_solve_result;
 
 /* plan_from_potentials + marginal_violation_l1 + primal_cost

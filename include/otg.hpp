@@ -127,12 +127,18 @@ class TransportProblem {
 };
 
 // ------------------------------------------------------------ configs / results
+struct ReferenceSolution {  // diag.hpp:46-49
+  Vec v_star;
+  double f_star = 0.0;
+};
+
 struct SolveConfig {  // sinkhorn.hpp:29-39
   double tol_l1 = 1e-6;
   long max_iters = 200000;
   bool record_trace = false;
   long trace_stride = 1;
   bool wall_clock = true;  // traces always carry wall_time_s = 0 (byte-stable)
+  const ReferenceSolution* reference = nullptr;  // acc_solve energy / radius columns
 };
 
 struct HomotopyConfig {  // accel.hpp:68-81
@@ -147,15 +153,16 @@ struct HomotopyConfig {  // accel.hpp:68-81
   bool wall_clock = true;
 };
 
-struct AccelInstrumentation {  // accel.hpp:37-40 (stability conditions only)
-  bool stability = false;
+struct AccelInstrumentation {  // accel.hpp:37-40
+  const ReferenceSolution* reference = nullptr;  // energy + radius columns
+  bool stability = false;                        // condition columns
 };
 
 struct TraceRecord {  // diag.hpp:15-33; NaN marks an empty optional cell
   long iter = 0;
   double wall_time_s = 0, marginal_violation_l1 = 0, grad_f_l1 = 0, reduced_f = 0, mu = 0,
          alpha = 0, cond1_lhs = NAN, cond1_rhs = NAN, cond2_lhs = NAN, cond2_rhs = NAN,
-         metric_drift_inf = NAN;
+         metric_drift_inf = NAN, energy = NAN, radius_x_d = NAN, radius_y = NAN;
 };
 
 struct DualPotentials {
@@ -175,12 +182,14 @@ struct StageBoundary {  // accel.hpp:84-90
   long stage = 0;
   double mu = 0, alpha = 0;
   long inner_before = 0;
+  double energy = NAN;  // E(x, w / alpha; mu) when a reference is given
 };
 
 struct HomotopyResult {  // accel.hpp:92-99
   SolveResult result;
   std::vector<StageBoundary> boundaries;
   long conditions_checked = 0, conditions_held = 0;
+  double r_hat = 0, c_star = 0;  // with a reference
 };
 
 struct AccelState {  // accel.hpp:11-20 (final state of acc_run)
@@ -194,6 +203,7 @@ struct AccRun {  // accel.hpp:42-50
   double final_violation = 0;
   std::vector<TraceRecord> trace;
   long conditions_checked = 0, conditions_held = 0;
+  double max_radius_x_d = 0, max_radius_y = 0;  // RadiusTracker, with a reference
 };
 
 struct StepEval {  // sinkhorn.hpp:18-24
@@ -207,7 +217,7 @@ struct Out {
   Vec u, v, w, trace, bounds;
   Out(const TransportProblem& p, bool trace_on, long cap, long bcap = 0)
       : u(p.info().n_local), v(p.m()), w(p.m()), trace(trace_on ? cap * OTG_TRACE_COLS : 0),
-        bounds(bcap * 4) {
+        bounds(bcap * 5) {
     r.u = u.data();
     r.v = v.data();
     r.w = w.data();
@@ -234,6 +244,9 @@ struct Out {
       rec.cond2_lhs = t[9];
       rec.cond2_rhs = t[10];
       rec.metric_drift_inf = t[11];
+      rec.energy = t[12];
+      rec.radius_x_d = t[13];
+      rec.radius_y = t[14];
       out.push_back(rec);
     }
     return out;
@@ -254,6 +267,17 @@ struct Out {
   }
 };
 inline long trace_cap(long iters, long stride) { return iters / (stride > 0 ? stride : 1) + 2; }
+inline otg_instr instr_of(const AccelInstrumentation* instr) {
+  otg_instr in{0, nullptr, 0.0};
+  if (instr) {
+    in.stability = instr->stability;
+    if (instr->reference) {
+      in.reference_v = instr->reference->v_star.data();
+      in.reference_f = instr->reference->f_star;
+    }
+  }
+  return in;
+}
 }  // namespace detail
 
 // ------------------------------------------------------------ dual.hpp / sinkhorn.hpp
@@ -300,7 +324,9 @@ inline Vec normalized_sinkhorn_map(const TransportProblem& p, const Vec& v) {  /
 inline SolveResult sinkhorn_solve(const TransportProblem& p, const Vec& v0,
                                   const SolveConfig& cfg) {
   detail::Out o(p, cfg.record_trace, detail::trace_cap(cfg.max_iters, cfg.trace_stride));
-  const otg_solve_config c{cfg.tol_l1, cfg.max_iters, cfg.record_trace, cfg.trace_stride};
+  const otg_solve_config c{cfg.tol_l1, cfg.max_iters, cfg.record_trace, cfg.trace_stride,
+                           cfg.reference ? cfg.reference->v_star.data() : nullptr,
+                           cfg.reference ? cfg.reference->f_star : 0.0};
   check(otg_sinkhorn_solve(p.handle(), v0.empty() ? nullptr : v0.data(), &c, &o.r));
   return o.result();
 }
@@ -309,7 +335,9 @@ inline SolveResult sinkhorn_solve(const TransportProblem& p, const Vec& v0,
 inline SolveResult acc_solve(const TransportProblem& p, const Vec& v0, double mu,
                              const SolveConfig& cfg) {
   detail::Out o(p, cfg.record_trace, detail::trace_cap(cfg.max_iters, cfg.trace_stride));
-  const otg_solve_config c{cfg.tol_l1, cfg.max_iters, cfg.record_trace, cfg.trace_stride};
+  const otg_solve_config c{cfg.tol_l1, cfg.max_iters, cfg.record_trace, cfg.trace_stride,
+                           cfg.reference ? cfg.reference->v_star.data() : nullptr,
+                           cfg.reference ? cfg.reference->f_star : 0.0};
   check(otg_acc_solve(p.handle(), v0.empty() ? nullptr : v0.data(), mu, &c, &o.r));
   return o.result();
 }
@@ -318,7 +346,7 @@ inline AccRun acc_run(const TransportProblem& p, const Vec& x0, const Vec& w0, d
                       bool record_trace = false, long trace_stride = 1, bool /*wall_clock*/ = true,
                       const AccelInstrumentation* instr = nullptr) {
   detail::Out o(p, record_trace, detail::trace_cap(m > 0 ? m : 1, trace_stride));
-  const otg_instr in{instr && instr->stability};
+  const otg_instr in = detail::instr_of(instr);
   check(otg_acc_run(p.handle(), x0.data(), w0.data(), mu, m, record_trace, trace_stride, &in,
                     &o.r));
   AccRun a;
@@ -328,6 +356,8 @@ inline AccRun acc_run(const TransportProblem& p, const Vec& x0, const Vec& w0, d
   a.trace = o.records();
   a.conditions_checked = o.r.conditions_checked;
   a.conditions_held = o.r.conditions_held;
+  a.max_radius_x_d = o.r.radius_x_max;
+  a.max_radius_y = o.r.radius_y_max;
   return a;
 }
 
@@ -339,17 +369,22 @@ inline HomotopyResult homotopy_solve_instrumented(const TransportProblem& p,
   detail::Out o(p, cfg.record_trace, detail::trace_cap(iters, cfg.trace_stride), bcap);
   const otg_homotopy_config c{cfg.mu0,    cfg.m0, cfg.max_outer, cfg.tol_l1, cfg.max_total_inner,
                               cfg.rescale_w_across_stages, cfg.record_trace, cfg.trace_stride};
-  const otg_instr in{instr && instr->stability};
+  const otg_instr in = detail::instr_of(instr);
   check(otg_homotopy_solve(p.handle(), &c, &in, &o.r));
   HomotopyResult h;
   h.result = o.result();
   const long nb = o.r.outer_stages < bcap ? o.r.outer_stages : bcap;
   for (long k = 0; k < nb; ++k) {
-    const double* b = o.bounds.data() + 4 * k;
-    h.boundaries.push_back({static_cast<long>(b[0]), b[1], b[2], static_cast<long>(b[3])});
+    const double* b = o.bounds.data() + 5 * k;
+    h.boundaries.push_back({static_cast<long>(b[0]), b[1], b[2], static_cast<long>(b[3]), b[4]});
   }
   h.conditions_checked = o.r.conditions_checked;
   h.conditions_held = o.r.conditions_held;
+  if (instr && instr->reference) {
+    h.r_hat = o.r.radius_x_max > o.r.radius_y_max ? o.r.radius_x_max : o.r.radius_y_max;
+    h.c_star = (std::sqrt(2.0) - 1.0) /  // homotopy_rate_constant (accel.cpp:307-311), L = 1
+               ((std::sqrt(2.0) + std::sqrt(2.0 * cfg.mu0)) * std::log(2.0 * (h.r_hat * h.r_hat + 1.0)));
+  }
   return h;
 }
 

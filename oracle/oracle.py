@@ -20,7 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "build", "liboracle.so")
 _lib = None
 
-TRACE_COLS = 12
+TRACE_COLS = 15
 TRACE_FIELDS = ("iter", "wall_time_s", "marginal_violation_l1", "grad_f_l1", "reduced_f",
                 "mu", "alpha", "cond1_lhs", "cond1_rhs", "cond2_lhs", "cond2_rhs",
                 "metric_drift_inf")
@@ -60,7 +60,19 @@ class _SolveResult(C.Structure):
                 ("outer_stages", C.c_int64), ("final_violation", C.c_double),
                 ("final_reduced_f", C.c_double), ("max_v_inf", C.c_double),
                 ("conditions_checked", C.c_int64), ("conditions_held", C.c_int64),
-                ("trace_len", C.c_int64)]
+                ("trace_len", C.c_int64), ("r_max_x", C.c_double), ("r_max_y", C.c_double)]
+
+
+class _Reference(C.Structure):  # ReferenceSolution (diag.hpp:46-49)
+    _fields_ = [("v_star", C.c_void_p), ("f_star", C.c_double)]
+
+
+def _ref(reference):
+    """reference = (v_star, f_star) or None -> (ctypes struct or None, keep-alive)."""
+    if reference is None:
+        return None, None
+    vs = _f64(reference[0])
+    return _Reference(vs.ctypes.data_as(C.c_void_p), float(reference[1])), vs
 
 
 def build() -> str:
@@ -168,12 +180,18 @@ class Result:
     w: np.ndarray = None
     trace: np.ndarray = None
     boundaries: np.ndarray = None
+    r_max_x: float = 0.0
+    r_max_y: float = 0.0
+
+    @property
+    def r_hat(self) -> float:  # RadiusTracker::r_hat (diag.hpp:130)
+        return max(self.r_max_x, self.r_max_y)
 
 
 def _result(r: _SolveResult, **kw) -> Result:
     return Result(bool(r.converged), r.iterations, r.evaluations, r.outer_stages,
                   r.final_violation, r.final_reduced_f, r.max_v_inf, r.conditions_checked,
-                  r.conditions_held, **kw)
+                  r.conditions_held, r_max_x=r.r_max_x, r_max_y=r.r_max_y, **kw)
 
 
 def synthetic_instance(n: int, m: int, seed: int):
@@ -313,14 +331,16 @@ def sinkhorn_solve(p: Problem, v0=None, tol_l1=1e-6, max_iters=200000, record_tr
 
 
 def acc_solve(p: Problem, v0=None, mu=0.5, tol_l1=1e-6, max_iters=200000, record_trace=False,
-              trace_stride=1, trace_cap=100000) -> Result:
+              trace_stride=1, trace_cap=100000, reference=None) -> Result:
     v0 = np.zeros(p.m) if v0 is None else _f64(v0)
     cfg = _SolveConfig(tol_l1, max_iters, int(record_trace), trace_stride)
     r = _SolveResult()
     u, v = np.empty(p.n), np.empty(p.m)
     tr = _trace_buf(record_trace, trace_cap)
+    ref, keep = _ref(reference)
     _check(lib().orc_acc_solve(p.ref, _p(v0), C.c_double(mu), C.byref(cfg), C.byref(r), _p(u),
-                               _p(v), _p(tr), C.c_int64(trace_cap if record_trace else 0)))
+                               _p(v), _p(tr), C.c_int64(trace_cap if record_trace else 0),
+                               None if ref is None else C.byref(ref)))
     return _result(r, u=u, v=v, trace=None if tr is None else tr[:min(r.trace_len, trace_cap)])
 
 
@@ -335,33 +355,54 @@ def acc_step(p: Problem, x, w, mu, Sx=None):
 
 
 def acc_run(p: Problem, x0, w0, mu, msteps, record_trace=False, trace_stride=1, stability=False,
-            trace_cap=100000) -> Result:
+            trace_cap=100000, reference=None) -> Result:
     x0, w0 = _f64(x0), _f64(w0)
     r = _SolveResult()
     x, w = np.empty(p.m), np.empty(p.m)
     tr = _trace_buf(record_trace, trace_cap)
+    ref, keep = _ref(reference)
     _check(lib().orc_acc_run(p.ref, _p(x0), _p(w0), C.c_double(mu), C.c_int64(msteps),
                              C.c_int(int(record_trace)), C.c_int64(trace_stride),
                              C.c_int(int(stability)), C.byref(r), _p(x), _p(w), _p(tr),
-                             C.c_int64(trace_cap if record_trace else 0)))
+                             C.c_int64(trace_cap if record_trace else 0),
+                             None if ref is None else C.byref(ref)))
     return _result(r, v=x, w=w, trace=None if tr is None else tr[:min(r.trace_len, trace_cap)])
 
 
 def homotopy_solve(p: Problem, mu0=0.5, m0=4, max_outer=64, tol_l1=1e-6,
                    max_total_inner=20000000, rescale_w_across_stages=False, record_trace=False,
-                   trace_stride=1, stability=False, trace_cap=100000, bcap=256) -> Result:
+                   trace_stride=1, stability=False, trace_cap=100000, bcap=256,
+                   reference=None) -> Result:
     cfg = _HomotopyConfig(mu0, m0, max_outer, tol_l1, max_total_inner,
                           int(rescale_w_across_stages), int(record_trace), trace_stride,
                           int(stability))
     r = _SolveResult()
     u, v = np.empty(p.n), np.empty(p.m)
-    bd = np.full((bcap, 4), np.nan)
+    bd = np.full((bcap, 5), np.nan)
     tr = _trace_buf(record_trace, trace_cap)
+    ref, keep = _ref(reference)
     _check(lib().orc_homotopy_solve(p.ref, C.byref(cfg), C.byref(r), _p(u), _p(v), _p(bd),
                                     C.c_int64(bcap), _p(tr),
-                                    C.c_int64(trace_cap if record_trace else 0)))
+                                    C.c_int64(trace_cap if record_trace else 0),
+                                    None if ref is None else C.byref(ref)))
     return _result(r, u=u, v=v, boundaries=bd[:min(r.outer_stages, bcap)],
                    trace=None if tr is None else tr[:min(r.trace_len, trace_cap)])
+
+
+def lyapunov_energy_from_parts(b, f_x, grad_x, y, mu, reference) -> float:
+    """diag.cpp:76-88."""
+    b, g, y = _f64(b), _f64(grad_x), _f64(y)
+    ref, keep = _ref(reference)
+    out = C.c_double(0.0)
+    _check(lib().orc_lyapunov_energy(_p(b), C.c_int64(b.size), C.c_double(f_x), _p(g), _p(y),
+                                     C.c_double(mu), C.byref(ref), C.byref(out)))
+    return out.value
+
+
+def reference_solve(p: Problem, tol=1e-12, max_iters=4000000):
+    """helpers.hpp:37-45: the ReferenceSolution of the reference's tests."""
+    r = sinkhorn_solve(p, np.zeros(p.m), tol_l1=tol, max_iters=max_iters)
+    return r.v, r.final_reduced_f
 
 
 def homotopy_rate_constant(mu0, r_hat, l_f=1.0) -> float:

@@ -283,6 +283,42 @@ Stab stability_from_grads(const double* b, int64_t m, const double* gk, const do
   return r;
 }
 
+// diag.cpp:76-88: E(x, y; mu) = f(x) - f* + mu/2 ||y - v*||^2_{D(p(x))}
+double lyapunov_from_parts(const double* b, int64_t m, double f_x, const double* grad_x,
+                           const double* y, double mu, const orc_reference& ref) {
+  if (ref.f_star > f_x + 1e-9) {
+    char buf[128];
+    std::snprintf(buf, sizeof buf, "reference value %.17g exceeds f(x) = %.17g", ref.f_star, f_x);
+    fail(ORC_E_OT, buf);
+  }
+  double e = f_x - ref.f_star;
+  if (mu != 0.0) {
+    const Vec pz = grad_phi_star(b, m, grad_x);
+    const Vec D = metric_D(b, m, pz.data());
+    double q = 0.0;  // MetricDiag::quad
+    for (int64_t j = 0; j < m; ++j) {
+      const double z = y[j] - ref.v_star[j];
+      q += D[j] * (z * z);
+    }
+    e += 0.5 * mu * q;
+  }
+  return e;
+}
+
+// diag.cpp:206-215 RadiusTracker::observe
+std::pair<double, double> radii(const double* b, int64_t m, const double* grad_x,
+                                const double* x, const double* y, const orc_reference& ref) {
+  const Vec pz = grad_phi_star(b, m, grad_x);
+  const Vec D = metric_D(b, m, pz.data());
+  double qx = 0.0, qy = 0.0;
+  for (int64_t j = 0; j < m; ++j) {
+    const double zx = x[j] - ref.v_star[j], zy = y[j] - ref.v_star[j];
+    qx += D[j] * (zx * zx);
+    qy += zy * zy;
+  }
+  return {std::sqrt(qx), std::sqrt(qy)};
+}
+
 // Trace writer (diag.hpp:15-42; optional cells as NaN).
 struct TraceOut {
   double* buf;
@@ -343,22 +379,38 @@ AccelState acc_step(const Prob& p, const AccelState& s, int64_t& evals) {
   return next;
 }
 
-// accel.cpp:27-133 (AccObserver) — scalar trace + stability counters only;
-// the energy/radius columns need a ReferenceSolution (out of scope, §8f).
+// accel.cpp:27-133 (AccObserver): scalar trace, stability counters, and with a
+// ReferenceSolution the energy / radius columns.
 class Observer {
  public:
-  Observer(const Prob& p, bool trace, int64_t stride, bool stability, TraceOut* out)
-      : p_(p), trace_(trace), stride_(stride > 0 ? stride : 1), stab_(stability), out_(out) {}
+  Observer(const Prob& p, bool trace, int64_t stride, bool stability, TraceOut* out,
+           const orc_reference* ref = nullptr)
+      : p_(p), trace_(trace), stride_(stride > 0 ? stride : 1), stab_(stability), out_(out),
+        ref_(ref) {}
 
   void observe(int64_t iter, const AccelState& s, bool terminal) {
     const StepEval& e = s.cache;
     max_v_inf_ = std::max(max_v_inf_, inf_norm(s.x.data(), p_.m));
     double c[5] = {kNaN, kNaN, kNaN, kNaN, kNaN};
+    double energy = kNaN, rx = kNaN, ry = kNaN;
     const bool want = trace_ && (iter % stride_ == 0 || terminal);
-    if (stab_) {
+    if (stab_ || ref_) {
       Vec y(p_.m);
       for (int64_t j = 0; j < p_.m; ++j) y[j] = s.w[j] / s.alpha;
-      if (have_prev_) {
+      if (ref_) {
+        try {
+          energy = lyapunov_from_parts(p_.b, p_.m, e.f_value, e.grad.data(), y.data(), s.mu, *ref_);
+          auto r = radii(p_.b, p_.m, e.grad.data(), s.x.data(), y.data(), *ref_);
+          max_x_ = std::max(max_x_, r.first);
+          max_y_ = std::max(max_y_, r.second);
+          rx = r.first;
+          ry = r.second;
+        } catch (const OrcError& err) {
+          if (err.code != ORC_E_DOMAIN) throw;
+          energy = kNaN;
+        }
+      }
+      if (stab_ && have_prev_) {
         try {
           Stab r = stability_from_grads(p_.b, p_.m, prev_grad_.data(), e.grad.data(),
                                         prev_x_.data(), s.x.data(), prev_y_.data(), y.data(),
@@ -377,13 +429,29 @@ class Observer {
     }
     if (want) {
       double row[ORC_TRACE_COLS] = {static_cast<double>(iter), 0.0, e.grad_l1, e.grad_l1,
-                                    e.f_value, s.mu, s.alpha, c[0], c[1], c[2], c[3], c[4]};
+                                    e.f_value, s.mu, s.alpha, c[0], c[1], c[2], c[3], c[4],
+                                    energy, rx, ry};
       out_->push(row);
+    }
+  }
+  // accel.cpp:104-114
+  double stage_energy(const AccelState& s) const {
+    if (!ref_) return kNaN;
+    Vec y(p_.m);
+    for (int64_t j = 0; j < p_.m; ++j) y[j] = s.w[j] / s.alpha;
+    try {
+      return lyapunov_from_parts(p_.b, p_.m, s.cache.f_value, s.cache.grad.data(), y.data(), s.mu,
+                                 *ref_);
+    } catch (const OrcError& err) {
+      if (err.code != ORC_E_DOMAIN) throw;
+      return kNaN;
     }
   }
   double max_v_inf() const { return max_v_inf_; }
   int64_t checked() const { return checked_; }
   int64_t held() const { return held_; }
+  double max_x() const { return max_x_; }
+  double max_y() const { return max_y_; }
 
  private:
   const Prob& p_;
@@ -391,9 +459,10 @@ class Observer {
   int64_t stride_;
   bool stab_;
   TraceOut* out_;
+  const orc_reference* ref_;
   Vec prev_grad_, prev_x_, prev_y_;
   bool have_prev_ = false;
-  double max_v_inf_ = 0.0;
+  double max_v_inf_ = 0.0, max_x_ = 0.0, max_y_ = 0.0;
   int64_t checked_ = 0, held_ = 0;
 };
 
@@ -839,7 +908,7 @@ int orc_acc_step(const orc_problem* pp, const double* x, const double* w, const 
 int orc_acc_run(const orc_problem* pp, const double* x0, const double* w0, double mu,
                 int64_t msteps, int record_trace, int64_t trace_stride, int stability,
                 orc_solve_result* res, double* x_out, double* w_out, double* trace,
-                int64_t trace_cap) {
+                int64_t trace_cap, const orc_reference* ref) {
   return guard([&] {
     Prob p = wrap(pp);
     validate(p, 1.0);
@@ -850,7 +919,7 @@ int orc_acc_run(const orc_problem* pp, const double* x0, const double* w0, doubl
     s.cache = eval_normalized_step(p, s.x.data());
     s.has_cache = true;
     ++res->evaluations;
-    Observer obs(p, record_trace != 0, trace_stride, stability != 0, &tr);
+    Observer obs(p, record_trace != 0, trace_stride, stability != 0, &tr, ref);
     obs.observe(0, s, msteps == 0);
     for (int64_t k = 0; k < msteps; ++k) {
       s = acc_step(p, s, res->evaluations);
@@ -863,6 +932,8 @@ int orc_acc_run(const orc_problem* pp, const double* x0, const double* w0, doubl
     res->conditions_checked = obs.checked();
     res->conditions_held = obs.held();
     res->trace_len = tr.len;
+    res->r_max_x = obs.max_x();
+    res->r_max_y = obs.max_y();
     copy_out(s.x, x_out);
     copy_out(s.w, w_out);
   });
@@ -871,7 +942,7 @@ int orc_acc_run(const orc_problem* pp, const double* x0, const double* w0, doubl
 // accel.cpp:200-232
 int orc_acc_solve(const orc_problem* pp, const double* v0, double mu,
                   const orc_solve_config* cfg, orc_solve_result* res, double* u_out,
-                  double* v_out, double* trace, int64_t trace_cap) {
+                  double* v_out, double* trace, int64_t trace_cap, const orc_reference* ref) {
   return guard([&] {
     Prob p = wrap(pp);
     validate(p, 1.0);
@@ -882,7 +953,7 @@ int orc_acc_solve(const orc_problem* pp, const double* v0, double mu,
     s.cache = eval_normalized_step(p, s.x.data());
     s.has_cache = true;
     ++res->evaluations;
-    Observer obs(p, cfg->record_trace != 0, cfg->trace_stride, false, &tr);
+    Observer obs(p, cfg->record_trace != 0, cfg->trace_stride, false, &tr, ref);
     for (int64_t k = 0;; ++k) {
       const double violation = s.cache.grad_l1;
       const bool done = violation < cfg->tol_l1 || k >= cfg->max_iters;
@@ -900,13 +971,16 @@ int orc_acc_solve(const orc_problem* pp, const double* v0, double mu,
     }
     res->max_v_inf = obs.max_v_inf();
     res->trace_len = tr.len;
+    res->r_max_x = obs.max_x();
+    res->r_max_y = obs.max_y();
   });
 }
 
 // accel.cpp:234-301
 int orc_homotopy_solve(const orc_problem* pp, const orc_homotopy_config* cfg,
                        orc_solve_result* res, double* u_out, double* v_out,
-                       double* boundaries, int64_t bcap, double* trace, int64_t trace_cap) {
+                       double* boundaries, int64_t bcap, double* trace, int64_t trace_cap,
+                       const orc_reference* ref) {
   return guard([&] {
     Prob p = wrap(pp);
     validate(p, 1.0);
@@ -921,7 +995,7 @@ int orc_homotopy_solve(const orc_problem* pp, const orc_homotopy_config* cfg,
     s.cache = eval_normalized_step(p, s.x.data());
     s.has_cache = true;
     ++res->evaluations;
-    Observer obs(p, cfg->record_trace != 0, cfg->trace_stride, cfg->stability != 0, &tr);
+    Observer obs(p, cfg->record_trace != 0, cfg->trace_stride, cfg->stability != 0, &tr, ref);
     obs.observe(0, s, false);
     int64_t total_inner = 0, m = cfg->m0, nb = 0;
     bool converged = s.cache.grad_l1 < cfg->tol_l1;
@@ -929,11 +1003,12 @@ int orc_homotopy_solve(const orc_problem* pp, const orc_homotopy_config* cfg,
     for (int64_t stage = 0; stage < cfg->max_outer && !converged && !capped; ++stage) {
       ++res->outer_stages;
       if (boundaries && nb < bcap) {
-        double* row = boundaries + 4 * nb;
+        double* row = boundaries + 5 * nb;
         row[0] = static_cast<double>(stage);
         row[1] = s.mu;
         row[2] = s.alpha;
         row[3] = static_cast<double>(total_inner);
+        row[4] = obs.stage_energy(s);
       }
       ++nb;
       for (int64_t i = 0; i < m; ++i) {
@@ -963,8 +1038,18 @@ int orc_homotopy_solve(const orc_problem* pp, const orc_homotopy_config* cfg,
     res->conditions_checked = obs.checked();
     res->conditions_held = obs.held();
     res->trace_len = tr.len;
+    res->r_max_x = obs.max_x();
+    res->r_max_y = obs.max_y();
     copy_out(s.cache.u, u_out);
     copy_out(s.x, v_out);
+  });
+}
+
+int orc_lyapunov_energy(const double* b, int64_t m, double f_x, const double* grad_x,
+                        const double* y, double mu, const orc_reference* ref, double* out) {
+  return guard([&] {
+    if (!ref || !out) fail(ORC_E_DIMENSION, "NULL reference / output");
+    *out = lyapunov_from_parts(b, m, f_x, grad_x, y, mu, *ref);
   });
 }
 

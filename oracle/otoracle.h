@@ -86,13 +86,21 @@ typedef struct {
   int64_t conditions_checked;
   int64_t conditions_held;
   int64_t trace_len;     /* records produced (may exceed trace_cap) */
+  double r_max_x;        /* RadiusTracker maxima (diag.hpp:120-135), with a reference */
+  double r_max_y;
 } orc_solve_result;
+
+/* ReferenceSolution (diag.hpp:46-49): the energy / radius columns. */
+typedef struct {
+  const double* v_star;  /* m */
+  double f_star;
+} orc_reference;
 
 /* Trace record layout: ORC_TRACE_COLS doubles per row:
  * iter, wall_time_s(=0), marginal_violation_l1, grad_f_l1, reduced_f, mu,
- * alpha, cond1_lhs, cond1_rhs, cond2_lhs, cond2_rhs, metric_drift_inf
- * (NaN = empty optional cell, diag.hpp:15-33). */
-#define ORC_TRACE_COLS 12
+ * alpha, cond1_lhs, cond1_rhs, cond2_lhs, cond2_rhs, metric_drift_inf,
+ * energy, radius_x_d, radius_y (NaN = empty optional cell, diag.hpp:15-33). */
+#define ORC_TRACE_COLS 15
 
 const char* orc_last_error(void);
 
@@ -165,18 +173,22 @@ int orc_sinkhorn_solve(const orc_problem* p, const double* v0, const orc_solve_c
 int orc_acc_step(const orc_problem* p, const double* x, const double* w, const double* Sx,
                  double mu, double* x_out, double* w_out, double* Sx_out,
                  int64_t* eval_count);
+/* ref (optional): ReferenceSolution -> energy / radius trace columns. */
 int orc_acc_run(const orc_problem* p, const double* x0, const double* w0, double mu,
                 int64_t msteps, int record_trace, int64_t trace_stride, int stability,
                 orc_solve_result* res, double* x_out, double* w_out, double* trace,
-                int64_t trace_cap);
+                int64_t trace_cap, const orc_reference* ref);
 int orc_acc_solve(const orc_problem* p, const double* v0, double mu,
                   const orc_solve_config* cfg, orc_solve_result* res, double* u_out,
-                  double* v_out, double* trace, int64_t trace_cap);
-/* boundaries: up to bcap rows of (stage, mu, alpha, inner_before). */
+                  double* v_out, double* trace, int64_t trace_cap, const orc_reference* ref);
+/* boundaries: up to bcap rows of (stage, mu, alpha, inner_before, energy). */
 int orc_homotopy_solve(const orc_problem* p, const orc_homotopy_config* cfg,
                        orc_solve_result* res, double* u_out, double* v_out,
                        double* boundaries, int64_t bcap, double* trace,
-                       int64_t trace_cap);
+                       int64_t trace_cap, const orc_reference* ref);
+/* lyapunov_energy_from_parts (diag.cpp:76-88) at (f(x), grad f(x), y, mu). */
+int orc_lyapunov_energy(const double* b, int64_t m, double f_x, const double* grad_x,
+                        const double* y, double mu, const orc_reference* ref, double* out);
 double orc_homotopy_rate_constant(double mu0, double r_hat, double l_f);
 
 /* ---- CPU baseline helpers (bench.py cpu_baseline / --impl reference) ---- */

@@ -36,9 +36,13 @@ class StepEvalC(C.Structure):
                 ("grad_l1", C.c_double), ("f_value", C.c_double)]
 
 
+TRACE_COLS = 15  # OTG_TRACE_COLS
+
+
 class SolveConfigC(C.Structure):
     _fields_ = [("tol_l1", C.c_double), ("max_iters", C.c_int64), ("record_trace", C.c_int),
-                ("trace_stride", C.c_int64)]
+                ("trace_stride", C.c_int64), ("reference_v", C.c_void_p),
+                ("reference_f", C.c_double)]
 
 
 class HomotopyConfigC(C.Structure):
@@ -49,7 +53,7 @@ class HomotopyConfigC(C.Structure):
 
 
 class InstrC(C.Structure):
-    _fields_ = [("stability", C.c_int)]
+    _fields_ = [("stability", C.c_int), ("reference_v", C.c_void_p), ("reference_f", C.c_double)]
 
 
 class SolveResultC(C.Structure):
@@ -63,7 +67,8 @@ class SolveResultC(C.Structure):
                 ("time_sweeps", C.c_int), ("device_seconds", C.c_double),
                 ("row_pass_seconds", C.c_double), ("col_pass_seconds", C.c_double),
                 ("kernel_launches", C.c_int64), ("row_redos", C.c_int64),
-                ("epilogue_seconds", C.c_double), ("fallback_columns", C.c_int64)]
+                ("epilogue_seconds", C.c_double), ("fallback_columns", C.c_int64),
+                ("radius_x_max", C.c_double), ("radius_y_max", C.c_double)]
 
 
 class PlanSummaryC(C.Structure):

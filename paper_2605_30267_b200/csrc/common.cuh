@@ -143,6 +143,12 @@ struct Ctrl {
   int pad1;
   double dmax2;       // max_j (p_new - p_old)_j * log2(e)
   long long redo_total;  // rows redone exactly over the solve (diagnostic)
+  // ReferenceSolution instrumentation (energy / radii, diag.cpp:76-88, 206-215)
+  int have_ref;
+  int boundary_pending;  // control_step pushed a boundary row this evaluation
+  double f_star;
+  double mu_step;        // mu of the evaluation being observed (before a halving)
+  double rmax_x, rmax_y;
   long long fb_total;    // columns that took the exact LSE fallback (diagnostic)
   // --- configuration (host-written) ---
   int mode;
@@ -163,6 +169,7 @@ struct Ctrl {
 };
 
 constexpr int kTraceCols = OTG_TRACE_COLS;
+constexpr int kBoundCols = 5;  // stage, mu, alpha, inner_before, energy
 constexpr int kEpiMaxGrid = 296;  // CTAs of the single-kernel epilogue, at most
 
 // ---------------------------------------------------------------- problem --
@@ -239,6 +246,7 @@ struct Problem {
   Ctrl* ctrl = nullptr;
   Ctrl* ctrl_host = nullptr;  // pinned mirror
   double* trace = nullptr;    // ring: trace_cap x kTraceCols
+  double* vstar = nullptr;    // ReferenceSolution v* (m), allocated on first use
   double* bounds = nullptr;   // boundary_cap x 4
 
   int64_t mpad = 0;

@@ -144,7 +144,7 @@ void problem_free(Problem& P) {
                   P.col_log,
                   P.y, P.grad, P.prev_grad,
                   P.prev_x, P.prev_y, P.flag_idx, P.fb_cols, P.fb_part, P.part, P.e1_part,
-                  P.e2_part, P.epi_part, P.sp_rec, P.sp_bad_rows, P.sp_bad_count, P.ctrl, P.trace, P.bounds, P.fbA, P.fbS, P.fbT};
+                  P.e2_part, P.epi_part, P.sp_rec, P.sp_bad_rows, P.sp_bad_count, P.ctrl, P.trace, P.vstar, P.bounds, P.fbA, P.fbS, P.fbT};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (P.ctrl_host) cudaFreeHost(P.ctrl_host);
@@ -191,12 +191,12 @@ void problem_alloc_state(Problem& P) {
                                        static_cast<size_t>(P.fused_clusters) + 1);
   P.part = dalloc<double>(P, prow * mp);
   P.e1_part = dalloc<double>(P, P.e_blocks * 8 + row_blocks(P) + 8);
-  P.e2_part = dalloc<double>(P, P.e_blocks * 8);
-  P.epi_part = dalloc<double>(P, 2 * kEpiMaxGrid * 8);
+  P.e2_part = dalloc<double>(P, P.e_blocks * 16);
+  P.epi_part = dalloc<double>(P, kEpiMaxGrid * (8 + 16));
   fused_alloc(P);
   P.ctrl = dalloc<Ctrl>(P, 1);
   P.trace = dalloc<double>(P, kTraceCap * kTraceCols);
-  P.bounds = dalloc<double>(P, kBoundaryCap * 4);
+  P.bounds = dalloc<double>(P, kBoundaryCap * kBoundCols);
   OTG_CUDA(cudaMallocHost(&P.ctrl_host, sizeof(Ctrl)));
   OTG_CUDA(cudaMemsetAsync(P.p, 0, mp * sizeof(double), P.stream));
   OTG_CUDA(cudaMemsetAsync(P.wacc, 0, mp * sizeof(double), P.stream));

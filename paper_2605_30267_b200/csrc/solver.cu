@@ -84,6 +84,8 @@ void d2h(Problem& P, double* dst, const double* src, int64_t count) {
 
 void raise_device_error(const Ctrl& c) {
   if (c.error == OTG_E_DOMAIN) fail(OTG_E_DOMAIN, "column log-mass degenerated (non-finite log c)");
+  if (c.error == OTG_E_OT)
+    fail(OTG_E_OT, "reference value f* exceeds f(x) (lyapunov_energy_from_parts, diag.cpp:78-81)");
   if (c.error) fail(static_cast<otg_status>(c.error), "device-side error");
 }
 
@@ -209,12 +211,14 @@ void fill_result(Problem& P, otg_solve_result* res, const LoopOut& lo) {
   res->kernel_launches = lo.launches;
   res->row_redos = c.redo_total;
   res->fallback_columns = c.fb_total;
+  res->radius_x_max = c.rmax_x;
+  res->radius_y_max = c.rmax_y;
   d2h(P, res->u, P.u, P.n_local);
   d2h(P, res->v, P.p, P.m);
   d2h(P, res->w, P.wacc, P.m);
   if (res->boundaries && res->boundaries_cap > 0) {
     const int64_t nb = std::min<int64_t>(c.boundary_count, std::min<int64_t>(res->boundaries_cap, c.boundary_cap));
-    if (nb > 0) d2h(P, res->boundaries, P.bounds, nb * 4);
+    if (nb > 0) d2h(P, res->boundaries, P.bounds, nb * kBoundCols);
   }
   OTG_CUDA(cudaStreamSynchronize(P.stream));
 }
@@ -368,6 +372,17 @@ otg_status otg_sinkhorn_solve(otg_problem h, const double* v0, const otg_solve_c
   });
 }
 
+// ReferenceSolution (diag.hpp:46-49) for the energy / radius columns.
+static void attach_reference(Problem& P, Ctrl& c, const double* v_star, double f_star) {
+  if (!v_star) return;
+  check_finite_vec(v_star, P.m, "reference v_star");
+  if (!std::isfinite(f_star)) fail(OTG_E_OT, "reference f_star is not finite");
+  if (!P.vstar) P.vstar = dalloc<double>(P, P.mpad);
+  h2d(P, P.vstar, v_star, P.m);
+  c.have_ref = 1;
+  c.f_star = f_star;
+}
+
 static void start_acc(Problem& P, Ctrl& c, const double* x0, const double* w0, double mu) {
   c.mu = mu;
   c.alpha_next = std::sqrt(2.0 * mu);  // accel.cpp:149
@@ -399,6 +414,7 @@ otg_status otg_acc_solve(otg_problem h, const double* v0, double mu, const otg_s
     c.max_iters = cfg->max_iters;
     c.record_trace = cfg->record_trace;
     c.trace_stride = cfg->trace_stride;
+    attach_reference(P, c, cfg->reference_v, cfg->reference_f);  // accel.cpp:211-213
     start_acc(P, c, x0.data(), nullptr, mu);
     const LoopOut lo = run_loop(P, res, res && res->time_sweeps);
     fill_result(P, res, lo);
@@ -422,6 +438,7 @@ otg_status otg_acc_run(otg_problem h, const double* x0, const double* w0, double
     c.record_trace = record_trace;
     c.trace_stride = trace_stride > 0 ? trace_stride : 1;
     c.stability = instr && instr->stability;
+    if (instr) attach_reference(P, c, instr->reference_v, instr->reference_f);
     start_acc(P, c, x0, w0, mu);
     const LoopOut lo = run_loop(P, res, res && res->time_sweeps);
     fill_result(P, res, lo);
@@ -448,6 +465,7 @@ otg_status otg_homotopy_solve(otg_problem h, const otg_homotopy_config* cfg,
     c.record_trace = cfg->record_trace;
     c.trace_stride = cfg->trace_stride;
     c.stability = instr && instr->stability;
+    if (instr) attach_reference(P, c, instr->reference_v, instr->reference_f);
     c.mu0 = cfg->mu0;
     const std::vector<double> zero(P.m, 0.0);
     start_acc(P, c, zero.data(), nullptr, cfg->mu0);

@@ -51,6 +51,7 @@ constexpr int kAuxTile = 256;
 constexpr int kEThreads = 256;
 constexpr int kFbChunks = 32;
 constexpr int kFbUnroll = 8;
+constexpr int kE2 = 16;  // doubles per CTA partial of the vector update (stability + energy)
 constexpr int kFlushRows = 16;
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -1077,9 +1078,17 @@ __device__ __forceinline__ void merge_body(const double* __restrict__ part, int 
     double c = 0.0;
     if (do_merge) {
       for (int s = 0; s < nshards; ++s) {
-        double loc = 0.0;
-        for (int k = 0; k < splits; ++k)
-          loc += part[(static_cast<int64_t>(s) * splits + k) * mpad + j];
+        // 8 independent chains keep 8 loads in flight (the splits are
+        // L2-resident; a single chain is latency-bound), folded in fixed order
+        const double* src = part + static_cast<int64_t>(s) * splits * mpad + j;
+        double l8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int k = 0;
+        for (; k + 8 <= splits; k += 8) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) l8[e] += src[static_cast<int64_t>(k + e) * mpad];
+        }
+        for (int e = 0; k < splits; ++k, ++e) l8[e] += src[static_cast<int64_t>(k) * mpad];
+        const double loc = ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
         c += loc;
       }
       col[j] = c;
@@ -1235,19 +1244,22 @@ __device__ void push_trace(Ctrl* C, double* trace, long long iter, double viol, 
 
 __device__ void push_boundary(Ctrl* C, double* bounds) {
   if (C->boundary_count < C->boundary_cap) {
-    double* r = bounds + C->boundary_count * 4;
+    double* r = bounds + C->boundary_count * kBoundCols;
     r[0] = static_cast<double>(C->stage);
     r[1] = C->mu;
     r[2] = C->alpha_next;
     r[3] = static_cast<double>(C->total_inner);
+    r[4] = __longlong_as_double(0x7ff8000000000000LL);  // energy: k_apply, with a reference
   }
   C->boundary_count += 1;
+  C->boundary_pending = 1;
 }
 
 // Scalar control flow after one evaluation (one thread).  Mirrors
 // sinkhorn.cpp:80-113, accel.cpp:176-197, 211-230, 245-301.
 __device__ void control_step(Ctrl* C, double* trace, double* bounds, double gl, double f) {
   const long long ev = ++C->evaluations;
+  C->mu_step = C->mu;  // the observed step's mu (a stage change below halves C->mu)
   const bool seed = ev == 1;
   C->grad_l1 = gl;
   C->f_value = f;
@@ -1515,6 +1527,8 @@ struct AppArgs {
   int fast;
   double* e2_part;
   double* trace;
+  const double* vstar;  // ReferenceSolution v* (energy / radii), or unused
+  double* bounds;
 };
 
 // The solver's vector update for work unit blk of nblk (accel.cpp:161-168,
@@ -1532,10 +1546,14 @@ __device__ __forceinline__ void apply_cols(const AppArgs& A, const Ctrl* ctrl_in
   const bool resc = ctrl->stage_changed && ctrl->rescale_w;
   const bool stab = ctrl->stability != 0 && mode >= MODE_ACC_RUN;
   const bool have_prev = ctrl->have_prev != 0;
+  // energy / radii (accel.cpp:46-60): acc_solve, acc_run, homotopy with a reference
+  const bool refq = ctrl->have_ref != 0 && mode >= MODE_ACC;
+  const bool bpend = refq && ctrl->boundary_pending != 0;
   // the next point replaces p: record max_j (p_new - p_old) and the split of
   // p_new for the fp32 row pass's shift estimate (k_row_shift)
   const bool moves = !done && mode != MODE_EVAL;
   double c1 = 0.0, br = 0.0, c2 = 0.0, qq = 0.0, drift = 0.0, ginf = 0.0, dom = 0.0;
+  double qe = 0.0, qx = 0.0, qy = 0.0, qb = 0.0, domr = 0.0;
   double dstep = -INFINITY;
   for (int64_t j = static_cast<int64_t>(blk) * kEThreads + threadIdx.x; j < A.m;
        j += static_cast<int64_t>(nblk) * kEThreads) {
@@ -1573,6 +1591,22 @@ __device__ __forceinline__ void apply_cols(const AppArgs& A, const Ctrl* ctrl_in
         A.prev_x[j] = x;
         A.prev_y[j] = yn;
       }
+      if (refq) {  // D(p(x)) at the evaluated point; y = w / alpha (accel.cpp:44)
+        const double bj = A.b[j], r1 = A.grad[j] / bj, vs = A.vstar[j];
+        const double yn = w / al, zy = yn - vs, zx = x - vs;
+        if (r1 <= -1.0) {
+          domr = 1.0;  // DomainViolation: the row keeps empty cells
+        } else {
+          const double D1 = bj * expm1_over_z(log1p(r1));
+          qe += D1 * (zy * zy);
+          qx += D1 * (zx * zx);
+          if (bpend) {  // stage_energy after the stage change (accel.cpp:104-114)
+            const double yb = (resc ? w * (an / al) : w) / an, zb = yb - vs;
+            qb += D1 * (zb * zb);
+          }
+        }
+        qy += zy * zy;
+      }
       if (resc) w *= an / al;  // accel.cpp:279
       A.wacc[j] = w;
       pn = (w + S) / (1.0 + an);  // accel.cpp:161
@@ -1596,8 +1630,20 @@ __device__ __forceinline__ void apply_cols(const AppArgs& A, const Ctrl* ctrl_in
     dom = block_max<kEThreads>(dom, sh);
   }
   dstep = block_max<kEThreads>(dstep, sh);
+  if (refq) {
+    qe = block_sum<kEThreads>(qe, sh);
+    qx = block_sum<kEThreads>(qx, sh);
+    qy = block_sum<kEThreads>(qy, sh);
+    qb = block_sum<kEThreads>(qb, sh);
+    domr = block_max<kEThreads>(domr, sh);
+  }
   if (threadIdx.x == 0) {
-    double* dst = A.e2_part + blk * 8;
+    double* dst = A.e2_part + blk * kE2;
+    dst[8] = qe;
+    dst[9] = qx;
+    dst[10] = qy;
+    dst[11] = qb;
+    dst[12] = domr;
     dst[0] = c1;
     dst[1] = br;
     dst[2] = c2;
@@ -1618,19 +1664,50 @@ __device__ __forceinline__ void apply_tail(const AppArgs& A, int nparts, double*
   const bool have_prev = cv->have_prev != 0;
   const double al = cv->alpha_step;
   const bool moves = !done && mode != MODE_EVAL;
-  double t[8] = {0, 0, 0, 0, 0, 0, 0, -INFINITY};
+  const bool refq = cv->have_ref != 0 && mode >= MODE_ACC;
+  double t[13] = {0, 0, 0, 0, 0, 0, 0, -INFINITY, 0, 0, 0, 0, 0};
   for (int k = threadIdx.x; k < nparts; k += kEThreads) {
-    const volatile double* src = A.e2_part + k * 8;
+    const volatile double* src = A.e2_part + k * kE2;
     for (int q = 0; q < 4; ++q) t[q] += src[q];
     for (int q = 4; q < 8; ++q) t[q] = fmax(t[q], src[q]);
+    if (refq) {
+      for (int q = 8; q < 12; ++q) t[q] += src[q];
+      t[12] = fmax(t[12], src[12]);
+    }
   }
   if (stab) {
     for (int q = 0; q < 4; ++q) t[q] = block_sum<kEThreads>(t[q], sh);
     for (int q = 4; q < 7; ++q) t[q] = block_max<kEThreads>(t[q], sh);
   }
   t[7] = block_max<kEThreads>(t[7], sh);
+  if (refq) {
+    for (int q = 8; q < 12; ++q) t[q] = block_sum<kEThreads>(t[q], sh);
+    t[12] = block_max<kEThreads>(t[12], sh);
+  }
   if (threadIdx.x != 0) return;
   Ctrl* C = ctrl;
+  if (refq) {  // lyapunov_energy_from_parts (diag.cpp:76-88) + RadiusTracker
+    const double f = C->f_value;
+    if (C->f_star > f + 1e-9) {  // OtError in the reference: the solve fails
+      C->error = OTG_E_OT;
+      C->done = 1;
+    } else if (t[12] == 0.0) {
+      const double energy = (f - C->f_star) + (C->mu_step != 0.0 ? 0.5 * C->mu_step * t[8] : 0.0);
+      const double rx = sqrt(t[9]), ry = sqrt(t[10]);
+      C->rmax_x = fmax(C->rmax_x, rx);
+      C->rmax_y = fmax(C->rmax_y, ry);
+      if (C->trace_row >= 0) {
+        double* r = A.trace + C->trace_row * kTraceCols;
+        r[12] = energy;
+        r[13] = rx;
+        r[14] = ry;
+      }
+      if (C->boundary_pending && C->boundary_count <= C->boundary_cap)
+        A.bounds[(C->boundary_count - 1) * kBoundCols + 4] =
+            (f - C->f_star) + (C->mu != 0.0 ? 0.5 * C->mu * t[11] : 0.0);
+    }
+    C->boundary_pending = 0;
+  }
   if (stab && have_prev) {
     double cells[5];
     bool valid = true;
@@ -2051,6 +2128,8 @@ static AppArgs app_args(const Problem& P) {
   A.fast = P.storage != OTG_STORE_F64;  // fp32 stored or on the fly: shift estimate
   A.e2_part = P.e2_part;
   A.trace = P.trace;
+  A.vstar = P.vstar;
+  A.bounds = P.bounds;
   return A;
 }
 
@@ -2089,7 +2168,7 @@ static void launch_epilogue(Problem& P, int grid) {
   E.F = fin_args(P, grid);
   E.F.e1_part = P.epi_part;
   E.P = app_args(P);
-  E.P.e2_part = P.epi_part + kEpiMaxGrid * 8;
+  E.P.e2_part = P.epi_part + kEpiMaxGrid * 8;  // (kEpiMaxGrid x kE2 after the e1 rows)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(kEThreads);

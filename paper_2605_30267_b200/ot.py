@@ -332,12 +332,19 @@ class StepEval:  # sinkhorn.hpp:18-24
 
 
 @dataclass
+class ReferenceSolution:  # diag.hpp:46-49 (the yardstick of the energy / radius columns)
+    v_star: np.ndarray
+    f_star: float
+
+
+@dataclass
 class SolveConfig:  # sinkhorn.hpp:29-39
     tol_l1: float = 1e-6
     max_iters: int = 200000
     record_trace: bool = False
     trace_stride: int = 1
     wall_clock: bool = True
+    reference: Optional[ReferenceSolution] = None  # acc_solve energy / radius columns
 
 
 @dataclass
@@ -354,16 +361,18 @@ class HomotopyConfig:  # accel.hpp:68-81
 
 
 @dataclass
-class AccelInstrumentation:  # accel.hpp:37-40 (stability only; energy needs a reference)
-    stability: bool = False
+class AccelInstrumentation:  # accel.hpp:37-40
+    reference: Optional[ReferenceSolution] = None  # energy + radius columns
+    stability: bool = False                        # condition columns
 
 
 TRACE_FIELDS = ("iter", "wall_time_s", "marginal_violation_l1", "grad_f_l1", "reduced_f", "mu",
-                "alpha", "cond1_lhs", "cond1_rhs", "cond2_lhs", "cond2_rhs", "metric_drift_inf")
+                "alpha", "cond1_lhs", "cond1_rhs", "cond2_lhs", "cond2_rhs", "metric_drift_inf",
+                "energy", "radius_x_d", "radius_y")
 
 
 @dataclass
-class TraceRecord:  # diag.hpp:15-33 (energy / radius columns not produced)
+class TraceRecord:  # diag.hpp:15-33
     iter: int
     wall_time_s: float
     marginal_violation_l1: float
@@ -376,6 +385,9 @@ class TraceRecord:  # diag.hpp:15-33 (energy / radius columns not produced)
     cond2_lhs: Optional[float] = None
     cond2_rhs: Optional[float] = None
     metric_drift_inf: Optional[float] = None
+    energy: Optional[float] = None
+    radius_x_d: Optional[float] = None
+    radius_y: Optional[float] = None
 
 
 @dataclass
@@ -398,13 +410,14 @@ class SolverTrace:
         for r in self.records:
             lines.append(",".join([str(r.iter), num(r.wall_time_s), num(r.marginal_violation_l1),
                                    num(r.grad_f_l1), num(r.reduced_f), num(r.mu), num(r.alpha),
-                                   "", opt(r.cond1_lhs), opt(r.cond1_rhs), opt(r.cond2_lhs),
-                                   opt(r.cond2_rhs), opt(r.metric_drift_inf), "", ""]))
+                                   opt(r.energy), opt(r.cond1_lhs), opt(r.cond1_rhs),
+                                   opt(r.cond2_lhs), opt(r.cond2_rhs), opt(r.metric_drift_inf),
+                                   opt(r.radius_x_d), opt(r.radius_y)]))
         return "\n".join(lines) + "\n"
 
     def as_array(self) -> np.ndarray:
         return np.array([[np.nan if getattr(r, f) is None else getattr(r, f)
-                          for f in TRACE_FIELDS] for r in self.records]).reshape(-1, 12)
+                          for f in TRACE_FIELDS] for r in self.records]).reshape(-1, len(TRACE_FIELDS))
 
 
 @dataclass
@@ -433,6 +446,7 @@ class StageBoundary:  # accel.hpp:84-90
     mu: float
     alpha: float
     inner_before: int
+    energy: Optional[float] = None  # E(x, w / alpha; mu) when a reference is given
 
 
 @dataclass
@@ -441,6 +455,8 @@ class HomotopyResult:  # accel.hpp:92-99
     boundaries: List[StageBoundary] = field(default_factory=list)
     conditions_checked: int = 0
     conditions_held: int = 0
+    r_hat: float = 0.0   # max tracked radius, with a reference
+    c_star: float = 0.0  # homotopy_rate_constant(mu0, r_hat), with a reference
 
 
 @dataclass
@@ -462,14 +478,29 @@ class AccRun:  # accel.hpp:42-50
     device_seconds: float = 0.0
     row_pass_seconds: float = 0.0
     col_pass_seconds: float = 0.0
+    max_radius_x_d: float = 0.0  # RadiusTracker (diag.hpp:120-135), with a reference
+    max_radius_y: float = 0.0
 
 
 def _records(tr: np.ndarray, n: int) -> SolverTrace:
     out = SolverTrace()
     for row in tr[:n]:
         vals = [None if np.isnan(x) else float(x) for x in row]
-        out.records.append(TraceRecord(int(vals[0]), *vals[1:7], *vals[7:12]))
+        out.records.append(TraceRecord(int(vals[0]), *vals[1:7], *vals[7:15]))
     return out
+
+
+def _instr_c(instr):
+    """AccelInstrumentation -> (InstrC, keep-alive)."""
+    ins = _capi.InstrC(0, None, 0.0)
+    keep = None
+    if instr is not None:
+        ins.stability = int(bool(instr.stability))
+        if instr.reference is not None:
+            keep = _f64(instr.reference.v_star)
+            ins.reference_v = _ptr(keep)
+            ins.reference_f = float(instr.reference.f_star)
+    return ins, keep
 
 
 class _Res:
@@ -481,10 +512,10 @@ class _Res:
         self.v = np.empty(h.info.m)
         self.w = np.empty(h.info.m)
         self.r.u, self.r.v, self.r.w = _ptr(self.u), _ptr(self.v), _ptr(self.w)
-        self.trace = np.full((trace_cap, 12), np.nan) if record_trace else None
+        self.trace = np.full((trace_cap, _capi.TRACE_COLS), np.nan) if record_trace else None
         self.r.trace = _ptr(self.trace)
         self.r.trace_cap = trace_cap if record_trace else 0
-        self.bounds = np.full((boundaries_cap, 4), np.nan) if boundaries_cap else None
+        self.bounds = np.full((boundaries_cap, 5), np.nan) if boundaries_cap else None
         self.r.boundaries = _ptr(self.bounds)
         self.r.boundaries_cap = boundaries_cap
         self.r.time_sweeps = int(time_sweeps)
@@ -578,6 +609,11 @@ def _solve_cfg(cfg: SolveConfig):
     c = _capi.SolveConfigC()
     c.tol_l1, c.max_iters = cfg.tol_l1, cfg.max_iters
     c.record_trace, c.trace_stride = int(cfg.record_trace), cfg.trace_stride
+    c._keep = None
+    if cfg.reference is not None:
+        c._keep = _f64(cfg.reference.v_star)
+        c.reference_v = _ptr(c._keep)
+        c.reference_f = float(cfg.reference.f_star)
     return c
 
 
@@ -630,34 +666,40 @@ def acc_run(p: TransportProblem, x0, w0, mu, m, record_trace=False, trace_stride
     if x0.size != p.m() or w0.size != p.m():
         raise DimensionMismatch("accelerated state size does not match b")
     res = _Res(h, record_trace, _trace_cap(max(m, 1), trace_stride), time_sweeps)
-    ins = _capi.InstrC(int(bool(instr and instr.stability)))
+    ins, keep = _instr_c(instr)
     _check(_lib().otg_acc_run(h.raw, _ptr(x0), _ptr(w0), float(mu), int(m), int(record_trace),
                               int(trace_stride), C.byref(ins), C.byref(res.r)))
     r = res.r
     sr = res.solve_result()
     return AccRun(AccelState(res.v, res.w, mu, math.sqrt(2.0 * mu)), r.evaluations,
                   r.final_violation, sr.trace, r.conditions_checked, r.conditions_held,
-                  r.device_seconds, r.row_pass_seconds, r.col_pass_seconds)
+                  r.device_seconds, r.row_pass_seconds, r.col_pass_seconds, r.radius_x_max,
+                  r.radius_y_max)
 
 
 def homotopy_solve_instrumented(p: TransportProblem, cfg: HomotopyConfig = HomotopyConfig(),
                                 instr: Optional[AccelInstrumentation] = None,
                                 time_sweeps=False) -> HomotopyResult:
-    """accel.cpp:234-301 (energy / radius instrumentation out of scope)."""
+    """accel.cpp:234-301, with the stability and energy / radius instrumentation."""
     h = p.handle
     c = _capi.HomotopyConfigC(cfg.mu0, cfg.m0, cfg.max_outer, cfg.tol_l1, cfg.max_total_inner,
                               int(cfg.rescale_w_across_stages), int(cfg.record_trace),
                               cfg.trace_stride)
-    ins = _capi.InstrC(int(bool(instr and instr.stability)))
+    ins, keep = _instr_c(instr)
     bcap = int(min(max(cfg.max_outer, 1), 4096))
     res = _Res(h, cfg.record_trace, _trace_cap(min(cfg.max_total_inner, 10_000_000), cfg.trace_stride),
                time_sweeps, boundaries_cap=bcap)
     _check(_lib().otg_homotopy_solve(h.raw, C.byref(c), C.byref(ins), C.byref(res.r)))
     sr = res.solve_result()
     nb = min(res.r.outer_stages, bcap)
-    bounds = [StageBoundary(int(b[0]), float(b[1]), float(b[2]), int(b[3]))
+    bounds = [StageBoundary(int(b[0]), float(b[1]), float(b[2]), int(b[3]),
+                            None if np.isnan(b[4]) else float(b[4]))
               for b in res.bounds[:nb]]
-    return HomotopyResult(sr, bounds, res.r.conditions_checked, res.r.conditions_held)
+    out = HomotopyResult(sr, bounds, res.r.conditions_checked, res.r.conditions_held)
+    if instr is not None and instr.reference is not None:
+        out.r_hat = max(res.r.radius_x_max, res.r.radius_y_max)
+        out.c_star = homotopy_rate_constant(cfg.mu0, out.r_hat)
+    return out
 
 
 def homotopy_solve(p: TransportProblem, cfg: HomotopyConfig = HomotopyConfig(),
