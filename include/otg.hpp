@@ -12,6 +12,9 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -35,6 +38,8 @@ struct NonPositiveEntry : OtError { using OtError::OtError; };
 struct DimensionMismatch : OtError { using OtError::OtError; };
 struct DimensionTooLarge : OtError { using OtError::OtError; };
 struct DegenerateColumn : OtError { using OtError::OtError; };
+struct MalformedLine : OtError { using OtError::OtError; };
+struct IoError : OtError { using OtError::OtError; };
 struct DeviceError : OtError { using OtError::OtError; };  // CUDA / NCCL / OOM / no device
 
 inline void check(otg_status s) {
@@ -125,6 +130,76 @@ class TransportProblem {
   otg_problem h_ = nullptr;
   Vec a_, b_;
 };
+
+// ------------------------------------------------------------ instance CSV (data.cpp:203-271)
+// The host instance (a, b, row-major C, epsilon) as the reference writes it;
+// TransportProblem::dense(inst.a, inst.b, inst.C, inst.epsilon) uploads it.
+struct Instance {
+  Vec a, b, C;
+  double epsilon = 1.0;
+};
+
+inline void write_instance_csv(const std::string& path, const Instance& p) {
+  if (p.a.empty() || p.b.empty() || p.C.size() != p.a.size() * p.b.size())
+    throw DimensionMismatch("instance sizes do not match");
+  std::ofstream os(path);
+  if (!os) throw IoError("cannot write " + path);
+  char buf[64];
+  auto num = [&](double x) {
+    std::snprintf(buf, sizeof buf, "%.17g", x);
+    return std::string(buf);
+  };
+  os << "name,index,value\n";
+  os << "n,0," << p.a.size() << "\n";
+  os << "m,0," << p.b.size() << "\n";
+  os << "epsilon,0," << num(p.epsilon) << "\n";
+  for (size_t i = 0; i < p.a.size(); ++i) os << "a," << i << "," << num(p.a[i]) << "\n";
+  for (size_t j = 0; j < p.b.size(); ++j) os << "b," << j << "," << num(p.b[j]) << "\n";
+  for (size_t k = 0; k < p.C.size(); ++k) os << "C," << k << "," << num(p.C[k]) << "\n";
+  if (!os) throw IoError("short write to " + path);
+}
+
+inline Instance read_instance_csv(const std::string& path) {
+  std::ifstream is(path);
+  if (!is) throw IoError("cannot open " + path);
+  std::string line;
+  if (!std::getline(is, line) || line != "name,index,value")
+    throw MalformedLine(path + ": missing 'name,index,value' header");
+  long n = -1, m = -1, line_no = 1;
+  Instance out;
+  out.epsilon = -1.0;
+  while (std::getline(is, line)) {
+    ++line_no;
+    if (line.empty()) continue;
+    const auto c1 = line.find(',');
+    const auto c2 = line.find(',', c1 == std::string::npos ? c1 : c1 + 1);
+    if (c1 == std::string::npos || c2 == std::string::npos)
+      throw MalformedLine(path + ":" + std::to_string(line_no) + ": expected three fields");
+    const std::string name = line.substr(0, c1);
+    const long index = std::strtol(line.substr(c1 + 1, c2 - c1 - 1).c_str(), nullptr, 10);
+    const double value = std::strtod(line.c_str() + c2 + 1, nullptr);
+    if (name == "n") {
+      n = static_cast<long>(value);
+    } else if (name == "m") {
+      m = static_cast<long>(value);
+    } else if (name == "epsilon") {
+      out.epsilon = value;
+    } else if (name == "a" || name == "b" || name == "C") {
+      Vec& dst = name == "a" ? out.a : name == "b" ? out.b : out.C;
+      if (static_cast<size_t>(index) != dst.size())
+        throw MalformedLine(path + ":" + std::to_string(line_no) + ": " + name + " index " +
+                            std::to_string(index) + " out of order");
+      dst.push_back(value);
+    } else {
+      throw MalformedLine(path + ":" + std::to_string(line_no) + ": unknown field '" + name + "'");
+    }
+  }
+  if (n < 1 || m < 1 || !(out.epsilon > 0.0)) throw MalformedLine(path + ": missing n / m / epsilon");
+  if (static_cast<long>(out.a.size()) != n || static_cast<long>(out.b.size()) != m ||
+      static_cast<long>(out.C.size()) != n * m)
+    throw MalformedLine(path + ": entry counts do not match n, m");
+  return out;
+}
 
 // ------------------------------------------------------------ configs / results
 struct ReferenceSolution {  // diag.hpp:46-49

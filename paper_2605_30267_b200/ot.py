@@ -64,6 +64,14 @@ class DegenerateColumn(OtError):
     pass
 
 
+class MalformedLine(OtError):
+    pass
+
+
+class IoError(OtError):
+    pass
+
+
 class DeviceError(OtError):
     """CUDA / NCCL / allocation failures of the device path (no reference analogue)."""
 
@@ -895,6 +903,79 @@ def time_sweeps(p: TransportProblem, v, reps=10):
 
 
 # ------------------------------------------------------------ inputs -----
+
+
+# -------------------------------------------- instance CSV (data.cpp:203-271) ----
+
+def write_instance_csv(path, p: TransportProblem):
+    """data.cpp:203-218: name,index,value rows; n, m, epsilon, a, b, C row-major,
+    every double as %.17g (exact round trip)."""
+    validate_problem(p)
+    C_ = p.C  # the solver-unit cost (DimensionMismatch for a device-only cost)
+    lines = ["name,index,value", f"n,0,{p.n()}", f"m,0,{p.m()}", "epsilon,0,%.17g" % p.epsilon]
+    lines += ["a,%d,%.17g" % (i, x) for i, x in enumerate(p.a)]
+    lines += ["b,%d,%.17g" % (j, x) for j, x in enumerate(p.b)]
+    flat = np.asarray(C_, dtype=np.float64).ravel()
+    lines += ["C,%d,%.17g" % (k, x) for k, x in enumerate(flat)]
+    try:
+        with open(path, "w") as fh:
+            fh.write("\n".join(lines) + "\n")
+    except OSError as e:
+        raise IoError(f"cannot write {path}") from e
+
+
+def read_instance_csv(path) -> TransportProblem:
+    """data.cpp:220-269 (MalformedLine for any structural problem)."""
+    try:
+        fh = open(path)
+    except OSError as e:
+        raise IoError(f"cannot open {path}") from e
+    with fh:
+        first = fh.readline().rstrip("\n")
+        if first != "name,index,value":
+            raise MalformedLine(f"{path}: missing 'name,index,value' header")
+        n = m = -1
+        eps = -1.0
+        vals = {"a": [], "b": [], "C": []}
+        for line_no, line in enumerate(fh, start=2):
+            line = line.rstrip("\n")
+            if not line:
+                continue
+            parts = line.split(",", 2)
+            if len(parts) < 3:
+                raise MalformedLine(f"{path}:{line_no}: expected three fields")
+            name, idx, value = parts[0], _strtol(parts[1]), _strtod(parts[2])
+            if name == "n":
+                n = int(value)
+            elif name == "m":
+                m = int(value)
+            elif name == "epsilon":
+                eps = value
+            elif name in vals:
+                if idx != len(vals[name]):
+                    raise MalformedLine(f"{path}:{line_no}: {name} index {idx} out of order")
+                vals[name].append(value)
+            else:
+                raise MalformedLine(f"{path}:{line_no}: unknown field '{name}'")
+    if n < 1 or m < 1 or not eps > 0.0:
+        raise MalformedLine(f"{path}: missing n / m / epsilon")
+    if len(vals["a"]) != n or len(vals["b"]) != m or len(vals["C"]) != n * m:
+        raise MalformedLine(f"{path}: entry counts do not match n = {n}, m = {m}")
+    return make_problem(np.array(vals["a"]), np.array(vals["b"]),
+                        np.array(vals["C"]).reshape(n, m), eps)
+
+
+def _strtol(t: str) -> int:  # std::strtol: leading integer, else 0
+    import re as _re
+    mt = _re.match(r"\s*[-+]?\d+", t)
+    return int(mt.group(0)) if mt else 0
+
+
+def _strtod(t: str) -> float:  # std::strtod: leading number, else 0
+    import re as _re
+    mt = _re.match(r"\s*[-+]?(?:inf(?:inity)?|nan|(?:\d+\.?\d*|\.\d+)(?:[eE][-+]?\d+)?)", t,
+                   _re.IGNORECASE)
+    return float(mt.group(0)) if mt else 0.0
 
 
 def synthetic_instance(n, m, seed):

@@ -65,6 +65,24 @@ static void cpu_checks() {  // test_core.cpp:30-71 through the C-ABI
   otg::check(otg_gen_synthetic_instance(2, 3, 7, a.data(), b.data(), C.data()));
   CHECK(approx(C[0], 0.17316924621916613, 1e-15));  // test_data.cpp:84
   CHECK(approx(a[1], 0.75663205931103994, 1e-15));  // test_data.cpp:80
+  // instance CSV round trip is exact (test_data.cpp:310-336)
+  otg::Instance inst;
+  inst.a.resize(3);
+  inst.b.resize(4);
+  inst.C.resize(12);
+  otg::check(otg_gen_synthetic_instance(3, 4, 99, inst.a.data(), inst.b.data(), inst.C.data()));
+  inst.epsilon = 0.037;
+  const std::string path = "/tmp/otg_test_instance.csv";
+  otg::write_instance_csv(path, inst);
+  const otg::Instance back = otg::read_instance_csv(path);
+  CHECK(back.a == inst.a && back.b == inst.b && back.C == inst.C && back.epsilon == inst.epsilon);
+  {
+    std::FILE* f = std::fopen(path.c_str(), "w");
+    std::fputs("name,index,value\nn,0,1\nm,0,1\nepsilon,0,1\na,1,1\n", f);
+    std::fclose(f);
+  }
+  CHECK_THROWS_AS(otg::read_instance_csv(path), otg::MalformedLine);
+  CHECK_THROWS_AS(otg::read_instance_csv("/nonexistent/otg.csv"), otg::IoError);
 }
 
 static void gpu_checks() {
