@@ -317,6 +317,16 @@ otg_status otg_plan_topk(otg_problem h, const double* u, const double* v, const 
 otg_status otg_nn_assign(const double* queries, int64_t nq, const double* refs, int64_t nref,
                          int d, int device, int* out);
 
+/* ---- diagnostics (dual.hpp) ---- */
+
+/* dual_F (dual.cpp:88-101): exp(LSE_ij(u_i + v_j - C'_ij)) - <u, a> - <v, b>;
+ * PotentialOverflow above exponent 700. */
+otg_status otg_dual_F(otg_problem h, const double* u, const double* v, double* out);
+
+/* hessian_f (dual.cpp:118-136): H = diag(c(v)) - P^T diag(a)^{-1} P at the row
+ * solve of v, m x m row-major; DimensionTooLarge past m = 2000. */
+otg_status otg_hessian_f(otg_problem h, const double* v, double* H);
+
 /* ---- batched path: many small independent problems, one CTA each ---- */
 typedef struct otg_batch_s* otg_batch;
 

@@ -376,6 +376,20 @@ inline double reduced_f(const TransportProblem& p, const Vec& v) {  // dual.cpp:
   return 1.0 - ua - vb;
 }
 
+inline double dual_F(const TransportProblem& p, const Vec& u, const Vec& v) {  // dual.cpp:88-101
+  if (static_cast<int64_t>(u.size()) != p.info().n_local || static_cast<int64_t>(v.size()) != p.m())
+    throw DimensionMismatch("(u, v) size");
+  double out = 0;
+  check(otg_dual_F(p.handle(), u.data(), v.data(), &out));
+  return out;
+}
+inline Vec hessian_f(const TransportProblem& p, const Vec& v) {  // dual.cpp:118-136, row-major m x m
+  if (static_cast<int64_t>(v.size()) != p.m()) throw DimensionMismatch("v size");
+  Vec H(static_cast<size_t>(p.m()) * p.m());
+  check(otg_hessian_f(p.handle(), v.data(), H.data()));
+  return H;
+}
+
 inline StepEval eval_normalized_step(const TransportProblem& p, const Vec& v) {
   if (static_cast<int64_t>(v.size()) != p.m()) throw DimensionMismatch("v size");
   StepEval e;

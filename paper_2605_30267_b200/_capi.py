@@ -112,6 +112,8 @@ SIGNATURES = {
     "otg_plan_row_argmax": (C.c_int, [H, VP, VP, VP]),
     "otg_plan_topk": (C.c_int, [H, VP, VP, VP, C.c_int64, C.c_int, VP]),
     "otg_nn_assign": (C.c_int, [VP, C.c_int64, VP, C.c_int64, C.c_int, C.c_int, VP]),
+    "otg_dual_F": (C.c_int, [H, VP, VP, VP]),
+    "otg_hessian_f": (C.c_int, [H, VP, VP]),
     "otg_batch_create_dense": (C.c_int, [I64, VP, VP, VP, VP, VP, C.c_double, VP, VP]),
     "otg_batch_create_cosine": (C.c_int, [I64, VP, VP, I64, VP, VP, VP, VP, C.c_int,
                                           C.c_double, VP, VP]),

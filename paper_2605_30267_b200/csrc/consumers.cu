@@ -224,6 +224,78 @@ k_nn(const double* __restrict__ q, int64_t nq, const double* __restrict__ ref, i
   if (p < nq) out[p] = static_cast<int>(best);
 }
 
+// ---- diagnostics (dual.cpp:88-101, 118-136) ----
+
+// Q_ij = P_ij / sqrt(a_i) with the plan of the row solve at v
+// (plan_from_workspace, dual.cpp:72-78): P_ij = exp((-C'_ij + v_j) - M_i) a_i / S_i.
+__global__ void __launch_bounds__(kT)
+k_plan_q(const Src s, int64_t n, int64_t m, const double* __restrict__ v,
+         const double* __restrict__ rowM, const double* __restrict__ wrow,
+         const double* __restrict__ a, double* __restrict__ Q) {
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y) {
+    const double Mi = rowM[i], wi = wrow[i], ra = 1.0 / sqrt(a[i]);
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; j < m;
+         j += static_cast<int64_t>(gridDim.x) * kT) {
+      const double c = cost_at(s.C64, s.C32, s.X, s.Y, s.ldc, s.kappa, i, j);
+      Q[i * m + j] = exp(((-c) + v[j]) - Mi) * wi * ra;
+    }
+  }
+}
+
+// H_jk = -sum_i Q_ij Q_ik (+ col_j on the diagonal, added on the host):
+// 32 x 32 output tiles, rows of Q staged through shared memory.
+constexpr int kHT = 32;
+__global__ void __launch_bounds__(kHT * kHT)
+k_syrk_neg(int64_t n, int64_t m, const double* __restrict__ Q, double* __restrict__ H) {
+  __shared__ double qa[kHT][kHT + 1], qb[kHT][kHT + 1];
+  const int tj = threadIdx.x % kHT, tk = threadIdx.x / kHT;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * kHT, k0 = static_cast<int64_t>(blockIdx.y) * kHT;
+  double acc = 0.0;
+  for (int64_t i0 = 0; i0 < n; i0 += kHT) {
+    const int64_t ir = i0 + tk;
+    qa[tk][tj] = (ir < n && j0 + tj < m) ? Q[ir * m + j0 + tj] : 0.0;
+    qb[tk][tj] = (ir < n && k0 + tj < m) ? Q[ir * m + k0 + tj] : 0.0;
+    __syncthreads();
+#pragma unroll 8
+    for (int r = 0; r < kHT; ++r) acc += qa[r][tj] * qb[r][tk];
+    __syncthreads();
+  }
+  if (j0 + tj < m && k0 + tk < m) H[(k0 + tk) * m + j0 + tj] = -acc;
+}
+
+// dual_F: per-row online (max, sum) of E_ij = ((-C'_ij) + u_i) + v_j.
+__global__ void __launch_bounds__(kT)
+k_dual_rows(const Src s, int64_t n, int64_t m, const double* __restrict__ u,
+            const double* __restrict__ v, double2* __restrict__ out) {
+  const int64_t i = blockIdx.x;
+  double top = -DBL_MAX, sum = 0.0;
+  for (int64_t j = threadIdx.x; j < m; j += kT) {
+    const double e = exponent(s, u, v, i, j);
+    if (e > top) {
+      sum = sum * exp(top - e) + 1.0;
+      top = e;
+    } else {
+      sum += exp(e - top);
+    }
+  }
+  __shared__ double st[kT], ss[kT];
+  st[threadIdx.x] = top;
+  __syncthreads();
+  for (int o = kT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) st[threadIdx.x] = fmax(st[threadIdx.x], st[threadIdx.x + o]);
+    __syncthreads();
+  }
+  const double T = st[0];
+  __syncthreads();
+  ss[threadIdx.x] = top > -DBL_MAX ? sum * exp(top - T) : 0.0;
+  __syncthreads();
+  for (int o = kT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) ss[threadIdx.x] += ss[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[i] = make_double2(T, ss[0]);
+}
+
 void check_vec(const double* x, int64_t count, const char* what) {  // dual.cpp:13-18
   if (!x) fail(OTG_E_DIMENSION, std::string(what) + " is NULL");
   for (int64_t k = 0; k < count; ++k)
@@ -247,6 +319,10 @@ void check_overflow(const std::vector<double>& emax) {  // core.cpp:66-69
     std::snprintf(buf, sizeof buf, "plan exponent %.3g exceeds bound", top);
     fail(OTG_E_OVERFLOW, buf);
   }
+}
+
+void check(otg_status st) {  // a nested C-ABI call: propagate its status and message
+  if (st != OTG_OK) fail(st, otg_last_error());
 }
 
 struct DevBuf {  // RAII for the consumers' scratch
@@ -395,6 +471,89 @@ otg_status otg_nn_assign(const double* queries, int64_t nq, const double* refs, 
     }
     OTG_CUDA(cudaGetLastError());
     OTG_CUDA(cudaMemcpy(out, dout.p, static_cast<size_t>(nq) * sizeof(int), cudaMemcpyDeviceToHost));
+  });
+}
+
+otg_status otg_dual_F(otg_problem h, const double* u, const double* v, double* out) {
+  return guard([&] {  // dual.cpp:88-101
+    Problem& P = problem_of(h);
+    if (!out) fail(OTG_E_DIMENSION, "NULL output");
+    const int64_t n = P.n_local, m = P.m;
+    DevBuf uvb(static_cast<size_t>(n + m) * sizeof(double));
+    double* uv = uvb.as<double>();
+    upload_uv(P, u, v, uv);
+    DevBuf rows(static_cast<size_t>(n) * sizeof(double2));
+    k_dual_rows<<<static_cast<unsigned>(n), kT, 0, P.stream>>>(src_of(P), n, m, uv, uv + n,
+                                                               rows.as<double2>());
+    OTG_CUDA(cudaGetLastError());
+    std::vector<double2> hr(n);
+    OTG_CUDA(cudaMemcpyAsync(hr.data(), rows.p, n * sizeof(double2), cudaMemcpyDeviceToHost,
+                             P.stream));
+    OTG_CUDA(cudaStreamSynchronize(P.stream));
+    double top = -DBL_MAX;
+    for (const auto& r : hr) top = std::max(top, r.x);
+    double sum = 0.0, ua = 0.0, vb = 0.0;
+    for (const auto& r : hr) sum += r.y * std::exp(r.x - top);
+    std::vector<double> ha(n), hb(m);
+    OTG_CUDA(cudaMemcpy(ha.data(), P.a, n * sizeof(double), cudaMemcpyDeviceToHost));
+    OTG_CUDA(cudaMemcpy(hb.data(), P.b, m * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n; ++i) ua += u[i] * ha[i];
+    for (int64_t j = 0; j < m; ++j) vb += v[j] * hb[j];
+    if (P.sharded) {  // global max, then the rescaled sums and <u, a>
+      DevBuf d(3 * sizeof(double));
+      double hv[3] = {top, 0.0, 0.0};
+      OTG_CUDA(cudaMemcpy(d.p, hv, sizeof(double), cudaMemcpyHostToDevice));
+      comm_allreduce_max(P, d.as<double>(), 1);
+      OTG_CUDA(cudaMemcpy(hv, d.p, sizeof(double), cudaMemcpyDeviceToHost));
+      const double g = hv[0];
+      hv[1] = sum * std::exp(top - g);
+      hv[2] = ua;
+      OTG_CUDA(cudaMemcpy(d.as<double>() + 1, hv + 1, 2 * sizeof(double), cudaMemcpyHostToDevice));
+      comm_allreduce_sum(P, d.as<double>() + 1, 2);
+      OTG_CUDA(cudaMemcpy(hv + 1, d.as<double>() + 1, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+      top = g;
+      sum = hv[1];
+      ua = hv[2];
+    }
+    const double lse = top + std::log(sum);
+    if (lse > kOverflow) {
+      char buf[96];
+      std::snprintf(buf, sizeof buf, "dual mass exponent %.3g exceeds bound", lse);
+      fail(OTG_E_OVERFLOW, buf);
+    }
+    *out = std::exp(lse) - ua - vb;
+  });
+}
+
+otg_status otg_hessian_f(otg_problem h, const double* v, double* H) {
+  return guard([&] {  // dual.cpp:118-136
+    Problem& P = problem_of(h);
+    if (!H) fail(OTG_E_DIMENSION, "NULL output");
+    const int64_t n = P.n_local, m = P.m;
+    if (m > 2000) {
+      char buf[96];
+      std::snprintf(buf, sizeof buf, "dense reduced Hessian capped at m = 2000, got %lld",
+                    static_cast<long long>(m));
+      fail(OTG_E_TOO_LARGE, buf);
+    }
+    std::vector<double> u(n), col(m);
+    check(otg_row_solve_marginals(h, v, u.data(), col.data()));  // rowM, wrow on the device
+    DevBuf dv(static_cast<size_t>(m) * sizeof(double));
+    OTG_CUDA(cudaMemcpyAsync(dv.p, v, m * sizeof(double), cudaMemcpyHostToDevice, P.stream));
+    DevBuf Q(static_cast<size_t>(n) * m * sizeof(double));
+    DevBuf dH(static_cast<size_t>(m) * m * sizeof(double));
+    const dim3 gq(static_cast<unsigned>(std::min<int64_t>((m + kT - 1) / kT, 64)),
+                  static_cast<unsigned>(std::min<int64_t>(n, 65535)));
+    k_plan_q<<<gq, kT, 0, P.stream>>>(src_of(P), n, m, dv.as<double>(), P.rowM, P.wrow, P.a,
+                                       Q.as<double>());
+    const unsigned gt = static_cast<unsigned>((m + kHT - 1) / kHT);
+    k_syrk_neg<<<dim3(gt, gt), kHT * kHT, 0, P.stream>>>(n, m, Q.as<double>(), dH.as<double>());
+    OTG_CUDA(cudaGetLastError());
+    if (P.sharded) comm_allreduce_sum(P, dH.as<double>(), static_cast<size_t>(m) * m);
+    OTG_CUDA(cudaMemcpyAsync(H, dH.p, static_cast<size_t>(m) * m * sizeof(double),
+                             cudaMemcpyDeviceToHost, P.stream));
+    OTG_CUDA(cudaStreamSynchronize(P.stream));
+    for (int64_t j = 0; j < m; ++j) H[j * m + j] += col[j];  // + col.asDiagonal()
   });
 }
 

@@ -581,6 +581,28 @@ def reduced_f(p, v) -> float:  # dual.cpp:103-108
     return 1.0 - u.dot(p.a) - v.dot(p.b)
 
 
+def dual_F(p: TransportProblem, u, v) -> float:
+    """dual.cpp:88-101: exp(LSE(u_i + v_j - C'_ij)) - <u, a> - <v, b>."""
+    h = p.handle
+    u, v = _f64(u), _f64(v)
+    if u.size != h.n_local or v.size != p.m():
+        raise DimensionMismatch(f"(u, v) sizes ({u.size}, {v.size}), expected ({h.n_local}, {p.m()})")
+    out = C.c_double()
+    _check(_lib().otg_dual_F(h.raw, _ptr(u), _ptr(v), C.byref(out)))
+    return out.value
+
+
+def hessian_f(p: TransportProblem, v) -> np.ndarray:
+    """dual.cpp:118-136: diag(c(v)) - P^T diag(a)^-1 P, dense m x m (m <= 2000)."""
+    h = p.handle
+    v = _f64(v)
+    if v.size != p.m():
+        raise DimensionMismatch(f"v has size {v.size}, expected {p.m()}")
+    H = np.empty((p.m(), p.m()))
+    _check(_lib().otg_hessian_f(h.raw, _ptr(v), _ptr(H)))
+    return H
+
+
 # ------------------------------------------------------- sinkhorn.hpp ----
 
 
