@@ -4,8 +4,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_2605_30267_b200 import ot, _capi
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
-x, y = ot.gen_config(3, n, n, 3)
-p = ot.TransportProblem.from_points(np.full(n, 1 / n), np.full(n, 1 / n), x, y, 1e-3)
+m = int(sys.argv[2]) if len(sys.argv) > 2 else n
+x, y = ot.gen_config(3, n, m, 3)
+p = ot.TransportProblem.from_points(np.full(n, 1 / n), np.full(m, 1 / m), x, y, 1e-3)
 ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=3))
 lib = ctypes.CDLL(os.path.join(os.path.dirname(_capi.__file__), "libotg.so"))
 buf = (ctypes.c_longlong * (256 * 8))()
