@@ -225,15 +225,10 @@ struct Problem {
 
   // single-pass fused sweep (fused.cu), fp32 storage only
   int fused = 0, fused_qpt = 0, fused_W = 0, fused_slots = 0, fused_smem = 0,
-      fused_clusters = 0, fused_cl = 8, fused_qpt4 = 8;
+      fused_clusters = 0, fused_cl = 8;
   double* sp_rec = nullptr;     // per-row 32-byte records (shift estimate, a, log a)
   int* sp_bad_rows = nullptr;   // rows whose shift estimate was loose, per cluster
   int* sp_bad_count = nullptr;
-  // variant 2 (k_sp2): one CTA per SM, chunked rows, L1 / L2 staging
-  int fused_kind = 1, fused_grid = 0, fused_chunks = 0, fused_lag = 2, fused_pf = 0;
-  void* sp_seg = nullptr;         // chunk ring of per-row segment partials
-  float* sp_lam = nullptr;        // fp32 w per row
-  unsigned* sp_sync = nullptr;    // cnt[chunks] | ready[chunks] | epoch | bad_epoch
 
   // column-pass partials
   int col_splits = 1;
@@ -293,8 +288,7 @@ void launch_split_p(Problem& P);  // vq <- split of p (after the host sets p)
 bool fused_configure(Problem& P);
 void fused_alloc(Problem& P);
 void launch_fused(Problem& P, float kh, float kl);
-void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int ncl,
-                    const unsigned* bad_epoch = nullptr, const unsigned* epoch = nullptr);
+void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int ncl);
 int partial_rows(const Problem& P);  // rows of P.part the merge sums
 
 // NCCL (comm.cpp)

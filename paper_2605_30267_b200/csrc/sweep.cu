@@ -630,11 +630,9 @@ k_sp_redo(const CostSrc src, int64_t n, int64_t m, const double* __restrict__ p,
           double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
           double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
           int* __restrict__ rowJ, const int* __restrict__ bad_rows,
-          const int* __restrict__ bad_count, int ncl, Ctrl* __restrict__ ctrl,
-          const unsigned* __restrict__ bad_epoch, const unsigned* __restrict__ epoch) {
+          const int* __restrict__ bad_count, int ncl, Ctrl* __restrict__ ctrl) {
   pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done || !ctrl->shift_valid) return;
-  if (bad_epoch != nullptr && *bad_epoch != *epoch) return;  // no loose row listed
   for (int c = 0; c < ncl; ++c) {
     const int nb = bad_count[c];
     const int64_t base = n * c / ncl;
@@ -2049,12 +2047,11 @@ void launch_split_p(Problem& P) {
   launch_k(k_split_p, g, 256, 0, P.stream, P.m, P.mpad, P.p, P.vq);
 }
 
-void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int ncl,
-                    const unsigned* bad_epoch, const unsigned* epoch) {
+void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int ncl) {
   launch_k(k_sp_redo, 148, kRowThreads, 0, P.stream, cost_src(P), P.n_local, P.m, P.p, P.kappa, P.a,
                                                 P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,
                                                 P.rowM2, P.rowJ, bad_rows, bad_count, ncl,
-                                                P.ctrl, bad_epoch, epoch);
+                                                P.ctrl);
 }
 
 int partial_rows(const Problem& P) { return P.vshards * P.col_splits; }

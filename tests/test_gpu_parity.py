@@ -334,7 +334,7 @@ def _points_problem(n, m, seed, eps, fused):
     import os
     x, y = ot.gen_config(3, n, m, seed)
     old = os.environ.get("OTG_FUSED")
-    os.environ["OTG_FUSED"] = str(int(fused))  # 0 two-pass, 1 cluster single pass, 2 L2-staged
+    os.environ["OTG_FUSED"] = "1" if fused else "0"
     try:
         p = ot.TransportProblem.from_points(np.full(n, 1 / n), np.full(m, 1 / m), x, y, eps)
     finally:
@@ -363,13 +363,11 @@ def test_fused_eval_matches_oracle_and_two_pass(n, m):
         assert abs(e.f_value - r["f_value"]) <= 1e-6 * max(1.0, abs(r["f_value"]))
 
 
-@pytest.mark.parametrize("n,m,eps,kind", [(300, 4100, 2e-3, 1), (257, 65536, 1e-3, 1),
-                                          (2048, 2048, 5e-4, 1), (257, 65536, 1e-3, 2),
-                                          (1000, 40004, 1e-3, 2), (4099, 16384, 5e-4, 2)])
-def test_fused_single_pass_matches_two_pass_solve(n, m, eps, kind):
-    """Steady-state single-pass kernels (cluster exchange or L2-staged chunks,
-    shift estimates, loose-row redo + column patch) against the two-pass kernels."""
-    pf = _points_problem(n, m, 11, eps, kind)
+@pytest.mark.parametrize("n,m,eps", [(300, 4100, 2e-3), (257, 65536, 1e-3), (2048, 2048, 5e-4)])
+def test_fused_single_pass_matches_two_pass_solve(n, m, eps):
+    """Steady-state single-pass kernel (cluster exchange, shift estimates,
+    loose-row redo + column patch) against the two-pass kernels."""
+    pf = _points_problem(n, m, 11, eps, True)
     p2 = _points_problem(n, m, 11, eps, False)
     assert pf.handle.info.sweep_mode == 2 and p2.handle.info.sweep_mode == 1
     cfg = ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=40)
@@ -381,11 +379,9 @@ def test_fused_single_pass_matches_two_pass_solve(n, m, eps, kind):
     assert abs(gf.final_violation - g2.final_violation) <= 1e-5 * max(g2.final_violation, 1e-3)
 
 
-@pytest.mark.parametrize("n,m,kind", [(512, 2048, 1), (600, 12000, 2)])
-def test_fused_homotopy_cost_and_iterations(n, m, kind):
-    eps, tol = 5e-3, 1e-6
-    pf = _points_problem(n, m, 9, eps, kind)
-    assert pf.handle.info.sweep_mode == 2
+def test_fused_homotopy_cost_and_iterations():
+    n, m, eps, tol = 512, 2048, 5e-3, 1e-6
+    pf = _points_problem(n, m, 9, eps, True)
     q = O.Problem(np.full(n, 1 / n), np.full(m, 1 / m), pf.stored_cost(), cost_div=eps)
     g = ot.homotopy_solve(pf, ot.HomotopyConfig(tol_l1=tol))
     o = O.homotopy_solve(q, tol_l1=tol)
