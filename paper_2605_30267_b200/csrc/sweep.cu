@@ -898,24 +898,29 @@ k_row_exact(const CostSrc src, int64_t n, int64_t m, const double* __restrict__ 
             int64_t mpad) {
   pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done || ctrl->shift_valid) return;
-  if (online_first_pass()) {
-    const double k2 = kappa * kLog2e;
-    const float kh = static_cast<float>(k2);
-    const float kl = static_cast<float>(k2 - static_cast<double>(kh));
-    row_online_block<R, OTF>(src, n, m, vq, mpad, kh, kl, a, loga, rowM, rowS, u, wrow, aux,
-                             rowM2, rowJ, static_cast<int64_t>(blockIdx.x) * R);
-    return;
-  }
-  int64_t rows[R];
-  bool valid[R];
+  // grid-stride over row blocks: the launch is a no-op in every evaluation but
+  // the first of a solve, so it is sized to the resident CTAs, not to n / R
+  for (int64_t blk = blockIdx.x; blk * R < n; blk += gridDim.x) {
+    if (online_first_pass()) {
+      const double k2 = kappa * kLog2e;
+      const float kh = static_cast<float>(k2);
+      const float kl = static_cast<float>(k2 - static_cast<double>(kh));
+      row_online_block<R, OTF>(src, n, m, vq, mpad, kh, kl, a, loga, rowM, rowS, u, wrow, aux,
+                               rowM2, rowJ, blk * R);
+    } else {
+      int64_t rows[R];
+      bool valid[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * R + r;
-    valid[r] = i < n;
-    rows[r] = valid[r] ? i : n - 1;
+      for (int r = 0; r < R; ++r) {
+        const int64_t i = blk * R + r;
+        valid[r] = i < n;
+        rows[r] = valid[r] ? i : n - 1;
+      }
+      row_exact_block<R, OTF>(rows, src, m, p, kappa, a, loga, rowM, rowS, u, wrow, aux, rowM2,
+                              rowJ, valid);
+    }
+    __syncthreads();  // (shared scratch of the block helpers)
   }
-  row_exact_block<R, OTF>(rows, src, m, p, kappa, a, loga, rowM, rowS, u, wrow, aux, rowM2, rowJ,
-                          valid);
 }
 
 template <int R, bool OTF, int PF>
@@ -1941,6 +1946,15 @@ int64_t row_blocks(const Problem& P) {
 }
 
 
+// Resident CTAs of a grid-stride kernel (capped at `blocks`).
+template <typename K>
+static unsigned resident_grid(const Problem& P, K kernel, int64_t blocks) {
+  int sms = 0, occ = 0;
+  OTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.device));
+  OTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kRowThreads, 0));
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(blocks, int64_t{sms} * std::max(occ, 1))));
+}
+
 void launch_row_pass(Problem& P) {
   const int64_t blocks = row_blocks(P);
   double* rowpart = P.e1_part + P.e_blocks * 8;  // scratch after the E1 partials
@@ -1974,7 +1988,8 @@ void launch_row_pass(Problem& P) {
   src, P.n_local, P.m, P.vq, P.dq, P.mpad, kh, kl, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow,  \
       P.aux, P.rowM2, P.rowJ, P.redo_rows, P.ctrl
 #define OTG_ROW(RR, OTF)                                                                      \
-  launch_k(k_row_exact<RR, OTF>, blocks, kRowThreads, 0, P.stream,                                  \
+  launch_k(k_row_exact<RR, OTF>, resident_grid(P, k_row_exact<RR, OTF>, blocks), kRowThreads, 0,  \
+           P.stream,                                                                          \
       src, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,     \
       P.rowM2, P.rowJ, P.ctrl, P.vq, P.mpad);                                                 \
   if (RR == 4 && !OTF && row_pf == 1)                                                         \
@@ -1991,7 +2006,8 @@ void launch_row_pass(Problem& P) {
     const bool otf = P.storage == OTG_STORE_ON_THE_FLY;
     if (P.fused) {
       // exact first evaluation (two-pass), then the single-pass kernel
-      launch_k(k_row_exact<4, false>, blocks, kRowThreads, 0, P.stream, 
+      launch_k(k_row_exact<4, false>, resident_grid(P, k_row_exact<4, false>, blocks), kRowThreads,
+               0, P.stream, 
           src, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,
           P.rowM2, P.rowJ, P.ctrl, P.vq, P.mpad);
       launch_fused(P, kh, kl);
