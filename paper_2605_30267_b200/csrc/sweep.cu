@@ -744,6 +744,14 @@ __device__ __forceinline__ void row_online_block(
     float4 c[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) c[r] = cost_quad<OTF>(src, rr[r], q, xr[r], y4);
+    if constexpr (!OTF) {  // L2 prefetch 4 chunks ahead: the rescale branch keeps the
+      const int64_t qp = q + 4 * kRowThreads;  // compiler from pipelining these loads
+      if (qp < nq) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          prefetch_l2(reinterpret_cast<const float4*>(src.C + rr[r] * src.ldc) + qp);
+      }
+    }
     const float2 V01 = make_float2(V.x, V.y), V23 = make_float2(V.z, V.w);
     const float2 F01 = make_float2(F.x, F.y), F23 = make_float2(F.z, F.w);
 #pragma unroll
