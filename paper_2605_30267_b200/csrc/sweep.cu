@@ -1988,10 +1988,13 @@ void launch_row_pass(Problem& P) {
     // L2::256B loads, 3 / 5 = prefetch 2 / 4 chunks ahead).  B200, 65536^2:
     // with the scalar inner loop 3.19 ms (off) -> 2.95 ms (3); with the packed
     // f32x2 loop both take ~2.92 ms (3 CTAs/SM either way), so it is off
-    static const int row_pf = [] {
+    static const int row_pf_env = [] {
       const char* s = getenv("OTG_ROW_PF");
-      return s ? atoi(s) : 0;
+      return s ? atoi(s) : -1;
     }();
+    // cfg2 (8192^2): 70.8 -> 65.7 us with the prefetch; cfg3: equal, so only
+    // rows short enough for the per-CTA latency to show get it by default
+    const int row_pf = row_pf_env >= 0 ? row_pf_env : (P.m <= 16384 ? 3 : 0);
 #define OTG_SHIFT_ARGS                                                                        \
   src, P.n_local, P.m, P.vq, P.dq, P.mpad, kh, kl, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow,  \
       P.aux, P.rowM2, P.rowJ, P.redo_rows, P.ctrl
