@@ -95,3 +95,42 @@ def test_config3_full_size_properties():
     for ch in range(3):
         assert bary[:, ch].min() >= x[:, ch].min() - 1e-9
         assert bary[:, ch].max() <= x[:, ch].max() + 1e-9
+
+
+def test_config5_full_size_properties():
+    """BASELINE config 5 at its full size (200000^2, cost never stored): a
+    short homotopy run is deterministic, drives the violation down, and the
+    plan of its potentials (one more streaming pass) has the marginal error
+    the solver reported."""
+    N = 200_000
+    x, y = ot.gen_config(5, N, N, 5)
+    a = np.full(N, 1.0 / N)
+    p = ot.TransportProblem.from_points(a, a, x, y, 1e-3, norm="none", storage="on_the_fly")
+    cfg = ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=12)
+    r1 = ot.homotopy_solve(p, cfg)
+    r2 = ot.homotopy_solve(p, cfg)
+    assert r1.iterations == r2.iterations == 12
+    assert np.array_equal(r1.potentials.v, r2.potentials.v)
+    assert np.array_equal(r1.potentials.u, r2.potentials.u)
+    assert np.isfinite(r1.potentials.v).all() and abs(r1.potentials.v.mean()) < 1e-9
+    st = ot.plan_stats(p, r1.potentials.u, r1.potentials.v)
+    assert abs(st.marginal_violation_l1 - r1.final_violation) <= 0.05 * r1.final_violation
+    r0 = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=1))
+    assert r1.final_violation < r0.final_violation
+
+
+def test_config2_full_size_properties():
+    """BASELINE config 2 (8192^2, stored fp32, both eps): converges to 1e-6,
+    bitwise reproducible, and the plan's marginal error matches."""
+    x, y = ot.gen_config(2, 8192, 8192, 2)
+    a = np.full(8192, 1.0 / 8192)
+    for eps in (1e-2, 1e-3):
+        p = ot.TransportProblem.from_points(a, a, x, y, eps)
+        for kind in ("sinkhorn", "acc-homotopy"):
+            r = ot.run_solver(p, ot.SolverSpec(kind=kind, max_iters=200000), 1e-6)
+            r2 = ot.run_solver(p, ot.SolverSpec(kind=kind, max_iters=200000), 1e-6)
+            assert r.converged and r.iterations == r2.iterations
+            assert np.array_equal(r.potentials.v, r2.potentials.v)
+            st = ot.plan_stats(p, r.potentials.u, r.potentials.v)
+            assert st.marginal_violation_l1 <= 1.2e-6
+        p.close()
