@@ -136,36 +136,59 @@ class ClockSampler:
 
 
 # ------------------------------------------------------- CPU baseline ----
-def cpu_baseline(x, y, threads: int, target_s: float = 12.0):
+class CpuArm:
     """The CPU oracle (a restatement of the reference's single-threaded fp64
-    sweep, oracle/otoracle.cpp) timed on this host on a bounded row sample of
-    the same workload, extrapolated to one full evaluation (= one iteration)."""
-    from oracle import oracle as O
-    a = np.full(N, 1.0 / N)
-    sample_rows = 16
-    v = np.zeros(M)
-    # cost rows: fp32, exactly as the GPU stores them (sqeuclid / max)
-    rawmax = O.sqeuclid_max(x, y, threads=os.cpu_count() or 1)
+    sweep, oracle/otoracle.cpp) on a bounded row sample of the same workload:
+    the fp32 cost rows are built once (exactly as the GPU stores them, sqeuclid
+    / max), then each `step()` times one sweep of the sample (repeated until
+    `target_s` of CPU work) and extrapolates to one full evaluation
+    (= one iteration)."""
 
-    def rows_cost(r0, r1):
-        xs = x[r0:r1]
-        raw = ((xs[:, None, :] - y[None, :, :]) ** 2).sum(-1)
-        return (raw / rawmax).astype(np.float32)
+    MAX_ROWS = 8192  # 2 GB of fp32 cost rows at m = 65536
 
-    def run(rows):
-        Cs = rows_cost(0, rows)
-        q = O.Problem(a[:rows] / a[:rows].sum(), np.full(M, 1.0 / M), Cs, cost_div=EPS)
+    def __init__(self, x, y, threads: int, target_s: float):
+        from oracle import oracle as O
+        self.O, self.threads, self.target_s = O, threads, target_s
+        self.v = np.zeros(M)
+        rawmax = O.sqeuclid_max(x, y, threads=os.cpu_count() or 1)
+
+        def rows_cost(rows):
+            out = np.empty((rows, M), dtype=np.float32)
+            for r0 in range(0, rows, 256):
+                xs = x[r0:min(rows, r0 + 256)]
+                raw = ((xs[:, None, :] - y[None, :, :]) ** 2).sum(-1)
+                out[r0:r0 + xs.shape[0]] = (raw / rawmax).astype(np.float32)
+            return out
+
+        def problem(rows):
+            a = np.full(rows, 1.0 / rows)
+            return O.Problem(a, np.full(M, 1.0 / M), rows_cost(rows), cost_div=EPS)
+
+        q = problem(16)
         t0 = time.perf_counter()
-        O.sweep_rows_mt(q, v, 0, rows, threads)
-        return time.perf_counter() - t0
+        O.sweep_rows_mt(q, self.v, 0, 16, threads)
+        t16 = max(time.perf_counter() - t0, 1e-6)
+        self.rows = int(min(self.MAX_ROWS, max(16, 16 * target_s / t16)))
+        self.q = problem(self.rows)
 
-    t = run(sample_rows)
-    rows = int(min(N, max(sample_rows, sample_rows * target_s / max(t, 1e-6))))
-    t = run(rows)
-    per_iter = t * (N / rows)
-    return {"value": 1.0 / per_iter, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{rows} of {N} rows x {M} cols (one full O(nm) sweep of those rows, "
-                      f"{t:.2f} s), extrapolated to one full iteration ({per_iter:.1f} s/iter)"}
+    def step(self):
+        t_sum, sweeps = 0.0, 0
+        while True:
+            t0 = time.perf_counter()
+            self.O.sweep_rows_mt(self.q, self.v, 0, self.rows, self.threads)
+            t_sum += time.perf_counter() - t0
+            sweeps += 1
+            if t_sum >= self.target_s or sweeps >= 1000:
+                break
+        per_iter = t_sum / sweeps * (N / self.rows)
+        return {"value": 1.0 / per_iter, "unit": UNIT, "cores": self.threads, "kind": "port",
+                "sample": f"{sweeps} sweep(s) of {self.rows} of {N} rows x {M} cols "
+                          f"({t_sum:.2f} s), extrapolated to one full iteration "
+                          f"({per_iter:.2f} s/iter)"}
+
+
+def cpu_baseline(x, y, threads: int, target_s: float = 12.0):
+    return CpuArm(x, y, threads, target_s).step()
 
 
 def lscpu_model():
@@ -188,8 +211,9 @@ def run_reference(args, rank, world):
     threads = os.cpu_count() or 1
     vals = []
     sample = None
+    arm = CpuArm(x, y, threads, target_s=max(1.0, min(20.0, 150.0 / (args.warmup + args.steps))))
     for k in range(args.warmup + args.steps):
-        cb = cpu_baseline(x, y, threads, target_s=max(2.0, min(20.0, 150.0 / (args.warmup + args.steps))))
+        cb = arm.step()
         if k >= args.warmup:
             vals.append(cb["value"])
             sample = cb["sample"]
