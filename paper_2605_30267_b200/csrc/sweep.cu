@@ -1860,7 +1860,11 @@ int64_t rows_per_cta_fast(const Problem& P) {
     const char* s = getenv("OTG_ROW_R");
     return s ? atoi(s) : 0;
   }();
-  const int64_t want = (env == 1 || env == 4 || env == 8) ? env : 4;
+  // on the fly, 8 rows share each column quad's coordinate / potential loads
+  // (cfg5-shaped 100000^2: 5.86 -> 5.38 ms per row pass); stored, 4 rows keep
+  // 3 CTAs per SM (8 rows: 65536^2 2.90 -> 4.06 ms)
+  const int64_t dflt = P.storage == OTG_STORE_ON_THE_FLY ? 8 : 4;
+  const int64_t want = (env == 1 || env == 4 || env == 8) ? env : dflt;
   return P.n_local >= want ? want : 1;
 }
 
