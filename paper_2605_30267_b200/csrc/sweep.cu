@@ -522,11 +522,18 @@ __device__ __forceinline__ void row_shift_block(
       fs2[r].x += ex2_approx(t);
     }
   }
+  // one barrier for all R rows: each warp leaves its (max, argmax code, sum)
+  // per row in smem; thread r then folds the 8 warps of row r in fixed order
+  constexpr int kW = kRowThreads / 32;
+  __shared__ float wT[R][kW];
+  __shared__ int wJ[R][kW];
+  __shared__ double wS[R][kW];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     ss[r] += static_cast<double>(fs2[r].x) + static_cast<double>(fs2[r].y);
     float t = tm[r];
     int jj = tq[r];
+    double sv = ss[r];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const float t2 = __shfl_xor_sync(0xffffffffu, t, o);
@@ -535,27 +542,31 @@ __device__ __forceinline__ void row_shift_block(
         t = t2;
         jj = j2;
       }
+      sv += __shfl_xor_sync(0xffffffffu, sv, o);
     }
-    __syncthreads();
     if ((threadIdx.x & 31) == 0) {
-      shf[threadIdx.x >> 5] = t;
-      shj[threadIdx.x >> 5] = jj;
+      wT[r][threadIdx.x >> 5] = t;
+      wJ[r][threadIdx.x >> 5] = jj;
+      wS[r][threadIdx.x >> 5] = sv;
     }
-    __syncthreads();
+  }
+  __syncthreads();
+  if (threadIdx.x < R) {
+    const int r = threadIdx.x;
     float T = -FLT_MAX;
     int J = 0;
+    double S = 0.0;
 #pragma unroll
-    for (int k = 0; k < kRowThreads / 32; ++k)
-      if (shf[k] > T || (shf[k] == T && shj[k] < J)) {
-        T = shf[k];
-        J = shj[k];
+    for (int k = 0; k < kW; ++k) {
+      if (wT[r][k] > T || (wT[r][k] == T && wJ[r][k] < J)) {
+        T = wT[r][k];
+        J = wJ[r][k];
       }
-    const double S = block_sum<kRowThreads>(ss[r], sh);
-    if (threadIdx.x == 0) {
-      resT[r] = T;
-      resS[r] = S;
-      resJ[r] = J;
+      S += wS[r][k];
     }
+    resT[r] = T;
+    resS[r] = S;
+    resJ[r] = J;
   }
   __syncthreads();
   if (threadIdx.x < R) {  // column of the max inside the winning quad
