@@ -568,7 +568,7 @@ __device__ __forceinline__ void row_shift_block(
     resS[r] = S;
     resJ[r] = J;
   }
-  __syncthreads();
+  // (the same threads r < R finish the rows: no barrier until the CTA-wide redo)
   if (threadIdx.x < R) {  // column of the max inside the winning quad
     const int r = threadIdx.x;
     const int code = resJ[r];
@@ -588,7 +588,6 @@ __device__ __forceinline__ void row_shift_block(
       resJ[r] = code + (t01.x == T ? 0 : t01.y == T ? 1 : t23.x == T ? 2 : t23.y == T ? 3 : 0);
     }
   }
-  __syncthreads();
   if (threadIdx.x < R) {
     const int r = threadIdx.x;
     const int64_t i = r0 + r;
