@@ -942,7 +942,7 @@ k_row_exact(const CostSrc src, int64_t n, int64_t m, const double* __restrict__ 
 }
 
 template <int R, bool OTF, int PF>
-__global__ void __launch_bounds__(kRowThreads)
+__global__ void __launch_bounds__(kRowThreads, (R == 4 && !OTF) ? 4 : 1)
 k_row_shift(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
             const double* __restrict__ dq, int64_t mpad, float kh, float kl,
             const double* __restrict__ a, const double* __restrict__ loga,
