@@ -40,6 +40,15 @@
 
 #include "common.cuh"
 
+// resident CTAs per SM the stored fp32 row / column kernels are compiled for
+// (the register cap follows: 4 -> 64, 5 -> 48 registers per thread)
+#ifndef OTG_ROW_MINB
+#define OTG_ROW_MINB 4
+#endif
+#ifndef OTG_COL_MINB
+#define OTG_COL_MINB 5
+#endif
+
 namespace otg {
 
 namespace {
@@ -942,7 +951,7 @@ k_row_exact(const CostSrc src, int64_t n, int64_t m, const double* __restrict__ 
 }
 
 template <int R, bool OTF, int PF>
-__global__ void __launch_bounds__(kRowThreads, (R == 4 && !OTF) ? 4 : 1)
+__global__ void __launch_bounds__(kRowThreads, (R == 4 && !OTF) ? OTG_ROW_MINB : 1)
 k_row_shift(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
             const double* __restrict__ dq, int64_t mpad, float kh, float kl,
             const double* __restrict__ a, const double* __restrict__ loga,
@@ -1006,7 +1015,7 @@ __device__ __forceinline__ void flush_acc(float2& acc01, float2& acc23, double* 
 // rows' shift / weight (aux) -- and, on the fly, the rows' points -- are
 // staged in shared memory per 256-row tile and read as broadcasts.
 template <bool OTF, int NT>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, (!OTF && NT == 256) ? OTG_COL_MINB : 1)
 k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh, float kl,
            const float4* __restrict__ aux, int64_t row_lo, int64_t row_hi,
            int64_t rows_per_split, double* __restrict__ part, int64_t mpad,
