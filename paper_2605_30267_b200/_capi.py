@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libotg.so")
+LIB_PATH = os.environ.get("OTG_LIB") or os.path.join(_HERE, "libotg.so")  # (OTG_LIB: A/B builds)
 
 c_double_p = C.POINTER(C.c_double)
 

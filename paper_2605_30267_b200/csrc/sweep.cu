@@ -48,6 +48,15 @@
 #ifndef OTG_COL_MINB
 #define OTG_COL_MINB 5
 #endif
+#ifndef OTG_EXACT_MINB
+#define OTG_EXACT_MINB 3
+#endif
+#ifndef OTG_ROW_OTF_MINB
+#define OTG_ROW_OTF_MINB 2
+#endif
+#ifndef OTG_COL_OTF_MINB
+#define OTG_COL_OTF_MINB 1
+#endif
 
 namespace otg {
 
@@ -916,7 +925,7 @@ __device__ __forceinline__ void row_online_block(
 // when its case does not apply.  (Kept as two kernels: one kernel holding both
 // bodies needs 76 registers and drops the shift pass to 3 CTAs per SM.)
 template <int R, bool OTF>
-__global__ void __launch_bounds__(kRowThreads, (R == 4 && !OTF) ? 3 : 1)
+__global__ void __launch_bounds__(kRowThreads, (R == 4 && !OTF) ? OTG_EXACT_MINB : 1)
 k_row_exact(const CostSrc src, int64_t n, int64_t m, const double* __restrict__ p, double kappa,
             const double* __restrict__ a, const double* __restrict__ loga,
             double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
@@ -951,7 +960,8 @@ k_row_exact(const CostSrc src, int64_t n, int64_t m, const double* __restrict__ 
 }
 
 template <int R, bool OTF, int PF>
-__global__ void __launch_bounds__(kRowThreads, (R == 4 && !OTF) ? OTG_ROW_MINB : 1)
+__global__ void __launch_bounds__(kRowThreads, (R == 4 && !OTF) ? OTG_ROW_MINB
+                                               : (R == 8 && OTF) ? OTG_ROW_OTF_MINB : 1)
 k_row_shift(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
             const double* __restrict__ dq, int64_t mpad, float kh, float kl,
             const double* __restrict__ a, const double* __restrict__ loga,
@@ -1015,7 +1025,8 @@ __device__ __forceinline__ void flush_acc(float2& acc01, float2& acc23, double* 
 // rows' shift / weight (aux) -- and, on the fly, the rows' points -- are
 // staged in shared memory per 256-row tile and read as broadcasts.
 template <bool OTF, int NT>
-__global__ void __launch_bounds__(NT, (!OTF && NT == 256) ? OTG_COL_MINB : 1)
+__global__ void __launch_bounds__(NT, (!OTF && NT == 256) ? OTG_COL_MINB
+                                      : (OTF && NT == 256) ? OTG_COL_OTF_MINB : 1)
 k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh, float kl,
            const float4* __restrict__ aux, int64_t row_lo, int64_t row_hi,
            int64_t rows_per_split, double* __restrict__ part, int64_t mpad,
