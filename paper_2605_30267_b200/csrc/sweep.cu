@@ -461,24 +461,27 @@ __device__ __forceinline__ void row_shift_block(
   // at half the FP32 issue slots.  The argmax is tracked per thread as the
   // quad index only (one compare + select per quad); the column inside the
   // winning quad is resolved once at the end.
-  float Sc[R], tm[R];
+  // loop-carried state kept small (the kernel runs 4 CTAs/SM at 64
+  // registers): the fp64 row sums live in shared memory, the rows are one
+  // base pointer + 32-bit offsets
+  float tm[R];
   int tq[R];       // column code of the running max: 4q (quad) or j (ragged tail)
   float2 fs2[R];   // fp32 partial sums, flushed to fp64 every 16 columns
-  float2 nSc2[R];
-  double ss[R];
-  int64_t rr[R];
+  float2 nSc2[R];  // -(row shift), twice (packed operand)
+  int rof[R];      // row r's offset from row r0, in elements / ldc
   float4 xr[R];
+  __shared__ double sSS[R][kRowThreads];  // this thread's fp64 row sums
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    Sc[r] = sSc[r];
-    nSc2[r] = make_float2(-Sc[r], -Sc[r]);
+    nSc2[r] = make_float2(-sSc[r], -sSc[r]);
     tm[r] = -FLT_MAX;
     tq[r] = 0;
     fs2[r] = make_float2(0.f, 0.f);
-    ss[r] = 0.0;
-    rr[r] = r0 + r < n ? r0 + r : n - 1;
-    xr[r] = OTF ? src.X[rr[r]] : make_float4(0.f, 0.f, 0.f, 0.f);
+    sSS[r][threadIdx.x] = 0.0;
+    rof[r] = static_cast<int>((r0 + r < n ? r0 + r : n - 1) - r0);
+    xr[r] = OTF ? src.X[r0 + rof[r]] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  const float* crow0 = OTF ? nullptr : src.C + r0 * src.ldc;
   const float2 nkh2 = make_float2(-kh, -kh), nkl2 = make_float2(-kl, -kl);
   const int64_t nq = m >> 2;
   const float4* Vq = reinterpret_cast<const float4*>(vq);
@@ -492,17 +495,21 @@ __device__ __forceinline__ void row_shift_block(
     if constexpr (!OTF && PF == 1) {
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        c[r] = ld_stream256(reinterpret_cast<const float4*>(src.C + rr[r] * src.ldc) + q);
+        c[r] = ld_stream256(reinterpret_cast<const float4*>(crow0 + static_cast<int64_t>(rof[r]) * src.ldc) + q);
+    } else if constexpr (!OTF) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        c[r] = ld_stream(reinterpret_cast<const float4*>(crow0 + static_cast<int64_t>(rof[r]) * src.ldc) + q);
     } else {
 #pragma unroll
-      for (int r = 0; r < R; ++r) c[r] = cost_quad<OTF>(src, rr[r], q, xr[r], y4);
+      for (int r = 0; r < R; ++r) c[r] = cost_quad<OTF>(src, r0 + rof[r], q, xr[r], y4);
     }
     if constexpr (!OTF && PF >= 2) {
       const int64_t qp = q + static_cast<int64_t>(PF - 1) * kRowThreads;
       if (qp < nq) {
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          prefetch_l2(reinterpret_cast<const float4*>(src.C + rr[r] * src.ldc) + qp);
+          prefetch_l2(reinterpret_cast<const float4*>(crow0 + static_cast<int64_t>(rof[r]) * src.ldc) + qp);
       }
     }
     const float2 V01 = make_float2(V.x, V.y), V23 = make_float2(V.z, V.w);
@@ -522,7 +529,7 @@ __device__ __forceinline__ void row_shift_block(
       chunk = 0;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        ss[r] += static_cast<double>(fs2[r].x) + static_cast<double>(fs2[r].y);
+        sSS[r][threadIdx.x] += static_cast<double>(fs2[r].x) + static_cast<double>(fs2[r].y);
         fs2[r] = make_float2(0.f, 0.f);
       }
     }
@@ -531,8 +538,8 @@ __device__ __forceinline__ void row_shift_block(
     const float V = vq[j], F = vq[mpad + j];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const float c = cost_one<OTF>(src, rr[r], j);
-      const float t = fmaf(-c, kh, V - Sc[r]) + fmaf(-c, kl, F);
+      const float c = cost_one<OTF>(src, r0 + rof[r], j);
+      const float t = fmaf(-c, kh, V + nSc2[r].x) + fmaf(-c, kl, F);
       if (t > tm[r]) {
         tm[r] = t;
         tq[r] = static_cast<int>(j);
@@ -548,10 +555,9 @@ __device__ __forceinline__ void row_shift_block(
   __shared__ double wS[R][kW];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    ss[r] += static_cast<double>(fs2[r].x) + static_cast<double>(fs2[r].y);
+    double sv = sSS[r][threadIdx.x] + (static_cast<double>(fs2[r].x) + static_cast<double>(fs2[r].y));
     float t = tm[r];
     int jj = tq[r];
-    double sv = ss[r];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const float t2 = __shfl_xor_sync(0xffffffffu, t, o);
@@ -620,7 +626,7 @@ __device__ __forceinline__ void row_shift_block(
           bad[r] = 1;
       } else {
         const double S = resS[r];
-        const double sc = static_cast<double>(Sc[r]);
+        const double sc = static_cast<double>(sSc[r]);
         const double M = sc * kLn2;
         const double ui = (loga[i] - M) - log(S);
         const double wi = a[i] / S;
@@ -630,7 +636,7 @@ __device__ __forceinline__ void row_shift_block(
         wrow[i] = wi;
         rowM2[i] = sc + static_cast<double>(T);
         rowJ[i] = resJ[r];
-        aux[i] = make_float4(Sc[r], 0.0f, static_cast<float>(wi), 0.0f);
+        aux[i] = make_float4(sSc[r], 0.0f, static_cast<float>(wi), 0.0f);
       }
     } else {
       bad[r] = 0;
