@@ -1060,7 +1060,19 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
   const float2 vf01 = make_float2(vf[0], vf[1]), vf23 = make_float2(vf[2], vf[3]);
   const float2 nkh2 = make_float2(-kh, -kh), nkl2 = make_float2(-kl, -kl);
   float2 acc01 = make_float2(0.f, 0.f), acc23 = make_float2(0.f, 0.f);
-  double acc64[4] = {0.0, 0.0, 0.0, 0.0};
+  // the fp64 column totals live in shared memory (registers stay under the
+  // 5-CTA/SM budget); flushed from the fp32 partials every kFlushRows rows
+  __shared__ double sAcc[4][NT];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) sAcc[e][threadIdx.x] = 0.0;
+  auto flush = [&]() {
+    sAcc[0][threadIdx.x] += static_cast<double>(acc01.x);
+    sAcc[1][threadIdx.x] += static_cast<double>(acc01.y);
+    sAcc[2][threadIdx.x] += static_cast<double>(acc23.x);
+    sAcc[3][threadIdx.x] += static_cast<double>(acc23.y);
+    acc01 = make_float2(0.f, 0.f);
+    acc23 = make_float2(0.f, 0.f);
+  };
   const bool active = j0 < m;
   for (int64_t t0 = i0; t0 < i1; t0 += kAuxTile) {
     const int64_t tn = min(static_cast<int64_t>(kAuxTile), i1 - t0);
@@ -1080,18 +1092,18 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
 #pragma unroll
       for (int r = 0; r < kColUnroll; ++r) col_quad_step(c[r], sh_aux[k + r], Vc01, Vc23, vf01,
                                                           vf23, nkh2, nkl2, acc01, acc23);
-      if (((k + kColUnroll) % kFlushRows) == 0) flush_acc(acc01, acc23, acc64);
+      if (((k + kColUnroll) % kFlushRows) == 0) flush();
     }
     for (; k < tn; ++k) {
       const float4 cv = cost_quad<OTF>(src, t0 + k, q, sh_x[OTF ? k : 0], y4);
       col_quad_step(cv, sh_aux[k], Vc01, Vc23, vf01, vf23, nkh2, nkl2, acc01, acc23);
     }
-    flush_acc(acc01, acc23, acc64);
+    flush();
   }
   if (active) {
     double* dst = part + static_cast<int64_t>(blockIdx.y) * mpad + j0;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) dst[e] = acc64[e];
+    for (int e = 0; e < 4; ++e) dst[e] = sAcc[e][threadIdx.x];
   }
 }
 
