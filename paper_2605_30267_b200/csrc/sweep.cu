@@ -49,7 +49,7 @@
 #define OTG_COL_MINB 5
 #endif
 #ifndef OTG_EXACT_MINB
-#define OTG_EXACT_MINB 3
+#define OTG_EXACT_MINB 4
 #endif
 #ifndef OTG_ROW_OTF_MINB
 #define OTG_ROW_OTF_MINB 2
@@ -719,7 +719,7 @@ __device__ __forceinline__ void row_online_block(
   float s[R], tm[R];
   int tq[R];
   float2 fs2[R];
-  double ss[R];
+  __shared__ double sSS[R][kRowThreads];  // fp64 partial sums (registers stay free)
   int64_t rr[R];
   float4 xr[R];
 #pragma unroll
@@ -728,7 +728,7 @@ __device__ __forceinline__ void row_online_block(
     tm[r] = -FLT_MAX;
     tq[r] = 0;
     fs2[r] = make_float2(0.f, 0.f);
-    ss[r] = 0.0;
+    sSS[r][threadIdx.x] = 0.0;
     rr[r] = r0 + r < n ? r0 + r : n - 1;
     xr[r] = OTF ? src.X[rr[r]] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
@@ -798,7 +798,7 @@ __device__ __forceinline__ void row_online_block(
         s[r] += d;
         const float sc = ex2_approx(-d);
         fs2[r] = make_float2(fs2[r].x * sc, fs2[r].y * sc);
-        ss[r] *= exp2(-static_cast<double>(d));
+        sSS[r][threadIdx.x] *= exp2(-static_cast<double>(d));
         tm[r] -= d;
         quad_exponents(c[r], V01, V23, F01, F23, make_float2(-s[r], -s[r]), nkh2, nkl2, t01, t23);
         mx = fmaxf(fmaxf(t01.x, t01.y), fmaxf(t23.x, t23.y));
@@ -813,7 +813,7 @@ __device__ __forceinline__ void row_online_block(
       chunk = 0;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        ss[r] += static_cast<double>(fs2[r].x) + static_cast<double>(fs2[r].y);
+        sSS[r][threadIdx.x] += static_cast<double>(fs2[r].x) + static_cast<double>(fs2[r].y);
         fs2[r] = make_float2(0.f, 0.f);
       }
     }
@@ -830,7 +830,7 @@ __device__ __forceinline__ void row_online_block(
         s[r] += d;
         const float sc = ex2_approx(-d);
         fs2[r] = make_float2(fs2[r].x * sc, fs2[r].y * sc);
-        ss[r] *= exp2(-static_cast<double>(d));
+        sSS[r][threadIdx.x] *= exp2(-static_cast<double>(d));
         tm[r] -= d;
         t = fmaf(-c, kh, V - s[r]) + fmaf(-c, kl, F);
       }
@@ -844,7 +844,7 @@ __device__ __forceinline__ void row_online_block(
   // fold the threads onto the CTA's largest running shift
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    ss[r] += static_cast<double>(fs2[r].x) + static_cast<double>(fs2[r].y);
+    sSS[r][threadIdx.x] += static_cast<double>(fs2[r].x) + static_cast<double>(fs2[r].y);
     float sb = s[r];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sb = fmaxf(sb, __shfl_xor_sync(0xffffffffu, sb, o));
@@ -855,7 +855,7 @@ __device__ __forceinline__ void row_online_block(
 #pragma unroll
     for (int k = 0; k < kRowThreads / 32; ++k) S0 = fmaxf(S0, shf[k]);
     const bool seen = s[r] != -FLT_MAX;
-    const double part = seen ? ss[r] * exp2(static_cast<double>(s[r] - S0)) : 0.0;
+    const double part = seen ? sSS[r][threadIdx.x] * exp2(static_cast<double>(s[r] - S0)) : 0.0;
     float t = seen ? (s[r] - S0) + tm[r] : -FLT_MAX;  // max relative to S0
     int jj = tq[r];
 #pragma unroll
