@@ -1235,6 +1235,76 @@ __device__ __forceinline__ void fallback_body(const double* __restrict__ C64, co
   }
 }
 
+// Many flagged columns (the seed evaluation at v = 0 flags ~2% of them at
+// cfg3): thread per flagged column instead of CTA per (column, chunk).  The
+// list is sorted by column in shared memory first, so the 32 columns of a warp
+// lie within a few KB of each row and its gathers hit few DRAM pages; each
+// thread keeps its column's online (max, sum) over the chunk -- no block
+// reduction.  Same (max, sum) per (column, chunk) as fallback_body up to the
+// summation order.
+constexpr int kFbSortMax = 4096;
+template <bool PRECISE, bool OTF>
+__device__ __forceinline__ void fallback_sorted_body(
+    const double* __restrict__ C64, const CostSrc& src, int64_t ldc, int64_t n, double kappa,
+    const double* __restrict__ u, const double* __restrict__ p, const int* __restrict__ fb_cols,
+    double2* __restrict__ fb_part, unsigned nf) {
+  __shared__ int2 skey[kFbSortMax];  // (column, slot), sorted by column
+  int P2 = 1;
+  while (P2 < static_cast<int>(nf)) P2 <<= 1;
+  for (int k = threadIdx.x; k < P2; k += kEThreads)
+    skey[k] = k < static_cast<int>(nf) ? make_int2(fb_cols[k], k) : make_int2(0x7fffffff, -1);
+  __syncthreads();
+  for (int size = 2; size <= P2; size <<= 1) {  // bitonic sort
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int k = threadIdx.x; k < P2 / 2; k += kEThreads) {
+        const int lo = 2 * k - (k & (stride - 1)), hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const int2 x = skey[lo], y = skey[hi];
+        if ((x.x > y.x) == up) {
+          skey[lo] = y;
+          skey[hi] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const int64_t rpc = (n + kFbChunks - 1) / kFbChunks;
+  const int groups = (static_cast<int>(nf) + kEThreads - 1) / kEThreads;
+  for (int it = blockIdx.x; it < groups * kFbChunks; it += gridDim.x) {
+    const int g = it / kFbChunks, ch = it % kFbChunks;
+    const int k = g * kEThreads + threadIdx.x;
+    if (k >= static_cast<int>(nf)) continue;
+    const int64_t j = skey[k].x;
+    const int f = skey[k].y;
+    const double vj = p[j];
+    const int64_t i0 = ch * rpc, i1 = min(n, i0 + rpc);
+    double top = -INFINITY, sum = 0.0;
+    for (int64_t i = i0; i < i1; i += kFbUnroll) {
+      double t[kFbUnroll];
+#pragma unroll
+      for (int e = 0; e < kFbUnroll; ++e) {
+        const int64_t ii = i + e;
+        t[e] = ii < i1 ? (PRECISE ? (u[ii] + vj) - C64[ii * ldc + j]
+                                  : fma(-static_cast<double>(cost_one<OTF>(src, ii, j)), kappa,
+                                        u[ii] + vj))
+                       : -INFINITY;
+      }
+      double mx = t[0];
+#pragma unroll
+      for (int e = 1; e < kFbUnroll; ++e) mx = fmax(mx, t[e]);
+      if (mx > -INFINITY) {
+        if (mx > top) {
+          sum = (top > -INFINITY) ? sum * exp(top - mx) : 0.0;
+          top = mx;
+        }
+#pragma unroll
+        for (int e = 0; e < kFbUnroll; ++e) sum += exp(t[e] - top);
+      }
+    }
+    fb_part[static_cast<int64_t>(f) * kFbChunks + ch] = make_double2(top, sum);
+  }
+}
+
 template <bool PRECISE, bool OTF>
 __global__ void __launch_bounds__(kEThreads)
 k_fallback(const double* __restrict__ C64, const CostSrc src, int64_t ldc, int64_t n,
@@ -1245,6 +1315,10 @@ k_fallback(const double* __restrict__ C64, const CostSrc src, int64_t ldc, int64
   if (ctrl->done) return;
   const unsigned nf = ctrl->fb_count;
   if (nf == 0) return;
+  if (nf >= 2 * kEThreads && nf <= kFbSortMax) {
+    fallback_sorted_body<PRECISE, OTF>(C64, src, ldc, n, kappa, u, p, fb_cols, fb_part, nf);
+    return;
+  }
   __shared__ double sh[kEThreads / 32];
   fallback_body<PRECISE, OTF>(C64, src, ldc, n, kappa, u, p, fb_cols, fb_part, nf, blockIdx.x,
                               gridDim.x, sh);
