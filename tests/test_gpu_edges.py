@@ -134,3 +134,24 @@ def test_config2_full_size_properties():
             st = ot.plan_stats(p, r.potentials.u, r.potentials.v)
             assert st.marginal_violation_l1 <= 1.2e-6
         p.close()
+
+
+def test_many_flagged_columns_sorted_fallback():
+    """> 512 columns whose linear-domain mass underflows (the sorted, thread-per-
+    column fallback of k_fallback): one evaluation at v = 0 against the oracle."""
+    rng = np.random.default_rng(5)
+    n, m = 384, 3000
+    x = rng.uniform(0.0, 0.1, size=(n, 3))
+    y = np.concatenate([rng.uniform(0.0, 0.1, size=(m // 3, 3)),
+                        rng.uniform(0.9, 1.0, size=(m - m // 3, 3))])
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    p = ot.TransportProblem.from_points(a, b, x, y, 5e-4)
+    q = O.Problem(a, b, p.stored_cost(), cost_div=5e-4)
+    e = ot.eval_normalized_step(p, np.zeros(m))
+    r = O.eval_normalized_step(q, np.zeros(m))
+    assert rel(e.v_next, r["v_next"]) <= 2e-6
+    assert rel(e.u, r["u"]) <= 2e-6
+    assert abs(e.grad_l1 - r["grad_l1"]) <= 2e-6 * max(r["grad_l1"], 1e-3)
+    # the exact column LSE ran for (at least) the far columns
+    s = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=1))
+    assert s.fallback_columns >= m - m // 3
