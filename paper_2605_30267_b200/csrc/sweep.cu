@@ -997,7 +997,17 @@ k_col_precise(const double* __restrict__ C, int64_t ldc, int64_t m,
   double acc = 0.0;
   if (j < m) {
     const double pj = p[j];
-    for (int64_t i = i0; i < i1; ++i) acc += exp(((-C[i * ldc + j]) + pj) - rowM[i]) * wrow[i];
+    // 4 rows' exponentials in flight, accumulated in the same row order (so
+    // the sum is bitwise the one-row-at-a-time loop)
+    int64_t i = i0;
+    for (; i + 4 <= i1; i += 4) {
+      double e[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) e[k] = exp(((-C[(i + k) * ldc + j]) + pj) - rowM[i + k]) * wrow[i + k];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc += e[k];
+    }
+    for (; i < i1; ++i) acc += exp(((-C[i * ldc + j]) + pj) - rowM[i]) * wrow[i];
     part[static_cast<int64_t>(blockIdx.y) * mpad + j] = acc;
   }
 }
