@@ -105,9 +105,22 @@ __device__ void eval_step(Smem& sm, int n, int m) {
   {
     const int j = tid % kBMax, g = tid / kBMax;
     double acc = 0.0;
-    if (j < m)
-      for (int i = g; i < n; i += kBGroups)
+    if (j < m) {
+      // 4 rows' exponentials in flight, accumulated in the same order
+      int i = g;
+      for (; i + 3 * kBGroups < n; i += 4 * kBGroups) {
+        double e[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int ii = i + k * kBGroups;
+          e[k] = exp(((-sm.C[ii * kBMax + j]) + sm.pt[j]) - sm.M[ii]) * sm.wr[ii];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc += e[k];
+      }
+      for (; i < n; i += kBGroups)
         acc += exp(((-sm.C[i * kBMax + j]) + sm.pt[j]) - sm.M[i]) * sm.wr[i];
+    }
     sm.colp[g][j] = acc;
   }
   __syncthreads();
