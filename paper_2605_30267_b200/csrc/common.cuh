@@ -213,7 +213,7 @@ struct Problem {
   int* rowJ = nullptr;      // fast path: its argmax column
   double* dq = nullptr;     // fast path: (p_new - p_old) * log2(e) per column
   int* redo_rows = nullptr; // rows whose shift estimate was off (exact redo)
-  float* vq = nullptr;      // fast path: split column potential (Vc[mpad], vf[mpad])
+  float* vq = nullptr;      // fast path: split column potential (Vc[mpad], vf[mpad], 2^vf[mpad])
 
   // per-column state (m, padded)
   double *p = nullptr, *wacc = nullptr, *col = nullptr, *col_log = nullptr, *y = nullptr,
@@ -229,6 +229,12 @@ struct Problem {
   double* sp_rec = nullptr;     // per-row 32-byte records (shift estimate, a, log a)
   int* sp_bad_rows = nullptr;   // rows whose shift estimate was loose, per cluster
   int* sp_bad_count = nullptr;
+
+  // on-the-fly transposed row pass (k_row_otf): column splits and their
+  // per-row partials (row_splits x n_local records of 16 B)
+  int row_splits = 0;  // 0: the row_shift_block kernel instead
+  int64_t row_cols_per_split = 0;
+  void* rpart = nullptr;
 
   // column-pass partials
   int col_splits = 1;

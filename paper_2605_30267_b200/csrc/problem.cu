@@ -169,7 +169,7 @@ void problem_alloc_state(Problem& P) {
   P.rowJ = dalloc<int>(P, n);
   P.dq = dalloc<double>(P, mp);
   P.redo_rows = dalloc<int>(P, n);
-  P.vq = dalloc<float>(P, 2 * mp);
+  P.vq = dalloc<float>(P, 3 * mp);  // [V | F | 2^F]
   P.p = dalloc<double>(P, mp);
   P.wacc = dalloc<double>(P, mp);
   P.col = dalloc<double>(P, mp + 8 + std::max<int64_t>((P.m + 255) / 256, kEpiMaxGrid));  // + <u, a> slices
@@ -190,6 +190,7 @@ void problem_alloc_state(Problem& P) {
   const size_t prow = std::max<size_t>(static_cast<size_t>(P.vshards) * P.col_splits,
                                        static_cast<size_t>(P.fused_clusters) + 1);
   P.part = dalloc<double>(P, prow * mp);
+  if (P.row_splits > 0) P.rpart = dalloc<double2>(P, static_cast<int64_t>(P.row_splits) * n);
   P.e1_part = dalloc<double>(P, P.e_blocks * 8 + row_blocks(P) + 8);
   P.e2_part = dalloc<double>(P, P.e_blocks * 16);
   P.epi_part = dalloc<double>(P, kEpiMaxGrid * (8 + 16));

@@ -163,6 +163,17 @@ __device__ __forceinline__ void split_q(double x2, float& hi, float& lo) {
   lo = static_cast<float>(x2 - h);
 }
 
+// The row pass's column potential, three planes of stride mpad: the quantised
+// split (V, F) and 2^F (fp32 round of the fp64 power), which the on-the-fly
+// kernels apply as a factor after the ex2 instead of adding F to the exponent.
+__device__ __forceinline__ void split_store(double x2, float* vq, int64_t mpad, int64_t j) {
+  float hi, lo;
+  split_q(x2, hi, lo);
+  vq[j] = hi;
+  vq[mpad + j] = lo;
+  vq[2 * mpad + j] = static_cast<float>(exp2(static_cast<double>(lo)));
+}
+
 // ------------------------------------------------------------------ K1 ----
 // fp64 storage: exact restatement of dual.cpp:34-38 for one row per G threads.
 template <int G>
@@ -429,6 +440,18 @@ __device__ __forceinline__ void quad_exponents(const float4& c, float2 V01, floa
   t23 = __fadd2_rn(__ffma2_rn(c23, nkh2, __fadd2_rn(V23, nSc2)), __ffma2_rn(c23, nkl2, F23));
 }
 
+// On the fly (FMA-pipe bound, ncu: the packed FP32 pipe at 65-84 % with MUFU
+// at 50-60 %): t = fmaf(-c, kl, fmaf(-c, kh, V - Sc)), the column's low part F
+// applied after the ex2 as the factor 2^F (vq plane 2) -- three FP32 ops per
+// element instead of four, each rounding at the scale of the small result.
+__device__ __forceinline__ void quad_exponents_nf(const float4& c, float2 V01, float2 V23,
+                                                  float2 nSc2, float2 nkh2, float2 nkl2,
+                                                  float2& t01, float2& t23) {
+  const float2 c01 = make_float2(c.x, c.y), c23 = make_float2(c.z, c.w);
+  t01 = __ffma2_rn(c01, nkl2, __ffma2_rn(c01, nkh2, __fadd2_rn(V01, nSc2)));
+  t23 = __ffma2_rn(c23, nkl2, __ffma2_rn(c23, nkh2, __fadd2_rn(V23, nSc2)));
+}
+
 constexpr float kRedoLo = 2.0f;
 constexpr float kRedoHi = 6.0f;
 
@@ -486,9 +509,10 @@ __device__ __forceinline__ void row_shift_block(
   const int64_t nq = m >> 2;
   const float4* Vq = reinterpret_cast<const float4*>(vq);
   const float4* Fq = reinterpret_cast<const float4*>(vq + mpad);
+  const float4* Eq = reinterpret_cast<const float4*>(vq + 2 * mpad);  // 2^F (on the fly)
   int chunk = 0;
   for (int64_t q = threadIdx.x; q < nq; q += kRowThreads) {
-    const float4 V = __ldg(Vq + q), F = __ldg(Fq + q);
+    const float4 V = __ldg(Vq + q), F = __ldg(OTF ? Eq + q : Fq + q);
     YQ y4;
     load_y4<OTF>(src, q, y4);
     float4 c[R];
@@ -517,13 +541,21 @@ __device__ __forceinline__ void row_shift_block(
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       float2 t01, t23;
-      quad_exponents(c[r], V01, V23, F01, F23, nSc2[r], nkh2, nkl2, t01, t23);
+      if constexpr (OTF)  // (F01, F23 hold 2^F here)
+        quad_exponents_nf(c[r], V01, V23, nSc2[r], nkh2, nkl2, t01, t23);
+      else
+        quad_exponents(c[r], V01, V23, F01, F23, nSc2[r], nkh2, nkl2, t01, t23);
       const float mx = fmaxf(fmaxf(fmaxf(tm[r], t01.x), t01.y), fmaxf(t23.x, t23.y));
       tq[r] = mx > tm[r] ? static_cast<int>(4 * q) : tq[r];
       tm[r] = mx;
-      const float2 e = __fadd2_rn(make_float2(ex2_approx(t01.x), ex2_approx(t23.x)),
-                                  make_float2(ex2_approx(t01.y), ex2_approx(t23.y)));
-      fs2[r] = __fadd2_rn(fs2[r], e);
+      if constexpr (OTF) {
+        fs2[r] = __ffma2_rn(make_float2(ex2_approx(t01.x), ex2_approx(t01.y)), F01, fs2[r]);
+        fs2[r] = __ffma2_rn(make_float2(ex2_approx(t23.x), ex2_approx(t23.y)), F23, fs2[r]);
+      } else {
+        const float2 e = __fadd2_rn(make_float2(ex2_approx(t01.x), ex2_approx(t23.x)),
+                                    make_float2(ex2_approx(t01.y), ex2_approx(t23.y)));
+        fs2[r] = __fadd2_rn(fs2[r], e);
+      }
     }
     if (++chunk == 4) {  // fp32 partials flushed into fp64 every 16 elements
       chunk = 0;
@@ -539,12 +571,16 @@ __device__ __forceinline__ void row_shift_block(
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const float c = cost_one<OTF>(src, r0 + rof[r], j);
-      const float t = fmaf(-c, kh, V + nSc2[r].x) + fmaf(-c, kl, F);
+      const float t = OTF ? fmaf(-c, kl, fmaf(-c, kh, V + nSc2[r].x))
+                          : fmaf(-c, kh, V + nSc2[r].x) + fmaf(-c, kl, F);
       if (t > tm[r]) {
         tm[r] = t;
         tq[r] = static_cast<int>(j);
       }
-      fs2[r].x += ex2_approx(t);
+      if constexpr (OTF)
+        fs2[r].x = fmaf(ex2_approx(t), vq[2 * mpad + j], fs2[r].x);
+      else
+        fs2[r].x += ex2_approx(t);
     }
   }
   // one barrier for all R rows: each warp leaves its (max, argmax code, sum)
@@ -606,8 +642,12 @@ __device__ __forceinline__ void row_shift_block(
       const float4 V = __ldg(Vq + q), F = __ldg(Fq + q);
       const float nsc = -sSc[r];
       float2 t01, t23;
-      quad_exponents(cq, make_float2(V.x, V.y), make_float2(V.z, V.w), make_float2(F.x, F.y),
-                     make_float2(F.z, F.w), make_float2(nsc, nsc), nkh2, nkl2, t01, t23);
+      if constexpr (OTF)
+        quad_exponents_nf(cq, make_float2(V.x, V.y), make_float2(V.z, V.w), make_float2(nsc, nsc),
+                          nkh2, nkl2, t01, t23);
+      else
+        quad_exponents(cq, make_float2(V.x, V.y), make_float2(V.z, V.w), make_float2(F.x, F.y),
+                       make_float2(F.z, F.w), make_float2(nsc, nsc), nkh2, nkl2, t01, t23);
       const float T = resT[r];
       resJ[r] = code + (t01.x == T ? 0 : t01.y == T ? 1 : t23.x == T ? 2 : t23.y == T ? 3 : 0);
     }
@@ -688,7 +728,7 @@ __global__ void k_split_p(int64_t m, int64_t mpad, const double* __restrict__ p,
   pdl_wait();
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
        j += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    split_q(p[j] * kLog2e, vq[j], vq[mpad + j]);
+    split_store(p[j] * kLog2e, vq, mpad, j);
 }
 
 __constant__ int c_online_first = 1;  // OTG_ONLINE_FIRST=0: fp64-argument first pass
@@ -981,6 +1021,204 @@ k_row_shift(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ v
                               nullptr, 0.0);
 }
 
+// ------------------------------------------------------------- K1-OTF ----
+// On-the-fly row pass, transposed (the column pass's layout): every thread
+// owns kOtfRT rows -- their points in registers as packed row pairs -- and
+// walks a column split whose (-y, V, 2^F) are staged in shared memory and
+// read as broadcasts, so a column's loads serve kOtfRT rows and no
+// cross-thread reduction sits in the inner loop.  Per element: cost 6, exponent
+// 3, accumulate 1 FP32 op (packed f32x2) + 1 ex2 + 1 FMNMX.  The max is kept
+// per 16-column block (argmax = block index); the finishing kernel folds the
+// column splits in order and resolves the column inside the winning block by
+// recomputing its 16 exponents bitwise.  The shift estimate, the redo rule and
+// the outputs are those of row_shift_block.
+constexpr int kOtfRT = 8;     // rows per thread (4 packed pairs)
+constexpr int kOtfTJ = 256;   // columns per staged tile
+constexpr int kOtfBlk = 16;   // columns per max block / fp64 flush
+
+struct RowPart {
+  float t;   // max exponent over the split (relative to the row shift)
+  int jb;    // first column of the 16-column block holding it
+  double s;  // sum of 2^t 2^F over the split
+};
+
+__device__ __forceinline__ float row_shift_estimate(const double* __restrict__ rowM2,
+                                                    const int* __restrict__ rowJ,
+                                                    const double* __restrict__ dq, double dmax2,
+                                                    int64_t i) {
+  const double M2 = rowM2[i];
+  const double lo = M2 + dq[rowJ[i]], hi = M2 + dmax2;
+  return static_cast<float>(ceil(fmin(lo + 1.0, hi) * 256.0) * (1.0 / 256.0));
+}
+
+__global__ void __launch_bounds__(kRowThreads, OTG_ROW_OTF_MINB)
+k_row_otf(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
+          const double* __restrict__ dq, int64_t mpad, float kh, float kl,
+          const double* __restrict__ rowM2, const int* __restrict__ rowJ, int64_t cols_per_split,
+          RowPart* __restrict__ rpart, const Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
+  if (ctrl->done || !ctrl->shift_valid) return;
+  constexpr int NP = kOtfRT / 2;
+  __shared__ float4 sA[kOtfTJ];  // (-x, -x, -y, -y)
+  __shared__ float4 sB[kOtfTJ];  // (-z, -z, V, V)
+  __shared__ float2 sE[kOtfTJ];  // (2^F, 2^F)
+  __shared__ double sSS[kOtfRT][kRowThreads];
+  const int64_t rbase = static_cast<int64_t>(blockIdx.x) * (kRowThreads * kOtfRT) + threadIdx.x;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.y) * cols_per_split;
+  const int64_t j1 = min(j0 + cols_per_split, m);
+  const double dmax2 = ctrl->dmax2;
+  float2 X[NP], Y[NP], Z[NP], nS[NP], bm[NP], fs[NP];
+  float tm[kOtfRT];
+  int tj[kOtfRT];
+#pragma unroll
+  for (int pp = 0; pp < NP; ++pp) {
+    const int64_t i0 = min(rbase + (2 * pp) * kRowThreads, n - 1);
+    const int64_t i1 = min(rbase + (2 * pp + 1) * kRowThreads, n - 1);
+    const float4 x0 = src.X[i0], x1 = src.X[i1];
+    X[pp] = make_float2(x0.x, x1.x);
+    Y[pp] = make_float2(x0.y, x1.y);
+    Z[pp] = make_float2(x0.z, x1.z);
+    nS[pp] = make_float2(-row_shift_estimate(rowM2, rowJ, dq, dmax2, i0),
+                         -row_shift_estimate(rowM2, rowJ, dq, dmax2, i1));
+    bm[pp] = make_float2(-FLT_MAX, -FLT_MAX);
+    fs[pp] = make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int r = 0; r < kOtfRT; ++r) {
+    tm[r] = -FLT_MAX;
+    tj[r] = static_cast<int>(j0);
+    sSS[r][threadIdx.x] = 0.0;
+  }
+  const float2 nkh2 = make_float2(-kh, -kh), nkl2 = make_float2(-kl, -kl);
+  const float* Vp = vq;
+  const float* Ep = vq + 2 * mpad;
+  for (int64_t t0 = j0; t0 < j1; t0 += kOtfTJ) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < kOtfTJ; k += kRowThreads) {
+      const int64_t j = t0 + k;
+      if (j < j1) {
+        const float nx = src.Yn[j], ny = src.Yn[src.ypad + j], nz = src.Yn[2 * src.ypad + j];
+        const float V = Vp[j];
+        sA[k] = make_float4(nx, nx, ny, ny);
+        sB[k] = make_float4(nz, nz, V, V);
+        const float E = Ep[j];
+        sE[k] = make_float2(E, E);
+      } else {  // padding: t = -inf, contributes 0, never the max
+        sA[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        sB[k] = make_float4(0.f, 0.f, -INFINITY, -INFINITY);
+        sE[k] = make_float2(0.f, 0.f);
+      }
+    }
+    __syncthreads();
+    const int tn = static_cast<int>(min(static_cast<int64_t>(kOtfTJ), j1 - t0));
+    for (int kb = 0; kb < tn; kb += kOtfBlk) {
+#pragma unroll 4
+      for (int k = kb; k < kb + kOtfBlk; ++k) {
+        const float4 A = sA[k], B = sB[k];
+        const float2 E2 = sE[k];
+        const float2 ax = make_float2(A.x, A.y), ay = make_float2(A.z, A.w);
+        const float2 az = make_float2(B.x, B.y), V2 = make_float2(B.z, B.w);
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) {
+          const float2 dx = __fadd2_rn(X[pp], ax), dy = __fadd2_rn(Y[pp], ay),
+                       dz = __fadd2_rn(Z[pp], az);
+          const float2 c = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+          const float2 t = __ffma2_rn(c, nkl2, __ffma2_rn(c, nkh2, __fadd2_rn(V2, nS[pp])));
+          bm[pp].x = fmaxf(bm[pp].x, t.x);
+          bm[pp].y = fmaxf(bm[pp].y, t.y);
+          fs[pp] = __ffma2_rn(make_float2(ex2_approx(t.x), ex2_approx(t.y)), E2, fs[pp]);
+        }
+      }
+      // block end: fp32 partials into fp64, block max into the running max
+      const int jb = static_cast<int>(t0 + kb);
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) {
+        sSS[2 * pp][threadIdx.x] += static_cast<double>(fs[pp].x);
+        sSS[2 * pp + 1][threadIdx.x] += static_cast<double>(fs[pp].y);
+        fs[pp] = make_float2(0.f, 0.f);
+        if (bm[pp].x > tm[2 * pp]) {
+          tm[2 * pp] = bm[pp].x;
+          tj[2 * pp] = jb;
+        }
+        if (bm[pp].y > tm[2 * pp + 1]) {
+          tm[2 * pp + 1] = bm[pp].y;
+          tj[2 * pp + 1] = jb;
+        }
+        bm[pp] = make_float2(-FLT_MAX, -FLT_MAX);
+      }
+    }
+  }
+  RowPart* dst = rpart + static_cast<int64_t>(blockIdx.y) * n;
+#pragma unroll
+  for (int r = 0; r < kOtfRT; ++r) {
+    const int64_t i = rbase + r * kRowThreads;
+    if (i < n) {
+      RowPart rp;
+      rp.t = tm[r];
+      rp.jb = tj[r];
+      rp.s = sSS[r][threadIdx.x];
+      dst[i] = rp;
+    }
+  }
+}
+
+// Fold the column splits of k_row_otf (split order: ties keep the lowest
+// column), resolve the argmax column inside its 16-column block, then the
+// row_shift_block epilogue (redo rule, u, w, shift, next estimate).
+__global__ void __launch_bounds__(kRowThreads)
+k_row_otf_fin(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
+              const double* __restrict__ dq, int64_t mpad, float kh, float kl,
+              const double* __restrict__ a, const double* __restrict__ loga,
+              double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
+              double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
+              int* __restrict__ rowJ, int* __restrict__ redo_rows, const RowPart* __restrict__ rpart,
+              int splits, Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
+  if (ctrl->done || !ctrl->shift_valid) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kRowThreads + threadIdx.x;
+  if (i >= n) return;
+  const float sc = row_shift_estimate(rowM2, rowJ, dq, ctrl->dmax2, i);
+  float T = -FLT_MAX;
+  int JB = 0;
+  double S = 0.0;
+  for (int k = 0; k < splits; ++k) {
+    const RowPart rp = rpart[static_cast<int64_t>(k) * n + i];
+    if (rp.t > T) {
+      T = rp.t;
+      JB = rp.jb;
+    }
+    S += rp.s;
+  }
+  if (!(T >= -kRedoLo && T <= kRedoHi)) {  // estimate too loose (or NaN): exact redo
+    const unsigned slot = atomicAdd(&ctrl->redo_count, 1u);
+    redo_rows[slot] = static_cast<int>(i);
+    return;
+  }
+  // the column of the max: first one in the block whose exponent equals T
+  const float4 xi = src.X[i];
+  int J = JB;
+  for (int k = 0; k < kOtfBlk && JB + k < m; ++k) {
+    const int64_t j = JB + k;
+    const float c = otf_sqeuclid(xi, src.Y[j]);
+    const float t = fmaf(c, -kl, fmaf(c, -kh, vq[j] + (-sc)));
+    if (t == T) {
+      J = static_cast<int>(j);
+      break;
+    }
+  }
+  const double scd = static_cast<double>(sc);
+  const double M = scd * kLn2;
+  const double ui = (loga[i] - M) - log(S);
+  const double wi = a[i] / S;
+  rowM[i] = M;
+  rowS[i] = S;
+  u[i] = ui;
+  wrow[i] = wi;
+  rowM2[i] = scd + static_cast<double>(T);
+  rowJ[i] = J;
+  aux[i] = make_float4(sc, 0.0f, static_cast<float>(wi), 0.0f);
+}
+
 // ------------------------------------------------------------------ K2 ----
 // fp64: partial c_j = sum_i exp(((-C'_ij) + p_j) - M_i) * w_i  (dual.cpp:36,41)
 __global__ void __launch_bounds__(kColThreads)
@@ -1024,6 +1262,21 @@ __device__ __forceinline__ void col_quad_step(const float4& c, const float4& ax,
                                 __ffma2_rn(c01, nkl2, __fadd2_rn(vf01, nm)));
   const float2 t23 = __fadd2_rn(__ffma2_rn(c23, nkh2, __fadd2_rn(Vc23, nM)),
                                 __ffma2_rn(c23, nkl2, __fadd2_rn(vf23, nm)));
+  acc01 = __ffma2_rn(w2, make_float2(ex2_approx(t01.x), ex2_approx(t01.y)), acc01);
+  acc23 = __ffma2_rn(w2, make_float2(ex2_approx(t23.x), ex2_approx(t23.y)), acc23);
+}
+
+// On the fly: A = Vc - Mc (exact), t = fmaf(-c, kl, fmaf(-c, kh, A)),
+// acc += w' ex2(t) with w' = w 2^-mf folded at staging and the column factor
+// 2^vf applied once to the fp64 totals: four FP32 ops per element instead of six.
+__device__ __forceinline__ void col_quad_step_nf(const float4& c, const float4& ax, float2 Vc01,
+                                                 float2 Vc23, float2 nkh2, float2 nkl2,
+                                                 float2& acc01, float2& acc23) {
+  const float2 nM = make_float2(-ax.x, -ax.x);
+  const float2 w2 = make_float2(ax.z, ax.z);
+  const float2 c01 = make_float2(c.x, c.y), c23 = make_float2(c.z, c.w);
+  const float2 t01 = __ffma2_rn(c01, nkl2, __ffma2_rn(c01, nkh2, __fadd2_rn(Vc01, nM)));
+  const float2 t23 = __ffma2_rn(c23, nkl2, __ffma2_rn(c23, nkh2, __fadd2_rn(Vc23, nM)));
   acc01 = __ffma2_rn(w2, make_float2(ex2_approx(t01.x), ex2_approx(t01.y)), acc01);
   acc23 = __ffma2_rn(w2, make_float2(ex2_approx(t23.x), ex2_approx(t23.y)), acc23);
 }
@@ -1088,8 +1341,12 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
     const int64_t tn = min(static_cast<int64_t>(kAuxTile), i1 - t0);
     __syncthreads();
     for (int k = threadIdx.x; k < tn; k += NT) {
-      sh_aux[k] = aux[t0 + k];
-      if (OTF) sh_x[k] = src.X[t0 + k];
+      float4 ax = aux[t0 + k];
+      if (OTF) {
+        sh_x[k] = src.X[t0 + k];
+        ax.z = ax.y == 0.0f ? ax.z : ax.z * exp2f(-ax.y);  // w' = w 2^-mf
+      }
+      sh_aux[k] = ax;
     }
     __syncthreads();
     if (!active) continue;
@@ -1100,20 +1357,28 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
       for (int r = 0; r < kColUnroll; ++r)
         c[r] = cost_quad<OTF>(src, t0 + k + r, q, sh_x[OTF ? k + r : 0], y4);
 #pragma unroll
-      for (int r = 0; r < kColUnroll; ++r) col_quad_step(c[r], sh_aux[k + r], Vc01, Vc23, vf01,
-                                                          vf23, nkh2, nkl2, acc01, acc23);
+      for (int r = 0; r < kColUnroll; ++r) {
+        if constexpr (OTF)
+          col_quad_step_nf(c[r], sh_aux[k + r], Vc01, Vc23, nkh2, nkl2, acc01, acc23);
+        else
+          col_quad_step(c[r], sh_aux[k + r], Vc01, Vc23, vf01, vf23, nkh2, nkl2, acc01, acc23);
+      }
       if (((k + kColUnroll) % kFlushRows) == 0) flush();
     }
     for (; k < tn; ++k) {
       const float4 cv = cost_quad<OTF>(src, t0 + k, q, sh_x[OTF ? k : 0], y4);
-      col_quad_step(cv, sh_aux[k], Vc01, Vc23, vf01, vf23, nkh2, nkl2, acc01, acc23);
+      if constexpr (OTF)
+        col_quad_step_nf(cv, sh_aux[k], Vc01, Vc23, nkh2, nkl2, acc01, acc23);
+      else
+        col_quad_step(cv, sh_aux[k], Vc01, Vc23, vf01, vf23, nkh2, nkl2, acc01, acc23);
     }
     flush();
   }
   if (active) {
     double* dst = part + static_cast<int64_t>(blockIdx.y) * mpad + j0;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) dst[e] = sAcc[e][threadIdx.x];
+    for (int e = 0; e < 4; ++e)
+      dst[e] = OTF ? sAcc[e][threadIdx.x] * exp2(static_cast<double>(vf[e])) : sAcc[e][threadIdx.x];
   }
 }
 
@@ -1760,7 +2025,7 @@ __device__ __forceinline__ void apply_cols(const AppArgs& A, const Ctrl* ctrl_in
       A.p[j] = pn;
       dstep = fmax(dstep, pn - x);
       if (A.fast) {
-        split_q(pn * kLog2e, A.vq[j], A.vq[A.mpad + j]);
+        split_store(pn * kLog2e, A.vq, A.mpad, j);
         A.dq[j] = (pn - x) * kLog2e;
       }
     }
@@ -2068,6 +2333,26 @@ void configure_sweeps(Problem& P) {
   splits = std::max<int64_t>(1, std::min<int64_t>(splits, max_splits));
   P.col_splits = static_cast<int>(splits);
   P.rows_per_split = (shard_rows + splits - 1) / splits;
+  // on the fly: the transposed row pass (OTG_ROW_OTF_T=0: row_shift_block).
+  // Column splits give ~8 waves of the resident CTAs, >= 256 columns each.
+  static const int env_rt = [] {
+    const char* s = getenv("OTG_ROW_OTF_T");
+    return s ? atoi(s) : 1;
+  }();
+  P.row_splits = 0;
+  if (P.storage == OTG_STORE_ON_THE_FLY && env_rt != 0) {
+    int occ = 0, sms = 0;
+    OTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_row_otf, kRowThreads, 0));
+    OTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.device));
+    const int64_t rb = (P.n_local + kRowThreads * kOtfRT - 1) / (kRowThreads * kOtfRT);
+    const int64_t slots = std::max<int64_t>(1, static_cast<int64_t>(occ) * sms);
+    int64_t S = (8 * slots + rb - 1) / rb;
+    S = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(S, 128), (P.m + 255) / 256));
+    int64_t cps = (P.m + S - 1) / S;
+    cps = (cps + kOtfBlk - 1) / kOtfBlk * kOtfBlk;
+    P.row_cols_per_split = cps;
+    P.row_splits = static_cast<int>((P.m + cps - 1) / cps);
+  }
   P.e_blocks = e_grid(P.m);
 }
 
@@ -2161,6 +2446,24 @@ void launch_row_pass(Problem& P) {
           src, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,
           P.rowM2, P.rowJ, P.ctrl, P.vq, P.mpad);
       launch_fused(P, kh, kl);
+    } else if (otf && P.row_splits > 0 && R == 8) {
+      launch_k(k_row_exact<8, true>, resident_grid(P, k_row_exact<8, true>, blocks), kRowThreads, 0,
+               P.stream, src, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u,
+               P.wrow, P.aux, P.rowM2, P.rowJ, P.ctrl, P.vq, P.mpad);
+      RowPart* rp = static_cast<RowPart*>(P.rpart);
+      const dim3 g(static_cast<unsigned>((P.n_local + kRowThreads * kOtfRT - 1) / (kRowThreads * kOtfRT)),
+                   static_cast<unsigned>(P.row_splits));
+      launch_k(k_row_otf, g, kRowThreads, 0, P.stream, src, P.n_local, P.m,
+               static_cast<const float*>(P.vq), static_cast<const double*>(P.dq), P.mpad, kh, kl,
+               static_cast<const double*>(P.rowM2), static_cast<const int*>(P.rowJ),
+               P.row_cols_per_split, rp, static_cast<const Ctrl*>(P.ctrl));
+      launch_k(k_row_otf_fin, static_cast<unsigned>((P.n_local + kRowThreads - 1) / kRowThreads),
+               kRowThreads, 0, P.stream, src, P.n_local, P.m, static_cast<const float*>(P.vq),
+               static_cast<const double*>(P.dq), P.mpad, kh, kl, static_cast<const double*>(P.a),
+               static_cast<const double*>(P.loga), P.rowM, P.rowS, P.u, P.wrow, P.aux, P.rowM2,
+               P.rowJ, P.redo_rows, static_cast<const RowPart*>(rp), P.row_splits, P.ctrl);
+      launch_k(k_row_redo<true>, 296, kRowThreads, 0, P.stream, src, P.m, P.p, P.kappa, P.a,
+               P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux, P.rowM2, P.rowJ, P.redo_rows, P.ctrl);
     } else if (R == 8) {
       if (otf) { OTG_ROW(8, true); } else { OTG_ROW(8, false); }
     } else if (R == 4) {

@@ -60,7 +60,10 @@ def test_otf_homotopy_cost_and_iterations():
 
 @pytest.mark.gpu
 def test_otf_matches_stored_fp32_path():
-    """Same fp32 cost stored vs recomputed: identical solver trajectory."""
+    """Same fp32 cost stored vs recomputed: the same solver trajectory up to
+    fp32 exponent rounding (the on-the-fly kernels form the exponent with
+    three FP32 ops and apply the column's low part as a factor 2^F, the
+    stored-cost kernels add it: relative 1e-7 on the potentials)."""
     n, m, eps = 400, 1200, 2e-3
     p, _, C32 = _pair(n, m, 13, eps)
     a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
@@ -69,4 +72,4 @@ def test_otf_matches_stored_fp32_path():
     g1 = ot.homotopy_solve(p, cfg)
     g2 = ot.homotopy_solve(ps, cfg)
     assert g1.iterations == g2.iterations
-    assert np.max(np.abs(g1.potentials.v - g2.potentials.v)) <= 1e-9 * max(1.0, np.max(np.abs(g2.potentials.v)))
+    assert np.max(np.abs(g1.potentials.v - g2.potentials.v)) <= 1e-7 * max(1.0, np.max(np.abs(g2.potentials.v)))
