@@ -54,6 +54,9 @@
 #ifndef OTG_ROW_OTF_MINB
 #define OTG_ROW_OTF_MINB 2
 #endif
+#ifndef OTG_ROW_OTF_UNROLL
+#define OTG_ROW_OTF_UNROLL 4
+#endif
 #ifndef OTG_COL_OTF_MINB
 #define OTG_COL_OTF_MINB 1
 #endif
@@ -1035,6 +1038,7 @@ k_row_shift(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ v
 constexpr int kOtfRT = 8;     // rows per thread (4 packed pairs)
 constexpr int kOtfTJ = 256;   // columns per staged tile
 constexpr int kOtfBlk = 16;   // columns per max block / fp64 flush
+constexpr int kOtfUnroll = OTG_ROW_OTF_UNROLL;  // columns in flight per thread
 
 struct RowPart {
   float t;   // max exponent over the split (relative to the row shift)
@@ -1068,7 +1072,7 @@ k_row_otf(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
   const int64_t j1 = min(j0 + cols_per_split, m);
   const double dmax2 = ctrl->dmax2;
   float2 X[NP], Y[NP], Z[NP], nS[NP], bm[NP], fs[NP];
-  float tm[kOtfRT];
+  float tm[kOtfRT];  // running max and the first column of its 16-column block
   int tj[kOtfRT];
 #pragma unroll
   for (int pp = 0; pp < NP; ++pp) {
@@ -1112,7 +1116,7 @@ k_row_otf(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
     __syncthreads();
     const int tn = static_cast<int>(min(static_cast<int64_t>(kOtfTJ), j1 - t0));
     for (int kb = 0; kb < tn; kb += kOtfBlk) {
-#pragma unroll 4
+#pragma unroll kOtfUnroll
       for (int k = kb; k < kb + kOtfBlk; ++k) {
         const float4 A = sA[k], B = sB[k];
         const float2 E2 = sE[k];
