@@ -1030,28 +1030,35 @@ k_row_shift(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ v
 // walks a column split whose (-y, V, 2^F) are staged in shared memory and
 // read as broadcasts, so a column's loads serve kOtfRT rows and no
 // cross-thread reduction sits in the inner loop.  Per element: cost 6, exponent
-// 3, accumulate 1 FP32 op (packed f32x2) + 1 ex2 + 1 FMNMX.  The max is kept
-// per 16-column block (argmax = block index); the finishing kernel folds the
-// column splits in order and resolves the column inside the winning block by
-// recomputing its 16 exponents bitwise.  The shift estimate, the redo rule and
-// the outputs are those of row_shift_block.
+// 3, accumulate 1 FP32 op (packed f32x2) + 1 ex2, no per-element max: each
+// row keeps its heaviest 16-column block (largest fp32 block sum, compared at
+// the fp64 flush); the finishing kernel folds the column splits in order and
+// takes the largest exponent T_J of that block (recomputed bitwise) as the
+// row's reference column.  The true max is within 4 of T_J (it lies in some
+// block whose sum is at most 16 2^T_J), which the redo rule and the next
+// shift estimate allow for; otherwise as row_shift_block.
 constexpr int kOtfRT = 8;     // rows per thread (4 packed pairs)
 constexpr int kOtfTJ = 256;   // columns per staged tile
 constexpr int kOtfBlk = 16;   // columns per max block / fp64 flush
 constexpr int kOtfUnroll = OTG_ROW_OTF_UNROLL;  // columns in flight per thread
 
 struct RowPart {
-  float t;   // max exponent over the split (relative to the row shift)
-  int jb;    // first column of the 16-column block holding it
+  float t;   // largest 16-column block sum of the split (fp32, relative to the row shift)
+  int jb;    // first column of that block
   double s;  // sum of 2^t 2^F over the split
 };
 
+constexpr double kOtfSlack = 4.0;  // log2(kOtfBlk): true max <= T_J + 4
+
+// rowM2 = s + T_J may sit up to kOtfSlack below the row's max, so the upper
+// bound carries the slack (for rows whose rowM2 is the exact max, as after
+// k_row_exact / k_row_redo, it is merely loose).
 __device__ __forceinline__ float row_shift_estimate(const double* __restrict__ rowM2,
                                                     const int* __restrict__ rowJ,
                                                     const double* __restrict__ dq, double dmax2,
                                                     int64_t i) {
   const double M2 = rowM2[i];
-  const double lo = M2 + dq[rowJ[i]], hi = M2 + dmax2;
+  const double lo = M2 + dq[rowJ[i]], hi = M2 + dmax2 + kOtfSlack;
   return static_cast<float>(ceil(fmin(lo + 1.0, hi) * 256.0) * (1.0 / 256.0));
 }
 
@@ -1071,8 +1078,8 @@ k_row_otf(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
   const int64_t j0 = static_cast<int64_t>(blockIdx.y) * cols_per_split;
   const int64_t j1 = min(j0 + cols_per_split, m);
   const double dmax2 = ctrl->dmax2;
-  float2 X[NP], Y[NP], Z[NP], nS[NP], bm[NP], fs[NP];
-  float tm[kOtfRT];  // running max and the first column of its 16-column block
+  float2 X[NP], Y[NP], Z[NP], nS[NP], fs[NP];
+  float tm[kOtfRT];  // heaviest block sum so far and the block's first column
   int tj[kOtfRT];
 #pragma unroll
   for (int pp = 0; pp < NP; ++pp) {
@@ -1084,7 +1091,6 @@ k_row_otf(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
     Z[pp] = make_float2(x0.z, x1.z);
     nS[pp] = make_float2(-row_shift_estimate(rowM2, rowJ, dq, dmax2, i0),
                          -row_shift_estimate(rowM2, rowJ, dq, dmax2, i1));
-    bm[pp] = make_float2(-FLT_MAX, -FLT_MAX);
     fs[pp] = make_float2(0.f, 0.f);
   }
 #pragma unroll
@@ -1128,27 +1134,24 @@ k_row_otf(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
                        dz = __fadd2_rn(Z[pp], az);
           const float2 c = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
           const float2 t = __ffma2_rn(c, nkl2, __ffma2_rn(c, nkh2, __fadd2_rn(V2, nS[pp])));
-          bm[pp].x = fmaxf(bm[pp].x, t.x);
-          bm[pp].y = fmaxf(bm[pp].y, t.y);
           fs[pp] = __ffma2_rn(make_float2(ex2_approx(t.x), ex2_approx(t.y)), E2, fs[pp]);
         }
       }
-      // block end: fp32 partials into fp64, block max into the running max
+      // block end: fp32 partials into fp64, the heaviest block remembered
       const int jb = static_cast<int>(t0 + kb);
 #pragma unroll
       for (int pp = 0; pp < NP; ++pp) {
         sSS[2 * pp][threadIdx.x] += static_cast<double>(fs[pp].x);
         sSS[2 * pp + 1][threadIdx.x] += static_cast<double>(fs[pp].y);
-        fs[pp] = make_float2(0.f, 0.f);
-        if (bm[pp].x > tm[2 * pp]) {
-          tm[2 * pp] = bm[pp].x;
+        if (fs[pp].x > tm[2 * pp]) {
+          tm[2 * pp] = fs[pp].x;
           tj[2 * pp] = jb;
         }
-        if (bm[pp].y > tm[2 * pp + 1]) {
-          tm[2 * pp + 1] = bm[pp].y;
+        if (fs[pp].y > tm[2 * pp + 1]) {
+          tm[2 * pp + 1] = fs[pp].y;
           tj[2 * pp + 1] = jb;
         }
-        bm[pp] = make_float2(-FLT_MAX, -FLT_MAX);
+        fs[pp] = make_float2(0.f, 0.f);
       }
     }
   }
@@ -1193,23 +1196,27 @@ k_row_otf_fin(const CostSrc src, int64_t n, int64_t m, const float* __restrict__
     }
     S += rp.s;
   }
-  if (!(T >= -kRedoLo && T <= kRedoHi)) {  // estimate too loose (or NaN): exact redo
-    const unsigned slot = atomicAdd(&ctrl->redo_count, 1u);
-    redo_rows[slot] = static_cast<int>(i);
-    return;
-  }
-  // the column of the max: first one in the block whose exponent equals T
+  // the reference column: the largest exponent of the heaviest block (first on ties)
   const float4 xi = src.X[i];
   int J = JB;
+  float TJ = -FLT_MAX;
   for (int k = 0; k < kOtfBlk && JB + k < m; ++k) {
     const int64_t j = JB + k;
     const float c = otf_sqeuclid(xi, src.Y[j]);
     const float t = fmaf(c, -kl, fmaf(c, -kh, vq[j] + (-sc)));
-    if (t == T) {
+    if (t > TJ) {
+      TJ = t;
       J = static_cast<int>(j);
-      break;
     }
   }
+  // the max lies in [T_J, T_J + 4]: exact redo unless it is within
+  // [-kRedoLo, kRedoHi + 4] (and the sum finite and positive)
+  if (!(TJ >= -kRedoLo && TJ <= kRedoHi && S > 0.0 && S < 1e300)) {
+    const unsigned slot = atomicAdd(&ctrl->redo_count, 1u);
+    redo_rows[slot] = static_cast<int>(i);
+    return;
+  }
+  T = TJ;
   const double scd = static_cast<double>(sc);
   const double M = scd * kLn2;
   const double ui = (loga[i] - M) - log(S);
