@@ -361,9 +361,13 @@ otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const doub
     if (storage == OTG_STORE_ON_THE_FLY) {
       // fp32 coordinates padded to float4; the cost is recomputed per tile in
       // the sweeps (sweep.cu: otf_cost) and never stored
+      // the instance's epsilon is log2(e) / fl32(log2(e) / epsilon) (relative
+      // change <= 2^-24): the base-2 scale kh of the sweeps is then exactly an
+      // fp32 number and the exponent needs no low-part term (ot.otf_epsilon)
       P.storage = OTG_STORE_ON_THE_FLY;
-      P.epsilon = epsilon;
-      P.kappa = 1.0 / epsilon;
+      const double eps_eff = kLog2e / static_cast<double>(static_cast<float>(kLog2e / epsilon));
+      P.epsilon = eps_eff;
+      P.kappa = 1.0 / eps_eff;
       upload_marginals(P, a, b);
       std::vector<float> hx(nl * 4, 0.f), hy(P.mpad * 4, 0.f);
       for (int64_t i = 0; i < nl; ++i)

@@ -1030,7 +1030,8 @@ k_row_shift(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ v
 // walks a column split whose (-y, V, 2^F) are staged in shared memory and
 // read as broadcasts, so a column's loads serve kOtfRT rows and no
 // cross-thread reduction sits in the inner loop.  Per element: cost 6, exponent
-// 3, accumulate 1 FP32 op (packed f32x2) + 1 ex2, no per-element max: each
+// 2 (V - s, then one FMA with the instance's exact fp32 kh), accumulate 1 FP32
+// op (packed f32x2) + 1 ex2, no per-element max: each
 // row keeps its heaviest 16-column block (largest fp32 block sum, compared at
 // the fp64 flush); the finishing kernel folds the column splits in order and
 // takes the largest exponent T_J of that block (recomputed bitwise) as the
@@ -1133,7 +1134,7 @@ k_row_otf(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
           const float2 dx = __fadd2_rn(X[pp], ax), dy = __fadd2_rn(Y[pp], ay),
                        dz = __fadd2_rn(Z[pp], az);
           const float2 c = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-          const float2 t = __ffma2_rn(c, nkl2, __ffma2_rn(c, nkh2, __fadd2_rn(V2, nS[pp])));
+          const float2 t = __ffma2_rn(c, nkh2, __fadd2_rn(V2, nS[pp]));
           fs[pp] = __ffma2_rn(make_float2(ex2_approx(t.x), ex2_approx(t.y)), E2, fs[pp]);
         }
       }
@@ -1203,7 +1204,7 @@ k_row_otf_fin(const CostSrc src, int64_t n, int64_t m, const float* __restrict__
   for (int k = 0; k < kOtfBlk && JB + k < m; ++k) {
     const int64_t j = JB + k;
     const float c = otf_sqeuclid(xi, src.Y[j]);
-    const float t = fmaf(c, -kl, fmaf(c, -kh, vq[j] + (-sc)));
+    const float t = fmaf(c, -kh, vq[j] + (-sc));
     if (t > TJ) {
       TJ = t;
       J = static_cast<int>(j);
@@ -1277,17 +1278,18 @@ __device__ __forceinline__ void col_quad_step(const float4& c, const float4& ax,
   acc23 = __ffma2_rn(w2, make_float2(ex2_approx(t23.x), ex2_approx(t23.y)), acc23);
 }
 
-// On the fly: A = Vc - Mc (exact), t = fmaf(-c, kl, fmaf(-c, kh, A)),
-// acc += w' ex2(t) with w' = w 2^-mf folded at staging and the column factor
-// 2^vf applied once to the fp64 totals: four FP32 ops per element instead of six.
+// On the fly: A = Vc - Mc (exact), t = fmaf(-c, kh, A) (the instance's
+// log2(e)/eps IS the fp32 kh: ot.otf_epsilon), acc += w' ex2(t) with
+// w' = w 2^-mf folded at staging and the column factor 2^vf applied once to
+// the fp64 totals: three FP32 ops per element instead of six.
 __device__ __forceinline__ void col_quad_step_nf(const float4& c, const float4& ax, float2 Vc01,
                                                  float2 Vc23, float2 nkh2, float2 nkl2,
                                                  float2& acc01, float2& acc23) {
   const float2 nM = make_float2(-ax.x, -ax.x);
   const float2 w2 = make_float2(ax.z, ax.z);
   const float2 c01 = make_float2(c.x, c.y), c23 = make_float2(c.z, c.w);
-  const float2 t01 = __ffma2_rn(c01, nkl2, __ffma2_rn(c01, nkh2, __fadd2_rn(Vc01, nM)));
-  const float2 t23 = __ffma2_rn(c23, nkl2, __ffma2_rn(c23, nkh2, __fadd2_rn(Vc23, nM)));
+  const float2 t01 = __ffma2_rn(c01, nkh2, __fadd2_rn(Vc01, nM));
+  const float2 t23 = __ffma2_rn(c23, nkh2, __fadd2_rn(Vc23, nM));
   acc01 = __ffma2_rn(w2, make_float2(ex2_approx(t01.x), ex2_approx(t01.y)), acc01);
   acc23 = __ffma2_rn(w2, make_float2(ex2_approx(t23.x), ex2_approx(t23.y)), acc23);
 }

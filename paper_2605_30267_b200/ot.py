@@ -104,6 +104,7 @@ def _ptr(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
+LOG2E = 1.4426950408889634074  # log2(e), the double of common.cuh kLog2e
 STORAGE = {"f64": 0, "f32": 1, "on_the_fly": 2}
 NORM = {"none": 0, "max": 1, "minmax": 2, "halfrange": 3}
 COST = {"sqeuclidean": 0, "cosine": 1}
@@ -1011,6 +1012,16 @@ def synthetic_rescaled(n, m, seed, eps) -> TransportProblem:
     """helpers.hpp:30-33."""
     a, b, Cm = synthetic_instance(n, m, seed)
     return rescale_problem(with_epsilon(make_problem(a, b, Cm, 1.0), eps))
+
+
+def otf_epsilon(epsilon: float) -> float:
+    """The epsilon an on-the-fly (storage="on_the_fly") instance is solved
+    with: log2(e) / fl32(log2(e) / epsilon), within 2^-24 relative of
+    `epsilon`.  The sweeps scale the fp32 cost by the fp32 number
+    fl32(log2(e) / epsilon) exactly (one FMA per exponent instead of a hi/lo
+    pair); oracle problems built for such an instance divide by this value."""
+    kh = float(np.float32(LOG2E / float(epsilon)))
+    return LOG2E / kh
 
 
 def gen_config(cfg: int, n: int, m: int, seed: int):

@@ -88,7 +88,7 @@ def _solved(kind, n, m, seed):
         else:
             p = ot.TransportProblem.from_points(a, b, x, y, 5e-3, norm="none", storage="on_the_fly")
             q = O.Problem(a, b, O.cost_sqeuclid_f32(x.astype(np.float32), y.astype(np.float32)),
-                          cost_div=5e-3)
+                          cost_div=ot.otf_epsilon(5e-3))
     r = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-6, max_total_inner=400))
     return p, q, r.potentials.u, r.potentials.v
 

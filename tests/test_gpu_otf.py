@@ -15,7 +15,17 @@ def _pair(n, m, seed, eps):
     a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
     p = ot.TransportProblem.from_points(a, b, x, y, eps, norm="none", storage="on_the_fly")
     C32 = O.cost_sqeuclid_f32(x.astype(np.float32), y.astype(np.float32))
-    return p, O.Problem(a, b, C32, cost_div=eps), C32
+    return p, O.Problem(a, b, C32, cost_div=ot.otf_epsilon(eps)), C32
+
+
+def test_otf_epsilon():
+    """The on-the-fly instance's epsilon: log2(e)/eps rounded to fp32 exactly."""
+    for eps in (1e-3, 2e-3, 5e-3, 2e-2, 0.05, 1.0, 3e-7):
+        e = ot.otf_epsilon(eps)
+        assert abs(e - eps) <= 2.0 ** -24 * eps
+        kh = np.float32(ot.LOG2E / eps)
+        assert np.float32(ot.LOG2E / e) == kh
+        assert np.float32((1.0 / e) * ot.LOG2E) == kh  # the sweeps' kh from kappa = 1/e
 
 
 def test_otf_rejects_unsupported_on_cpu():
@@ -54,7 +64,7 @@ def test_otf_homotopy_cost_and_iterations():
     assert g.converged and o.converged
     assert abs(g.iterations - o.iterations) <= max(1, int(0.01 * o.iterations))
     cg = ot.plan_stats(p, g.potentials.u, g.potentials.v).primal_cost
-    co = O.plan_stats(q, o.u, o.v, eps)["primal_cost"]
+    co = O.plan_stats(q, o.u, o.v, ot.otf_epsilon(eps))["primal_cost"]
     assert abs(cg - co) <= REL32 * abs(co)
 
 
@@ -67,7 +77,7 @@ def test_otf_matches_stored_fp32_path():
     n, m, eps = 400, 1200, 2e-3
     p, _, C32 = _pair(n, m, 13, eps)
     a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
-    ps = ot.rescale_problem(ot.make_problem(a, b, C32, eps))
+    ps = ot.rescale_problem(ot.make_problem(a, b, C32, ot.otf_epsilon(eps)))
     cfg = ot.HomotopyConfig(tol_l1=1e-6, max_total_inner=300)
     g1 = ot.homotopy_solve(p, cfg)
     g2 = ot.homotopy_solve(ps, cfg)
