@@ -231,7 +231,13 @@ otg_status otg_problem_create_dense(int64_t n, int64_t m, const double* a, const
 /* Cost built on the device from points (data.cpp:69-110): x is n_local x d,
  * y is m x d, fp64 row-major.  SQEUCLID with NORM_MAX = cost_sqeuclidean;
  * COSINE with MINMAX / HALFRANGE / NONE = cost_cosine (+ raw, BASELINE cfg4).
- * The normaliser is a global reduction (MAX all-reduce when sharded). */
+ * The normaliser is a global reduction (MAX all-reduce when sharded).
+ * STORAGE_ON_THE_FLY (SQEUCLID, NORM_NONE, d <= 3; BASELINE cfg5): the cost
+ * fl32((x - y)^2) of the fp32-rounded points is recomputed per tile and never
+ * stored, and the instance is solved with epsilon_eff = log2(e) /
+ * fl32(log2(e) / epsilon) (within 2^-24 relative of epsilon; the sweeps then
+ * scale by an exact fp32 number).  Oracle instances built for parity divide
+ * the fp32 cost by epsilon_eff (ot.otf_epsilon). */
 otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const double* a,
                                      const double* b, const double* x, const double* y,
                                      otg_cost cost, otg_norm norm, otg_storage storage,
