@@ -158,6 +158,16 @@ __device__ __forceinline__ float neg_f64_to_f32(double x) {
   return __uint_as_float((w - 0xC0000000u + rb) | 0x80000000u);
 }
 
+// fp32 partial -> fp64 in the on-the-fly sweeps, whose XU pipe carries the
+// ex2 stream: OTG_OTF_INT_CVT=1 converts with integer ops (f32_to_f64; a zero
+// partial maps to 2^-127-scale, negligible in a sum), 0 with F2F.
+#ifndef OTG_OTF_INT_CVT
+#define OTG_OTF_INT_CVT 0
+#endif
+__device__ __forceinline__ double otf_cvt(float x) {
+  return OTG_OTF_INT_CVT ? f32_to_f64(x) : static_cast<double>(x);
+}
+
 // Quantised split of a base-2 value: hi is a multiple of 2^-8 (exact in fp32
 // for |x| < 2^15), lo = x - hi rounded to fp32 (|lo| <= 2^-9).
 __device__ __forceinline__ void split_q(double x2, float& hi, float& lo) {
@@ -1142,8 +1152,8 @@ k_row_otf(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
       const int jb = static_cast<int>(t0 + kb);
 #pragma unroll
       for (int pp = 0; pp < NP; ++pp) {
-        sSS[2 * pp][threadIdx.x] += static_cast<double>(fs[pp].x);
-        sSS[2 * pp + 1][threadIdx.x] += static_cast<double>(fs[pp].y);
+        sSS[2 * pp][threadIdx.x] += otf_cvt(fs[pp].x);
+        sSS[2 * pp + 1][threadIdx.x] += otf_cvt(fs[pp].y);
         if (fs[pp].x > tm[2 * pp]) {
           tm[2 * pp] = fs[pp].x;
           tj[2 * pp] = jb;
@@ -1342,10 +1352,10 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
 #pragma unroll
   for (int e = 0; e < 4; ++e) sAcc[e][threadIdx.x] = 0.0;
   auto flush = [&]() {
-    sAcc[0][threadIdx.x] += static_cast<double>(acc01.x);
-    sAcc[1][threadIdx.x] += static_cast<double>(acc01.y);
-    sAcc[2][threadIdx.x] += static_cast<double>(acc23.x);
-    sAcc[3][threadIdx.x] += static_cast<double>(acc23.y);
+    sAcc[0][threadIdx.x] += OTF ? otf_cvt(acc01.x) : static_cast<double>(acc01.x);
+    sAcc[1][threadIdx.x] += OTF ? otf_cvt(acc01.y) : static_cast<double>(acc01.y);
+    sAcc[2][threadIdx.x] += OTF ? otf_cvt(acc23.x) : static_cast<double>(acc23.x);
+    sAcc[3][threadIdx.x] += OTF ? otf_cvt(acc23.y) : static_cast<double>(acc23.y);
     acc01 = make_float2(0.f, 0.f);
     acc23 = make_float2(0.f, 0.f);
   };
