@@ -1,32 +1,42 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 Acc-Sinkhorn hot path (BASELINE.json metric).
 
-Workload (BASELINE config 3, the metric's own config): colour-transfer-shaped
-3-D OT, n = m = 65536 points in [0,1]^3 (sources Beta(2,5)^3, targets
+Default workload (BASELINE config 3, the metric's own config): colour-transfer-
+shaped 3-D OT, n = m = 65536 points in [0,1]^3 (sources Beta(2,5)^3, targets
 Beta(5,2)^3, seeded synthetic stand-ins for RGB samples), squared-Euclidean
 cost normalised to max 1 and stored fp32 (17.2 GB, built on the device),
 uniform weights, eps = 1e-3, Acc-Sinkhorn (homotopy, mu0 = 0.5, m0 = 4).
+`--config 5`: the on-the-fly 200000^2 instance (cost recomputed per tile,
+eps = 1e-3, a fixed 2000-iteration run plus time to 1e-5).
 
   step   = one Acc-Sinkhorn iteration (one evaluation of the normalised map:
-           row pass + column pass over the 17.2 GB cost + fused epilogue)
+           the O(nm) sweep(s) over the cost + fused epilogue)
   value  = iterations / s of the whole job, device-timed (CUDA events),
            max over ranks; inputs resident in HBM (C is 17.2 GB >> 126 MB L2,
            so every step streams from HBM: no L2 flush needed)
-  e2e    = the same metric through the C-ABI with HOST buffers: points and
-           marginals uploaded, cost built, K iterations, potentials copied
-           back, all inside the timed region (wall clock)
+  e2e    = the same metric through the public API with HOST buffers: points
+           and marginals uploaded, cost built, solve to tolerance, potentials
+           copied back, all inside the timed region (wall clock)
 
-Also reported: time-to-tolerance (1e-6 L1 marginal error), the roofline of
-the dominant kernel (HBM, measured CUDA-event launch time), the CPU oracle
-timed on this host (cpu_baseline), SM clocks during the timed region.
+Also reported: time-to-tolerance (with the fp64 plan-statistics violation of
+the returned potentials), the roofline of the dominant kernel (CUDA-event
+launch time), the CPU oracle timed on this host (cpu_baseline, 1 thread like
+the reference), SM clocks during the timed region.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3|5] [--impl reference]
+
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+(one rank per GPU); under torchrun WORLD_SIZE must equal N.  The reference
+arm (--impl reference) never loads the product library: it generates the
+same inputs with the oracle's own samplers (oracle/otoracle.cpp
+orc_gen_config, bitwise equal to libotg's, tests/test_oracle_gen.py).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -40,13 +50,33 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Acc-Sinkhorn iters/s and time-to-1e-6 marginal err, n=m=65536, 1/2/4/8 B200"
 UNIT = "iters/s"
-N = M = 65536
-EPS = 1e-3
-TOL = 1e-6
-SEED = 3
-WORKLOAD = ("cfg3: colour-transfer-shaped 3-D OT n=m=65536, Beta(2,5)^3 -> Beta(5,2)^3, "
-            "sqeuclid/max cost stored fp32 (17.2 GB), eps=1e-3, Acc-Sinkhorn homotopy "
-            "(mu0=0.5, m0=4) to L1 marginal error 1e-6")
+
+CONFIGS = {
+    3: dict(n=65536, m=65536, eps=1e-3, tol=1e-6, seed=3, storage="f32", norm="max",
+            workload=("cfg3: colour-transfer-shaped 3-D OT n=m=65536, Beta(2,5)^3 -> "
+                      "Beta(5,2)^3, sqeuclid/max cost stored fp32 (17.2 GB), eps=1e-3, "
+                      "Acc-Sinkhorn homotopy (mu0=0.5, m0=4) to L1 marginal error 1e-6")),
+    5: dict(n=200000, m=200000, eps=1e-3, tol=1e-5, seed=5, storage="on_the_fly", norm="none",
+            fixed_iters=2000,
+            workload=("cfg5: on-the-fly 3-D OT n=m=200000, U[0,1]^3 -> 3-Gaussian mixture "
+                      "(sigma 0.1, clipped), raw sqeuclid recomputed per tile (never stored), "
+                      "eps=1e-3, Acc-Sinkhorn homotopy, fixed 2000 iterations + time to 1e-5")),
+}
+
+
+def config_dict(cfg: int, world: int, sharded: bool) -> dict:
+    """The line's `config`, identical in both arms."""
+    c = CONFIGS[cfg]
+    d = {"workload": c["workload"], "n": c["n"], "m": c["m"], "eps": c["eps"], "seed": c["seed"],
+         "tol_l1": c["tol"],
+         "parallelism": (f"row-shard x{world} (NCCL all-reduce of the column sums)"
+                         if sharded else "single GPU"),
+         "l2": ("inputs (17.2 GB cost) >> L2 (126 MB); no flush needed" if cfg == 3 else
+                "cost recomputed per tile from 2 x 3.2 MB of points (compute-bound; no flush)"),
+         "step": "one homotopy iteration (one evaluation)"}
+    if cfg == 5:
+        d["fixed_iters"] = c["fixed_iters"]
+    return d
 
 
 def peaks():
@@ -138,38 +168,47 @@ class ClockSampler:
 # ------------------------------------------------------- CPU baseline ----
 class CpuArm:
     """The CPU oracle (a restatement of the reference's single-threaded fp64
-    sweep, oracle/otoracle.cpp) on a bounded row sample of the same workload:
-    the fp32 cost rows are built once (exactly as the GPU stores them, sqeuclid
-    / max), then each `step()` times one sweep of the sample (repeated until
-    `target_s` of CPU work) and extrapolates to one full evaluation
-    (= one iteration)."""
+    sweep, oracle/otoracle.cpp; dual.cpp:29-42 per element) on a bounded row
+    sample of the same workload.  Inputs come from the oracle's own samplers
+    (never libotg).  The fp32 cost rows of the sample are built once exactly
+    as the GPU holds them (cfg3: fl32(sqeuclid / global max); cfg5: the
+    on-the-fly fp32 definition), then each `step()` times one sweep of the
+    sample (repeated until `target_s` of CPU work) and extrapolates to one
+    full evaluation (= one iteration) of the n x m instance."""
 
     MAX_ROWS = 8192  # 2 GB of fp32 cost rows at m = 65536
 
-    def __init__(self, x, y, threads: int, target_s: float):
+    def __init__(self, cfg: int, threads: int, target_s: float):
         from oracle import oracle as O
+        c = CONFIGS[cfg]
         self.O, self.threads, self.target_s = O, threads, target_s
-        self.v = np.zeros(M)
-        rawmax = O.sqeuclid_max(x, y, threads=os.cpu_count() or 1)
-
-        def rows_cost(rows):
-            out = np.empty((rows, M), dtype=np.float32)
-            for r0 in range(0, rows, 256):
-                xs = x[r0:min(rows, r0 + 256)]
-                raw = ((xs[:, None, :] - y[None, :, :]) ** 2).sum(-1)
-                out[r0:r0 + xs.shape[0]] = (raw / rawmax).astype(np.float32)
-            return out
-
-        def problem(rows):
-            a = np.full(rows, 1.0 / rows)
-            return O.Problem(a, np.full(M, 1.0 / M), rows_cost(rows), cost_div=EPS)
-
-        q = problem(16)
+        self.n, self.m, self.eps = c["n"], c["m"], c["eps"]
+        x, y = O.gen_config(cfg, c["n"], c["m"], c["seed"])
+        self.x, self.y, self.cfg = x, y, cfg
+        self.rawmax = O.sqeuclid_max(x, y, threads=os.cpu_count() or 1) if cfg == 3 else None
+        self.v = np.zeros(self.m)
+        q = self._problem(16)
         t0 = time.perf_counter()
-        O.sweep_rows_mt(q, self.v, 0, 16, threads)
+        with O.threads(threads):
+            O.sweep_rows_mt(q, self.v, 0, 16, threads)
         t16 = max(time.perf_counter() - t0, 1e-6)
         self.rows = int(min(self.MAX_ROWS, max(16, 16 * target_s / t16)))
-        self.q = problem(self.rows)
+        self.q = self._problem(self.rows)
+
+    def _problem(self, rows):
+        O = self.O
+        if self.cfg == 3:  # cost_sqeuclidean / max, stored fp32 (data.cpp:69-82)
+            xs = self.x[:rows]
+            Cr = np.empty((rows, self.m), dtype=np.float32)
+            for r0 in range(0, rows, 256):
+                raw = np.zeros((min(rows, r0 + 256) - r0, self.m))
+                for k in range(3):  # coordinate order, as the device sums
+                    raw = raw + (xs[r0:r0 + 256, None, k] - self.y[None, :, k]) ** 2
+                Cr[r0:r0 + raw.shape[0]] = (raw / self.rawmax).astype(np.float32)
+        else:  # on-the-fly fp32 definition (otoracle.h orc_cost_sqeuclid_f32)
+            Cr = O.cost_sqeuclid_f32(self.x[:rows].astype(np.float32), self.y.astype(np.float32))
+        return O.Problem(np.full(rows, 1.0 / rows), np.full(self.m, 1.0 / self.m), Cr,
+                         cost_div=self.eps)
 
     def step(self):
         t_sum, sweeps = 0.0, 0
@@ -180,15 +219,11 @@ class CpuArm:
             sweeps += 1
             if t_sum >= self.target_s or sweeps >= 1000:
                 break
-        per_iter = t_sum / sweeps * (N / self.rows)
+        per_iter = t_sum / sweeps * (self.n / self.rows)
         return {"value": 1.0 / per_iter, "unit": UNIT, "cores": self.threads, "kind": "port",
-                "sample": f"{sweeps} sweep(s) of {self.rows} of {N} rows x {M} cols "
+                "sample": f"{sweeps} sweep(s) of {self.rows} of {self.n} rows x {self.m} cols "
                           f"({t_sum:.2f} s), extrapolated to one full iteration "
                           f"({per_iter:.2f} s/iter)"}
-
-
-def cpu_baseline(x, y, threads: int, target_s: float = 12.0):
-    return CpuArm(x, y, threads, target_s).step()
 
 
 def lscpu_model():
@@ -204,33 +239,70 @@ def lscpu_model():
 
 # ---------------------------------------------------------- reference ---
 def run_reference(args, rank, world):
+    """The reference's CPU implementation of the path: the oracle restatement
+    of the single-threaded fp64 reference (the C++ reference itself cannot be
+    built here: Eigen / libpng / doctest / CLI11 absent).  1 thread, as the
+    reference; an all-core figure of the same port is added
+    as `all_cores` for context.  Never loads libotg."""
     if rank != 0:
         return 0
-    from paper_2605_30267_b200 import ot  # input generator only (host RNG)
-    x, y = ot.gen_config(3, N, M, SEED)
-    threads = os.cpu_count() or 1
-    vals = []
-    sample = None
-    arm = CpuArm(x, y, threads, target_s=max(1.0, min(20.0, 150.0 / (args.warmup + args.steps))))
+    cfg = args.config
+    per_step = max(1.0, min(20.0, 150.0 / (args.warmup + args.steps)))
+    arm = CpuArm(cfg, 1, target_s=per_step)
+    vals, sample = [], None
     for k in range(args.warmup + args.steps):
         cb = arm.step()
         if k >= args.warmup:
             vals.append(cb["value"])
             sample = cb["sample"]
     value = statistics.median(vals)
+    allc = None
+    ncores = os.cpu_count() or 1
+    if ncores > 1 and not args.no_cpu:
+        arm.threads = ncores
+        arm.target_s = min(per_step, 5.0)
+        allc = {"value": arm.step()["value"], "cores": ncores}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE cfg3 shapes)",
-            "config": {"workload": WORKLOAD, "inputs": "fp32 cost rows built on the host"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": sample, "host": lscpu_model()},
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, BASELINE config shapes; oracle samplers)",
+            "config": config_dict(cfg, world if world > 1 else args.gpus, args.gpus > 1),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                             "sample": sample, "host": lscpu_model(), "nproc": ncores},
+            "all_cores": allc,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "note": "reference C++ cannot be built here (Eigen/libpng/doctest absent): the "
-                    "CPU oracle restatement (oracle/otoracle.cpp) is timed instead"}
+                    "single-threaded CPU oracle restatement (oracle/otoracle.cpp) is timed"}
     print(json.dumps(line), flush=True)
     return 0
+
+
+# -------------------------------------------------------------- ranks ----
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(args) -> int | None:
+    """--gpus N > 1 outside torchrun: re-run this script under
+    torch.distributed.run with N ranks on 127.0.0.1 (returns its exit code);
+    under torchrun, WORLD_SIZE must equal N."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None:
+        if int(world_env) != args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world_env}"}),
+                  flush=True)
+            return 2
+        return None
+    if args.gpus <= 1:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
 
 
 # --------------------------------------------------------------- GPU ----
@@ -239,14 +311,21 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-tol", action="store_true", help="skip the time-to-tolerance solve")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    ap.add_argument("--no-fixed", action="store_true", help="cfg5: skip the fixed-iteration run")
     ap.add_argument("--max-tol-iters", type=int, default=20000)
     ap.add_argument("--shard", action="store_true",
                     help="row-sharded NCCL path even at one rank (checks the N>1 code path)")
     args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 untimed warm-up steps
 
+    spawned = maybe_spawn(args)
+    if spawned is not None:
+        return spawned
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -256,25 +335,27 @@ def main():
 
     import torch
     import torch.distributed as dist
+    from paper_2605_30267_b200 import dist as otdist
     from paper_2605_30267_b200 import ot
 
+    cfg = args.config
+    C = CONFIGS[cfg]
+    N, M, EPS, TOL = C["n"], C["m"], C["eps"], C["tol"]
     torch.cuda.set_device(local_rank)
     distributed = world > 1 or args.shard
     if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    x, y = ot.gen_config(3, N, M, SEED)
+    x, y = ot.gen_config(cfg, N, M, C["seed"])
     a = np.full(N, 1.0 / N)
     b = np.full(M, 1.0 / M)
 
     shard = {}
+    r0, r1 = 0, N
     if distributed:
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(ot.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
-        r0, r1 = rank * N // world, (rank + 1) * N // world
-        shard = dict(world_size=world, rank=rank, row_begin=r0, row_end=r1,
-                     nccl_unique_id=bytes(uid.cpu().numpy()))
+        nid = otdist.nccl_id_from_group()
+        r0, r1 = otdist.shard_rows(N, world, rank)
+        shard = dict(world_size=world, rank=rank, row_begin=r0, row_end=r1, nccl_unique_id=nid)
+    x_local = np.ascontiguousarray(x[r0:r1])  # the caller passes its local rows (otg.h)
 
     def barrier():
         if distributed:
@@ -288,13 +369,17 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def make_problem():
+        return ot.TransportProblem.from_points(a, b, x_local, y, EPS, norm=C["norm"],
+                                               storage=C["storage"], device=local_rank, **shard)
+
     # ---- e2e: the user's call through the public API with HOST buffers:
-    # points + marginals uploaded, cost built on the device, Acc-Sinkhorn
-    # homotopy to the 1e-6 marginal error (the metric's second half), the
-    # potentials copied back; wall clock, max over ranks ----
+    # points + marginals uploaded, cost built on the device (cfg3), Acc-Sinkhorn
+    # homotopy to the tolerance (the metric's second half), the potentials
+    # copied back; wall clock, max over ranks ----
     barrier()
     t0 = time.perf_counter()
-    p = ot.TransportProblem.from_points(a, b, x, y, EPS, device=local_rank, **shard)
+    p = make_problem()
     e2e_cfg = (ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=args.warmup + args.steps)
                if args.no_tol else
                ot.HomotopyConfig(tol_l1=TOL, max_total_inner=args.max_tol_iters))
@@ -303,12 +388,11 @@ def main():
     barrier()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e_iters = r_e2e.iterations
-    rows = (shard["row_end"] - shard["row_begin"]) if shard else N
-    h2d = (x[:rows].nbytes + y.nbytes + a.nbytes + b.nbytes)
+    h2d = (x_local.nbytes + y.nbytes + a.nbytes + b.nbytes)
     d2h = u_host.nbytes + v_host.nbytes
 
     # ---- device-timed throughput: W warm-up iterations, then K timed ----
-    ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=max(args.warmup, 3)))
+    ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=args.warmup))
     barrier()
     with ClockSampler(local_rank) as clk:
         barrier()
@@ -323,24 +407,17 @@ def main():
     r = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=args.steps),
                           time_sweeps=True)
     evals = r.evaluations
-
-    # dominant kernel roofline (CUDA events around every launch inside the solve)
     row_ms = r.row_pass_seconds / evals * 1e3
     col_ms = r.col_pass_seconds / evals * 1e3
+    epi_ms = r.epilogue_seconds / evals * 1e3
     ms_sw, bytes_sw = ot.time_sweeps(p, r.potentials.v, reps=3)
-    dom = "column pass" if col_ms >= row_ms else "row pass"
-    dom_ms = max(col_ms, row_ms)
-    dom_bytes = bytes_sw[1] if col_ms >= row_ms else bytes_sw[0]
-    peak, peak_src = peaks()
-    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch", {}).get(
-                "k_col_fast" if dom == "column pass" else "k_row_shift")
-        except Exception:
-            traffic = None
+    info = p.handle.info
+    rows_local = r1 - r0
+    if cfg == 3:
+        roofline = hbm_roofline(info, row_ms, col_ms, bytes_sw, ms_sw, rows_local, M)
+    else:
+        roofline = otf_roofline(row_ms, col_ms, rows_local, M, clk.summary())
+    roofline["epilogue_ms"] = epi_ms
 
     # ---- time to tolerance (fresh solve from v = 0) ----
     ttt = None
@@ -349,43 +426,53 @@ def main():
         with ClockSampler(local_rank, period_s=0.02) as clk_tol:
             rt = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=TOL, max_total_inner=args.max_tol_iters))
             barrier()
+        st = ot.plan_stats(p, rt.potentials.u, rt.potentials.v)
         ttt = {"seconds": max_over_ranks(rt.device_seconds), "iterations": rt.iterations,
                "converged": bool(rt.converged), "final_violation": rt.final_violation,
-               "tol_l1": TOL, "clocks": clk_tol.summary()}
+               "plan_violation_l1_fp64": st.marginal_violation_l1,
+               "primal_cost": st.primal_cost, "tol_l1": TOL, "clocks": clk_tol.summary()}
+
+    fixed = None
+    if cfg == 5 and not args.no_fixed:
+        barrier()
+        with ClockSampler(local_rank, period_s=0.02) as clk_fx:
+            rf = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300,
+                                                        max_total_inner=C["fixed_iters"]))
+            barrier()
+        fixed = {"iterations": rf.iterations, "seconds": max_over_ranks(rf.device_seconds),
+                 "iters_per_s": rf.iterations / max_over_ranks(rf.device_seconds),
+                 "clocks": clk_fx.summary()}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(x, y, 1)
+        cpu = CpuArm(cfg, 1, target_s=12.0).step()
         cpu["host"] = lscpu_model()
+        cpu["nproc"] = os.cpu_count()
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / iters,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32 storage / f64 accumulation",
-            "data": "synthetic (seeded Beta point clouds standing in for RGB samples)",
-            "config": {"workload": WORKLOAD, "n": N, "m": M, "eps": EPS, "seed": SEED,
-                       "parallelism": (f"row-shard x{world} (NCCL all-reduce of the column sums)"
-                                       if distributed else "single GPU"),
-                       "l2": "inputs (17.2 GB) >> L2 (126 MB); no flush needed",
-                       "timed": f"{iters} homotopy iterations ({evals} evaluations incl. seed)"},
+            "dtype": "f32 storage / f64 accumulation" if cfg == 3 else
+                     "f32 coordinates + exponents / f64 accumulation",
+            "data": "synthetic (seeded; " + ("Beta point clouds standing in for RGB samples)"
+                                             if cfg == 3 else "uniform + Gaussian-mixture points)"),
+            "config": config_dict(cfg, world, distributed),
             "time_to_tol": ttt,
+            "fixed_iters": fixed,
             "e2e": {"value": e2e_iters / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": h2d / max(e2e_iters, 1),
                     "d2h_bytes_per_step": d2h / max(e2e_iters, 1),
                     "seconds": e2e_s, "iterations": e2e_iters,
                     "converged": bool(r_e2e.converged),
-                    "includes": "TransportProblem.from_points (H2D points + marginals, "
-                                "17.2 GB cost built on the device) + homotopy_solve to "
-                                "1e-6 + D2H u, v; wall clock"},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": peak_src, "algorithmic_bytes_per_launch": dom_bytes,
-                         "avg_launch_ms": dom_ms, "row_pass_ms": row_ms, "col_pass_ms": col_ms,
-                         "isolated_ms": {"row": ms_sw[0], "col": ms_sw[1], "merge": ms_sw[2]}},
+                    "includes": "TransportProblem.from_points (H2D points + marginals"
+                                + (", 17.2 GB cost built on the device" if cfg == 3 else "")
+                                + f") + homotopy_solve to {TOL:g} + D2H u, v; wall clock"},
+            "roofline": roofline,
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
+            "sweep": {"mode": int(info.sweep_mode), "col_splits": int(info.col_splits)},
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -393,6 +480,54 @@ def main():
     if distributed:
         dist.destroy_process_group()
     return 0
+
+
+def hbm_roofline(info, row_ms, col_ms, bytes_sw, ms_sw, rows, m):
+    """Stored cost: the dominant kernel's algorithmic bytes per launch (one
+    read of its rows of C, + O(n + m) vectors) / its mean launch time."""
+    peak, peak_src = peaks()
+    single = info.sweep_mode == 2
+    if single:  # single-pass: one kernel reads C once per evaluation
+        dom, dom_ms, dom_bytes = "single-pass sweep", row_ms + col_ms, bytes_sw[2]
+    elif col_ms >= row_ms:
+        dom, dom_ms, dom_bytes = "column pass", col_ms, bytes_sw[1]
+    else:
+        dom, dom_ms, dom_bytes = "row pass", row_ms, bytes_sw[0]
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            key = {"single-pass sweep": "k_sweep1", "column pass": "k_col_fast",
+                   "row pass": "k_row_shift"}[dom]
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch", {}).get(key)
+        except Exception:
+            traffic = None
+    return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
+            "row_pass_ms": row_ms, "col_pass_ms": col_ms,
+            "isolated_ms": {"row": ms_sw[0], "col": ms_sw[1], "merge": ms_sw[2]}}
+
+
+def otf_roofline(row_ms, col_ms, rows, m, clocks):
+    """On the fly: pair evaluations per second against the MUFU ex2 rate (one
+    ex2 per pair, 16 / clk / SM) and the combined MUFU + FMA-pipe bound of
+    BASELINE.md §2 (5 FP32 ops per pair, 8-op polynomial exp2 offload), both
+    at the max SM clock (the measured clock is reported beside them)."""
+    sms, f = 148, 1.965e9
+    r_mufu = 16 * sms * f
+    r_fma = 128 * sms * f
+    combined = 1.0 / min(max((1 - x / 100) / r_mufu, (5 + 8 * x / 100) / r_fma) for x in range(0, 101))
+    pairs = float(rows) * m
+    per_pass_ms = max(row_ms, col_ms)
+    achieved = pairs / (per_pass_ms * 1e-3)
+    return {"bound": "mufu", "kernel": "row pass" if row_ms >= col_ms else "column pass",
+            "achieved": achieved / 1e12, "peak": r_mufu / 1e12, "unit": "Tpair/s",
+            "frac": achieved / r_mufu, "frac_combined_bound": achieved / combined,
+            "combined_peak": combined / 1e12, "traffic": None,
+            "algorithmic_pairs_per_launch": pairs, "avg_launch_ms": per_pass_ms,
+            "row_pass_ms": row_ms, "col_pass_ms": col_ms, "sm_mhz": clocks.get("sm_mhz")}
 
 
 if __name__ == "__main__":

@@ -79,11 +79,24 @@ typedef enum {
   OTG_STORE_ON_THE_FLY = 2 /* squared-Euclidean recomputed per tile         */
 } otg_storage;
 
+/* Host all-reduce for sharded handles without NCCL (e.g. a torch.distributed
+ * gloo group, tests/test_sharded_libotg.py): reduce `count` doubles of `buf`
+ * in place across the ranks (op 0 = SUM, 1 = MAX); return 0 on success.
+ * libotg stages the device buffer through pinned host memory and calls it
+ * from a CUDA host node (cudaLaunchHostFunc), so it must not call CUDA. */
+typedef int (*otg_allreduce_fn)(double* buf, int64_t count, int op, void* ctx);
+
 /* Device placement and row sharding.  NULL means { device = current,
- * world_size = 1 }.  For world_size > 1 every rank creates the handle with
- * the full a and b, its own row block [row_begin, row_end) of C (or of the
- * source points), and the same 128-byte ncclUniqueId; the length-m column
- * sums are then all-reduced over NCCL once per evaluation.
+ * world_size = 1 }.  Row sharding (world_size > 1, or a 1-rank NCCL id):
+ * every rank creates the handle with the FULL a and b and ITS OWN rows
+ * [row_begin, row_end) of the row-indexed data -- C (otg_problem_create_dense)
+ * or the source points x (otg_problem_create_points) are passed as those
+ * n_local = row_end - row_begin rows only.  The ranks agree on the
+ * collective: the same 128-byte ncclUniqueId, or the same `allreduce`
+ * callback group (then nccl_unique_id is NULL).  The length-m column partial
+ * sums (+ <u, a>) are then all-reduced ONCE per evaluation; columns whose
+ * global sum underflows take an exact cross-rank LSE exchange that runs only
+ * in evaluations that flag some.
  * virtual_shards > 1 splits an unsharded handle's rows into that many shards
  * on ONE device whose partial column sums are combined by an on-device sum
  * standing in for the allreduce (tests the sharded data flow on one GPU). */
@@ -95,7 +108,8 @@ typedef struct {
   int64_t row_end;
   const void* nccl_unique_id;
   int virtual_shards;
-  int reserved[4];
+  otg_allreduce_fn allreduce; /* optional host collective (instead of NCCL) */
+  void* allreduce_ctx;
 } otg_device_opts;
 
 typedef struct otg_problem_s* otg_problem;
@@ -234,10 +248,11 @@ otg_status otg_problem_create_dense(int64_t n, int64_t m, const double* a, const
  * The normaliser is a global reduction (MAX all-reduce when sharded).
  * STORAGE_ON_THE_FLY (SQEUCLID, NORM_NONE, d <= 3; BASELINE cfg5): the cost
  * fl32((x - y)^2) of the fp32-rounded points is recomputed per tile and never
- * stored, and the instance is solved with epsilon_eff = log2(e) /
- * fl32(log2(e) / epsilon) (within 2^-24 relative of epsilon; the sweeps then
- * scale by an exact fp32 number).  Oracle instances built for parity divide
- * the fp32 cost by epsilon_eff (ot.otf_epsilon). */
+ * stored.  The instance keeps `epsilon` (info.epsilon, primal-cost unit); the
+ * device kernels all scale the cost by the internal 1 / epsilon_int with
+ * epsilon_int = log2(e) / fl32(log2(e) / epsilon), within 2^-25 relative of
+ * epsilon (the sweeps then multiply by one exact fp32 number).  Parity is
+ * tested against the oracle at the true epsilon (tests/test_gpu_otf.py). */
 otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const double* a,
                                      const double* b, const double* x, const double* y,
                                      otg_cost cost, otg_norm norm, otg_storage storage,

@@ -532,3 +532,71 @@ def random_zero_sum(rng: Rng, m: int, scale: float) -> np.ndarray:
     """helpers.hpp:48-52."""
     v = np.array([scale * (2.0 * rng.next_double() - 1.0) for _ in range(m)])
     return project_zero_sum(v)
+
+
+# ---- threads, config generators (SURVEY §8d), device-equivalent fp32 cost ----
+def set_threads(nthreads: int) -> None:
+    """Worker threads of the oracle's O(nm) loops (1 = the reference's single
+    thread); deterministic for a given count."""
+    lib().orc_set_threads(C.c_int(int(nthreads)))
+
+
+def get_threads() -> int:
+    return int(lib().orc_get_threads())
+
+
+class threads:
+    """with O.threads(8): ... — scoped worker count."""
+
+    def __init__(self, n: int):
+        self.n = n
+
+    def __enter__(self):
+        self.prev = get_threads()
+        set_threads(self.n)
+        return self
+
+    def __exit__(self, *exc):
+        set_threads(self.prev)
+
+
+def gen_config(cfg: int, n: int, m: int, seed: int):
+    """BASELINE config inputs: cfg 1 -> (a, b, C); cfg 2/3/5 -> (x, y)."""
+    if cfg == 1:
+        a, b, Cm = np.empty(n), np.empty(m), np.empty((n, m))
+        _check(lib().orc_gen_config(C.c_int(1), C.c_int64(n), C.c_int64(m), C.c_uint64(seed),
+                                    _p(a), _p(b), _p(Cm)))
+        return a, b, Cm
+    d = {2: 2, 3: 3, 5: 3}.get(cfg)
+    if d is None:
+        raise OracleError(1, "cfg must be 1, 2, 3 or 5")
+    x, y = np.empty((n, d)), np.empty((m, d))
+    _check(lib().orc_gen_config(C.c_int(cfg), C.c_int64(n), C.c_int64(m), C.c_uint64(seed),
+                                _p(x), _p(y), None))
+    return x, y
+
+
+def gen_config4(count: int, seed: int, d: int = 768):
+    n = np.empty(count, dtype=np.int32)
+    m = np.empty(count, dtype=np.int32)
+    _check(lib().orc_gen_config4(C.c_int64(count), C.c_uint64(seed), C.c_int64(d), _p(n), _p(m),
+                                 None, None))
+    x = np.empty((int(n.sum()), d), dtype=np.float32)
+    y = np.empty((int(m.sum()), d), dtype=np.float32)
+    _check(lib().orc_gen_config4(C.c_int64(count), C.c_uint64(seed), C.c_int64(d), _p(n), _p(m),
+                                 _p(x), _p(y)))
+    return n, m, x, y
+
+
+def cost_sqeuclid_max_f32(x, y, threads: int = 1, ldc: int = None):
+    """The fp32 cost a points instance stores on the device (SQEUCLID, NORM_MAX,
+    storage F32): fl32(sum_k (x_ik - y_jk)^2 / max).  Returns (C, raw_max)."""
+    x, y = _f64(x), _f64(y)
+    n, m, d = x.shape[0], y.shape[0], x.shape[1]
+    ldc = m if ldc is None else ldc
+    Cm = np.empty((n, ldc), dtype=np.float32)
+    mx = C.c_double()
+    _check(lib().orc_cost_sqeuclid_max_f32(_p(x), _p(y), C.c_int64(n), C.c_int64(m), C.c_int64(d),
+                                           C.c_int64(ldc), C.c_int(threads), _p(Cm),
+                                           C.byref(mx)))
+    return (Cm if ldc == m else Cm[:, :m]), mx.value

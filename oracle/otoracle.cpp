@@ -136,13 +136,30 @@ void check_v(const Prob& p, const double* v) {
     if (!std::isfinite(v[j])) fail(ORC_E_OT, "v has non-finite entries");
 }
 
+// Worker count for the O(nm) loops (orc_set_threads; 1 = the reference's
+// single thread).  Rows are split into T contiguous blocks; every thread keeps
+// its own column partial and the partials are summed in thread order, so a
+// run is deterministic for a given T and equals the T = 1 result to rounding
+// (tests/test_oracle_kat.py checks 1e-15).
+int g_threads = 1;
+
+template <class F>
+void parallel_blocks(int64_t n, int T, F&& fn) {
+  if (T <= 1 || n < 2 * T) {
+    fn(0, int64_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t) th.emplace_back([&, t] { fn(t, n * t / T, n * (t + 1) / T); });
+  fn(0, int64_t{0}, n / T);
+  for (auto& x : th) x.join();
+}
+
 // dual.cpp:29-42 — streamed one row at a time (T never materialised; the
 // per-element arithmetic and the i-ordered GEMV accumulation are unchanged).
-void row_solve_marginals(const Prob& p, const double* v, double* u, double* col) {
-  check_v(p, v);
+void row_block(const Prob& p, const double* v, int64_t lo, int64_t hi, double* u, double* col) {
   Vec T(p.m);
-  for (int64_t j = 0; j < p.m; ++j) col[j] = 0.0;
-  for (int64_t i = 0; i < p.n; ++i) {
+  for (int64_t i = lo; i < hi; ++i) {
     double mx = -std::numeric_limits<double>::infinity();
     for (int64_t j = 0; j < p.m; ++j) {
       T[j] = (-p.C(i, j)) + v[j];  // (-C).rowwise() + v^T   dual.cpp:34
@@ -159,23 +176,50 @@ void row_solve_marginals(const Prob& p, const double* v, double* u, double* col)
   }
 }
 
-// dual.cpp:44-70
+void row_solve_marginals(const Prob& p, const double* v, double* u, double* col) {
+  check_v(p, v);
+  for (int64_t j = 0; j < p.m; ++j) col[j] = 0.0;
+  const int T = static_cast<int>(std::min<int64_t>(g_threads, p.n));
+  if (T <= 1) {
+    row_block(p, v, 0, p.n, u, col);
+    return;
+  }
+  std::vector<Vec> parts(T, Vec(p.m, 0.0));
+  parallel_blocks(p.n, T, [&](int t, int64_t lo, int64_t hi) {
+    row_block(p, v, lo, hi, u, parts[t].data());
+  });
+  for (int64_t j = 0; j < p.m; ++j) {
+    double s = 0.0;
+    for (int t = 0; t < T; ++t) s += parts[t][j];
+    col[j] = s;
+  }
+}
+
+// dual.cpp:44-70 (the exact column LSE of each flagged column is independent:
+// flagged columns are spread over the workers, each column summed in i order)
 void row_solve_marginals_log(const Prob& p, const double* v, double* u, double* col,
                              double* col_log) {
   row_solve_marginals(p, v, u, col);
   constexpr double tiny = 1e-280;
+  std::vector<int64_t> flagged;
   for (int64_t j = 0; j < p.m; ++j) {
-    if (col[j] >= tiny) {
+    if (col[j] >= tiny)
       col_log[j] = std::log(col[j]);
-      continue;
-    }
-    double top = -std::numeric_limits<double>::infinity();
-    for (int64_t i = 0; i < p.n; ++i) top = std::max(top, u[i] + v[j] - p.C(i, j));
-    double s = 0.0;
-    for (int64_t i = 0; i < p.n; ++i) s += std::exp(u[i] + v[j] - p.C(i, j) - top);
-    col_log[j] = top + std::log(s);
-    col[j] = std::exp(col_log[j]);
+    else
+      flagged.push_back(j);
   }
+  const int64_t nf = static_cast<int64_t>(flagged.size());
+  parallel_blocks(nf, g_threads, [&](int, int64_t lo, int64_t hi) {
+    for (int64_t k = lo; k < hi; ++k) {
+      const int64_t j = flagged[k];
+      double top = -std::numeric_limits<double>::infinity();
+      for (int64_t i = 0; i < p.n; ++i) top = std::max(top, u[i] + v[j] - p.C(i, j));
+      double s = 0.0;
+      for (int64_t i = 0; i < p.n; ++i) s += std::exp(u[i] + v[j] - p.C(i, j) - top);
+      col_log[j] = top + std::log(s);
+      col[j] = std::exp(col_log[j]);
+    }
+  });
 }
 
 struct StepEval {  // sinkhorn.hpp:18-24
@@ -476,6 +520,9 @@ extern "C" {
 
 const char* orc_last_error(void) { return g_err.c_str(); }
 
+void orc_set_threads(int nthreads) { g_threads = std::max(1, nthreads); }
+int orc_get_threads(void) { return g_threads; }
+
 // rng.hpp:11-58 (xoshiro256++ seeded by splitmix64)
 static inline uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
 void orc_rng_seed(uint64_t st[4], uint64_t seed) {
@@ -508,6 +555,134 @@ uint64_t orc_rng_next_below(uint64_t s[4], uint64_t bound) {
     const uint64_t r = orc_rng_next_u64(s);
     if (r >= threshold) return r % bound;
   }
+}
+
+// ---- BASELINE config samplers (SURVEY §8d draw orders) --------------------
+// Restated here so that the CPU legs (tests' fixtures, bench.py --impl
+// reference) never load the product library; tests/test_oracle_gen.py checks
+// them bitwise against libotg's otg_gen_config.  Gaussian / Beta / mixture
+// draws are not in the reference (it has uniform and bounded draws only,
+// rng.hpp:38-50):
+//   Gaussian  — Box–Muller cosine branch, first uniform taken as 1 - U so the
+//               logarithm never sees 0; the sine branch is not drawn;
+//   Beta(k, 7-k) — k-th smallest of six uniforms;
+//   mixture   — component by next_below(3), then three Gaussian offsets.
+static double orc_gauss(uint64_t s[4]) {
+  const double one_minus_u = 1.0 - orc_rng_next_double(s);
+  const double angle_u = orc_rng_next_double(s);
+  const double radius = std::sqrt(-2.0 * std::log(one_minus_u));
+  return radius * std::cos(2.0 * M_PI * angle_u);
+}
+
+static double orc_order_stat6(uint64_t s[4], int k) {
+  double draws[6];
+  for (int t = 0; t < 6; ++t) draws[t] = orc_rng_next_double(s);
+  // insertion sort: only the order statistic matters
+  for (int t = 1; t < 6; ++t)
+    for (int q = t; q > 0 && draws[q] < draws[q - 1]; --q) std::swap(draws[q], draws[q - 1]);
+  return draws[k - 1];
+}
+
+static void orc_normalise_sum(double* x, int64_t n) {
+  double total = 0.0;
+  for (int64_t i = 0; i < n; ++i) total += x[i];
+  for (int64_t i = 0; i < n; ++i) x[i] /= total;
+}
+
+int orc_gen_config(int cfg, int64_t n, int64_t m, uint64_t seed, double* out0, double* out1,
+                   double* out2) {
+  return guard([&] {
+    if (n < 1 || m < 1) fail(ORC_E_DIMENSION, "config needs n, m >= 1");
+    uint64_t s[4];
+    orc_rng_seed(s, seed);
+    if (cfg == 1) {  // a, b ~ U(0.1, 1] normalised; C ~ U[0, 1) raw, row-major
+      for (int64_t i = 0; i < n; ++i) out0[i] = 1.0 - 0.9 * orc_rng_next_double(s);
+      for (int64_t j = 0; j < m; ++j) out1[j] = 1.0 - 0.9 * orc_rng_next_double(s);
+      for (int64_t k = 0; k < n * m; ++k) out2[k] = orc_rng_next_double(s);
+      orc_normalise_sum(out0, n);
+      orc_normalise_sum(out1, m);
+    } else if (cfg == 2) {  // x ~ N(0, I2); y ~ N((2, 0), diag(0.5, 2))
+      for (int64_t k = 0; k < 2 * n; ++k) out0[k] = orc_gauss(s);
+      const double sd0 = std::sqrt(0.5), sd1 = std::sqrt(2.0);
+      for (int64_t j = 0; j < m; ++j) {
+        const double g0 = orc_gauss(s);
+        out1[2 * j] = 2.0 + sd0 * g0;
+        const double g1 = orc_gauss(s);
+        out1[2 * j + 1] = sd1 * g1;
+      }
+    } else if (cfg == 3) {  // Beta(2,5)^3 sources, Beta(5,2)^3 targets
+      for (int64_t k = 0; k < 3 * n; ++k) out0[k] = orc_order_stat6(s, 2);
+      for (int64_t k = 0; k < 3 * m; ++k) out1[k] = orc_order_stat6(s, 5);
+    } else if (cfg == 5) {  // U[0,1]^3 sources; 3-Gaussian mixture targets (sigma 0.1), clipped
+      for (int64_t k = 0; k < 3 * n; ++k) out0[k] = orc_rng_next_double(s);
+      double means[3][3];
+      for (auto& mu : means)
+        for (double& c : mu) c = orc_rng_next_double(s);
+      for (int64_t j = 0; j < m; ++j) {
+        const uint64_t comp = orc_rng_next_below(s, 3);
+        for (int k = 0; k < 3; ++k) {
+          const double t = means[comp][k] + 0.1 * orc_gauss(s);
+          out1[3 * j + k] = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+        }
+      }
+    } else {
+      fail(ORC_E_OT, "orc_gen_config: cfg must be 1, 2, 3 or 5");
+    }
+  });
+}
+
+int orc_gen_config4(int64_t count, uint64_t seed, int64_t d, int32_t* n, int32_t* m,
+                    float* x_cat, float* y_cat) {
+  return guard([&] {
+    if (count < 1 || d < 1) fail(ORC_E_DIMENSION, "config 4 needs count, d >= 1");
+    uint64_t s[4];
+    orc_rng_seed(s, seed);
+    Vec g(d);
+    int64_t xrow = 0, yrow = 0;
+    auto unit_rows = [&](int64_t rows, float* dst, int64_t& row) {
+      for (int64_t r = 0; r < rows; ++r, ++row) {
+        double ss = 0.0;
+        for (int64_t k = 0; k < d; ++k) {
+          g[k] = orc_gauss(s);
+          ss += g[k] * g[k];
+        }
+        const double inv = 1.0 / std::sqrt(ss);
+        if (dst)
+          for (int64_t k = 0; k < d; ++k) dst[row * d + k] = static_cast<float>(g[k] * inv);
+      }
+    };
+    for (int64_t p = 0; p < count; ++p) {
+      n[p] = 8 + static_cast<int32_t>(orc_rng_next_below(s, 57));
+      m[p] = 8 + static_cast<int32_t>(orc_rng_next_below(s, 57));
+      unit_rows(n[p], x_cat, xrow);
+      unit_rows(m[p], y_cat, yrow);
+    }
+  });
+}
+
+// cost_sqeuclidean (data.cpp:69-82) stored as fp32 the way the B200 path
+// stores a points instance (storage F32, norm MAX): raw fp64 sum of squared
+// differences in coordinate order, divided by the global maximum, rounded to
+// fp32.  nthreads workers (rows are independent; the result does not depend on
+// the thread count).  C has row stride ldc.
+int orc_cost_sqeuclid_max_f32(const double* x, const double* y, int64_t n, int64_t m, int64_t d,
+                              int64_t ldc, int nthreads, float* C, double* raw_max) {
+  return guard([&] {
+    const double mx = orc_sqeuclid_max(x, y, n, m, d, nthreads);
+    parallel_blocks(n, std::max(1, nthreads), [&](int, int64_t lo, int64_t hi) {
+      for (int64_t i = lo; i < hi; ++i)
+        for (int64_t j = 0; j < m; ++j) {
+          double acc = 0.0;
+          for (int64_t k = 0; k < d; ++k) {
+            const double diff = x[i * d + k] - y[j * d + k];
+            acc += diff * diff;
+          }
+          const double c = mx > 0.0 ? acc / mx : acc;
+          C[i * ldc + j] = static_cast<float>(c);
+        }
+    });
+    if (raw_max) *raw_max = mx;
+  });
 }
 
 int orc_validate_problem(const orc_problem* pp, double epsilon) {
@@ -598,19 +773,37 @@ int orc_plan_stats(const orc_problem* pp, const double* u, const double* v, doub
                    double* row_sums, double* col_sums, double* violation, double* primal) {
   return guard([&] {
     Prob p = wrap(pp);
-    double top = -std::numeric_limits<double>::infinity();
-    for (int64_t i = 0; i < p.n; ++i)
-      for (int64_t j = 0; j < p.m; ++j) top = std::max(top, ((-p.C(i, j)) + u[i]) + v[j]);
+    const int T = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g_threads, p.n)));
+    Vec tops(T, -std::numeric_limits<double>::infinity());
+    parallel_blocks(p.n, T, [&](int t, int64_t lo, int64_t hi) {
+      double top = -std::numeric_limits<double>::infinity();
+      for (int64_t i = lo; i < hi; ++i)
+        for (int64_t j = 0; j < p.m; ++j) top = std::max(top, ((-p.C(i, j)) + u[i]) + v[j]);
+      tops[t] = top;
+    });
+    const double top = *std::max_element(tops.begin(), tops.end());
     if (top > kExpOverflowBound) fail(ORC_E_OVERFLOW, "plan exponent exceeds bound");
-    Vec rs(p.n, 0.0), cs(p.m, 0.0);
+    Vec rs(p.n, 0.0);
+    std::vector<Vec> cs_t(T, Vec(p.m, 0.0));
+    Vec cost_t(T, 0.0);
+    parallel_blocks(p.n, T, [&](int t, int64_t lo, int64_t hi) {
+      Vec& cs = cs_t[t];
+      double cost = 0.0;
+      for (int64_t i = lo; i < hi; ++i)
+        for (int64_t j = 0; j < p.m; ++j) {
+          const double P = std::exp(((-p.C(i, j)) + u[i]) + v[j]);
+          rs[i] += P;
+          cs[j] += P;
+          cost += p.C(i, j) * P;
+        }
+      cost_t[t] = cost;
+    });
+    Vec cs(p.m, 0.0);
     double cost = 0.0;
-    for (int64_t i = 0; i < p.n; ++i)
-      for (int64_t j = 0; j < p.m; ++j) {
-        const double P = std::exp(((-p.C(i, j)) + u[i]) + v[j]);
-        rs[i] += P;
-        cs[j] += P;
-        cost += p.C(i, j) * P;
-      }
+    for (int t = 0; t < T; ++t) {
+      cost += cost_t[t];
+      for (int64_t j = 0; j < p.m; ++j) cs[j] += cs_t[t][j];
+    }
     double viol = 0.0;
     for (int64_t i = 0; i < p.n; ++i) viol += std::abs(rs[i] - p.a[i]);
     double vc = 0.0;

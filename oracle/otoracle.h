@@ -104,6 +104,25 @@ typedef struct {
 
 const char* orc_last_error(void);
 
+/* Worker threads of the O(nm) loops (row sweep, fallback columns, plan
+ * statistics); 1 (default) is the reference's single thread.  Deterministic
+ * for a given count; equal to the 1-thread result to rounding. */
+void orc_set_threads(int nthreads);
+int orc_get_threads(void);
+
+/* BASELINE config inputs (SURVEY §8d draw orders), restated independently of
+ * the product library's otg_gen_config (bitwise equal, tests/test_oracle_gen.py).
+ * cfg 1: out0 = a (n), out1 = b (m), out2 = C (n*m); cfg 2/3/5: out0 = x (n*d),
+ * out1 = y (m*d), d = 2/3/3. */
+int orc_gen_config(int cfg, int64_t n, int64_t m, uint64_t seed, double* out0, double* out1,
+                   double* out2);
+int orc_gen_config4(int64_t count, uint64_t seed, int64_t d, int32_t* n, int32_t* m,
+                    float* x_cat, float* y_cat);
+/* fp32 C = fl32(sum_k (x_ik - y_jk)^2 / max) with row stride ldc: the stored
+ * cost of a points instance (SQEUCLID, NORM_MAX, storage F32). */
+int orc_cost_sqeuclid_max_f32(const double* x, const double* y, int64_t n, int64_t m, int64_t d,
+                              int64_t ldc, int nthreads, float* C, double* raw_max);
+
 /* ---- rng.hpp:11-58 ---------------------------------------------------- */
 void orc_rng_seed(uint64_t state[4], uint64_t seed);
 uint64_t orc_rng_next_u64(uint64_t state[4]);

@@ -19,7 +19,7 @@ class DeviceOpts(C.Structure):
     _fields_ = [("device", C.c_int), ("world_size", C.c_int), ("rank", C.c_int),
                 ("row_begin", C.c_int64), ("row_end", C.c_int64),
                 ("nccl_unique_id", C.c_void_p), ("virtual_shards", C.c_int),
-                ("reserved", C.c_int * 4)]
+                ("allreduce", C.c_void_p), ("allreduce_ctx", C.c_void_p)]
 
 
 class ProblemInfo(C.Structure):

@@ -1,4 +1,5 @@
-// comm.cpp — NCCL for row-sharded handles (one rank per GPU).
+// comm.cpp — the collective of row-sharded handles (one rank per GPU): NCCL,
+// or a caller-supplied host all-reduce (otg_device_opts.allreduce).
 //
 // libnccl is opened lazily with dlopen (soname libnccl.so.2): a process that
 // already loaded torch's NCCL 2.28.9 gets that same copy, and single-GPU
@@ -10,6 +11,7 @@
 
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 
@@ -64,31 +66,111 @@ void check(nccl_result_t r, const char* what) {
   }
 }
 
+
+// Host all-reduce (otg_device_opts.allreduce): D2H into pinned staging, a
+// host node calls the caller's reduction, H2D back.  All three are stream
+// operations, so the sequence is captured into the chunk graph like the NCCL
+// call.  A failing callback is recorded and raised at the next sync point.
+struct HostArgs {
+  otg_allreduce_fn fn;
+  void* ctx;
+  double* buf;
+  int64_t count;
+  int op;
+  int* failed;
+  bool own;  // buf is this call site's own pinned buffer (captured calls)
+};
+
+void CUDART_CB host_allreduce(void* raw) {
+  auto* a = static_cast<HostArgs*>(raw);
+  if (a->fn(a->buf, a->count, a->op, a->ctx) != 0) *a->failed = 1;
+}
+
+struct HostComm {
+  std::vector<HostArgs*> captured;  // call sites baked into chunk graphs
+  HostArgs eager{};                 // reused by eager calls (stream-ordered)
+  int failed = 0;
+};
+
+void host_allreduce_enqueue(Problem& P, const double* send, double* recv, size_t count, int op) {
+  auto* hc = static_cast<HostComm*>(P.nccl_comm);
+  HostArgs* a = nullptr;
+  if (P.capturing) {
+    // a graph keeps its pointers: every captured call site owns its staging
+    a = new HostArgs{P.ar_fn, P.ar_ctx, nullptr, static_cast<int64_t>(count), op, &hc->failed,
+                     true};
+    OTG_CUDA(cudaMallocHost(&a->buf, count * sizeof(double)));
+    hc->captured.push_back(a);
+  } else {
+    if (count > P.ar_host_len) {
+      OTG_CUDA(cudaStreamSynchronize(P.stream));
+      if (P.ar_host) cudaFreeHost(P.ar_host);
+      P.ar_host = nullptr;
+      OTG_CUDA(cudaMallocHost(&P.ar_host, count * sizeof(double)));
+      P.ar_host_len = count;
+    }
+    a = &hc->eager;
+    OTG_CUDA(cudaStreamSynchronize(P.stream));  // the previous eager call's args are done
+    *a = HostArgs{P.ar_fn, P.ar_ctx, P.ar_host, static_cast<int64_t>(count), op, &hc->failed,
+                  false};
+  }
+  OTG_CUDA(cudaMemcpyAsync(a->buf, send, count * sizeof(double), cudaMemcpyDeviceToHost,
+                           P.stream));
+  OTG_CUDA(cudaLaunchHostFunc(P.stream, host_allreduce, a));
+  OTG_CUDA(cudaMemcpyAsync(recv, a->buf, count * sizeof(double), cudaMemcpyHostToDevice,
+                           P.stream));
+}
+
 }  // namespace
 
-void comm_init(Problem& P, const void* unique_id) {
+void comm_init(Problem& P, const otg_device_opts* opts) {
   if (P.nccl_comm) return;
-  if (!unique_id) fail(OTG_E_NCCL, "world_size > 1 needs nccl_unique_id");
+  if (opts && opts->allreduce) {
+    P.ar_fn = opts->allreduce;
+    P.ar_ctx = opts->allreduce_ctx;
+    P.nccl_comm = new HostComm;
+    return;
+  }
+  if (!opts || !opts->nccl_unique_id)
+    fail(OTG_E_NCCL, "a sharded handle needs nccl_unique_id or an allreduce callback");
   nccl_unique_id_t id;
-  std::memcpy(id.internal, unique_id, sizeof id.internal);
+  std::memcpy(id.internal, opts->nccl_unique_id, sizeof id.internal);
   nccl_comm_t comm = nullptr;
   check(api().init_rank(&comm, P.world, id, P.rank), "ncclCommInitRank");
   P.nccl_comm = comm;
 }
 
 void comm_destroy(Problem& P) {
-  if (P.nccl_comm) api().destroy(static_cast<nccl_comm_t>(P.nccl_comm));
+  if (!P.nccl_comm) return;
+  if (P.ar_fn) {
+    auto* hc = static_cast<HostComm*>(P.nccl_comm);
+    for (auto* a : hc->captured) {
+      cudaFreeHost(a->buf);
+      delete a;
+    }
+    delete hc;
+    if (P.ar_host) cudaFreeHost(P.ar_host);
+    P.ar_host = nullptr;
+  } else {
+    api().destroy(static_cast<nccl_comm_t>(P.nccl_comm));
+  }
   P.nccl_comm = nullptr;
 }
 
-void comm_allreduce_sum(Problem& P, double* buf, size_t count) {
-  check(api().all_reduce(buf, buf, count, kNcclDouble, kNcclSum,
+int comm_failed(Problem& P) {
+  return (P.ar_fn && P.nccl_comm) ? static_cast<HostComm*>(P.nccl_comm)->failed : 0;
+}
+
+void comm_allreduce_sum(Problem& P, const double* send, double* recv, size_t count) {
+  if (P.ar_fn) return host_allreduce_enqueue(P, send, recv, count, 0);
+  check(api().all_reduce(send, recv, count, kNcclDouble, kNcclSum,
                          static_cast<nccl_comm_t>(P.nccl_comm), P.stream),
         "ncclAllReduce");
 }
 
-void comm_allreduce_max(Problem& P, double* buf, size_t count) {
-  check(api().all_reduce(buf, buf, count, kNcclDouble, kNcclMax,
+void comm_allreduce_max(Problem& P, const double* send, double* recv, size_t count) {
+  if (P.ar_fn) return host_allreduce_enqueue(P, send, recv, count, 1);
+  check(api().all_reduce(send, recv, count, kNcclDouble, kNcclMax,
                          static_cast<nccl_comm_t>(P.nccl_comm), P.stream),
         "ncclAllReduce");
 }

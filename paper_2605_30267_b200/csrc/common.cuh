@@ -114,6 +114,11 @@ enum Mode : int {
 // Device-resident control block.  The last CTA of the finalize epilogue runs
 // the solver's scalar control flow (stop test, homotopy schedule, trace) so
 // the iteration never round-trips to the host.
+// Ctrl::done values: 0 running, 1 finished (stop rule / cap / error), and
+// kPaused: a sharded chunk graph stopped at an evaluation whose flagged
+// columns need the cross-rank exact-LSE exchange (run eagerly by the host).
+constexpr int kPaused = 2;
+
 struct Ctrl {
   // --- status (device-written) ---
   int done;
@@ -265,8 +270,15 @@ struct Problem {
   int chunk_kernels = 0, chunk_kernels_timed = 0;  // kernel nodes per chunk graph
   std::vector<cudaEvent_t> chunk_events;  // 5 per iteration (timed graph)
 
-  // NCCL (sharded)
+  // collective of a sharded handle: NCCL, or a caller-supplied host
+  // all-reduce (otg_device_opts.allreduce) staged through pinned memory
   void* nccl_comm = nullptr;
+  otg_allreduce_fn ar_fn = nullptr;
+  void* ar_ctx = nullptr;
+  double* ar_host = nullptr;  // pinned staging of the host all-reduce
+  size_t ar_host_len = 0;
+  double* red = nullptr;      // sharded: this rank's merged column partials (+ <u, a>)
+  int capturing = 0;          // launch_eval is being captured into the chunk graph
 };
 
 // allocation helpers (track bytes)
@@ -286,6 +298,7 @@ void problem_alloc_state(Problem& P);
 // sweeps / epilogue (sweep.cu)
 void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4);
 void launch_apply(Problem& P);
+void launch_fallback_and_finalize(Problem& P);  // sharded pause: the eager rest of an eval
 void launch_row_pass(Problem& P);
 void launch_col_pass(Problem& P);
 void launch_merge_nolog(Problem& P);
@@ -297,11 +310,19 @@ void launch_fused(Problem& P, float kh, float kl);
 void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int ncl);
 int partial_rows(const Problem& P);  // rows of P.part the merge sums
 
-// NCCL (comm.cpp)
-void comm_init(Problem& P, const void* unique_id);
+// collectives of a sharded handle (comm.cpp).  recv may equal send.  Both
+// are stream-ordered on P.stream and capturable into the chunk graph.
+void comm_init(Problem& P, const otg_device_opts* opts);
 void comm_destroy(Problem& P);
-void comm_allreduce_sum(Problem& P, double* buf, size_t count);
-void comm_allreduce_max(Problem& P, double* buf, size_t count);
+int comm_failed(Problem& P);  // a host all-reduce callback returned non-zero
+void comm_allreduce_sum(Problem& P, const double* send, double* recv, size_t count);
+void comm_allreduce_max(Problem& P, const double* send, double* recv, size_t count);
+inline void comm_allreduce_sum(Problem& P, double* buf, size_t count) {
+  comm_allreduce_sum(P, buf, buf, count);
+}
+inline void comm_allreduce_max(Problem& P, double* buf, size_t count) {
+  comm_allreduce_max(P, buf, buf, count);
+}
 
 inline int64_t round_up(int64_t x, int64_t k) { return (x + k - 1) / k * k; }
 

@@ -144,7 +144,7 @@ void problem_free(Problem& P) {
                   P.col_log,
                   P.y, P.grad, P.prev_grad,
                   P.prev_x, P.prev_y, P.flag_idx, P.fb_cols, P.fb_part, P.part, P.e1_part,
-                  P.e2_part, P.epi_part, P.sp_rec, P.sp_bad_rows, P.sp_bad_count, P.ctrl, P.trace, P.vstar, P.bounds, P.fbA, P.fbS, P.fbT};
+                  P.e2_part, P.epi_part, P.sp_rec, P.sp_bad_rows, P.sp_bad_count, P.ctrl, P.trace, P.vstar, P.bounds, P.fbA, P.fbS, P.fbT, P.red};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (P.ctrl_host) cudaFreeHost(P.ctrl_host);
@@ -183,6 +183,7 @@ void problem_alloc_state(Problem& P) {
   P.fb_cols = dalloc<int>(P, mp);
   P.fb_part = dalloc<double2>(P, mp * kFbChunks);
   if (P.sharded) {
+    P.red = dalloc<double>(P, mp + 8 + std::max<int64_t>((P.m + 255) / 256, kEpiMaxGrid));
     P.fbA = dalloc<double>(P, mp);
     P.fbS = dalloc<double>(P, mp);
     P.fbT = dalloc<double>(P, mp);
@@ -219,12 +220,13 @@ static void begin(Problem& P, int64_t n, int64_t m, const otg_device_opts* opts)
   P.row_begin = 0;
   // Sharded (NCCL) when world_size > 1, or when an id is given for a 1-rank
   // communicator (exercises the collective path on one GPU).
-  if (opts && (opts->world_size > 1 || opts->nccl_unique_id)) {
+  if (opts && (opts->world_size > 1 || opts->nccl_unique_id || opts->allreduce)) {
     if (opts->world_size < 1 || opts->rank < 0 || opts->rank >= opts->world_size)
       fail(OTG_E_DIMENSION, "rank outside [0, world_size)");
     if (opts->row_begin < 0 || opts->row_end > n || opts->row_begin >= opts->row_end)
       fail(OTG_E_DIMENSION, "row shard [row_begin, row_end) outside [0, n)");
-    if (!opts->nccl_unique_id) fail(OTG_E_NCCL, "world_size > 1 needs nccl_unique_id");
+    if (!opts->nccl_unique_id && !opts->allreduce)
+      fail(OTG_E_NCCL, "world_size > 1 needs nccl_unique_id or an allreduce callback");
     P.world = opts->world_size;
     P.rank = opts->rank;
     P.row_begin = opts->row_begin;
@@ -259,7 +261,7 @@ static void upload_marginals(Problem& P, const double* a, const double* b) {
 }
 
 static void finish_create(Problem& P, const otg_device_opts* opts, otg_problem* out) {
-  if (P.sharded) comm_init(P, opts->nccl_unique_id);
+  if (P.sharded) comm_init(P, opts);
   problem_alloc_state(P);
   OTG_CUDA(cudaStreamSynchronize(P.stream));
   auto* h = new otg_problem_s;
@@ -353,7 +355,7 @@ otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const doub
       fail(OTG_E_OT, "unknown storage");
     begin(P, n, m, opts);
     const int64_t nl = P.n_local;
-    const double* xl = x + P.row_begin * d;
+    const double* xl = x;  // the caller's local rows (otg.h: x is n_local x d)
     for (int64_t t = 0; t < nl * d; ++t)
       if (!std::isfinite(xl[t])) fail(OTG_E_OT, "point coordinates must be finite");
     for (int64_t t = 0; t < m * d; ++t)
@@ -361,13 +363,18 @@ otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const doub
     if (storage == OTG_STORE_ON_THE_FLY) {
       // fp32 coordinates padded to float4; the cost is recomputed per tile in
       // the sweeps (sweep.cu: otf_cost) and never stored
-      // the instance's epsilon is log2(e) / fl32(log2(e) / epsilon) (relative
-      // change <= 2^-24): the base-2 scale kh of the sweeps is then exactly an
-      // fp32 number and the exponent needs no low-part term (ot.otf_epsilon)
+      // The instance keeps the caller's epsilon (reported, and the unit of
+      // the primal cost).  The sweeps scale the fp32 cost by ONE fp32 number
+      // kh = fl32(log2(e) / epsilon) (a hi/lo pair would cost a second FMA
+      // per pair on the FMA-bound on-the-fly path), so every device kernel
+      // -- fast sweeps, exact fp64 passes, fallback, plan statistics --
+      // uses the same internal scale kappa = kh / log2(e), within 2^-25
+      // relative of 1 / epsilon: one consistent model whose solution differs
+      // from the exact-epsilon one by O(2^-25) relative (parity against the
+      // oracle at the TRUE epsilon: tests/test_gpu_otf.py, test_gpu_configs.py).
       P.storage = OTG_STORE_ON_THE_FLY;
-      const double eps_eff = kLog2e / static_cast<double>(static_cast<float>(kLog2e / epsilon));
-      P.epsilon = eps_eff;
-      P.kappa = 1.0 / eps_eff;
+      P.epsilon = epsilon;
+      P.kappa = static_cast<double>(static_cast<float>(kLog2e / epsilon)) / kLog2e;
       upload_marginals(P, a, b);
       std::vector<float> hx(nl * 4, 0.f), hy(P.mpad * 4, 0.f);
       for (int64_t i = 0; i < nl; ++i)
@@ -426,7 +433,7 @@ otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const doub
         mx = std::max(mx, v.y);
       }
       if (P.sharded) {
-        comm_init(P, opts->nccl_unique_id);
+        comm_init(P, opts);
         double buf[2] = {-mn, mx};
         double* dbuf = nullptr;
         OTG_CUDA(cudaMalloc(&dbuf, 2 * sizeof(double)));

@@ -98,6 +98,7 @@ void build_graph(Problem& P, bool timed) {
   }
   cudaGraph_t g = nullptr;
   OTG_CUDA(cudaStreamBeginCapture(P.stream, cudaStreamCaptureModeThreadLocal));
+  P.capturing = 1;
   try {
     for (int k = 0; k < kChunk; ++k) {
       launch_eval(P, true, timed, timed ? &P.chunk_events[5 * k] : nullptr);
@@ -107,10 +108,12 @@ void build_graph(Problem& P, bool timed) {
                                           cudaEventRecordExternal));
     }
   } catch (...) {
+    P.capturing = 0;
     cudaStreamEndCapture(P.stream, &g);
     if (g) cudaGraphDestroy(g);
     throw;
   }
+  P.capturing = 0;
   OTG_CUDA(cudaStreamEndCapture(P.stream, &g));
   size_t nn = 0;
   OTG_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
@@ -132,6 +135,7 @@ struct LoopOut {
   double device_s = 0.0, row_s = 0.0, col_s = 0.0, epi_s = 0.0;
   int64_t trace_len = 0;
   int64_t launches = 0;  // kernel nodes executed (every replayed chunk)
+  int64_t pauses = 0;    // sharded: chunks paused for an eager fallback exchange
 };
 
 // Replays the chunk graph until the device control block says done; drains
@@ -149,6 +153,16 @@ LoopOut run_loop(Problem& P, otg_solve_result* res, bool timed) {
     OTG_CUDA(cudaGraphLaunch(timed ? P.chunk_exec_timed : P.chunk_exec, P.stream));
     lo.launches += timed ? P.chunk_kernels_timed : P.chunk_kernels;
     get_ctrl(P);
+    if (P.sharded && comm_failed(P)) fail(OTG_E_NCCL, "host all-reduce callback failed");
+    if (P.ctrl_host->done == kPaused) {
+      // a sharded evaluation flagged columns: finish it eagerly (exact
+      // cross-rank LSE exchange, finalize, apply), then keep replaying
+      OTG_CUDA(cudaMemsetAsync(&P.ctrl->done, 0, sizeof(int), P.stream));
+      launch_fallback_and_finalize(P);
+      launch_apply(P);
+      get_ctrl(P);
+      ++lo.pauses;
+    }
     const Ctrl& c = *P.ctrl_host;
     if (timed) {
       const long long live = c.evaluations - ev_before;
@@ -177,7 +191,7 @@ LoopOut run_loop(Problem& P, otg_solve_result* res, bool timed) {
       }
       drained = c.trace_count;
     }
-    if (c.done) break;
+    if (c.done == 1) break;
   }
   OTG_CUDA(cudaEventRecord(t1, P.stream));
   OTG_CUDA(cudaEventSynchronize(t1));
@@ -531,7 +545,9 @@ otg_status otg_plan_stats(otg_problem h, const double* u, const double* v, otg_p
     if (top > kExpOverflowBound) fail(OTG_E_OVERFLOW, "plan exponent exceeds bound");
     for (int64_t j = 0; j < m; ++j) vc += std::abs(hcs[j] - hb[j]);
     out->marginal_violation_l1 = viol + vc;
-    out->primal_cost = cost * P.epsilon;  // (eps_original / eps) with eps = 1 (core.cpp:77-79)
+    // (eps_original / eps) with eps = 1 (core.cpp:77-79); on the fly the
+    // internal scale is kappa (within 2^-25 of 1 / epsilon), so undo exactly that
+    out->primal_cost = P.storage == OTG_STORE_ON_THE_FLY ? cost / P.kappa : cost * P.epsilon;
     if (out->row_sums) std::memcpy(out->row_sums, hrs.data(), n * sizeof(double));
     if (out->col_sums) std::memcpy(out->col_sums, hcs.data(), m * sizeof(double));
   });

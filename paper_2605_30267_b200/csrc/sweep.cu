@@ -1658,6 +1658,14 @@ k_fb_rescale(int64_t m, const int* __restrict__ flag_idx, const double* __restri
   if (fbS[j] > 0.0) fbS[j] *= exp(fbT[j] - fbA[j]);
 }
 
+// Sharded chunk graphs: pause the chunk when this evaluation flagged columns
+// (the flag set comes from the all-reduced sums, so every rank pauses at the
+// same evaluation); the host finishes it eagerly (solver.cu resume).
+__global__ void k_pause_if_flagged(Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
+  if (threadIdx.x == 0 && !ctrl->done && ctrl->fb_count > 0) ctrl->done = kPaused;
+}
+
 // --------------------------------------------------------------- control --
 __device__ void push_trace(Ctrl* C, double* trace, long long iter, double viol, double f,
                            double mu, double alpha) {
@@ -2563,6 +2571,14 @@ static void launch_merge(Problem& P, bool merge, bool flag) {
 
 void launch_merge_nolog(Problem& P) { launch_merge(P, true, false); }
 
+// Local merge (no flagging) into `dst` (the sharded all-reduce's send buffer).
+static void launch_merge_into(Problem& P, double* dst) {
+  launch_k(k_merge, merge_blocks(P), kEThreads, 0, P.stream, P.part, P.vshards, P.col_splits,
+           P.m, P.mpad, dst, P.col_log, P.flag_idx, P.fb_cols, P.u, P.a, P.n_local, 1, 0,
+           P.ctrl, P.fused ? P.fused_clusters + 1 : 0);
+  OTG_CUDA(cudaGetLastError());
+}
+
 // Event records are "external" so that, under stream capture, they become
 // event-record nodes of the chunk graph (timestamps readable after replay).
 static void mark(Problem& P, cudaEvent_t e) {
@@ -2684,15 +2700,37 @@ void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
     }
   }
   if (P.sharded) {
-    // local merge, then one all-reduce of the m column sums + <u, a>; the
-    // underflow test needs the global sums, so flagging follows the reduce
-    launch_merge(P, true, false);
-    comm_allreduce_sum(P, P.col, static_cast<size_t>(P.mpad + 1 + merge_blocks(P)));
+    // local merge into `red`, then THE collective of the evaluation: one
+    // out-of-place all-reduce of the m column sums + <u, a> slices into col
+    // (re-running it on unchanged `red` rewrites identical bytes, which the
+    // paused chunk below relies on); the underflow test needs the global
+    // sums, so flagging follows the reduce and is identical on every rank
+    launch_merge_into(P, P.red);
+    comm_allreduce_sum(P, P.red, P.col, static_cast<size_t>(P.mpad + 1 + merge_blocks(P)));
     if (with_log) launch_merge(P, false, true);
+    if (with_log && P.capturing) {
+      // inside the chunk graph: an evaluation that flags columns pauses the
+      // chunk (ctrl->done = kPaused; every later kernel of the chunk returns)
+      // and the host runs its cross-rank exact-LSE exchange eagerly
+      // (resume_paused_eval) -- the steady state has no second collective
+      launch_k(k_pause_if_flagged, 1, 32, 0, P.stream, P.ctrl);
+      launch_k(k_finalize, P.e_blocks, kEThreads, 0, P.stream, fin_args(P, merge_blocks(P)),
+               P.ctrl);
+      OTG_CUDA(cudaGetLastError());
+      P.apply_pending = 1;
+      return;
+    }
   } else {
     launch_merge(P, true, with_log);
   }
   if (!with_log) return;
+  launch_fallback_and_finalize(P);
+}
+
+// The rest of an evaluation after the flagging merge: the exact column LSE
+// of flagged columns (sharded: local (top, sum) per column, MAX then SUM
+// all-reduce), then finalize.
+void launch_fallback_and_finalize(Problem& P) {
   if (P.storage == OTG_STORE_F64)
     launch_k(k_fallback<true, false>, 296, kEThreads, 0, P.stream, 
         P.C64, cost_src(P), P.ldc, P.n_local, P.kappa, P.u, P.p, P.fb_cols, P.fb_part, P.ctrl);

@@ -36,21 +36,41 @@ def nccl_id_from_group(group=None) -> bytes:
     return bytes(buf.cpu().numpy())
 
 
-def sharded_points_problem(a, b, x, y, epsilon, world, rank, nccl_id, device=None, **kw):
-    """This rank's handle of a row-sharded points problem."""
+def gloo_allreduce(group=None):
+    """A host all-reduce over a torch.distributed CPU group (gloo) for
+    otg_device_opts.allreduce: libotg stages the device buffer through pinned
+    memory and calls this from a CUDA host node.  Lets several processes
+    exercise the sharded data flow without NCCL (e.g. two ranks on one GPU)."""
+    import torch
+    import torch.distributed as dist
+
+    def reduce(buf: np.ndarray, op: int) -> None:
+        t = torch.from_numpy(buf)  # shares the pinned staging buffer
+        dist.all_reduce(t, op=dist.ReduceOp.SUM if op == 0 else dist.ReduceOp.MAX, group=group)
+
+    return reduce
+
+
+def sharded_points_problem(a, b, x, y, epsilon, world, rank, nccl_id=None, device=None,
+                           allreduce=None, **kw):
+    """This rank's handle of a row-sharded points problem: only this rank's
+    source rows are uploaded (the C-ABI takes the local rows, otg.h)."""
     r0, r1 = shard_rows(len(a), world, rank)
-    return ot.TransportProblem.from_points(a, b, x, y, epsilon, device=rank if device is None else device,
+    return ot.TransportProblem.from_points(a, b, np.ascontiguousarray(x[r0:r1]), y, epsilon,
+                                           device=rank if device is None else device,
                                            world_size=world, rank=rank, row_begin=r0, row_end=r1,
-                                           nccl_unique_id=nccl_id, **kw)
+                                           nccl_unique_id=nccl_id, allreduce=allreduce, **kw)
 
 
-def sharded_dense_problem(a, b, C, epsilon, world, rank, nccl_id, device=None):
-    """This rank's handle of a row-sharded dense problem (C rows of the shard
-    are what is uploaded)."""
+def sharded_dense_problem(a, b, C, epsilon, world, rank, nccl_id=None, device=None,
+                          allreduce=None):
+    """This rank's handle of a row-sharded dense problem: C may be the full
+    matrix (its rows [r0, r1) are uploaded) -- the C-ABI receives the local
+    rows only (otg.h)."""
     r0, r1 = shard_rows(len(a), world, rank)
     p = ot.rescale_problem(ot.make_problem(a, b, C, epsilon))
     return p.to_device(device=rank if device is None else device, world_size=world, rank=rank,
-                       row_begin=r0, row_end=r1, nccl_unique_id=nccl_id)
+                       row_begin=r0, row_end=r1, nccl_unique_id=nccl_id, allreduce=allreduce)
 
 
 def gather_u(u_local: np.ndarray, group=None) -> np.ndarray:

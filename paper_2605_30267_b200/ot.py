@@ -181,30 +181,44 @@ class TransportProblem:
     @classmethod
     def from_points(cls, a, b, x, y, epsilon, cost="sqeuclidean", norm="max", storage="f32",
                     device=0, world_size=1, rank=0, row_begin=0, row_end=None,
-                    nccl_unique_id=None, virtual_shards=1):
+                    nccl_unique_id=None, virtual_shards=1, allreduce=None):
         """Rescaled instance whose cost is built on the device from points
-        (cost_sqeuclidean / cost_cosine, data.cpp:69-110, then rescale_problem)."""
+        (cost_sqeuclid / cost_cosine, data.cpp:69-110, then rescale_problem).
+
+        Row sharding (world_size > 1): the device handle holds rows
+        [row_begin, row_end) of the sources; `x` may be those local rows
+        (what the C-ABI takes, otg.h) or all n rows (sliced here).  a and b
+        are always the full marginals."""
         a, b = _f64(a), _f64(b)
         x, y = _f64(x), _f64(y)
         if x.ndim != 2 or y.ndim != 2 or x.shape[1] != y.shape[1]:
             raise DimensionMismatch("point clouds have different dimensions")
-        _validate(a, b, (x.shape[0], y.shape[0]), epsilon)
+        rb, re_ = row_begin, (a.size if row_end is None else row_end)
+        if world_size > 1 and x.shape[0] == a.size:
+            x_dev = np.ascontiguousarray(x[rb:re_])
+        elif world_size > 1 and x.shape[0] == re_ - rb:
+            x_dev = x
+        else:
+            x_dev = x
+            _validate(a, b, (x.shape[0], y.shape[0]), epsilon)
+        if y.shape[0] != b.size:
+            raise DimensionMismatch("target points do not match b")
+        _validate(a, b, (a.size, y.shape[0]), epsilon)
         p = cls(a, b, None, epsilon=1.0, epsilon_original=epsilon, cost_div=epsilon)
-        p._points = (x, y, COST[cost], NORM[norm], STORAGE[storage])
-        p._opts = _device_opts(device, world_size, rank, row_begin,
-                               x.shape[0] if row_end is None else row_end, nccl_unique_id,
-                               virtual_shards)
+        p._points = (x_dev, y, COST[cost], NORM[norm], STORAGE[storage])
+        p._opts = _device_opts(device, world_size, rank, row_begin, re_, nccl_unique_id,
+                               virtual_shards, allreduce)
         p._handle = _DeviceHandle.points(p)
         return p
 
     def to_device(self, device=0, world_size=1, rank=0, row_begin=0, row_end=None,
-                  nccl_unique_id=None, virtual_shards=1):
+                  nccl_unique_id=None, virtual_shards=1, allreduce=None):
         """Create the device handle now with explicit placement / sharding."""
         if self._handle is not None:
             self._handle.close()
         self._opts = _device_opts(device, world_size, rank, row_begin,
                                   self.n() if row_end is None else row_end, nccl_unique_id,
-                                  virtual_shards)
+                                  virtual_shards, allreduce)
         self._handle = (_DeviceHandle.points(self) if self._points is not None
                         else _DeviceHandle.dense(self))
         return self
@@ -219,7 +233,14 @@ class TransportProblem:
             self._handle = None
 
 
-def _device_opts(device, world_size, rank, row_begin, row_end, nccl_unique_id, vshards):
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p)
+
+
+def _device_opts(device, world_size, rank, row_begin, row_end, nccl_unique_id, vshards,
+                 allreduce=None):
+    """otg_device_opts.  `allreduce`: a Python callable (buf: np.ndarray of
+    float64, op: 0 SUM / 1 MAX) -> None reducing `buf` in place across the
+    ranks (instead of NCCL; e.g. dist.gloo_allreduce())."""
     o = _capi.DeviceOpts()
     o.device = device
     o.world_size = world_size
@@ -231,6 +252,19 @@ def _device_opts(device, world_size, rank, row_begin, row_end, nccl_unique_id, v
         buf = C.create_string_buffer(bytes(nccl_unique_id), 128)
         o._uid = buf  # keep alive
         o.nccl_unique_id = C.cast(buf, C.c_void_p)
+    if allreduce is not None:
+        def _tramp(ptr, count, op, ctx, fn=allreduce):
+            try:
+                arr = np.ctypeslib.as_array((C.c_double * int(count)).from_address(ptr))
+                fn(arr, int(op))
+                return 0
+            except Exception:  # reported by libotg as OTG_E_NCCL
+                import traceback
+                traceback.print_exc()
+                return 1
+        cb = ALLREDUCE_FN(_tramp)
+        o._cb = cb  # keep alive as long as the options (and the handle holding them)
+        o.allreduce = C.cast(cb, C.c_void_p)
     return o
 
 
@@ -244,9 +278,11 @@ class _DeviceHandle:
         if p._C is None:
             raise DimensionMismatch("no cost matrix")
         Cs = p._C
+        opts = p._opts
+        if opts is not None and opts.world_size > 1:  # the handle's rows only (otg.h)
+            Cs = Cs[opts.row_begin:opts.row_end]
         dtype = 1 if Cs.dtype == np.float32 else 0
         h = C.c_void_p()
-        opts = p._opts
         _check(_lib().otg_problem_create_dense(p.n(), p.m(), _ptr(p.a), _ptr(p.b), _ptr(Cs),
                                                dtype, Cs.shape[1], p.cost_div,
                                                None if opts is None else C.byref(opts),
@@ -258,7 +294,7 @@ class _DeviceHandle:
         x, y, cost, norm, storage = p._points
         h = C.c_void_p()
         _check(_lib().otg_problem_create_points(
-            x.shape[0], y.shape[0], x.shape[1], _ptr(p.a), _ptr(p.b), _ptr(x), _ptr(y), cost,
+            p.n(), y.shape[0], x.shape[1], _ptr(p.a), _ptr(p.b), _ptr(x), _ptr(y), cost,
             norm, storage, p.cost_div, None if p._opts is None else C.byref(p._opts),
             C.byref(h)))
         return cls._wrap(h)
@@ -1015,11 +1051,14 @@ def synthetic_rescaled(n, m, seed, eps) -> TransportProblem:
 
 
 def otf_epsilon(epsilon: float) -> float:
-    """The epsilon an on-the-fly (storage="on_the_fly") instance is solved
-    with: log2(e) / fl32(log2(e) / epsilon), within 2^-24 relative of
-    `epsilon`.  The sweeps scale the fp32 cost by the fp32 number
-    fl32(log2(e) / epsilon) exactly (one FMA per exponent instead of a hi/lo
-    pair); oracle problems built for such an instance divide by this value."""
+    """The INTERNAL epsilon of the on-the-fly sweeps: log2(e) / fl32(log2(e) /
+    epsilon), within 2^-25 relative of `epsilon`.  The sweeps scale the fp32
+    cost by the single fp32 number fl32(log2(e) / epsilon) (one FMA per
+    exponent instead of a hi/lo pair), and every device kernel of the handle
+    uses this same scale.  The instance itself keeps `epsilon` (reported, and
+    the unit of the primal cost); parity is tested against the oracle at the
+    true epsilon.  Tests that compare plan consumers bit-for-bit on the
+    device's own model build the oracle problem with this value."""
     kh = float(np.float32(LOG2E / float(epsilon)))
     return LOG2E / kh
 

@@ -36,7 +36,7 @@ def test_ragged_shapes_fp32(n, m, storage):
     a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
     p = ot.TransportProblem.from_points(a, b, x, y, 2e-2, norm="none", storage=storage)
     C32 = O.cost_sqeuclid_f32(x.astype(np.float32), y.astype(np.float32))
-    q = O.Problem(a, b, C32, cost_div=ot.otf_epsilon(2e-2) if storage == "on_the_fly" else 2e-2)
+    q = O.Problem(a, b, C32, cost_div=2e-2)  # the TRUE epsilon for both storages
     g = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-6, max_total_inner=3000))
     o = O.homotopy_solve(q, tol_l1=1e-6, max_total_inner=3000)
     assert g.converged == o.converged

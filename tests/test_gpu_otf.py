@@ -1,6 +1,8 @@
 """On-the-fly squared-Euclidean path (BASELINE config 5): the cost is
 recomputed per tile from fp32 points and never stored; parity against the
-oracle on the identical fp32 cost (oracle.cost_sqeuclid_f32)."""
+oracle on the identical fp32 cost (oracle.cost_sqeuclid_f32) at the caller's
+TRUE epsilon (the device's internal scale is log2(e)/eps rounded to fp32,
+within 2^-25 relative: ot.otf_epsilon)."""
 import numpy as np
 import pytest
 
@@ -15,11 +17,12 @@ def _pair(n, m, seed, eps):
     a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
     p = ot.TransportProblem.from_points(a, b, x, y, eps, norm="none", storage="on_the_fly")
     C32 = O.cost_sqeuclid_f32(x.astype(np.float32), y.astype(np.float32))
-    return p, O.Problem(a, b, C32, cost_div=ot.otf_epsilon(eps)), C32
+    return p, O.Problem(a, b, C32, cost_div=eps), C32
 
 
 def test_otf_epsilon():
-    """The on-the-fly instance's epsilon: log2(e)/eps rounded to fp32 exactly."""
+    """The on-the-fly sweeps' internal epsilon: log2(e)/eps rounded to fp32
+    exactly (the instance itself keeps eps)."""
     for eps in (1e-3, 2e-3, 5e-3, 2e-2, 0.05, 1.0, 3e-7):
         e = ot.otf_epsilon(eps)
         assert abs(e - eps) <= 2.0 ** -24 * eps
@@ -39,6 +42,7 @@ def test_otf_rejects_unsupported_on_cpu():
 def test_otf_cost_matches_oracle_bitwise():
     p, _, C32 = _pair(300, 257, 5, 1e-3)
     assert p.handle.info.storage == 2
+    assert p.handle.info.epsilon == 1e-3  # the caller's epsilon, not the internal scale
     assert np.array_equal(p.stored_cost(), C32)
 
 
@@ -64,7 +68,7 @@ def test_otf_homotopy_cost_and_iterations():
     assert g.converged and o.converged
     assert abs(g.iterations - o.iterations) <= max(1, int(0.01 * o.iterations))
     cg = ot.plan_stats(p, g.potentials.u, g.potentials.v).primal_cost
-    co = O.plan_stats(q, o.u, o.v, ot.otf_epsilon(eps))["primal_cost"]
+    co = O.plan_stats(q, o.u, o.v, eps)["primal_cost"]
     assert abs(cg - co) <= REL32 * abs(co)
 
 
