@@ -110,6 +110,8 @@ typedef struct {
   int virtual_shards;
   otg_allreduce_fn allreduce; /* optional host collective (instead of NCCL) */
   void* allreduce_ctx;
+  int sweep;                  /* fp32 stored cost: 0 = auto (the single-HBM-pass
+                                 sweep where it applies), 1 = the two-pass kernels */
 } otg_device_opts;
 
 typedef struct otg_problem_s* otg_problem;

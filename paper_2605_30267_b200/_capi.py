@@ -19,7 +19,7 @@ class DeviceOpts(C.Structure):
     _fields_ = [("device", C.c_int), ("world_size", C.c_int), ("rank", C.c_int),
                 ("row_begin", C.c_int64), ("row_end", C.c_int64),
                 ("nccl_unique_id", C.c_void_p), ("virtual_shards", C.c_int),
-                ("allreduce", C.c_void_p), ("allreduce_ctx", C.c_void_p)]
+                ("allreduce", C.c_void_p), ("allreduce_ctx", C.c_void_p), ("sweep", C.c_int)]
 
 
 class ProblemInfo(C.Structure):

@@ -99,7 +99,12 @@ void host_allreduce_enqueue(Problem& P, const double* send, double* recv, size_t
     // a graph keeps its pointers: every captured call site owns its staging
     a = new HostArgs{P.ar_fn, P.ar_ctx, nullptr, static_cast<int64_t>(count), op, &hc->failed,
                      true};
-    OTG_CUDA(cudaMallocHost(&a->buf, count * sizeof(double)));
+    // (pinned allocation is not a stream operation: relax the capture mode for it)
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    OTG_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));
+    const cudaError_t e = cudaMallocHost(&a->buf, count * sizeof(double));
+    OTG_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));
+    OTG_CUDA(e);
     hc->captured.push_back(a);
   } else {
     if (count > P.ar_host_len) {

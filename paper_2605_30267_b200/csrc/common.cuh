@@ -228,12 +228,20 @@ struct Problem {
   int* fb_cols = nullptr;   // flagged column list (m)
   double2* fb_part = nullptr;  // (max, sum) per flagged column per row chunk
 
-  // single-pass fused sweep (fused.cu), fp32 storage only
-  int fused = 0, fused_qpt = 0, fused_W = 0, fused_slots = 0, fused_smem = 0,
-      fused_clusters = 0, fused_cl = 8;
+  // single-pass sweep (fused.cu), fp32 storage only.  fused_clusters = H
+  // groups of sp_group CTAs (one per SM); each group streams every H-th row
+  // band and writes one row of column partials (merge sums H + 1 rows).
+  int fused = 0, fused_slots = 0, fused_smem = 0, fused_clusters = 0;
+  int two_pass = 0;             // otg_device_opts.sweep == 1: never the single pass
+  int sp_group = 0;             // CTAs (SMs) sharing one row band
+  int sp_fix = 40;              // fixed-point scale 2^sp_fix of the row sums
+  int64_t sp_bands = 0;         // row bands of 16 rows
+  int64_t sp_cap = 0;           // capacity of each CTA's loose-row list
   double* sp_rec = nullptr;     // per-row 32-byte records (shift estimate, a, log a)
-  int* sp_bad_rows = nullptr;   // rows whose shift estimate was loose, per cluster
+  int* sp_bad_rows = nullptr;   // rows whose shift estimate was loose, per CTA (row order)
   int* sp_bad_count = nullptr;
+  void* sp_sums = nullptr;      // [2][n] fixed-point row sums, [2][n] (max, argmax) keys
+  unsigned* sp_cnt = nullptr;   // [2][bands] arrivals per band, + [2] parity / finish
 
   // on-the-fly transposed row pass (k_row_otf): column splits and their
   // per-row partials (row_splits x n_local records of 16 B)
@@ -307,7 +315,7 @@ void launch_split_p(Problem& P);  // vq <- split of p (after the host sets p)
 bool fused_configure(Problem& P);
 void fused_alloc(Problem& P);
 void launch_fused(Problem& P, float kh, float kl);
-void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int ncl);
+void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int ncl, int64_t cap);
 int partial_rows(const Problem& P);  // rows of P.part the merge sums
 
 // collectives of a sharded handle (comm.cpp).  recv may equal send.  Both

@@ -144,7 +144,7 @@ void problem_free(Problem& P) {
                   P.col_log,
                   P.y, P.grad, P.prev_grad,
                   P.prev_x, P.prev_y, P.flag_idx, P.fb_cols, P.fb_part, P.part, P.e1_part,
-                  P.e2_part, P.epi_part, P.sp_rec, P.sp_bad_rows, P.sp_bad_count, P.ctrl, P.trace, P.vstar, P.bounds, P.fbA, P.fbS, P.fbT, P.red};
+                  P.e2_part, P.epi_part, P.sp_rec, P.sp_bad_rows, P.sp_bad_count, P.ctrl, P.trace, P.vstar, P.bounds, P.fbA, P.fbS, P.fbT, P.red, P.sp_sums, P.sp_cnt};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (P.ctrl_host) cudaFreeHost(P.ctrl_host);
@@ -234,9 +234,10 @@ static void begin(Problem& P, int64_t n, int64_t m, const otg_device_opts* opts)
     P.sharded = 1;
   }
   P.vshards = (opts && opts->virtual_shards > 1) ? opts->virtual_shards : 1;
+  P.two_pass = (opts && opts->sweep == 1) ? 1 : 0;
   if (P.vshards > P.n_local) P.vshards = static_cast<int>(P.n_local);
   P.mpad = round_up(m, 4);
-  // rows padded to whole 8-CTA-cluster slices of 16-byte multiples (fused.cu)
+  // rows padded to 128-byte multiples (16-byte aligned bulk copies of any quad slice)
   static const int64_t ldc_pad = [] {  // tuning knob: extra floats per cost row
     const char* s = getenv("OTG_LDC_PAD");
     return s ? static_cast<int64_t>(atoi(s)) : int64_t{0};

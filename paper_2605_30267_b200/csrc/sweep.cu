@@ -709,20 +709,20 @@ __device__ __forceinline__ void row_shift_block(
   }
 }
 
-// Exact redo of the rows the single-pass kernel (fused.cu) listed as loose,
-// per cluster c at bad_rows[n c / ncl + k], k < bad_count[c].
+// Exact redo of the rows the single-pass kernel (fused.cu) listed as loose:
+// list c (c < ncl, in order) holds bad_rows[c cap + k], k < bad_count[c].
 __global__ void __launch_bounds__(kRowThreads)
 k_sp_redo(const CostSrc src, int64_t n, int64_t m, const double* __restrict__ p, double kappa,
           const double* __restrict__ a, const double* __restrict__ loga,
           double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
           double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
           int* __restrict__ rowJ, const int* __restrict__ bad_rows,
-          const int* __restrict__ bad_count, int ncl, Ctrl* __restrict__ ctrl) {
+          const int* __restrict__ bad_count, int ncl, int64_t cap, Ctrl* __restrict__ ctrl) {
   pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done || !ctrl->shift_valid) return;
   for (int c = 0; c < ncl; ++c) {
     const int nb = bad_count[c];
-    const int64_t base = n * c / ncl;
+    const int64_t base = cap * c;
     for (int k = blockIdx.x; k < nb; k += gridDim.x) {
       const int64_t rows[1] = {bad_rows[base + k]};
       const bool valid[1] = {true};
@@ -2547,10 +2547,10 @@ void launch_split_p(Problem& P) {
   launch_k(k_split_p, g, 256, 0, P.stream, P.m, P.mpad, P.p, P.vq);
 }
 
-void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int ncl) {
+void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int ncl, int64_t cap) {
   launch_k(k_sp_redo, 148, kRowThreads, 0, P.stream, cost_src(P), P.n_local, P.m, P.p, P.kappa, P.a,
                                                 P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,
-                                                P.rowM2, P.rowJ, bad_rows, bad_count, ncl,
+                                                P.rowM2, P.rowJ, bad_rows, bad_count, ncl, cap,
                                                 P.ctrl);
 }
 

@@ -181,7 +181,7 @@ class TransportProblem:
     @classmethod
     def from_points(cls, a, b, x, y, epsilon, cost="sqeuclidean", norm="max", storage="f32",
                     device=0, world_size=1, rank=0, row_begin=0, row_end=None,
-                    nccl_unique_id=None, virtual_shards=1, allreduce=None):
+                    nccl_unique_id=None, virtual_shards=1, allreduce=None, sweep="auto"):
         """Rescaled instance whose cost is built on the device from points
         (cost_sqeuclid / cost_cosine, data.cpp:69-110, then rescale_problem).
 
@@ -207,18 +207,18 @@ class TransportProblem:
         p = cls(a, b, None, epsilon=1.0, epsilon_original=epsilon, cost_div=epsilon)
         p._points = (x_dev, y, COST[cost], NORM[norm], STORAGE[storage])
         p._opts = _device_opts(device, world_size, rank, row_begin, re_, nccl_unique_id,
-                               virtual_shards, allreduce)
+                               virtual_shards, allreduce, sweep)
         p._handle = _DeviceHandle.points(p)
         return p
 
     def to_device(self, device=0, world_size=1, rank=0, row_begin=0, row_end=None,
-                  nccl_unique_id=None, virtual_shards=1, allreduce=None):
+                  nccl_unique_id=None, virtual_shards=1, allreduce=None, sweep="auto"):
         """Create the device handle now with explicit placement / sharding."""
         if self._handle is not None:
             self._handle.close()
         self._opts = _device_opts(device, world_size, rank, row_begin,
                                   self.n() if row_end is None else row_end, nccl_unique_id,
-                                  virtual_shards, allreduce)
+                                  virtual_shards, allreduce, sweep)
         self._handle = (_DeviceHandle.points(self) if self._points is not None
                         else _DeviceHandle.dense(self))
         return self
@@ -236,12 +236,19 @@ class TransportProblem:
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p)
 
 
+SWEEPS = {"auto": 0, "two_pass": 1}
+
+
 def _device_opts(device, world_size, rank, row_begin, row_end, nccl_unique_id, vshards,
-                 allreduce=None):
+                 allreduce=None, sweep="auto"):
     """otg_device_opts.  `allreduce`: a Python callable (buf: np.ndarray of
     float64, op: 0 SUM / 1 MAX) -> None reducing `buf` in place across the
-    ranks (instead of NCCL; e.g. dist.gloo_allreduce())."""
+    ranks (instead of NCCL; e.g. dist.gloo_allreduce()).  `sweep`: "auto"
+    (the single-HBM-pass sweep where it applies) or "two_pass"."""
+    if sweep not in SWEEPS:
+        raise OtError(f"unknown sweep '{sweep}'")
     o = _capi.DeviceOpts()
+    o.sweep = SWEEPS[sweep]
     o.device = device
     o.world_size = world_size
     o.rank = rank

@@ -331,18 +331,9 @@ def test_config1_full_size_fp64_both_solvers():
 # ------------------------------------------- fused single-pass sweep ----
 
 def _points_problem(n, m, seed, eps, fused):
-    import os
     x, y = ot.gen_config(3, n, m, seed)
-    old = os.environ.get("OTG_FUSED")
-    os.environ["OTG_FUSED"] = "1" if fused else "0"
-    try:
-        p = ot.TransportProblem.from_points(np.full(n, 1 / n), np.full(m, 1 / m), x, y, eps)
-    finally:
-        if old is None:
-            del os.environ["OTG_FUSED"]
-        else:
-            os.environ["OTG_FUSED"] = old
-    return p
+    return ot.TransportProblem.from_points(np.full(n, 1 / n), np.full(m, 1 / m), x, y, eps,
+                                           sweep="auto" if fused else "two_pass")
 
 
 @pytest.mark.parametrize("n,m", [(512, 8192), (300, 4100), (1000, 1024), (257, 65536)])
@@ -365,8 +356,9 @@ def test_fused_eval_matches_oracle_and_two_pass(n, m):
 
 @pytest.mark.parametrize("n,m,eps", [(300, 4100, 2e-3), (257, 65536, 1e-3), (2048, 2048, 5e-4)])
 def test_fused_single_pass_matches_two_pass_solve(n, m, eps):
-    """Steady-state single-pass kernel (cluster exchange, shift estimates,
-    loose-row redo + column patch) against the two-pass kernels."""
+    """Steady-state single-pass kernel (grid-wide band pipeline, tensor-memory
+    staging, shift estimates, loose-row redo + column patch) against the
+    two-pass kernels."""
     pf = _points_problem(n, m, 11, eps, True)
     p2 = _points_problem(n, m, 11, eps, False)
     assert pf.handle.info.sweep_mode == 2 and p2.handle.info.sweep_mode == 1
