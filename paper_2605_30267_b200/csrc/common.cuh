@@ -234,14 +234,15 @@ struct Problem {
   int fused = 0, fused_slots = 0, fused_smem = 0, fused_clusters = 0;
   int two_pass = 0;             // otg_device_opts.sweep == 1: never the single pass
   int sp_group = 0;             // CTAs (SMs) sharing one row band
-  int sp_fix = 40;              // fixed-point scale 2^sp_fix of the row sums
-  int64_t sp_bands = 0;         // row bands of 16 rows
+  int sp_fix = 28;              // fixed-point scale 2^sp_fix of the row sums
+  int sp_bw = 0, sp_nbox = 0;   // TMA box: chunk width (columns), chunks per slice
+  alignas(64) unsigned char sp_tmap[128] = {};  // CUtensorMap of the stored cost (2-D)
   int64_t sp_cap = 0;           // capacity of each CTA's loose-row list
   double* sp_rec = nullptr;     // per-row 32-byte records (shift estimate, a, log a)
   int* sp_bad_rows = nullptr;   // rows whose shift estimate was loose, per CTA (row order)
   int* sp_bad_count = nullptr;
   void* sp_sums = nullptr;      // [2][n] fixed-point row sums, [2][n] (max, argmax) keys
-  unsigned* sp_cnt = nullptr;   // [2][bands] arrivals per band, + [2] parity / finish
+  unsigned* sp_cnt = nullptr;   // [0] buffer parity of the next launch, [1] finished CTAs
 
   // on-the-fly transposed row pass (k_row_otf): column splits and their
   // per-row partials (row_splits x n_local records of 16 B)
@@ -312,6 +313,11 @@ void launch_col_pass(Problem& P);
 void launch_merge_nolog(Problem& P);
 void launch_sweeps(Problem& P, bool timed, cudaEvent_t* ev4);
 void launch_split_p(Problem& P);  // vq <- split of p (after the host sets p)
+struct SpLayout {  // column layout of the single-pass sweep (fused.cu)
+  bool ok = false;
+  int H = 0, group = 0, cw = 0, nch = 0;
+};
+SpLayout sp_layout(int64_t m, int sms);
 bool fused_configure(Problem& P);
 void fused_alloc(Problem& P);
 void launch_fused(Problem& P, float kh, float kl);

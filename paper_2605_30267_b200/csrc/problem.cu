@@ -243,6 +243,12 @@ static void begin(Problem& P, int64_t n, int64_t m, const otg_device_opts* opts)
     return s ? static_cast<int64_t>(atoi(s)) : int64_t{0};
   }();
   P.ldc = round_up(m, 32) + round_up(ldc_pad, 32);
+  {  // a row stride the single-pass sweep's 3-D tensor view can use (fused.cu)
+    int sms = 0;
+    OTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.device));
+    const SpLayout L = sp_layout(m, sms);
+    if (L.ok && ldc_pad == 0) P.ldc = round_up(m, L.cw);
+  }
   OTG_CUDA(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
 }
 
