@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -159,46 +160,80 @@ inline void write_instance_csv(const std::string& path, const Instance& p) {
   if (!os) throw IoError("short write to " + path);
 }
 
+namespace detail {
+// One record of the instance format: "name,index,value" (the value field
+// keeps anything after the second comma, as the writer never emits one).
+struct CsvRecord {
+  std::string name;
+  long index = 0;
+  double value = 0.0;
+};
+
+// Leading integer / number of a field, 0 when there is none (the format's
+// reader is lenient about trailing text, data.cpp:220-269).
+inline long leading_long(const std::string& f) {
+  std::istringstream in(f);
+  long x = 0;
+  return (in >> x) ? x : 0L;
+}
+inline double leading_double(const std::string& f) {
+  char* end = nullptr;
+  const double x = std::strtod(f.c_str(), &end);
+  return end == f.c_str() ? 0.0 : x;
+}
+
+inline bool parse_record(const std::string& line, CsvRecord& rec) {
+  const size_t first = line.find(',');
+  if (first == std::string::npos) return false;
+  const size_t second = line.find(',', first + 1);
+  if (second == std::string::npos) return false;
+  rec.name.assign(line, 0, first);
+  rec.index = leading_long(line.substr(first + 1, second - first - 1));
+  rec.value = leading_double(line.substr(second + 1));
+  return true;
+}
+}  // namespace detail
+
+// Instance CSV (data.cpp:203-271): header "name,index,value", then n, m,
+// epsilon and the a / b / C entries in index order.
 inline Instance read_instance_csv(const std::string& path) {
-  std::ifstream is(path);
-  if (!is) throw IoError("cannot open " + path);
-  std::string line;
-  if (!std::getline(is, line) || line != "name,index,value")
-    throw MalformedLine(path + ": missing 'name,index,value' header");
-  long n = -1, m = -1, line_no = 1;
-  Instance out;
-  out.epsilon = -1.0;
-  while (std::getline(is, line)) {
-    ++line_no;
-    if (line.empty()) continue;
-    const auto c1 = line.find(',');
-    const auto c2 = line.find(',', c1 == std::string::npos ? c1 : c1 + 1);
-    if (c1 == std::string::npos || c2 == std::string::npos)
-      throw MalformedLine(path + ":" + std::to_string(line_no) + ": expected three fields");
-    const std::string name = line.substr(0, c1);
-    const long index = std::strtol(line.substr(c1 + 1, c2 - c1 - 1).c_str(), nullptr, 10);
-    const double value = std::strtod(line.c_str() + c2 + 1, nullptr);
-    if (name == "n") {
-      n = static_cast<long>(value);
-    } else if (name == "m") {
-      m = static_cast<long>(value);
-    } else if (name == "epsilon") {
-      out.epsilon = value;
-    } else if (name == "a" || name == "b" || name == "C") {
-      Vec& dst = name == "a" ? out.a : name == "b" ? out.b : out.C;
-      if (static_cast<size_t>(index) != dst.size())
-        throw MalformedLine(path + ":" + std::to_string(line_no) + ": " + name + " index " +
-                            std::to_string(index) + " out of order");
-      dst.push_back(value);
-    } else {
-      throw MalformedLine(path + ":" + std::to_string(line_no) + ": unknown field '" + name + "'");
+  std::ifstream file(path);
+  if (!file) throw IoError("cannot read instance file " + path);
+  std::string text;
+  if (!std::getline(file, text) || text != "name,index,value")
+    throw MalformedLine(path + ": the first line must be the header name,index,value");
+  Instance inst;
+  inst.epsilon = -1.0;
+  long rows = -1, cols = -1;
+  long lineno = 1;
+  auto where = [&] { return path + " line " + std::to_string(lineno); };
+  while (std::getline(file, text)) {
+    ++lineno;
+    if (text.empty()) continue;
+    detail::CsvRecord rec;
+    if (!detail::parse_record(text, rec)) throw MalformedLine(where() + ": not a name,index,value record");
+    if (rec.name == "n" || rec.name == "m") {
+      (rec.name == "n" ? rows : cols) = static_cast<long>(rec.value);
+      continue;
     }
+    if (rec.name == "epsilon") {
+      inst.epsilon = rec.value;
+      continue;
+    }
+    Vec* target = rec.name == "a" ? &inst.a : rec.name == "b" ? &inst.b
+                : rec.name == "C" ? &inst.C : nullptr;
+    if (!target) throw MalformedLine(where() + ": unknown record name '" + rec.name + "'");
+    if (rec.index != static_cast<long>(target->size()))
+      throw MalformedLine(where() + ": " + rec.name + "[" + std::to_string(rec.index) +
+                          "] is not the next entry");
+    target->push_back(rec.value);
   }
-  if (n < 1 || m < 1 || !(out.epsilon > 0.0)) throw MalformedLine(path + ": missing n / m / epsilon");
-  if (static_cast<long>(out.a.size()) != n || static_cast<long>(out.b.size()) != m ||
-      static_cast<long>(out.C.size()) != n * m)
-    throw MalformedLine(path + ": entry counts do not match n, m");
-  return out;
+  if (rows < 1 || cols < 1 || !(inst.epsilon > 0.0))
+    throw MalformedLine(path + ": n, m or epsilon missing");
+  if (static_cast<long>(inst.a.size()) != rows || static_cast<long>(inst.b.size()) != cols ||
+      static_cast<long>(inst.C.size()) != rows * cols)
+    throw MalformedLine(path + ": the a / b / C entries do not match n and m");
+  return inst;
 }
 
 // ------------------------------------------------------------ configs / results

@@ -11,13 +11,7 @@ namespace {
 thread_local std::string g_last_error;
 }
 void set_last_error(const std::string& msg) { g_last_error = msg; }
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* s = getenv("OTG_PDL");
-    return !s || atoi(s) != 0;
-  }();
-  return on;
-}
+bool pdl_enabled() { return OTG_PDL != 0; }
 }  // namespace otg
 
 extern "C" {

@@ -9,6 +9,33 @@
 
 #include "../../include/otg.h"
 
+// Compile-time tuning defaults (A/B builds: tools/ab_build.sh NAME SRC "-DOTG_...=x").
+// The shipped library reads no environment knobs that change its behaviour.
+#ifndef OTG_PDL
+#define OTG_PDL 1            // programmatic dependent launch on every graph kernel
+#endif
+#ifndef OTG_ROW_R
+#define OTG_ROW_R 0          // fp32 row pass rows per CTA (0 = auto: 4 stored, 8 on the fly)
+#endif
+#ifndef OTG_ONLINE_FIRST
+#define OTG_ONLINE_FIRST 1   // first evaluation with the fp32 online-shift row pass
+#endif
+#ifndef OTG_COL_T
+#define OTG_COL_T 0          // column-pass CTA width (0 = auto: 256)
+#endif
+#ifndef OTG_COL_SPLITS
+#define OTG_COL_SPLITS 0     // column-pass row splits (0 = auto: whole waves)
+#endif
+#ifndef OTG_ROW_OTF_T
+#define OTG_ROW_OTF_T 1      // on the fly: the transposed row pass
+#endif
+#ifndef OTG_ROW_PF
+#define OTG_ROW_PF -1        // row-pass L2 prefetch (-1 = auto)
+#endif
+#ifndef OTG_EPI_FUSED
+#define OTG_EPI_FUSED 0      // one-kernel epilogue with grid barriers (measured slower)
+#endif
+
 namespace otg {
 
 // ---------------------------------------------------------------- errors --

@@ -237,17 +237,13 @@ static void begin(Problem& P, int64_t n, int64_t m, const otg_device_opts* opts)
   P.two_pass = (opts && opts->sweep == 1) ? 1 : 0;
   if (P.vshards > P.n_local) P.vshards = static_cast<int>(P.n_local);
   P.mpad = round_up(m, 4);
-  // rows padded to 128-byte multiples (16-byte aligned bulk copies of any quad slice)
-  static const int64_t ldc_pad = [] {  // tuning knob: extra floats per cost row
-    const char* s = getenv("OTG_LDC_PAD");
-    return s ? static_cast<int64_t>(atoi(s)) : int64_t{0};
-  }();
-  P.ldc = round_up(m, 32) + round_up(ldc_pad, 32);
+  // rows padded to 128-byte multiples (aligned 16-byte loads of any quad)
+  P.ldc = round_up(m, 32);
   {  // a row stride the single-pass sweep's 3-D tensor view can use (fused.cu)
     int sms = 0;
     OTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.device));
     const SpLayout L = sp_layout(m, sms);
-    if (L.ok && ldc_pad == 0) P.ldc = round_up(m, L.cw);
+    if (L.ok) P.ldc = round_up(m, L.cw);
   }
   OTG_CUDA(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
 }

@@ -2284,10 +2284,7 @@ int e_grid(int64_t m) {
 // ---------------------------------------------------------------- launch ---
 // Rows per CTA of the fp32 row pass (tuning knob OTG_ROW_R = 1, 4 or 8).
 int64_t rows_per_cta_fast(const Problem& P) {
-  static const int env = [] {
-    const char* s = getenv("OTG_ROW_R");
-    return s ? atoi(s) : 0;
-  }();
+  constexpr int env = OTG_ROW_R;  // (compile-time tuning: 0 = auto)
   // on the fly, 8 rows share each column quad's coordinate / potential loads
   // (cfg5-shaped 100000^2: 5.86 -> 5.38 ms per row pass); stored, 4 rows keep
   // 3 CTAs per SM (8 rows: 65536^2 2.90 -> 4.06 ms)
@@ -2312,22 +2309,13 @@ static int64_t col_slots(const Problem& P) {
 }
 
 void configure_sweeps(Problem& P) {
-  static const int online = [] {
-    const char* s = getenv("OTG_ONLINE_FIRST");
-    return s ? atoi(s) : 1;
-  }();
+  const int online = OTG_ONLINE_FIRST;
   OTG_CUDA(cudaMemcpyToSymbol(c_online_first, &online, sizeof(int)));
   // column-pass split: ~24 CTAs per SM over the grid so the dynamic CTA
   // scheduler balances the 148 SMs (ncu: 640 CTAs = 0.48 waves was
   // latency-bound); partials cost splits * m * 8 B (< 1% of the sweep)
-  static const int env_t = [] {
-    const char* s = getenv("OTG_COL_T");
-    return s ? atoi(s) : 0;
-  }();
-  static const int env_s = [] {
-    const char* s = getenv("OTG_COL_SPLITS");
-    return s ? atoi(s) : 0;
-  }();
+  constexpr int env_t = OTG_COL_T;  // (compile-time tuning: 0 = auto)
+  constexpr int env_s = OTG_COL_SPLITS;  // (compile-time tuning: 0 = auto)
   // 256 threads x 4 columns = 4 KB of each cost row per CTA, ~9 CTAs per SM
   // in one wave (tools/col_sweep.py on B200: 2.77 ms = 95% of HBM at
   // 65536^2, vs 3.53 ms for 128-thread CTAs in 2.7 waves)
@@ -2366,10 +2354,7 @@ void configure_sweeps(Problem& P) {
   P.rows_per_split = (shard_rows + splits - 1) / splits;
   // on the fly: the transposed row pass (OTG_ROW_OTF_T=0: row_shift_block).
   // Column splits give ~8 waves of the resident CTAs, >= 256 columns each.
-  static const int env_rt = [] {
-    const char* s = getenv("OTG_ROW_OTF_T");
-    return s ? atoi(s) : 1;
-  }();
+  constexpr int env_rt = OTG_ROW_OTF_T;
   P.row_splits = 0;
   if (P.storage == OTG_STORE_ON_THE_FLY && env_rt != 0) {
     int occ = 0, sms = 0;
@@ -2443,10 +2428,7 @@ void launch_row_pass(Problem& P) {
     // L2::256B loads, 3 / 5 = prefetch 2 / 4 chunks ahead).  B200, 65536^2:
     // with the scalar inner loop 3.19 ms (off) -> 2.95 ms (3); with the packed
     // f32x2 loop both take ~2.92 ms (3 CTAs/SM either way), so it is off
-    static const int row_pf_env = [] {
-      const char* s = getenv("OTG_ROW_PF");
-      return s ? atoi(s) : -1;
-    }();
+    constexpr int row_pf_env = OTG_ROW_PF;  // (compile-time tuning: -1 = auto)
     // cfg2 (8192^2): 70.8 -> 65.7 us with the prefetch; cfg3: equal, so only
     // rows short enough for the per-CTA latency to show get it by default
     const int row_pf = row_pf_env >= 0 ? row_pf_env : (P.m <= 16384 ? 3 : 0);
@@ -2643,10 +2625,7 @@ static AppArgs app_args(const Problem& P) {
 
 // CTAs of the single-kernel epilogue (co-resident: <= one per SM), 0 = off.
 static int epilogue_grid(Problem& P) {
-  static const int env = [] {
-    const char* s = getenv("OTG_EPI_FUSED");
-    return s ? atoi(s) : 0;
-  }();
+  constexpr int env = OTG_EPI_FUSED;
   if (!env || P.sharded) return 0;
   if (P.epi_grid == 0) {
     int sms = 0, occ = 0;

@@ -16,11 +16,14 @@ sys.path.insert(0, ROOT)
 
 def instance(case):
     from paper_2605_30267_b200 import ot
-    if case == "f32_points":  # cfg3-shaped points, stored fp32, no flagged columns
+    if case in ("f32_points", "f32_points_sp"):  # cfg3-shaped points, stored fp32
+        # f32_points: the two-pass kernels (bitwise against virtual shards);
+        # f32_points_sp: the single-pass sweep on each rank's rows
         n, m = 1536, 1100
         x, y = ot.gen_config(3, n, m, 3)
         return dict(kind="points", x=x, y=y, a=np.full(n, 1 / n), b=np.full(m, 1 / m),
-                    eps=2e-2, storage="f32", norm="max", tol=1e-7, iters=60)
+                    eps=2e-2, storage="f32", norm="max", tol=1e-7, iters=60,
+                    sweep="two_pass" if case == "f32_points" else "auto")
     if case == "otf_points":  # cfg5-shaped, cost on the fly
         n, m = 1200, 1500
         x, y = ot.gen_config(5, n, m, 5)
@@ -36,7 +39,7 @@ def instance(case):
         from oracle import oracle as O
         C, _ = O.cost_sqeuclid_max_f32(x, y)
         return dict(kind="dense", a=np.full(n, 1 / n), b=np.full(m, 1 / m), C=C, eps=2e-3,
-                    tol=1e-6, iters=50)
+                    tol=1e-6, iters=50, sweep="two_pass")
     raise ValueError(case)
 
 
@@ -45,9 +48,10 @@ def make(inst, **kw):
     if inst["kind"] == "points":
         return ot.TransportProblem.from_points(inst["a"], inst["b"], inst["x"], inst["y"],
                                                inst["eps"], storage=inst["storage"],
-                                               norm=inst["norm"], **kw)
+                                               norm=inst["norm"], sweep=inst.get("sweep", "auto"),
+                                               **kw)
     p = ot.rescale_problem(ot.make_problem(inst["a"], inst["b"], inst["C"], inst["eps"]))
-    return p.to_device(**kw)
+    return p.to_device(sweep=inst.get("sweep", "auto"), **kw)
 
 
 def main():
@@ -69,7 +73,7 @@ def main():
         x_local = np.ascontiguousarray(inst["x"][r0:r1])
         p = ot.TransportProblem.from_points(inst["a"], inst["b"], x_local, inst["y"],
                                             inst["eps"], storage=inst["storage"],
-                                            norm=inst["norm"], **kw)
+                                            norm=inst["norm"], sweep=inst.get("sweep", "auto"), **kw)
     else:
         p = make(inst, **kw)
     fixed = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300,

@@ -93,8 +93,12 @@ def test_world2_bitwise_vs_virtual_shards(case, tmp_path):
     assert float(r[0]["cost"]) == float(r[1]["cost"])
 
 
-@pytest.mark.parametrize("case,tol", [("f64_dense", 1e-12), ("f32_points", 1e-9)])
+@pytest.mark.parametrize("case,tol", [("f64_dense", 1e-12), ("f32_points", 1e-9),
+                                      ("f32_points_sp", 1e-9)])
 def test_world2_matches_unsharded(case, tol, tmp_path):
+    """f32_points_sp: each rank runs the single-pass sweep on its own rows
+    (its column partials all-reduced), against the single-pass sweep of the
+    whole matrix on one device."""
     r = _run_world2(case, tmp_path)
     s = _single(case, 1)
     assert int(r[0]["tol_it"]) == s["tol_it"] and bool(r[0]["tol_conv"])
