@@ -522,13 +522,21 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
           row_pair<true>(slot, sh_l, 2 * rp, rv, rs4, off, V, F, nkh2, nkl2, E, fxr, hkr, qbr);
         else
           row_pair<false>(slot, sh_l, 2 * rp, rv, rs4, off, V, F, nkh2, nkl2, E, fxr, hkr, qbr);
+#if SP_EXPER != 1
         tmem_st32(taddr + static_cast<uint32_t>(rp * 32), E);
+#else
+        if (E[0] == 12345.f) tmem_st32(taddr + static_cast<uint32_t>(rp * 32), E);
+#endif
         // warp totals of the two rows (integer sums: deterministic)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           unsigned long long sw;
           unsigned hm, lm;
+#if SP_EXPER == 5  // (timing experiment: no warp reductions)
+          sw = fxr[h] * 32; hm = hkr[h]; lm = 0;
+#else
           warp_row(fxr[h], hkr[h], sw, hm, lm);
+#endif
           const unsigned qm = static_cast<unsigned>(q0) + lm +
                               32u * __shfl_sync(0xffffffffu, qbr[h], static_cast<int>(lm));
           if (lane == 2 * rp + h) {
