@@ -295,6 +295,32 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
       "f"(v[29]), "f"(v[30]), "f"(v[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, float (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+        "=f"(v[7]), "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]),
+        "=f"(v[14]), "=f"(v[15]), "=f"(v[16]), "=f"(v[17]), "=f"(v[18]), "=f"(v[19]),
+        "=f"(v[20]), "=f"(v[21]), "=f"(v[22]), "=f"(v[23]), "=f"(v[24]), "=f"(v[25]),
+        "=f"(v[26]), "=f"(v[27]), "=f"(v[28]), "=f"(v[29]), "=f"(v[30]), "=f"(v[31])
+      : "r"(taddr)
+      : "memory");
+}
+// wait for this thread's outstanding tensor-memory loads; the registers of
+// `v` (and of any earlier load) are defined only after it
+__device__ __forceinline__ void tmem_wait_ld32(float (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]),
+                 "+f"(v[6]), "+f"(v[7]), "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]),
+                 "+f"(v[12]), "+f"(v[13]), "+f"(v[14]), "+f"(v[15]), "+f"(v[16]), "+f"(v[17]),
+                 "+f"(v[18]), "+f"(v[19]), "+f"(v[20]), "+f"(v[21]), "+f"(v[22]), "+f"(v[23]),
+                 "+f"(v[24]), "+f"(v[25]), "+f"(v[26]), "+f"(v[27]), "+f"(v[28]), "+f"(v[29]),
+                 "+f"(v[30]), "+f"(v[31])
+               :
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
@@ -400,11 +426,11 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
     if (lane == 0) {
       for (int s = 0; s < nslots; ++s) {
         mbar_init(&S.full[s], 1);
-        mbar_init(&S.empty[s], 1);
+        mbar_init(&S.empty[s], 2);  // both half-band row warps
         S.slot_band[s] = -1;
       }
       for (int s = 0; s < kTSlots; ++s) {
-        mbar_init(&S.tfull[s], 1);
+        mbar_init(&S.tfull[s], 2);  // both half-band row warps
         mbar_init(&S.tempty[s], 1);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -462,7 +488,10 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
     // reduction is amortised over 16 elements per lane; two row warps share
     // each SMSP (and TMEM lane quarter), so one's reductions and waits
     // overlap the other's exponentials.
-    const int wq = warp - kLoaders;  // bands t = wq mod 8
+    // warps w and w + 4 (same TMEM lane quarter) take rows 0-7 and 8-15 of
+    // the bands t = w mod 4, so a ring slot is held for half a band's work
+    const int wq = (warp - kLoaders) % 4;      // bands t = wq mod 4
+    const int hr = 8 * ((warp - kLoaders) / 4);  // first row of this warp's half
     bool qv[kQPL];
     float V[kQPL][4], F[kQPL][4];
 #pragma unroll
@@ -488,13 +517,13 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
       return (lane < kR && t < nb && i < A.n) ? A.rec[i].shift : 0.0f;
     };
     float sh_next = shift_of(wq);
-    for (int64_t t = wq; t < nb; t += kRowWarps) {
+    for (int64_t t = wq; t < nb; t += 4) {
       const int s = static_cast<int>(t % nslots);
       const int ts = static_cast<int>(t % kTSlots);
       const int64_t i0 = band_row0(t);
       const int rv = static_cast<int>(A.n - i0 < kR ? A.n - i0 : kR);
       const float sh_l = sh_next;
-      sh_next = shift_of(t + kRowWarps);
+      sh_next = shift_of(t + 4);
       if (t >= kTSlots) {
         mbar_wait(&S.tempty[ts], static_cast<uint32_t>((t / kTSlots - 1) & 1));
         tc_fence_after();
@@ -514,14 +543,13 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
       const uint32_t taddr = tmem_of(warp, t);
       unsigned long long my_sum = 0ull, my_key = 0ull;  // lane r: row r's warp totals
 #pragma unroll kUnroll
-      for (int rp = 0; rp < kR / 2; ++rp) {
+      for (int rp = hr / 2; rp < hr / 2 + 4; ++rp) {
         float E[32];
         unsigned long long fxr[2];
         unsigned hkr[2], qbr[2];
-        if (rv == kR)
-          row_pair<true>(slot, sh_l, 2 * rp, rv, rs4, off, V, F, nkh2, nkl2, E, fxr, hkr, qbr);
-        else
-          row_pair<false>(slot, sh_l, 2 * rp, rv, rs4, off, V, F, nkh2, nkl2, E, fxr, hkr, qbr);
+        // (rows past the matrix are zero-filled by the copy and have shift 0:
+        // their values are finite and never used -- not published, weight 0)
+        row_pair<true>(slot, sh_l, 2 * rp, rv, rs4, off, V, F, nkh2, nkl2, E, fxr, hkr, qbr);
 #if SP_EXPER != 1
         tmem_st32(taddr + static_cast<uint32_t>(rp * 32), E);
 #else
@@ -557,7 +585,7 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
       // this CTA's partial of the band's rows -> the group's global words:
       // (sum << 8) + one arrival (the sum clamped at 2^48: 255 arrivals cannot
       // carry out of the word) and the (max, quad) key
-      if (lane < rv) {
+      if (lane >= hr && lane < hr + 8 && lane < rv) {
         const unsigned long long sm = my_sum < kFixSat ? my_sum : kFixSat;
         atomicMax(tkey + i0 + lane, my_key);
         atomicAdd(sfix + i0 + lane, (sm << 8) + 1ull);
@@ -604,38 +632,20 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
         if (spins > (kSpinLimit >> 4)) __trap();
       }
       if (lane == 0) stamp(A, 4, t);
+      // the band's weights (only w gates the fold; the owner's row outputs
+      // are written after the tensor-memory slot is released)
       float w_l = 0.0f;
       bool bad = false;
-      const bool owner = (t % A.group) == k;  // band t's rows belong to CTA t mod group
+      double Sv = 1.0, wi = 0.0;
       if (present) {
-        const double Sv = static_cast<double>(sx >> 8) * scale;
+        Sv = static_cast<double>(sx >> 8) * scale;
         bad = !(Sv >= 0.25 && Sv < 1048576.0);  // outside the fixed-point range: redo
-        const double wi = rc.a / Sv;
+        wi = rc.a / Sv;
         w_l = bad ? 0.0f : static_cast<float>(wi);
-        if (owner) {
-          if (!bad) {
-            const double sc = static_cast<double>(rc.shift);
-            const double M = sc * kLn2;
-            A.rowM[i] = M;
-            A.rowS[i] = Sv;
-            A.u[i] = (rc.loga - M) - log(Sv);
-            A.wrow[i] = wi;
-            A.rowJ[i] = -1;  // base-2 max + argmax quad: from this pass's key (k_sp_prep)
-            A.aux[i] = make_float4(rc.shift, 0.0f, w_l, 0.0f);
-          }
-          // zero the other parity's words for the next launch
-          A.sfix[static_cast<int64_t>(par ^ 1u) * A.n + i] = 0ull;
-          A.tkey[static_cast<int64_t>(par ^ 1u) * A.n + i] = 0ull;
-        }
       }
-      if (owner) {  // loose rows of owned bands, in row order
-        const unsigned bm = __ballot_sync(0xffffffffu, present && bad);
-        if (present && bad)
-          A.bad_rows[list * A.cap + nbad + __popc(bm & ((1u << lane) - 1u))] = static_cast<int>(i);
-        nbad += __popc(bm);
-      }
+      const RowRec rc_t = rc;
       prefetch(t + kColWarps, sx, rc);
-      // the band's exponentials (row warp cw + 1)
+      // the band's exponentials (row warps of this lane quarter)
       mbar_wait(&S.tfull[ts], ph);
       tc_fence_after();
       if (lane == 0) stamp(A, 5, t);
@@ -668,6 +678,29 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
       if (lane == 0) stamp(A, 6, t);
 #pragma unroll
       for (int e = 0; e < 4 * kQPL; ++e) acc[e] += static_cast<double>(a32[e]);
+      // owner: the row outputs of band t and its loose rows (in row order)
+      const bool owner = (t % A.group) == k;  // band t's rows belong to CTA t mod group
+      if (owner) {
+        if (present) {
+          if (!bad) {
+            const double sc = static_cast<double>(rc_t.shift);
+            const double M = sc * kLn2;
+            A.rowM[i] = M;
+            A.rowS[i] = Sv;
+            A.u[i] = (rc_t.loga - M) - log(Sv);
+            A.wrow[i] = wi;
+            A.rowJ[i] = -1;  // base-2 max + argmax quad: from this pass's key (k_sp_prep)
+            A.aux[i] = make_float4(rc_t.shift, 0.0f, w_l, 0.0f);
+          }
+          // zero the other parity's words for the next launch
+          A.sfix[static_cast<int64_t>(par ^ 1u) * A.n + i] = 0ull;
+          A.tkey[static_cast<int64_t>(par ^ 1u) * A.n + i] = 0ull;
+        }
+        const unsigned bm = __ballot_sync(0xffffffffu, present && bad);
+        if (present && bad)
+          A.bad_rows[list * A.cap + nbad + __popc(bm & ((1u << lane) - 1u))] = static_cast<int>(i);
+        nbad += __popc(bm);
+      }
     }
     if (lane == 0) A.bad_count[list] = nbad;
     // the four column warps' partials, summed in warp order (the ring is free:
