@@ -111,7 +111,9 @@ typedef struct {
   otg_allreduce_fn allreduce; /* optional host collective (instead of NCCL) */
   void* allreduce_ctx;
   int sweep;                  /* fp32 stored cost: 0 = auto (the single-HBM-pass
-                                 sweep where it applies), 1 = the two-pass kernels */
+                                 sweep for long row-band runs, else two-pass),
+                                 1 = the two-pass kernels, 2 = the single pass
+                                 whenever its column layout applies */
 } otg_device_opts;
 
 typedef struct otg_problem_s* otg_problem;

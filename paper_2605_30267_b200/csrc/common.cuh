@@ -260,6 +260,7 @@ struct Problem {
   // band and writes one row of column partials (merge sums H + 1 rows).
   int fused = 0, fused_slots = 0, fused_smem = 0, fused_clusters = 0;
   int two_pass = 0;             // otg_device_opts.sweep == 1: never the single pass
+  int force_single_pass = 0;    // otg_device_opts.sweep == 2: single pass whenever it applies
   int sp_group = 0;             // CTAs (SMs) sharing one row band
   int sp_fix = 28;              // fixed-point scale 2^sp_fix of the row sums
   int sp_bw = 0, sp_nbox = 0;   // TMA box: chunk width (columns), chunks per slice

@@ -488,10 +488,10 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
     // reduction is amortised over 16 elements per lane; two row warps share
     // each SMSP (and TMEM lane quarter), so one's reductions and waits
     // overlap the other's exponentials.
-    // warps w and w + 4 (same TMEM lane quarter) take rows 0-7 and 8-15 of
+    // warps w and w + 4 (same TMEM lane quarter) take the two halves of
     // the bands t = w mod 4, so a ring slot is held for half a band's work
     const int wq = (warp - kLoaders) % 4;      // bands t = wq mod 4
-    const int hr = 8 * ((warp - kLoaders) / 4);  // first row of this warp's half
+    const int hr = (kR / 2) * ((warp - kLoaders) / 4);  // first row of this warp's half
     bool qv[kQPL];
     float V[kQPL][4], F[kQPL][4];
 #pragma unroll
@@ -543,7 +543,7 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
       const uint32_t taddr = tmem_of(warp, t);
       unsigned long long my_sum = 0ull, my_key = 0ull;  // lane r: row r's warp totals
 #pragma unroll kUnroll
-      for (int rp = hr / 2; rp < hr / 2 + 4; ++rp) {
+      for (int rp = hr / 2; rp < hr / 2 + kR / 4; ++rp) {
         float E[32];
         unsigned long long fxr[2];
         unsigned hkr[2], qbr[2];
@@ -585,7 +585,7 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
       // this CTA's partial of the band's rows -> the group's global words:
       // (sum << 8) + one arrival (the sum clamped at 2^48: 255 arrivals cannot
       // carry out of the word) and the (max, quad) key
-      if (lane >= hr && lane < hr + 8 && lane < rv) {
+      if (lane >= hr && lane < hr + kR / 2 && lane < rv) {
         const unsigned long long sm = my_sum < kFixSat ? my_sum : kFixSat;
         atomicMax(tkey + i0 + lane, my_key);
         atomicAdd(sfix + i0 + lane, (sm << 8) + 1ull);
@@ -818,7 +818,12 @@ bool fused_configure(Problem& P) {
   int sms = 0;
   OTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.device));
   const SpLayout L = sp_layout(P.m, sms);
-  if (!L.ok || P.n_local < 2 * kR || P.ldc % L.cw != 0) return false;
+  // the grid-wide band pipeline needs a long run of bands per group to pay
+  // for its fill (B200: 8192^2 in 9 groups of 57 bands 0.18 ms vs two-pass
+  // 0.11 ms; 2048 x 65536, 128 bands 0.27 vs 0.20; 65536^2, 4096 bands 3.5 vs 5.1)
+  const int64_t bands_per_group = ((P.n_local + kR - 1) / kR + L.H - 1) / std::max(L.H, 1);
+  if (!L.ok || P.ldc % L.cw != 0 || P.n_local < 2 * kR) return false;
+  if (bands_per_group < 512 && !P.force_single_pass) return false;
   const int64_t W = static_cast<int64_t>(L.cw) * L.nch;
   const int64_t head = ((sizeof(S1Shared) + 127) / 128) * 128;
   const int64_t slot = kR * W * 4;

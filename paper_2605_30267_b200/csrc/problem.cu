@@ -235,6 +235,7 @@ static void begin(Problem& P, int64_t n, int64_t m, const otg_device_opts* opts)
   }
   P.vshards = (opts && opts->virtual_shards > 1) ? opts->virtual_shards : 1;
   P.two_pass = (opts && opts->sweep == 1) ? 1 : 0;
+  P.force_single_pass = (opts && opts->sweep == 2) ? 1 : 0;
   if (P.vshards > P.n_local) P.vshards = static_cast<int>(P.n_local);
   P.mpad = round_up(m, 4);
   // rows padded to 128-byte multiples (aligned 16-byte loads of any quad)

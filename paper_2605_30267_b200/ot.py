@@ -236,15 +236,17 @@ class TransportProblem:
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p)
 
 
-SWEEPS = {"auto": 0, "two_pass": 1}
+SWEEPS = {"auto": 0, "two_pass": 1, "single_pass": 2}
 
 
 def _device_opts(device, world_size, rank, row_begin, row_end, nccl_unique_id, vshards,
                  allreduce=None, sweep="auto"):
     """otg_device_opts.  `allreduce`: a Python callable (buf: np.ndarray of
     float64, op: 0 SUM / 1 MAX) -> None reducing `buf` in place across the
-    ranks (instead of NCCL; e.g. dist.gloo_allreduce()).  `sweep`: "auto"
-    (the single-HBM-pass sweep where it applies) or "two_pass"."""
+    ranks (instead of NCCL; e.g. dist.gloo_allreduce()).  `sweep` (fp32 stored
+    cost): "auto" (the single-HBM-pass sweep for long runs of row bands, else
+    the two-pass kernels), "two_pass", or "single_pass" (whenever its column
+    layout applies: tests and A/B)."""
     if sweep not in SWEEPS:
         raise OtError(f"unknown sweep '{sweep}'")
     o = _capi.DeviceOpts()

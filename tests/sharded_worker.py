@@ -23,7 +23,7 @@ def instance(case):
         x, y = ot.gen_config(3, n, m, 3)
         return dict(kind="points", x=x, y=y, a=np.full(n, 1 / n), b=np.full(m, 1 / m),
                     eps=2e-2, storage="f32", norm="max", tol=1e-7, iters=60,
-                    sweep="two_pass" if case == "f32_points" else "auto")
+                    sweep="two_pass" if case == "f32_points" else "single_pass")
     if case == "otf_points":  # cfg5-shaped, cost on the fly
         n, m = 1200, 1500
         x, y = ot.gen_config(5, n, m, 5)

@@ -333,7 +333,7 @@ def test_config1_full_size_fp64_both_solvers():
 def _points_problem(n, m, seed, eps, fused):
     x, y = ot.gen_config(3, n, m, seed)
     return ot.TransportProblem.from_points(np.full(n, 1 / n), np.full(m, 1 / m), x, y, eps,
-                                           sweep="auto" if fused else "two_pass")
+                                           sweep="single_pass" if fused else "two_pass")
 
 
 @pytest.mark.parametrize("n,m", [(512, 8192), (300, 4100), (1000, 1024), (257, 65536)])

@@ -18,7 +18,7 @@ if len(sys.argv) > 1:
 for n, m, iters in sizes:
     x, y = ot.gen_config(3, n, m, 3)
     out = {}
-    for sweep in ("auto", "two_pass"):
+    for sweep in ("single_pass", "two_pass"):
         p = ot.TransportProblem.from_points(np.full(n, 1 / n), np.full(m, 1 / m), x, y, 1e-3,
                                             sweep=sweep)
         cfg = ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=iters)
@@ -26,7 +26,7 @@ for n, m, iters in sizes:
         t = ot.homotopy_solve(p, cfg, time_sweeps=True)
         out[sweep] = (r, t, p.handle.info.sweep_mode)
         p.close()
-    (ra, ta, ma), (r2, t2, m2) = out["auto"], out["two_pass"]
+    (ra, ta, ma), (r2, t2, m2) = out["single_pass"], out["two_pass"]
     dv = np.max(np.abs(ra.potentials.v - r2.potentials.v)) / max(1.0, np.max(np.abs(r2.potentials.v)))
     du = np.max(np.abs(ra.potentials.u - r2.potentials.u)) / max(1.0, np.max(np.abs(r2.potentials.u)))
     ev = ta.evaluations
