@@ -45,6 +45,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
@@ -135,21 +136,42 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 constexpr unsigned kSpinLimit = 1u << 28;
 // try_wait with a suspend-time hint: a waiting warp is parked (up to the
 // hint) instead of spinning on issue slots the row warps of its SMSP need
+#ifndef SP_SUSPEND_NS
+#define SP_SUSPEND_NS 0  // try_wait suspend-time hint (0: the instruction's default)
+#endif
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
+#if SP_SUSPEND_NS > 0
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, P1;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity), "r"(100000u)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(static_cast<unsigned>(SP_SUSPEND_NS))
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+#endif
   return ok != 0;
 }
+#ifndef SP_BACKOFF_NS
+#define SP_BACKOFF_NS 64  // sleep between failed mbarrier tests (spinning warps steal issue slots)
+#endif
+#ifndef SP_POLL_NS
+#define SP_POLL_NS 128    // sleep between polls of a band's row-sum words
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   unsigned spins = 0;
-  while (!mbar_try(bar, parity))
+  while (!mbar_try(bar, parity)) {
+    if (SP_BACKOFF_NS > 0) __nanosleep(SP_BACKOFF_NS);
     if (++spins > (kSpinLimit >> 8)) __trap();
+  }
 }
 // 3-D tensor copy (TMA) of box {cw, nch, 16} at (x, chunk, row); rows past
 // the matrix are zero-filled (and still counted in the bytes)
@@ -295,6 +317,15 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
       "f"(v[29]), "f"(v[30]), "f"(v[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16f(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
+      "f"(v[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, float (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
@@ -336,21 +367,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
       : "memory");
 }
 
-// Two rows of a band for one lane's 16 columns (quads lane + 32 kq) from the
+// K (1 or 2) rows of a band for one lane's 16 columns (quads lane + 32 kq) from the
 // smem slot (row stride rs4 float4):
 // exponents against each row's shift (bitwise the k_row_shift exponents,
 // sweep.cu quad_exponents), ex2 into E (tensor memory order: row, quad, 4),
 // the lane's fixed-point row partials (fp32 sum of its 16 elements) and the
 // (max, argmax quad) of its elements.  FULL: both rows exist (no masking).
-template <bool FULL>
+template <bool FULL, int K>
 __device__ __forceinline__ void row_pair(const float4* __restrict__ slot,
                                          float sh_l, int r0, int rv, int rs4,
                                          const int (&off)[kQPL], const float (&V)[kQPL][4],
                                          const float (&F)[kQPL][4], float2 nkh2, float2 nkl2,
-                                         float (&E)[32], unsigned long long (&fxr)[2],
-                                         unsigned (&hkr)[2], unsigned (&qbr)[2]) {
+                                         float (&E)[16 * K], unsigned long long (&fxr)[K],
+                                         unsigned (&hkr)[K], unsigned (&qbr)[K]) {
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < K; ++h) {
     const int r = r0 + h;
     const bool live = FULL || r < rv;
     const int rr = FULL ? r : (live ? r : 0);
@@ -542,38 +573,37 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
       const float4* slot = ring + s * slot_f4;
       const uint32_t taddr = tmem_of(warp, t);
       unsigned long long my_sum = 0ull, my_key = 0ull;  // lane r: row r's warp totals
-#pragma unroll kUnroll
-      for (int rp = hr / 2; rp < hr / 2 + kR / 4; ++rp) {
-        float E[32];
-        unsigned long long fxr[2];
-        unsigned hkr[2], qbr[2];
+      // this warp's rows hr .. hr + kR/2 - 1: pairs, then a single row when kR/2 is odd
+      auto fold_rows = [&](auto kk, int r) {
+        constexpr int K = decltype(kk)::value;
+        float E[16 * K];
+        unsigned long long fxr[K];
+        unsigned hkr[K], qbr[K];
         // (rows past the matrix are zero-filled by the copy and have shift 0:
         // their values are finite and never used -- not published, weight 0)
-        row_pair<true>(slot, sh_l, 2 * rp, rv, rs4, off, V, F, nkh2, nkl2, E, fxr, hkr, qbr);
-#if SP_EXPER != 1
-        tmem_st32(taddr + static_cast<uint32_t>(rp * 32), E);
-#else
-        if (E[0] == 12345.f) tmem_st32(taddr + static_cast<uint32_t>(rp * 32), E);
-#endif
-        // warp totals of the two rows (integer sums: deterministic)
+        row_pair<true, K>(slot, sh_l, r, rv, rs4, off, V, F, nkh2, nkl2, E, fxr, hkr, qbr);
+        if constexpr (K == 2)
+          tmem_st32(taddr + static_cast<uint32_t>(r * 16), E);
+        else
+          tmem_st16f(taddr + static_cast<uint32_t>(r * 16), E);
+        // warp totals of the rows (integer sums: deterministic)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < K; ++h) {
           unsigned long long sw;
           unsigned hm, lm;
-#if SP_EXPER == 5  // (timing experiment: no warp reductions)
-          sw = fxr[h] * 32; hm = hkr[h]; lm = 0;
-#else
           warp_row(fxr[h], hkr[h], sw, hm, lm);
-#endif
           const unsigned qm = static_cast<unsigned>(q0) + lm +
                               32u * __shfl_sync(0xffffffffu, qbr[h], static_cast<int>(lm));
-          if (lane == 2 * rp + h) {
+          if (lane == r + h) {
             my_sum = sw;
             // (max, quad) as one ordered word: ties resolve to the lower quad
             my_key = (static_cast<unsigned long long>(hm) << 32) | ~qm;
           }
         }
-      }
+      };
+#pragma unroll kUnroll
+      for (int rr = 0; rr + 1 < kR / 2; rr += 2) fold_rows(std::integral_constant<int, 2>{}, hr + rr);
+      if constexpr ((kR / 2) % 2 == 1) fold_rows(std::integral_constant<int, 1>{}, hr + kR / 2 - 1);
       // the slot's cost rows are no longer needed
       if (lane == 0) stamp(A, 7, t);
       __syncwarp();
@@ -627,7 +657,7 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
       for (unsigned spins = 0;; ++spins) {
         const bool done = !present || (sx & 0xffull) >= static_cast<unsigned long long>(A.group);
         if (__all_sync(0xffffffffu, done)) break;
-        __nanosleep(32);
+        __nanosleep(SP_POLL_NS);
         if (!done) sx = ld_relaxed64(sfix + i);
         if (spins > (kSpinLimit >> 4)) __trap();
       }
