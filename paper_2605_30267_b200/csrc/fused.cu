@@ -166,6 +166,9 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 #ifndef SP_POLL_NS
 #define SP_POLL_NS 128    // sleep between polls of a band's row-sum words
 #endif
+#ifndef SP_FOLD_PIPE
+#define SP_FOLD_PIPE 0  // column fold: next row's tensor-memory load in flight during the FMAs
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   unsigned spins = 0;
   while (!mbar_try(bar, parity)) {
@@ -325,6 +328,24 @@ __device__ __forceinline__ void tmem_st16f(uint32_t taddr, const float (&v)[16])
       "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
       "f"(v[15])
       : "memory");
+}
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, float (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+        "=f"(v[7]), "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]),
+        "=f"(v[14]), "=f"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld16(float (&v)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]),
+                 "+f"(v[6]), "+f"(v[7]), "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]),
+                 "+f"(v[12]), "+f"(v[13]), "+f"(v[14]), "+f"(v[15])
+               :
+               : "memory");
 }
 __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, float (&v)[32]) {
   asm volatile(
@@ -683,6 +704,39 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
       float a32[4 * kQPL];
 #pragma unroll
       for (int e = 0; e < 4 * kQPL; ++e) a32[e] = 0.0f;
+#if SP_FOLD_PIPE
+      // one row (16 columns) per tensor-memory load, the next row's load in
+      // flight while this one is folded (tcgen05.wait::ld waits for all of
+      // this thread's loads: only one is outstanding at each wait)
+      {
+        float Ea[16], Eb[16];
+        auto fold16 = [&](const float (&E)[16], int r) {
+          const float wr = __shfl_sync(0xffffffffu, w_l, r);
+          if (wr != 0.0f) {  // uniform over the warp (one row); 0 = loose or absent row
+            const float2 w2 = make_float2(wr, wr);
+#pragma unroll
+            for (int e = 0; e < 4 * kQPL; e += 2) {
+              const float2 r2 = __ffma2_rn(make_float2(E[e], E[e + 1]), w2,
+                                           make_float2(a32[e], a32[e + 1]));
+              a32[e] = r2.x;
+              a32[e + 1] = r2.y;
+            }
+          }
+        };
+        tmem_ld16_nowait(taddr, Ea);
+#pragma unroll
+        for (int r = 0; r < kR; r += 2) {
+          tmem_wait_ld16(Ea);
+          if (r + 1 < kR) tmem_ld16_nowait(taddr + static_cast<uint32_t>((r + 1) * 16), Eb);
+          fold16(Ea, r);
+          if (r + 1 < kR) {
+            tmem_wait_ld16(Eb);
+            if (r + 2 < kR) tmem_ld16_nowait(taddr + static_cast<uint32_t>((r + 2) * 16), Ea);
+            fold16(Eb, r + 1);
+          }
+        }
+      }
+#else
 #pragma unroll 2
       for (int rp = 0; rp < kR / 2; ++rp) {
         float E[32];
@@ -702,6 +756,7 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
           }
         }
       }
+#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.tempty[ts]);
