@@ -32,6 +32,9 @@
 #ifndef OTG_ROW_PF
 #define OTG_ROW_PF -1        // row-pass L2 prefetch (-1 = auto)
 #endif
+#ifndef OTG_FIN_SORTED_FB
+#define OTG_FIN_SORTED_FB 0  // k_finalize's folded fallback: column-sorted work items (32 KB smem)
+#endif
 #ifndef OTG_EPI_FUSED
 #define OTG_EPI_FUSED 0      // one-kernel epilogue with grid barriers (measured slower)
 #endif

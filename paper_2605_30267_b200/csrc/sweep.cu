@@ -138,6 +138,32 @@ __device__ double block_max(double v, double* sh) {
   return r;
 }
 
+// NS sums then NM maxima in one pass (two barriers instead of two per value);
+// each value reduced exactly as block_sum / block_max would (same shuffle
+// tree, same warp order), so results are bitwise those of separate calls.
+template <int NT, int NS, int NM>
+__device__ void block_multi(double (&v)[NS + NM], double* shm /* NT / 32 * (NS + NM) */) {
+  constexpr int N = NS + NM, W = NT / 32;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) v[q] = warp_sum(v[q]);
+#pragma unroll
+  for (int q = NS; q < N; ++q) v[q] = warp_max(v[q]);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) shm[q * W + w] = v[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    double r = q < NS ? 0.0 : -DBL_MAX;
+#pragma unroll
+    for (int k = 0; k < W; ++k) r = q < NS ? r + shm[q * W + k] : fmax(r, shm[q * W + k]);
+    v[q] = r;
+  }
+}
+
 // Exact fp32 -> fp64 with integer ops (ALU pipe, no F2F on the XU pipe).
 // Normal and zero inputs map exactly except +-0 and subnormals, which land
 // within 2^-126 of their value (|error| < 1.2e-38; irrelevant for a cost).
@@ -205,18 +231,74 @@ k_row_precise(const double* __restrict__ C, int64_t ldc, int64_t n, int64_t m,
   const int64_t i = static_cast<int64_t>(blockIdx.x) * RPB + sub;
   const bool valid = i < n;
   const double* Ci = C + (valid ? i : 0) * ldc;
+  // the thread's first kRC exponents stay in registers (all loads in flight;
+  // cfg1, 1000^2 with G = 128: the whole row); longer rows stream the rest in
+  // kRC-wide chunks.  Sums in column order per thread, as the plain loop.
+  constexpr int kRC = 8;
+  double t0[kRC];
+#pragma unroll
+  for (int k = 0; k < kRC; ++k) {
+    const int64_t j = lane + static_cast<int64_t>(k) * G;
+    t0[k] = (valid && j < m) ? (-Ci[j]) + p[j] : -INFINITY;
+  }
   double mx = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < kRC; ++k) mx = fmax(mx, t0[k]);
   if (valid)
-    for (int64_t j = lane; j < m; j += G) mx = fmax(mx, (-Ci[j]) + p[j]);
+    for (int64_t j0 = lane + kRC * G; j0 < m; j0 += kRC * G) {
+      double t[kRC];
+#pragma unroll
+      for (int k = 0; k < kRC; ++k) {
+        const int64_t j = j0 + static_cast<int64_t>(k) * G;
+        t[k] = j < m ? (-Ci[j]) + p[j] : -INFINITY;
+      }
+#pragma unroll
+      for (int k = 0; k < kRC; ++k) mx = fmax(mx, t[k]);
+    }
+  auto row_sum = [&](double mxr) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < kRC; ++k)
+      if (lane + static_cast<int64_t>(k) * G < m) acc += exp(t0[k] - mxr);
+    for (int64_t j0 = lane + kRC * G; j0 < m; j0 += kRC * G) {
+      double t[kRC];
+#pragma unroll
+      for (int k = 0; k < kRC; ++k) {
+        const int64_t j = j0 + static_cast<int64_t>(k) * G;
+        t[k] = j < m ? (-Ci[j]) + p[j] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < kRC; ++k)
+        if (j0 + static_cast<int64_t>(k) * G < m) acc += exp(t[k] - mxr);
+    }
+    return acc;
+  };
   double s = 0.0;
   if (G == 32) {
     mx = warp_max(mx);
-    if (valid)
-      for (int64_t j = lane; j < m; j += G) s += exp(((-Ci[j]) + p[j]) - mx);
+    if (valid) s = row_sum(mx);
     s = warp_sum(s);
+  } else if (G < kRowThreads) {
+    // G / 32 warps per row: shuffle trees, then the group's warps in order
+    constexpr int WG = G / 32;
+    const int w0 = sub * WG;
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    mx = -DBL_MAX;
+#pragma unroll
+    for (int k = 0; k < WG; ++k) mx = fmax(mx, sh[w0 + k]);
+    if (valid) s = row_sum(mx);
+    s = warp_sum(s);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    s = 0.0;
+#pragma unroll
+    for (int k = 0; k < WG; ++k) s += sh[w0 + k];
   } else {
     mx = block_max<kRowThreads>(mx, sh);
-    for (int64_t j = lane; j < m; j += G) s += exp(((-Ci[j]) + p[j]) - mx);
+    s = row_sum(mx);
     s = block_sum<kRowThreads>(s, sh);
   }
   if (lane == 0) {
@@ -1418,43 +1500,49 @@ __device__ __forceinline__ void merge_body(const double* __restrict__ part, int 
                                            const double* __restrict__ u,
                                            const double* __restrict__ a, int64_t nrows,
                                            int do_merge, int flag, Ctrl* __restrict__ ctrl,
-                                           int blk, int nblk, double* sh, int fused_rows) {
+                                           int blk, int nblk, double* sh, int fused_rows,
+                                           int ua_n) {
   // single-pass steady state: the cluster partials + the patch row
   if (fused_rows && ctrl->shift_valid) {
     nshards = 1;
     splits = fused_rows;
   }
-  if (do_merge) {  // <u, a> over the local rows (for f)
-    const int64_t r0 = nrows * blk / nblk, r1 = nrows * (blk + 1) / nblk;
+  if (do_merge && blk < ua_n) {  // <u, a> over the local rows (for f): slice blk of ua_n
+    const int64_t r0 = nrows * blk / ua_n, r1 = nrows * (blk + 1) / ua_n;
     double t = 0.0;
     for (int64_t k = r0 + threadIdx.x; k < r1; k += kEThreads) t += u[k] * a[k];
     t = block_sum<kEThreads>(t, sh);
     if (threadIdx.x == 0) col[mpad + 1 + blk] = t;
   }
   const double tiny = ctrl->tiny;
-  for (int64_t j = static_cast<int64_t>(blk) * kEThreads + threadIdx.x; j < m;
-       j += static_cast<int64_t>(nblk) * kEThreads) {
+  // groups of 32 columns: warp w sums the splits k = w (mod 8) of the group
+  // (coalesced 256-byte rows, 8 loads in flight per column), warp 0 folds
+  // the 8 chains -- the same tree as one thread per column with 8 chains
+  __shared__ double chain[kEThreads / 32][32];
+  static_assert(kEThreads == 256, "8 chains = 8 warps");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t grp = blk; grp * 32 < m; grp += nblk) {
+    const int64_t j = grp * 32 + lane;
+    const bool in = j < m;
     double c = 0.0;
     if (do_merge) {
       for (int s = 0; s < nshards; ++s) {
-        // 8 independent chains keep 8 loads in flight (the splits are
-        // L2-resident; a single chain is latency-bound), folded in fixed order
-        const double* src = part + static_cast<int64_t>(s) * splits * mpad + j;
-        double l8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        int k = 0;
-        for (; k + 8 <= splits; k += 8) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) l8[e] += src[static_cast<int64_t>(k + e) * mpad];
-        }
-        for (int e = 0; k < splits; ++k, ++e) l8[e] += src[static_cast<int64_t>(k) * mpad];
-        const double loc = ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
-        c += loc;
+        const double* src = part + static_cast<int64_t>(s) * splits * mpad + (in ? j : 0);
+        double l = 0.0;
+        if (in)
+          for (int k = w; k < splits; k += 8) l += src[static_cast<int64_t>(k) * mpad];
+        chain[w][lane] = l;
+        __syncthreads();
+        if (w == 0)
+          c += ((chain[0][lane] + chain[1][lane]) + (chain[2][lane] + chain[3][lane])) +
+               ((chain[4][lane] + chain[5][lane]) + (chain[6][lane] + chain[7][lane]));
+        __syncthreads();
       }
-      col[j] = c;
-    } else {
+      if (w == 0 && in) col[j] = c;
+    } else if (w == 0 && in) {
       c = col[j];  // already merged (and all-reduced across ranks)
     }
-    if (flag) {
+    if (flag && w == 0 && in) {
       if (c >= tiny) {
         col_log[j] = log(c);
         flag_idx[j] = -1;
@@ -1471,12 +1559,13 @@ __global__ void __launch_bounds__(kEThreads)
 k_merge(const double* __restrict__ part, int nshards, int splits, int64_t m, int64_t mpad,
         double* __restrict__ col, double* __restrict__ col_log, int* __restrict__ flag_idx,
         int* __restrict__ fb_cols, const double* __restrict__ u, const double* __restrict__ a,
-        int64_t nrows, int do_merge, int flag, Ctrl* __restrict__ ctrl, int fused_rows) {
+        int64_t nrows, int do_merge, int flag, Ctrl* __restrict__ ctrl, int fused_rows,
+        int ua_n) {
   pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done) return;
   __shared__ double sh[kEThreads / 32];
   merge_body(part, nshards, splits, m, mpad, col, col_log, flag_idx, fb_cols, u, a, nrows,
-             do_merge, flag, ctrl, blockIdx.x, gridDim.x, sh, fused_rows);
+             do_merge, flag, ctrl, blockIdx.x, gridDim.x, sh, fused_rows, ua_n);
 }
 
 // ------------------------------------------------------------------ K5 ----
@@ -1545,8 +1634,8 @@ template <bool PRECISE, bool OTF>
 __device__ __forceinline__ void fallback_sorted_body(
     const double* __restrict__ C64, const CostSrc& src, int64_t ldc, int64_t n, double kappa,
     const double* __restrict__ u, const double* __restrict__ p, const int* __restrict__ fb_cols,
-    double2* __restrict__ fb_part, unsigned nf) {
-  __shared__ int2 skey[kFbSortMax];  // (column, slot), sorted by column
+    double2* __restrict__ fb_part, unsigned nf, int2* skey /* shared, kFbSortMax */) {
+  // skey: (column, slot), sorted by column
   int P2 = 1;
   while (P2 < static_cast<int>(nf)) P2 <<= 1;
   for (int k = threadIdx.x; k < P2; k += kEThreads)
@@ -1614,7 +1703,8 @@ k_fallback(const double* __restrict__ C64, const CostSrc src, int64_t ldc, int64
   const unsigned nf = ctrl->fb_count;
   if (nf == 0) return;
   if (nf >= 2 * kEThreads && nf <= kFbSortMax) {
-    fallback_sorted_body<PRECISE, OTF>(C64, src, ldc, n, kappa, u, p, fb_cols, fb_part, nf);
+    __shared__ int2 skey[kFbSortMax];
+    fallback_sorted_body<PRECISE, OTF>(C64, src, ldc, n, kappa, u, p, fb_cols, fb_part, nf, skey);
     return;
   }
   __shared__ double sh[kEThreads / 32];
@@ -1833,64 +1923,85 @@ struct FinArgs {
   double* e1_part;
   double* trace;
   double* bounds;
+  // the exact column LSE of flagged columns, folded into k_finalize when the
+  // handle is not sharded (fold_fb): K5's inputs
+  int fold_fb;
+  int storage;
+  const double* C64;
+  CostSrc src;
+  int64_t ldc, nrows;
+  double kappa;
+  const double* u;
+  const int* fb_cols;
+  double2* fb_part_w;
 };
 
 // Per-column finalize of work unit blk of nblk; its partials -> e1_part[blk].
-__device__ __forceinline__ void finalize_cols(const FinArgs& A, int blk, int nblk, double* sh) {
+// One column (after the merge): the exact LSE of a flagged column from the
+// fallback partials, grad, y and the column's share of the E1 sums.
+struct E1Acc {
   double s_abs = 0.0, s_y = 0.0, s_pb = 0.0, mx_p = 0.0, bad = 0.0;
-  for (int64_t j = static_cast<int64_t>(blk) * kEThreads + threadIdx.x; j < A.m;
-       j += static_cast<int64_t>(nblk) * kEThreads) {
-    double c = A.col[j], cl;
-    const int slot = A.flag_idx[j];
-    if (slot >= 0) {
-      double top, s;
-      if (A.sharded) {  // combined across ranks (k_fb_local / k_fb_rescale + all-reduces)
-        top = A.fbA[j];
-        s = A.fbS[j];
-      } else {
-        top = -INFINITY;
-        for (int k = 0; k < kFbChunks; ++k) top = fmax(top, A.fb_part[slot * kFbChunks + k].x);
-        s = 0.0;
-        for (int k = 0; k < kFbChunks; ++k) {
-          const double2 fp = A.fb_part[slot * kFbChunks + k];
-          if (fp.y > 0.0) s += fp.y * exp(fp.x - top);
-        }
-      }
-      cl = top + log(s);
-      c = exp(cl);
-      A.col[j] = c;
-      A.col_log[j] = cl;
+};
+__device__ __forceinline__ void finalize_col(const FinArgs& A, int64_t j, int slot, E1Acc& e) {
+  double c = A.col[j], cl;
+  if (slot >= 0) {
+    double top, s;
+    if (A.sharded) {  // combined across ranks (k_fb_local / k_fb_rescale + all-reduces)
+      top = A.fbA[j];
+      s = A.fbS[j];
     } else {
-      cl = A.col_log[j];
+      top = -INFINITY;
+      for (int k = 0; k < kFbChunks; ++k) top = fmax(top, A.fb_part[slot * kFbChunks + k].x);
+      s = 0.0;
+      for (int k = 0; k < kFbChunks; ++k) {
+        const double2 fp = A.fb_part[slot * kFbChunks + k];
+        if (fp.y > 0.0) s += fp.y * exp(fp.x - top);
+      }
     }
-    if (!isfinite(cl)) bad = 1.0;
-    const double g = c - A.b[j];
-    A.grad[j] = g;
-    const double pj = A.p[j];
-    const double yj = pj + (A.logb[j] - cl);
-    A.y[j] = yj;
-    s_abs += fabs(g);
-    s_y += yj;
-    s_pb += pj * A.b[j];
-    mx_p = fmax(mx_p, fabs(pj));
+    cl = top + log(s);
+    c = exp(cl);
+    A.col[j] = c;
+    A.col_log[j] = cl;
+  } else {
+    cl = A.col_log[j];
   }
-  s_abs = block_sum<kEThreads>(s_abs, sh);
-  s_y = block_sum<kEThreads>(s_y, sh);
-  s_pb = block_sum<kEThreads>(s_pb, sh);
-  mx_p = block_max<kEThreads>(mx_p, sh);
-  bad = block_max<kEThreads>(bad, sh);
+  if (!isfinite(cl)) e.bad = 1.0;
+  const double g = c - A.b[j];
+  A.grad[j] = g;
+  const double pj = A.p[j];
+  const double yj = pj + (A.logb[j] - cl);
+  A.y[j] = yj;
+  e.s_abs += fabs(g);
+  e.s_y += yj;
+  e.s_pb += pj * A.b[j];
+  e.mx_p = fmax(e.mx_p, fabs(pj));
+}
+
+__device__ __forceinline__ void store_e1(const FinArgs& A, int part, E1Acc& e, double* shm) {
+  double v[5] = {e.s_abs, e.s_y, e.s_pb, e.mx_p, e.bad};
+  block_multi<kEThreads, 3, 2>(v, shm);
   if (threadIdx.x == 0) {
-    double* dst = A.e1_part + blk * 8;
-    dst[0] = s_abs;
-    dst[1] = s_y;
-    dst[2] = s_pb;
-    dst[3] = mx_p;
-    dst[4] = bad;
+    double* dst = A.e1_part + part * 8;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) dst[q] = v[q];
   }
 }
 
-// One CTA folds the nparts partials (all threads, fixed order) and its thread
-// 0 runs the solver's scalar control flow.
+// Per-column finalize of work unit blk of nblk; its partials -> e1_part[blk].
+// defer: flagged columns are left to the last CTA (their fallback partials
+// are complete only once every CTA has run its share of the fallback).
+__device__ __forceinline__ void finalize_cols(const FinArgs& A, int blk, int nblk, double* shm,
+                                              bool defer = false) {
+  E1Acc e;
+  for (int64_t j = static_cast<int64_t>(blk) * kEThreads + threadIdx.x; j < A.m;
+       j += static_cast<int64_t>(nblk) * kEThreads) {
+    const int slot = A.flag_idx[j];
+    if (defer && slot >= 0) continue;
+    finalize_col(A, j, slot, e);
+  }
+  store_e1(A, blk, e, shm);
+}
+
 __device__ __forceinline__ void finalize_tail(const FinArgs& A, int nparts, double* sh,
                                               Ctrl* __restrict__ ctrl) {
   double gl = 0.0, sy = 0.0, pb = 0.0, mp = 0.0, bd = 0.0;
@@ -1902,14 +2013,18 @@ __device__ __forceinline__ void finalize_tail(const FinArgs& A, int nparts, doub
     mp = fmax(mp, src[3]);
     bd = fmax(bd, src[4]);
   }
-  gl = block_sum<kEThreads>(gl, sh);
-  sy = block_sum<kEThreads>(sy, sh);
-  pb = block_sum<kEThreads>(pb, sh);
-  mp = block_max<kEThreads>(mp, sh);
-  bd = block_max<kEThreads>(bd, sh);
   double ua = 0.0;  // <u, a> partials of the merge work units (col[mpad + 1 + k])
   for (int k = threadIdx.x; k < A.ua_slices; k += kEThreads) ua += A.col[A.mpad + 1 + k];
-  ua = block_sum<kEThreads>(ua, sh);
+  {
+    double v[6] = {gl, sy, pb, ua, mp, bd};
+    block_multi<kEThreads, 4, 2>(v, sh);
+    gl = v[0];
+    sy = v[1];
+    pb = v[2];
+    ua = v[3];
+    mp = v[4];
+    bd = v[5];
+  }
   if (threadIdx.x != 0) return;
   Ctrl* C = ctrl;
   C->e1_counter = 0;
@@ -1929,13 +2044,40 @@ __device__ __forceinline__ void finalize_tail(const FinArgs& A, int nparts, doub
   control_step(C, A.trace, A.bounds, gl, f);
 }
 
-__global__ void __launch_bounds__(kEThreads)
+template <bool PRECISE, bool OTF>
+__device__ __forceinline__ void fallback_all(const FinArgs& A, unsigned nf, double* sh,
+                                             int2* skey) {
+  if (skey && nf >= 2 * kEThreads && nf <= kFbSortMax)
+    fallback_sorted_body<PRECISE, OTF>(A.C64, A.src, A.ldc, A.nrows, A.kappa, A.u, A.p, A.fb_cols,
+                                       A.fb_part_w, nf, skey);
+  else
+    fallback_body<PRECISE, OTF>(A.C64, A.src, A.ldc, A.nrows, A.kappa, A.u, A.p, A.fb_cols,
+                                A.fb_part_w, nf, blockIdx.x, gridDim.x, sh);
+}
+
+__global__ void __launch_bounds__(kEThreads, 2)
 k_finalize(const FinArgs A, Ctrl* __restrict__ ctrl) {
   pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done) return;
-  __shared__ double sh[kEThreads / 32];
+  __shared__ double sh[kEThreads / 32 * 8];
   __shared__ bool last;
-  finalize_cols(A, blockIdx.x, gridDim.x, sh);
+  // K5 folded in (unsharded): every CTA takes its share of the flagged
+  // columns' exact LSE, the last CTA finalizes those columns
+  const unsigned nf = A.fold_fb ? ctrl->fb_count : 0u;
+  if (nf > 0) {
+#if OTG_FIN_SORTED_FB
+    __shared__ int2 skey[kFbSortMax];
+#else
+    int2* skey = nullptr;  // (unsorted work items only: no 32 KB static buffer)
+#endif
+    if (A.storage == OTG_STORE_F64)
+      fallback_all<true, false>(A, nf, sh, skey);
+    else if (A.storage == OTG_STORE_ON_THE_FLY)
+      fallback_all<false, true>(A, nf, sh, skey);
+    else
+      fallback_all<false, false>(A, nf, sh, skey);
+  }
+  finalize_cols(A, blockIdx.x, gridDim.x, sh, nf > 0);
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned prev = atomicAdd(&ctrl->e1_counter, 1u);
@@ -1944,7 +2086,18 @@ k_finalize(const FinArgs A, Ctrl* __restrict__ ctrl) {
   __syncthreads();
   if (!last) return;
   __threadfence();
-  finalize_tail(A, gridDim.x, sh, ctrl);
+  int parts = gridDim.x;
+  if (nf > 0) {  // the flagged columns, in list order: one more partial
+    E1Acc e;
+    for (unsigned f = threadIdx.x; f < nf; f += kEThreads) {
+      const int64_t j = A.fb_cols[f];
+      finalize_col(A, j, static_cast<int>(f), e);
+    }
+    store_e1(A, parts, e, sh);
+    __syncthreads();
+    ++parts;
+  }
+  finalize_tail(A, parts, sh, ctrl);
 }
 
 // ------------------------------------------------------------------ E2 ----
@@ -2061,22 +2214,22 @@ __device__ __forceinline__ void apply_cols(const AppArgs& A, const Ctrl* ctrl_in
       }
     }
   }
-  if (stab) {
-    c1 = block_sum<kEThreads>(c1, sh);
-    br = block_sum<kEThreads>(br, sh);
-    c2 = block_sum<kEThreads>(c2, sh);
-    qq = block_sum<kEThreads>(qq, sh);
-    drift = block_max<kEThreads>(drift, sh);
-    ginf = block_max<kEThreads>(ginf, sh);
-    dom = block_max<kEThreads>(dom, sh);
-  }
-  dstep = block_max<kEThreads>(dstep, sh);
-  if (refq) {
-    qe = block_sum<kEThreads>(qe, sh);
-    qx = block_sum<kEThreads>(qx, sh);
-    qy = block_sum<kEThreads>(qy, sh);
-    qb = block_sum<kEThreads>(qb, sh);
-    domr = block_max<kEThreads>(domr, sh);
+  {  // (unused quantities stay 0 / -inf: reduced anyway, in one pass)
+    double v[13] = {c1, br, c2, qq, qe, qx, qy, qb, drift, ginf, dom, dstep, domr};
+    block_multi<kEThreads, 8, 5>(v, sh);
+    c1 = v[0];
+    br = v[1];
+    c2 = v[2];
+    qq = v[3];
+    qe = v[4];
+    qx = v[5];
+    qy = v[6];
+    qb = v[7];
+    drift = v[8];
+    ginf = v[9];
+    dom = v[10];
+    dstep = v[11];
+    domr = v[12];
   }
   if (threadIdx.x == 0) {
     double* dst = A.e2_part + blk * kE2;
@@ -2116,14 +2269,13 @@ __device__ __forceinline__ void apply_tail(const AppArgs& A, int nparts, double*
       t[12] = fmax(t[12], src[12]);
     }
   }
-  if (stab) {
-    for (int q = 0; q < 4; ++q) t[q] = block_sum<kEThreads>(t[q], sh);
-    for (int q = 4; q < 7; ++q) t[q] = block_max<kEThreads>(t[q], sh);
-  }
-  t[7] = block_max<kEThreads>(t[7], sh);
-  if (refq) {
-    for (int q = 8; q < 12; ++q) t[q] = block_sum<kEThreads>(t[q], sh);
-    t[12] = block_max<kEThreads>(t[12], sh);
+  {
+    double v[13] = {t[0], t[1], t[2], t[3], t[8], t[9], t[10], t[11], t[4], t[5], t[6], t[7], t[12]};
+    block_multi<kEThreads, 8, 5>(v, sh);
+    for (int q = 0; q < 4; ++q) t[q] = v[q];
+    for (int q = 8; q < 12; ++q) t[q] = v[q - 4];
+    for (int q = 4; q < 8; ++q) t[q] = v[q + 4];
+    t[12] = v[12];
   }
   if (threadIdx.x != 0) return;
   Ctrl* C = ctrl;
@@ -2180,11 +2332,11 @@ __device__ __forceinline__ void apply_tail(const AppArgs& A, int nparts, double*
   C->live_e2 = 0;
 }
 
-__global__ void __launch_bounds__(kEThreads)
+__global__ void __launch_bounds__(kEThreads, 2)
 k_apply(const AppArgs A, Ctrl* __restrict__ ctrl) {
   pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (!ctrl->live_e2) return;
-  __shared__ double sh[kEThreads / 32];
+  __shared__ double sh[kEThreads / 32 * 16];
   __shared__ bool last;
   apply_cols(A, ctrl, blockIdx.x, gridDim.x, sh);
   if (threadIdx.x == 0) {
@@ -2245,11 +2397,11 @@ __global__ void __launch_bounds__(kEThreads)
 k_epilogue(const EpiArgs E, Ctrl* __restrict__ ctrl) {
   pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done) return;  // uniform: written by an earlier launch
-  __shared__ double sh[kEThreads / 32];
+  __shared__ double sh[kEThreads / 32 * 16];
   const int blk = blockIdx.x, nblk = gridDim.x;
   merge_body(E.part, E.nshards, E.splits, E.F.m, E.F.mpad, E.F.col, E.F.col_log,
              const_cast<int*>(E.F.flag_idx), E.fb_cols, E.u, E.a, E.nrows, 1, 1, ctrl, blk, nblk,
-             sh, E.fused_rows);
+             sh, E.fused_rows, nblk);
   grid_sync(ctrl);
   const unsigned nf = *static_cast<volatile unsigned*>(&ctrl->fb_count);
   if (nf > 0) {
@@ -2327,7 +2479,13 @@ void configure_sweeps(Problem& P) {
   // (<= 64 partial rows: the merge reads every split of every column, so past
   // that the merge costs more than the column grid gains -- cfg2, 8192^2:
   // 92 splits 8.38 K it/s, 64 splits 8.51 K it/s)
-  const int64_t max_splits = std::max<int64_t>(1, std::min<int64_t>(64, (shard_rows + 63) / 64));
+  // fp64 (precise exp, latency-bound): small problems need the splits for
+  // parallelism -- cfg1, 1000^2: 8 column blocks x 16 splits of 63 rows left
+  // half the SMs idle (20.8 us); >= 8 rows per split, <= 256 splits
+  const int64_t max_splits =
+      P.storage == OTG_STORE_F64
+          ? std::max<int64_t>(1, std::min<int64_t>(256, (shard_rows + 7) / 8))
+          : std::max<int64_t>(1, std::min<int64_t>(64, (shard_rows + 63) / 64));
   int64_t splits = 1;
   if (env_s > 0) {
     splits = env_s;
@@ -2383,9 +2541,16 @@ static CostSrc cost_src(const Problem& P) {
   return s;
 }
 
+// threads per row of the fp64 row pass: one warp for short rows, four warps
+// up to 16384 columns (cfg1, 1000^2: 2 rows per CTA, 500 CTAs, ~8 exps per
+// thread instead of 31), the whole CTA beyond
+static int precise_row_group(const Problem& P) {
+  return P.m <= 256 ? 32 : P.m <= 16384 ? 128 : kRowThreads;
+}
+
 int64_t row_blocks(const Problem& P) {
   if (P.storage == OTG_STORE_F64) {
-    const int G = P.m <= 2048 ? 32 : kRowThreads;
+    const int G = precise_row_group(P);
     const int64_t rpb = kRowThreads / G;
     return (P.n_local + rpb - 1) / rpb;
   }
@@ -2405,10 +2570,15 @@ static unsigned resident_grid(const Problem& P, K kernel, int64_t blocks) {
 
 void launch_row_pass(Problem& P) {
   const int64_t blocks = row_blocks(P);
-  double* rowpart = P.e1_part + P.e_blocks * 8;  // scratch after the E1 partials
+  double* rowpart = P.e1_part + (P.e_blocks + 1) * 8;  // scratch after the E1 partials
   if (P.storage == OTG_STORE_F64) {
-    if (P.m <= 2048)
+    const int G = precise_row_group(P);
+    if (G == 32)
       launch_k(k_row_precise<32>, blocks, kRowThreads, 0, P.stream, 
+          P.C64, P.ldc, P.n_local, P.m, P.p, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, rowpart,
+          P.ctrl);
+    else if (G == 128)
+      launch_k(k_row_precise<128>, blocks, kRowThreads, 0, P.stream, 
           P.C64, P.ldc, P.n_local, P.m, P.p, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, rowpart,
           P.ctrl);
     else
@@ -2540,14 +2710,18 @@ int partial_rows(const Problem& P) { return P.vshards * P.col_splits; }
 
 int64_t merge_blocks(const Problem& P) { return (P.m + kEThreads - 1) / kEThreads; }
 
+// k_merge CTAs: 32 columns each (<u, a> slices: the first merge_blocks(P))
+static unsigned merge_grid(const Problem& P) { return static_cast<unsigned>((P.m + 31) / 32); }
+
 static void launch_merge(Problem& P, bool merge, bool flag) {
-  const int64_t blocks = merge_blocks(P);
+  const unsigned blocks = merge_grid(P);
   const int shards = P.vshards;
   const int splits = P.col_splits;
   launch_k(k_merge, blocks, kEThreads, 0, P.stream, P.part, shards, splits, P.m, P.mpad, P.col,
                                               P.col_log, P.flag_idx, P.fb_cols, P.u, P.a,
                                               P.n_local, merge ? 1 : 0, flag ? 1 : 0, P.ctrl,
-                                              P.fused ? P.fused_clusters + 1 : 0);
+                                              P.fused ? P.fused_clusters + 1 : 0,
+                                              static_cast<int>(merge_blocks(P)));
   OTG_CUDA(cudaGetLastError());
 }
 
@@ -2555,9 +2729,9 @@ void launch_merge_nolog(Problem& P) { launch_merge(P, true, false); }
 
 // Local merge (no flagging) into `dst` (the sharded all-reduce's send buffer).
 static void launch_merge_into(Problem& P, double* dst) {
-  launch_k(k_merge, merge_blocks(P), kEThreads, 0, P.stream, P.part, P.vshards, P.col_splits,
+  launch_k(k_merge, merge_grid(P), kEThreads, 0, P.stream, P.part, P.vshards, P.col_splits,
            P.m, P.mpad, dst, P.col_log, P.flag_idx, P.fb_cols, P.u, P.a, P.n_local, 1, 0,
-           P.ctrl, P.fused ? P.fused_clusters + 1 : 0);
+           P.ctrl, P.fused ? P.fused_clusters + 1 : 0, static_cast<int>(merge_blocks(P)));
   OTG_CUDA(cudaGetLastError());
 }
 
@@ -2598,6 +2772,16 @@ static FinArgs fin_args(const Problem& P, int64_t ua_slices) {
   A.e1_part = P.e1_part;
   A.trace = P.trace;
   A.bounds = P.bounds;
+  A.fold_fb = P.sharded ? 0 : 1;
+  A.storage = P.storage;
+  A.C64 = P.C64;
+  A.src = cost_src(P);
+  A.ldc = P.ldc;
+  A.nrows = P.n_local;
+  A.kappa = P.kappa;
+  A.u = P.u;
+  A.fb_cols = P.fb_cols;
+  A.fb_part_w = P.fb_part;
   return A;
 }
 
@@ -2710,6 +2894,13 @@ void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
 // of flagged columns (sharded: local (top, sum) per column, MAX then SUM
 // all-reduce), then finalize.
 void launch_fallback_and_finalize(Problem& P) {
+  if (!P.sharded) {
+    // K5 runs inside k_finalize (fin_args: fold_fb) -- no separate launch
+    launch_k(k_finalize, P.e_blocks, kEThreads, 0, P.stream, fin_args(P, merge_blocks(P)), P.ctrl);
+    OTG_CUDA(cudaGetLastError());
+    P.apply_pending = 1;
+    return;
+  }
   if (P.storage == OTG_STORE_F64)
     launch_k(k_fallback<true, false>, 296, kEThreads, 0, P.stream, 
         P.C64, cost_src(P), P.ldc, P.n_local, P.kappa, P.u, P.p, P.fb_cols, P.fb_part, P.ctrl);
