@@ -1575,7 +1575,7 @@ k_merge(const double* __restrict__ part, int nshards, int splits, int64_t m, int
 // loads in flight (the column is strided in memory, so the item is latency-
 // bound, not bandwidth-bound), keeps an online (max, sum) and the CTA merges
 // the per-thread pairs.  Same value as the two-pass LSE up to rounding.
-template <bool PRECISE, bool OTF>
+template <bool PRECISE, bool OTF, int NT = kEThreads>
 __device__ __forceinline__ void fallback_body(const double* __restrict__ C64, const CostSrc& src,
                                               int64_t ldc, int64_t n, double kappa,
                                               const double* __restrict__ u,
@@ -1591,11 +1591,11 @@ __device__ __forceinline__ void fallback_body(const double* __restrict__ C64, co
     const double vj = p[j];
     const int64_t i0 = ch * rpc, i1 = min(n, i0 + rpc);
     double top = -INFINITY, sum = 0.0;
-    for (int64_t base = i0 + threadIdx.x; base < i1; base += kEThreads * kFbUnroll) {
+    for (int64_t base = i0 + threadIdx.x; base < i1; base += NT * kFbUnroll) {
       double t[kFbUnroll];
 #pragma unroll
       for (int k = 0; k < kFbUnroll; ++k) {
-        const int64_t i = base + static_cast<int64_t>(k) * kEThreads;
+        const int64_t i = base + static_cast<int64_t>(k) * NT;
         if (i < i1) {
           t[k] = PRECISE ? (u[i] + vj) - C64[i * ldc + j]
                          : fma(-static_cast<double>(cost_one<OTF>(src, i, j)), kappa, u[i] + vj);
@@ -1615,9 +1615,9 @@ __device__ __forceinline__ void fallback_body(const double* __restrict__ C64, co
         for (int k = 0; k < kFbUnroll; ++k) sum += exp(t[k] - top);
       }
     }
-    const double T = block_max<kEThreads>(top, sh);
+    const double T = block_max<NT>(top, sh);
     const double part = (top > -INFINITY) ? sum * exp(top - T) : 0.0;
-    const double S = block_sum<kEThreads>(part, sh);
+    const double S = block_sum<NT>(part, sh);
     if (threadIdx.x == 0) fb_part[f * kFbChunks + ch] = make_double2(T, S);
   }
 }
@@ -1977,9 +1977,10 @@ __device__ __forceinline__ void finalize_col(const FinArgs& A, int64_t j, int sl
   e.mx_p = fmax(e.mx_p, fabs(pj));
 }
 
+template <int NT = kEThreads>
 __device__ __forceinline__ void store_e1(const FinArgs& A, int part, E1Acc& e, double* shm) {
   double v[5] = {e.s_abs, e.s_y, e.s_pb, e.mx_p, e.bad};
-  block_multi<kEThreads, 3, 2>(v, shm);
+  block_multi<NT, 3, 2>(v, shm);
   if (threadIdx.x == 0) {
     double* dst = A.e1_part + part * 8;
 #pragma unroll
@@ -1990,22 +1991,24 @@ __device__ __forceinline__ void store_e1(const FinArgs& A, int part, E1Acc& e, d
 // Per-column finalize of work unit blk of nblk; its partials -> e1_part[blk].
 // defer: flagged columns are left to the last CTA (their fallback partials
 // are complete only once every CTA has run its share of the fallback).
+template <int NT = kEThreads>
 __device__ __forceinline__ void finalize_cols(const FinArgs& A, int blk, int nblk, double* shm,
                                               bool defer = false) {
   E1Acc e;
-  for (int64_t j = static_cast<int64_t>(blk) * kEThreads + threadIdx.x; j < A.m;
-       j += static_cast<int64_t>(nblk) * kEThreads) {
+  for (int64_t j = static_cast<int64_t>(blk) * NT + threadIdx.x; j < A.m;
+       j += static_cast<int64_t>(nblk) * NT) {
     const int slot = A.flag_idx[j];
     if (defer && slot >= 0) continue;
     finalize_col(A, j, slot, e);
   }
-  store_e1(A, blk, e, shm);
+  store_e1<NT>(A, blk, e, shm);
 }
 
+template <int NT = kEThreads>
 __device__ __forceinline__ void finalize_tail(const FinArgs& A, int nparts, double* sh,
                                               Ctrl* __restrict__ ctrl) {
   double gl = 0.0, sy = 0.0, pb = 0.0, mp = 0.0, bd = 0.0;
-  for (int k = threadIdx.x; k < nparts; k += kEThreads) {
+  for (int k = threadIdx.x; k < nparts; k += NT) {
     const volatile double* src = A.e1_part + k * 8;
     gl += src[0];
     sy += src[1];
@@ -2014,10 +2017,10 @@ __device__ __forceinline__ void finalize_tail(const FinArgs& A, int nparts, doub
     bd = fmax(bd, src[4]);
   }
   double ua = 0.0;  // <u, a> partials of the merge work units (col[mpad + 1 + k])
-  for (int k = threadIdx.x; k < A.ua_slices; k += kEThreads) ua += A.col[A.mpad + 1 + k];
+  for (int k = threadIdx.x; k < A.ua_slices; k += NT) ua += A.col[A.mpad + 1 + k];
   {
     double v[6] = {gl, sy, pb, ua, mp, bd};
-    block_multi<kEThreads, 4, 2>(v, sh);
+    block_multi<NT, 4, 2>(v, sh);
     gl = v[0];
     sy = v[1];
     pb = v[2];
@@ -2044,15 +2047,15 @@ __device__ __forceinline__ void finalize_tail(const FinArgs& A, int nparts, doub
   control_step(C, A.trace, A.bounds, gl, f);
 }
 
-template <bool PRECISE, bool OTF>
+template <bool PRECISE, bool OTF, int NT = kEThreads>
 __device__ __forceinline__ void fallback_all(const FinArgs& A, unsigned nf, double* sh,
                                              int2* skey) {
-  if (skey && nf >= 2 * kEThreads && nf <= kFbSortMax)
+  if (skey && nf >= 2 * NT && nf <= kFbSortMax)
     fallback_sorted_body<PRECISE, OTF>(A.C64, A.src, A.ldc, A.nrows, A.kappa, A.u, A.p, A.fb_cols,
                                        A.fb_part_w, nf, skey);
   else
-    fallback_body<PRECISE, OTF>(A.C64, A.src, A.ldc, A.nrows, A.kappa, A.u, A.p, A.fb_cols,
-                                A.fb_part_w, nf, blockIdx.x, gridDim.x, sh);
+    fallback_body<PRECISE, OTF, NT>(A.C64, A.src, A.ldc, A.nrows, A.kappa, A.u, A.p, A.fb_cols,
+                                    A.fb_part_w, nf, blockIdx.x, gridDim.x, sh);
 }
 
 __global__ void __launch_bounds__(kEThreads, 2)
@@ -2063,8 +2066,11 @@ k_finalize(const FinArgs A, Ctrl* __restrict__ ctrl) {
   __shared__ bool last;
   // K5 folded in (unsharded): every CTA takes its share of the flagged
   // columns' exact LSE, the last CTA finalizes those columns
-  const unsigned nf = A.fold_fb ? ctrl->fb_count : 0u;
-  if (nf > 0) {
+  // flagged columns are finalized by the last CTA in list order whether the
+  // fallback ran here or (sharded) in k_fallback + the all-reduces, so the
+  // two paths sum the E1 partials identically
+  const unsigned nf = ctrl->fb_count;
+  if (nf > 0 && A.fold_fb) {
 #if OTG_FIN_SORTED_FB
     __shared__ int2 skey[kFbSortMax];
 #else
@@ -2101,6 +2107,8 @@ k_finalize(const FinArgs A, Ctrl* __restrict__ ctrl) {
 }
 
 // ------------------------------------------------------------------ E2 ----
+
+
 __device__ __forceinline__ double expm1_over_z(double z) {  // mirror.cpp:21-24
   if (fabs(z) < 1e-8) return 1.0 + z / 2.0 + z * z / 6.0;
   return expm1(z) / z;
@@ -2129,6 +2137,7 @@ struct AppArgs {
 // 279; stability sums of diag.cpp); partials -> e2_part[blk].  The control
 // fields are read through a volatile view: inside the single-kernel
 // epilogue they were written by another CTA before a grid barrier.
+template <int NT = kEThreads>
 __device__ __forceinline__ void apply_cols(const AppArgs& A, const Ctrl* ctrl_in, int blk, int nblk,
                                            double* sh) {
   const volatile Ctrl* ctrl = ctrl_in;
@@ -2149,8 +2158,8 @@ __device__ __forceinline__ void apply_cols(const AppArgs& A, const Ctrl* ctrl_in
   double c1 = 0.0, br = 0.0, c2 = 0.0, qq = 0.0, drift = 0.0, ginf = 0.0, dom = 0.0;
   double qe = 0.0, qx = 0.0, qy = 0.0, qb = 0.0, domr = 0.0;
   double dstep = -INFINITY;
-  for (int64_t j = static_cast<int64_t>(blk) * kEThreads + threadIdx.x; j < A.m;
-       j += static_cast<int64_t>(nblk) * kEThreads) {
+  for (int64_t j = static_cast<int64_t>(blk) * NT + threadIdx.x; j < A.m;
+       j += static_cast<int64_t>(nblk) * NT) {
     const double S = A.y[j] - mean;  // project_zero_sum (mirror.cpp:103-105)
     if (mode == MODE_EVAL) {
       A.y[j] = S;
@@ -2216,7 +2225,7 @@ __device__ __forceinline__ void apply_cols(const AppArgs& A, const Ctrl* ctrl_in
   }
   {  // (unused quantities stay 0 / -inf: reduced anyway, in one pass)
     double v[13] = {c1, br, c2, qq, qe, qx, qy, qb, drift, ginf, dom, dstep, domr};
-    block_multi<kEThreads, 8, 5>(v, sh);
+    block_multi<NT, 8, 5>(v, sh);
     c1 = v[0];
     br = v[1];
     c2 = v[2];
@@ -2249,6 +2258,7 @@ __device__ __forceinline__ void apply_cols(const AppArgs& A, const Ctrl* ctrl_in
   }
 }
 
+template <int NT = kEThreads>
 __device__ __forceinline__ void apply_tail(const AppArgs& A, int nparts, double* sh,
                                            Ctrl* __restrict__ ctrl) {
   const volatile Ctrl* cv = ctrl;
@@ -2260,7 +2270,7 @@ __device__ __forceinline__ void apply_tail(const AppArgs& A, int nparts, double*
   const bool moves = !done && mode != MODE_EVAL;
   const bool refq = cv->have_ref != 0 && mode >= MODE_ACC;
   double t[13] = {0, 0, 0, 0, 0, 0, 0, -INFINITY, 0, 0, 0, 0, 0};
-  for (int k = threadIdx.x; k < nparts; k += kEThreads) {
+  for (int k = threadIdx.x; k < nparts; k += NT) {
     const volatile double* src = A.e2_part + k * kE2;
     for (int q = 0; q < 4; ++q) t[q] += src[q];
     for (int q = 4; q < 8; ++q) t[q] = fmax(t[q], src[q]);
@@ -2271,7 +2281,7 @@ __device__ __forceinline__ void apply_tail(const AppArgs& A, int nparts, double*
   }
   {
     double v[13] = {t[0], t[1], t[2], t[3], t[8], t[9], t[10], t[11], t[4], t[5], t[6], t[7], t[12]};
-    block_multi<kEThreads, 8, 5>(v, sh);
+    block_multi<NT, 8, 5>(v, sh);
     for (int q = 0; q < 4; ++q) t[q] = v[q];
     for (int q = 8; q < 12; ++q) t[q] = v[q - 4];
     for (int q = 4; q < 8; ++q) t[q] = v[q + 4];
@@ -2349,6 +2359,7 @@ k_apply(const AppArgs A, Ctrl* __restrict__ ctrl) {
   __threadfence();
   apply_tail(A, gridDim.x, sh, ctrl);
 }
+
 
 // ------------------------------------------------------ fused epilogue ----
 // Merge + flag, exact fallback, finalize + control step and the vector update
