@@ -32,6 +32,9 @@
 #ifndef OTG_ROW_PF
 #define OTG_ROW_PF -1        // row-pass L2 prefetch (-1 = auto)
 #endif
+#ifndef OTG_CULL
+#define OTG_CULL 1  // on-the-fly sweeps: Morton-ordered, exact (FTZ) block culling
+#endif
 #ifndef OTG_FIN_SORTED_FB
 #define OTG_FIN_SORTED_FB 0  // k_finalize's folded fallback: column-sorted work items (32 KB smem)
 #endif
@@ -237,6 +240,18 @@ struct Problem {
   float* X = nullptr;     // on-the-fly: x (n_local x 4 padded), y (m x 4)
   float* Y = nullptr;
   float* Yn = nullptr;    // on-the-fly: -y as SoA [x | y | z], stride mpad (packed kernels)
+  // on the fly, culled sweeps (sweep.cu: k_row_otf<true>, k_col_fast<true, T, true>):
+  // Morton orders of the rows and columns, the points in those orders, the
+  // static boxes of the culling blocks and their per-evaluation potential bounds
+  int cull = 0;
+  int* perm_r = nullptr;
+  int* perm_c = nullptr;
+  float* Xs = nullptr;    // n_local x 4, sorted rows
+  float* Yns = nullptr;   // -y SoA in sorted column order, stride mpad
+  float* cbox = nullptr;  // 2 float4 per 64 sorted columns
+  float* rbox = nullptr;  // 2 float4 per 16 sorted rows
+  float* cvmax = nullptr;
+  float* rnegm = nullptr;
 
   // marginals (fp64)
   double *a = nullptr, *loga = nullptr, *b = nullptr, *logb = nullptr;

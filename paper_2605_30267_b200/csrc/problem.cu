@@ -144,7 +144,8 @@ void problem_free(Problem& P) {
                   P.col_log,
                   P.y, P.grad, P.prev_grad,
                   P.prev_x, P.prev_y, P.flag_idx, P.fb_cols, P.fb_part, P.part, P.e1_part,
-                  P.e2_part, P.epi_part, P.sp_rec, P.sp_bad_rows, P.sp_bad_count, P.ctrl, P.trace, P.vstar, P.bounds, P.fbA, P.fbS, P.fbT, P.red, P.sp_sums, P.sp_cnt};
+                  P.e2_part, P.epi_part, P.sp_rec, P.sp_bad_rows, P.sp_bad_count, P.ctrl, P.trace, P.vstar, P.bounds, P.fbA, P.fbS, P.fbT, P.red, P.sp_sums, P.sp_cnt,
+                  P.perm_r, P.perm_c, P.Xs, P.Yns, P.cbox, P.rbox, P.cvmax, P.rnegm};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (P.ctrl_host) cudaFreeHost(P.ctrl_host);
@@ -262,6 +263,81 @@ static void upload_marginals(Problem& P, const double* a, const double* b) {
   k_log<<<(n + kT - 1) / kT, kT, 0, P.stream>>>(P.a, P.loga, n);
   k_log<<<(m + kT - 1) / kT, kT, 0, P.stream>>>(P.b, P.logb, m);
   OTG_CUDA(cudaGetLastError());
+}
+
+// Culled on-the-fly sweeps: Morton orders (10 bits per axis over the joint
+// bounding box; ties by index) of the rows and the columns, the points in
+// those orders and the static boxes of the culling blocks (64 sorted
+// columns, 16 sorted rows).  Only the two steady-state on-the-fly sweep
+// kernels visit rows / columns in these orders; every array the API sees
+// stays in the caller's order.
+static void setup_cull(Problem& P, const std::vector<float>& hx, const std::vector<float>& hy) {
+  constexpr int64_t kCB = 64, kRB = 16;
+  const int64_t n = P.n_local, m = P.m;
+  if (!OTG_CULL || n < 4096 || m < 4096) return;
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < 3; ++k) lo[k] = std::min(lo[k], hx[i * 4 + k]), hi[k] = std::max(hi[k], hx[i * 4 + k]);
+  for (int64_t j = 0; j < m; ++j)
+    for (int k = 0; k < 3; ++k) lo[k] = std::min(lo[k], hy[j * 4 + k]), hi[k] = std::max(hi[k], hy[j * 4 + k]);
+  auto code = [&](const float* pt) {
+    uint32_t c = 0;
+    for (int k = 0; k < 3; ++k) {
+      const double span = static_cast<double>(hi[k]) - lo[k];
+      const uint32_t q = span > 0 ? static_cast<uint32_t>(std::min(
+                                        1023.0, std::floor((pt[k] - lo[k]) / span * 1024.0)))
+                                  : 0u;
+      for (int b = 0; b < 10; ++b) c |= ((q >> b) & 1u) << (3 * b + k);
+    }
+    return c;
+  };
+  auto order = [&](const std::vector<float>& pts, int64_t cnt) {
+    std::vector<std::pair<uint32_t, int>> key(cnt);
+    for (int64_t t = 0; t < cnt; ++t) key[t] = {code(&pts[t * 4]), static_cast<int>(t)};
+    std::sort(key.begin(), key.end());
+    std::vector<int> perm(cnt);
+    for (int64_t t = 0; t < cnt; ++t) perm[t] = key[t].second;
+    return perm;
+  };
+  const std::vector<int> pr = order(hx, n), pc = order(hy, m);
+  std::vector<float> xs(n * 4), yns(P.mpad * 3, 0.f);
+  for (int64_t s = 0; s < n; ++s)
+    for (int k = 0; k < 4; ++k) xs[s * 4 + k] = hx[pr[s] * 4 + k];
+  for (int64_t s = 0; s < m; ++s)
+    for (int k = 0; k < 3; ++k) yns[k * P.mpad + s] = -hy[pc[s] * 4 + k];
+  auto boxes = [](const std::vector<float>& pts, const std::vector<int>& perm, int64_t cnt,
+                  int64_t B) {
+    const int64_t nb = (cnt + B - 1) / B;
+    std::vector<float> bx(nb * 8, 0.f);
+    for (int64_t b = 0; b < nb; ++b) {
+      float l[3] = {INFINITY, INFINITY, INFINITY}, h[3] = {-INFINITY, -INFINITY, -INFINITY};
+      for (int64_t s = b * B; s < std::min(cnt, (b + 1) * B); ++s)
+        for (int k = 0; k < 3; ++k) {
+          const float v = pts[static_cast<int64_t>(perm[s]) * 4 + k];
+          l[k] = std::min(l[k], v);
+          h[k] = std::max(h[k], v);
+        }
+      for (int k = 0; k < 3; ++k) bx[b * 8 + k] = l[k], bx[b * 8 + 4 + k] = h[k];
+    }
+    return bx;
+  };
+  const std::vector<float> cb = boxes(hy, pc, m, kCB), rb = boxes(hx, pr, n, kRB);
+  P.perm_r = dalloc<int>(P, n);
+  P.perm_c = dalloc<int>(P, m);
+  P.Xs = dalloc<float>(P, n * 4);
+  P.Yns = dalloc<float>(P, P.mpad * 3);
+  P.cbox = dalloc<float>(P, cb.size());
+  P.rbox = dalloc<float>(P, rb.size());
+  P.cvmax = dalloc<float>(P, cb.size() / 8);
+  P.rnegm = dalloc<float>(P, rb.size() / 8);
+  OTG_CUDA(cudaMemcpyAsync(P.perm_r, pr.data(), n * 4, cudaMemcpyHostToDevice, P.stream));
+  OTG_CUDA(cudaMemcpyAsync(P.perm_c, pc.data(), m * 4, cudaMemcpyHostToDevice, P.stream));
+  OTG_CUDA(cudaMemcpyAsync(P.Xs, xs.data(), xs.size() * 4, cudaMemcpyHostToDevice, P.stream));
+  OTG_CUDA(cudaMemcpyAsync(P.Yns, yns.data(), yns.size() * 4, cudaMemcpyHostToDevice, P.stream));
+  OTG_CUDA(cudaMemcpyAsync(P.cbox, cb.data(), cb.size() * 4, cudaMemcpyHostToDevice, P.stream));
+  OTG_CUDA(cudaMemcpyAsync(P.rbox, rb.data(), rb.size() * 4, cudaMemcpyHostToDevice, P.stream));
+  OTG_CUDA(cudaStreamSynchronize(P.stream));  // (host vectors go out of scope)
+  P.cull = 1;
 }
 
 static void finish_create(Problem& P, const otg_device_opts* opts, otg_problem* out) {
@@ -395,6 +471,7 @@ otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const doub
       OTG_CUDA(cudaMemcpyAsync(P.Y, hy.data(), hy.size() * 4, cudaMemcpyHostToDevice, P.stream));
       OTG_CUDA(cudaMemcpyAsync(P.Yn, hyn.data(), hyn.size() * 4, cudaMemcpyHostToDevice,
                                P.stream));
+      setup_cull(P, hx, hy);
       OTG_CUDA(cudaStreamSynchronize(P.stream));
       finish_create(P, opts, out);
       return;

@@ -334,7 +334,31 @@ struct CostSrc {
   const float4* Y;   // on-the-fly: m points (x, y, z, 0)
   const float* Yn;   // on-the-fly: the same points negated, SoA [-x | -y | -z], stride ypad
   int64_t ypad;
+  // on the fly, spatially sorted sweeps with exact block culling (P.cull):
+  // rows / columns visited in Morton order; a block is skipped when a bound
+  // proves every exponent in it below -127 (ex2.approx.ftz returns +0 there,
+  // so skipping is bitwise the same sum)
+  const int* perm_r;   // sorted row position -> row
+  const int* perm_c;   // sorted column position -> column
+  const float4* Xs;    // rows in sorted order
+  const float4* cbox;  // per kCullCB sorted columns: (lo, hi) boxes
+  const float* cvmax;  // per kCullCB sorted columns: max V (this evaluation)
+  const float4* rbox;  // per kCullRB sorted rows: (lo, hi) boxes
+  const float* rnegm;  // per kCullRB sorted rows: max -M (this evaluation)
 };
+
+constexpr int kCullCB = 64;  // columns per culling block (row pass)
+constexpr int kCullRB = 16;  // rows per culling block (column pass)
+constexpr float kCullT = -127.0f;  // bound below which a block is skipped (FTZ below -126)
+constexpr float kCullSlack = 1.0f - 1.0f / 65536.0f;  // relative slack on the box distance
+
+// squared distance from a point to an axis-aligned box (0 inside), fp32
+__device__ __forceinline__ float box_d2(float x, float y, float z, const float4& lo, const float4& hi) {
+  const float gx = fmaxf(fmaxf(lo.x - x, x - hi.x), 0.0f);
+  const float gy = fmaxf(fmaxf(lo.y - y, y - hi.y), 0.0f);
+  const float gz = fmaxf(fmaxf(lo.z - z, z - hi.z), 0.0f);
+  return fmaf(gz, gz, fmaf(gy, gy, gx * gx));
+}
 
 __device__ __forceinline__ float otf_cost(const float4& x, const float4& y) {
   return otf_sqeuclid(x, y);
@@ -1155,6 +1179,7 @@ __device__ __forceinline__ float row_shift_estimate(const double* __restrict__ r
   return static_cast<float>(ceil(fmin(lo + 1.0, hi) * 256.0) * (1.0 / 256.0));
 }
 
+template <bool CULL>
 __global__ void __launch_bounds__(kRowThreads, OTG_ROW_OTF_MINB)
 k_row_otf(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
           const double* __restrict__ dq, int64_t mpad, float kh, float kl,
@@ -1167,7 +1192,17 @@ k_row_otf(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
   __shared__ float4 sB[kOtfTJ];  // (-z, -z, V, V)
   __shared__ float2 sE[kOtfTJ];  // (2^F, 2^F)
   __shared__ double sSS[kOtfRT][kRowThreads];
-  const int64_t rbase = static_cast<int64_t>(blockIdx.x) * (kRowThreads * kOtfRT) + threadIdx.x;
+  // rows of this thread: r-th = base + r * stride.  CULL: sorted positions,
+  // each warp's 256 rows consecutive (spatially compact: one culling test
+  // per warp and column block)
+  const int64_t cbase = static_cast<int64_t>(blockIdx.x) * (kRowThreads * kOtfRT);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t rbase = CULL ? cbase + warp * (32 * kOtfRT) + lane : cbase + threadIdx.x;
+  constexpr int64_t rstride = CULL ? 32 : kRowThreads;
+  auto row_of = [&](int64_t pos) -> int64_t {  // row index (original order) at position pos
+    const int64_t q = min(pos, n - 1);
+    return CULL ? static_cast<int64_t>(src.perm_r[q]) : q;
+  };
   const int64_t j0 = static_cast<int64_t>(blockIdx.y) * cols_per_split;
   const int64_t j1 = min(j0 + cols_per_split, m);
   const double dmax2 = ctrl->dmax2;
@@ -1176,9 +1211,10 @@ k_row_otf(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
   int tj[kOtfRT];
 #pragma unroll
   for (int pp = 0; pp < NP; ++pp) {
-    const int64_t i0 = min(rbase + (2 * pp) * kRowThreads, n - 1);
-    const int64_t i1 = min(rbase + (2 * pp + 1) * kRowThreads, n - 1);
-    const float4 x0 = src.X[i0], x1 = src.X[i1];
+    const int64_t p0 = rbase + (2 * pp) * rstride, p1 = rbase + (2 * pp + 1) * rstride;
+    const int64_t i0 = row_of(p0), i1 = row_of(p1);
+    const float4 x0 = CULL ? src.Xs[min(p0, n - 1)] : src.X[i0];
+    const float4 x1 = CULL ? src.Xs[min(p1, n - 1)] : src.X[i1];
     X[pp] = make_float2(x0.x, x1.x);
     Y[pp] = make_float2(x0.y, x1.y);
     Z[pp] = make_float2(x0.z, x1.z);
@@ -1195,12 +1231,14 @@ k_row_otf(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
   const float2 nkh2 = make_float2(-kh, -kh), nkl2 = make_float2(-kl, -kl);
   const float* Vp = vq;
   const float* Ep = vq + 2 * mpad;
+  const float kcull = kh * kCullSlack;
   for (int64_t t0 = j0; t0 < j1; t0 += kOtfTJ) {
     __syncthreads();
     for (int k = threadIdx.x; k < kOtfTJ; k += kRowThreads) {
-      const int64_t j = t0 + k;
-      if (j < j1) {
-        const float nx = src.Yn[j], ny = src.Yn[src.ypad + j], nz = src.Yn[2 * src.ypad + j];
+      const int64_t jp = t0 + k;  // (CULL: sorted position; coordinates stored sorted)
+      if (jp < j1) {
+        const int64_t j = CULL ? static_cast<int64_t>(src.perm_c[jp]) : jp;
+        const float nx = src.Yn[jp], ny = src.Yn[src.ypad + jp], nz = src.Yn[2 * src.ypad + jp];
         const float V = Vp[j];
         sA[k] = make_float4(nx, nx, ny, ny);
         sB[k] = make_float4(nz, nz, V, V);
@@ -1215,6 +1253,25 @@ k_row_otf(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
     __syncthreads();
     const int tn = static_cast<int>(min(static_cast<int64_t>(kOtfTJ), j1 - t0));
     for (int kb = 0; kb < tn; kb += kOtfBlk) {
+      if constexpr (CULL) {
+        if ((kb % kCullCB) == 0) {  // a culling block starts: does any row of the warp see it?
+          const int64_t cbk = (t0 + kb) / kCullCB;
+          const float4 lo = __ldg(src.cbox + 2 * cbk), hi = __ldg(src.cbox + 2 * cbk + 1);
+          const float vmax = __ldg(src.cvmax + cbk);
+          bool live = false;
+#pragma unroll
+          for (int pp = 0; pp < NP; ++pp) {
+            const float d0 = box_d2(X[pp].x, Y[pp].x, Z[pp].x, lo, hi);
+            const float d1 = box_d2(X[pp].y, Y[pp].y, Z[pp].y, lo, hi);
+            live |= fmaf(-kcull, d0, vmax + nS[pp].x) >= kCullT;
+            live |= fmaf(-kcull, d1, vmax + nS[pp].y) >= kCullT;
+          }
+          if (!__any_sync(0xffffffffu, live)) {
+            kb += kCullCB - kOtfBlk;  // every exponent of the block is below -127
+            continue;
+          }
+        }
+      }
 #pragma unroll kOtfUnroll
       for (int k = kb; k < kb + kOtfBlk; ++k) {
         const float4 A = sA[k], B = sB[k];
@@ -1251,13 +1308,13 @@ k_row_otf(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
   RowPart* dst = rpart + static_cast<int64_t>(blockIdx.y) * n;
 #pragma unroll
   for (int r = 0; r < kOtfRT; ++r) {
-    const int64_t i = rbase + r * kRowThreads;
-    if (i < n) {
+    const int64_t pos = rbase + r * rstride;
+    if (pos < n) {
       RowPart rp;
       rp.t = tm[r];
-      rp.jb = tj[r];
+      rp.jb = tj[r];  // (CULL: sorted column position; k_row_otf_fin maps it)
       rp.s = sSS[r][threadIdx.x];
-      dst[i] = rp;
+      dst[row_of(pos)] = rp;
     }
   }
 }
@@ -1294,7 +1351,7 @@ k_row_otf_fin(const CostSrc src, int64_t n, int64_t m, const float* __restrict__
   int J = JB;
   float TJ = -FLT_MAX;
   for (int k = 0; k < kOtfBlk && JB + k < m; ++k) {
-    const int64_t j = JB + k;
+    const int64_t j = src.perm_c ? static_cast<int64_t>(src.perm_c[JB + k]) : JB + k;
     const float c = otf_sqeuclid(xi, src.Y[j]);
     const float t = fmaf(c, -kh, vq[j] + (-sc));
     if (t > TJ) {
@@ -1321,6 +1378,39 @@ k_row_otf_fin(const CostSrc src, int64_t n, int64_t m, const float* __restrict__
   rowM2[i] = scd + static_cast<double>(T);
   rowJ[i] = J;
   aux[i] = make_float4(sc, 0.0f, static_cast<float>(wi), 0.0f);
+}
+
+// Per-evaluation bounds of the culled on-the-fly sweeps: the largest column
+// potential (base 2, hi part) of each 64-column sorted block, and the largest
+// -M (negated row shift) of each 16-row sorted block.
+__global__ void __launch_bounds__(256)
+k_cull_cols(int64_t m, const float* __restrict__ vq, const int* __restrict__ perm_c,
+            float* __restrict__ cvmax, const Ctrl* __restrict__ ctrl) {
+  pdl_wait();
+  if (ctrl->done) return;
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b * kCullCB >= m) return;
+  float v = -INFINITY;
+  for (int k = lane; k < kCullCB; k += 32) {
+    const int64_t s = b * kCullCB + k;
+    if (s < m) v = fmaxf(v, vq[perm_c[s]]);
+  }
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) cvmax[b] = v;
+}
+
+__global__ void __launch_bounds__(256)
+k_cull_rows(int64_t n, const float4* __restrict__ aux, const int* __restrict__ perm_r,
+            float* __restrict__ rnegm, const Ctrl* __restrict__ ctrl) {
+  pdl_wait();
+  if (ctrl->done) return;
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * 16 + (threadIdx.x >> 4);
+  const int l = threadIdx.x & 15;
+  const int64_t s = b * kCullRB + l;
+  float v = s < n ? -aux[perm_r[s]].x : -INFINITY;
+  for (int o = 8; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (l == 0 && b * kCullRB < n) rnegm[b] = v;
 }
 
 // ------------------------------------------------------------------ K2 ----
@@ -1398,7 +1488,7 @@ __device__ __forceinline__ void flush_acc(float2& acc01, float2& acc23, double* 
 // fp32: thread owns 4 consecutive columns, loops over the split's rows.  The
 // rows' shift / weight (aux) -- and, on the fly, the rows' points -- are
 // staged in shared memory per 256-row tile and read as broadcasts.
-template <bool OTF, int NT>
+template <bool OTF, int NT, bool CULL = false>
 __global__ void __launch_bounds__(NT, (!OTF && NT == 256) ? OTG_COL_MINB
                                       : (OTF && NT == 256) ? OTG_COL_OTF_MINB : 1)
 k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh, float kl,
@@ -1417,7 +1507,8 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
   float Vc[4], vf[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const double pj = (j0 + k < m) ? p[j0 + k] : 0.0;
+    // (CULL: j0 + k is a sorted column position)
+    const double pj = (j0 + k < m) ? p[CULL ? src.perm_c[j0 + k] : j0 + k] : 0.0;
     split_q(pj * kLog2e, Vc[k], vf[k]);
   }
   YQ y4;
@@ -1442,13 +1533,15 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
     acc23 = make_float2(0.f, 0.f);
   };
   const bool active = j0 < m;
+  const unsigned amask = __ballot_sync(0xffffffffu, active);
+  const float kcull = kh * kCullSlack;
   for (int64_t t0 = i0; t0 < i1; t0 += kAuxTile) {
     const int64_t tn = min(static_cast<int64_t>(kAuxTile), i1 - t0);
     __syncthreads();
     for (int k = threadIdx.x; k < tn; k += NT) {
-      float4 ax = aux[t0 + k];
+      float4 ax = aux[CULL ? src.perm_r[t0 + k] : t0 + k];
       if (OTF) {
-        sh_x[k] = src.X[t0 + k];
+        sh_x[k] = CULL ? src.Xs[t0 + k] : src.X[t0 + k];
         ax.z = ax.y == 0.0f ? ax.z : ax.z * exp2f(-ax.y);  // w' = w 2^-mf
       }
       sh_aux[k] = ax;
@@ -1457,6 +1550,25 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
     if (!active) continue;
     int k = 0;
     for (; k + kColUnroll <= tn; k += kColUnroll) {
+      if constexpr (CULL) {
+        if (((t0 + k) % kCullRB) == 0 && k + kCullRB <= tn) {
+          // a culling block of rows starts: is any of the warp's columns live?
+          const int64_t rb = (t0 + k) / kCullRB;
+          const float4 lo = __ldg(src.rbox + 2 * rb), hi = __ldg(src.rbox + 2 * rb + 1);
+          const float nm = __ldg(src.rnegm + rb);
+          const float yx[4] = {y4.x.x, y4.x.y, y4.x.z, y4.x.w};
+          const float yy[4] = {y4.y.x, y4.y.y, y4.y.z, y4.y.w};
+          const float yz[4] = {y4.z.x, y4.z.y, y4.z.z, y4.z.w};
+          bool live = false;
+#pragma unroll
+          for (int e = 0; e < 4; ++e)  // (y4 holds the negated coordinates)
+            live |= fmaf(-kcull, box_d2(-yx[e], -yy[e], -yz[e], lo, hi), Vc[e] + nm) >= kCullT;
+          if (!__any_sync(amask, live)) {
+            k += kCullRB - kColUnroll;  // every exponent of the block is below -127
+            continue;
+          }
+        }
+      }
       float4 c[kColUnroll];
 #pragma unroll
       for (int r = 0; r < kColUnroll; ++r)
@@ -1480,10 +1592,13 @@ k_col_fast(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
     flush();
   }
   if (active) {
-    double* dst = part + static_cast<int64_t>(blockIdx.y) * mpad + j0;
+    double* dst = part + static_cast<int64_t>(blockIdx.y) * mpad;
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-      dst[e] = OTF ? sAcc[e][threadIdx.x] * exp2(static_cast<double>(vf[e])) : sAcc[e][threadIdx.x];
+    for (int e = 0; e < 4; ++e) {
+      if (CULL && j0 + e >= m) continue;
+      const int64_t j = CULL ? static_cast<int64_t>(src.perm_c[j0 + e]) : j0 + e;
+      dst[j] = OTF ? sAcc[e][threadIdx.x] * exp2(static_cast<double>(vf[e])) : sAcc[e][threadIdx.x];
+    }
   }
 }
 
@@ -2521,13 +2636,14 @@ void configure_sweeps(Problem& P) {
   splits = std::max<int64_t>(1, std::min<int64_t>(splits, max_splits));
   P.col_splits = static_cast<int>(splits);
   P.rows_per_split = (shard_rows + splits - 1) / splits;
+  if (P.cull) P.rows_per_split = (P.rows_per_split + kCullRB - 1) / kCullRB * kCullRB;  // whole blocks
   // on the fly: the transposed row pass (OTG_ROW_OTF_T=0: row_shift_block).
   // Column splits give ~8 waves of the resident CTAs, >= 256 columns each.
   constexpr int env_rt = OTG_ROW_OTF_T;
   P.row_splits = 0;
   if (P.storage == OTG_STORE_ON_THE_FLY && env_rt != 0) {
     int occ = 0, sms = 0;
-    OTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_row_otf, kRowThreads, 0));
+    OTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_row_otf<true>, kRowThreads, 0));
     OTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.device));
     const int64_t rb = (P.n_local + kRowThreads * kOtfRT - 1) / (kRowThreads * kOtfRT);
     const int64_t slots = std::max<int64_t>(1, static_cast<int64_t>(occ) * sms);
@@ -2535,10 +2651,26 @@ void configure_sweeps(Problem& P) {
     S = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(S, 128), (P.m + 255) / 256));
     int64_t cps = (P.m + S - 1) / S;
     cps = (cps + kOtfBlk - 1) / kOtfBlk * kOtfBlk;
+    if (P.cull) cps = (cps + kCullCB - 1) / kCullCB * kCullCB;  // whole culling blocks
     P.row_cols_per_split = cps;
     P.row_splits = static_cast<int>((P.m + cps - 1) / cps);
   }
   P.e_blocks = e_grid(P.m);
+}
+
+static CostSrc cost_src(const Problem& P);
+// the culled sweeps' view: sorted coordinates, orders, block boxes / bounds
+static CostSrc cull_src(const Problem& P) {
+  CostSrc s = cost_src(P);
+  s.Yn = P.Yns;
+  s.perm_r = P.perm_r;
+  s.perm_c = P.perm_c;
+  s.Xs = reinterpret_cast<const float4*>(P.Xs);
+  s.cbox = reinterpret_cast<const float4*>(P.cbox);
+  s.cvmax = P.cvmax;
+  s.rbox = reinterpret_cast<const float4*>(P.rbox);
+  s.rnegm = P.rnegm;
+  return s;
 }
 
 static CostSrc cost_src(const Problem& P) {
@@ -2549,6 +2681,11 @@ static CostSrc cost_src(const Problem& P) {
   s.Y = reinterpret_cast<const float4*>(P.Y);
   s.Yn = P.Yn;
   s.ypad = P.mpad;
+  s.perm_r = nullptr;
+  s.perm_c = nullptr;
+  s.Xs = nullptr;
+  s.cbox = s.rbox = nullptr;
+  s.cvmax = s.rnegm = nullptr;
   return s;
 }
 
@@ -2647,12 +2784,24 @@ void launch_row_pass(Problem& P) {
       RowPart* rp = static_cast<RowPart*>(P.rpart);
       const dim3 g(static_cast<unsigned>((P.n_local + kRowThreads * kOtfRT - 1) / (kRowThreads * kOtfRT)),
                    static_cast<unsigned>(P.row_splits));
-      launch_k(k_row_otf, g, kRowThreads, 0, P.stream, src, P.n_local, P.m,
-               static_cast<const float*>(P.vq), static_cast<const double*>(P.dq), P.mpad, kh, kl,
-               static_cast<const double*>(P.rowM2), static_cast<const int*>(P.rowJ),
-               P.row_cols_per_split, rp, static_cast<const Ctrl*>(P.ctrl));
+      CostSrc fsrc = src;
+      if (P.cull) {
+        launch_k(k_cull_cols, static_cast<unsigned>((P.m + 8 * kCullCB - 1) / (8 * kCullCB)), 256, 0,
+                 P.stream, P.m, static_cast<const float*>(P.vq), static_cast<const int*>(P.perm_c),
+                 P.cvmax, static_cast<const Ctrl*>(P.ctrl));
+        launch_k(k_row_otf<true>, g, kRowThreads, 0, P.stream, cull_src(P), P.n_local, P.m,
+                 static_cast<const float*>(P.vq), static_cast<const double*>(P.dq), P.mpad, kh, kl,
+                 static_cast<const double*>(P.rowM2), static_cast<const int*>(P.rowJ),
+                 P.row_cols_per_split, rp, static_cast<const Ctrl*>(P.ctrl));
+        fsrc.perm_c = P.perm_c;  // (the heaviest block's columns, in sorted order)
+      } else {
+        launch_k(k_row_otf<false>, g, kRowThreads, 0, P.stream, src, P.n_local, P.m,
+                 static_cast<const float*>(P.vq), static_cast<const double*>(P.dq), P.mpad, kh, kl,
+                 static_cast<const double*>(P.rowM2), static_cast<const int*>(P.rowJ),
+                 P.row_cols_per_split, rp, static_cast<const Ctrl*>(P.ctrl));
+      }
       launch_k(k_row_otf_fin, static_cast<unsigned>((P.n_local + kRowThreads - 1) / kRowThreads),
-               kRowThreads, 0, P.stream, src, P.n_local, P.m, static_cast<const float*>(P.vq),
+               kRowThreads, 0, P.stream, fsrc, P.n_local, P.m, static_cast<const float*>(P.vq),
                static_cast<const double*>(P.dq), P.mpad, kh, kl, static_cast<const double*>(P.a),
                static_cast<const double*>(P.loga), P.rowM, P.rowS, P.u, P.wrow, P.aux, P.rowM2,
                P.rowJ, P.redo_rows, static_cast<const RowPart*>(rp), P.row_splits, P.ctrl);
@@ -2691,7 +2840,14 @@ void launch_col_pass(Problem& P) {
   launch_k(k_col_fast<OTF, T>, grid, T, 0, P.stream, cost_src(P), P.m, P.p, kh, kl, P.aux, lo, hi, \
                                                P.rows_per_split, part, P.mpad, P.ctrl, P.fused)
       const bool otf = P.storage == OTG_STORE_ON_THE_FLY;
-      if (NT == 512) {
+      if (otf && P.cull && P.vshards == 1 && NT == 256) {
+        // culled on-the-fly column pass (sorted rows / columns, exact skips)
+        launch_k(k_cull_rows, static_cast<unsigned>((P.n_local + 16 * kCullRB - 1) / (16 * kCullRB)),
+                 256, 0, P.stream, P.n_local, static_cast<const float4*>(P.aux),
+                 static_cast<const int*>(P.perm_r), P.rnegm, static_cast<const Ctrl*>(P.ctrl));
+        launch_k(k_col_fast<true, 256, true>, grid, 256, 0, P.stream, cull_src(P), P.m, P.p, kh, kl,
+                 P.aux, lo, hi, P.rows_per_split, part, P.mpad, P.ctrl, P.fused);
+      } else if (NT == 512) {
         if (otf) { OTG_COL(true, 512); } else { OTG_COL(false, 512); }
       } else if (NT == 256) {
         if (otf) { OTG_COL(true, 256); } else { OTG_COL(false, 256); }
