@@ -35,6 +35,12 @@
 #ifndef OTG_CULL
 #define OTG_CULL 1  // on-the-fly sweeps: Morton-ordered, exact (FTZ) block culling
 #endif
+#ifndef OTG_CULL_COL_SPLITS
+#define OTG_CULL_COL_SPLITS 64  // culled on-the-fly column pass: row splits
+#endif
+#ifndef OTG_CULL_ROW_WAVES
+#define OTG_CULL_ROW_WAVES 16   // culled on-the-fly row pass: waves of column splits
+#endif
 #ifndef OTG_FIN_SORTED_FB
 #define OTG_FIN_SORTED_FB 0  // k_finalize's folded fallback: column-sorted work items (32 KB smem)
 #endif

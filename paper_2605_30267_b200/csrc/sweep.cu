@@ -352,6 +352,20 @@ constexpr int kCullRB = 16;  // rows per culling block (column pass)
 constexpr float kCullT = -127.0f;  // bound below which a block is skipped (FTZ below -126)
 constexpr float kCullSlack = 1.0f - 1.0f / 65536.0f;  // relative slack on the box distance
 
+// squared distances of two points (packed) to an axis-aligned box (0 inside)
+__device__ __forceinline__ float2 box_d2x2(float2 x, float2 y, float2 z, const float4& lo,
+                                           const float4& hi) {
+  const float2 gxa = __fadd2_rn(make_float2(lo.x, lo.x), make_float2(-x.x, -x.y));
+  const float2 gxb = __fadd2_rn(x, make_float2(-hi.x, -hi.x));
+  const float2 gya = __fadd2_rn(make_float2(lo.y, lo.y), make_float2(-y.x, -y.y));
+  const float2 gyb = __fadd2_rn(y, make_float2(-hi.y, -hi.y));
+  const float2 gza = __fadd2_rn(make_float2(lo.z, lo.z), make_float2(-z.x, -z.y));
+  const float2 gzb = __fadd2_rn(z, make_float2(-hi.z, -hi.z));
+  const float2 gx = make_float2(fmaxf(fmaxf(gxa.x, gxb.x), 0.f), fmaxf(fmaxf(gxa.y, gxb.y), 0.f));
+  const float2 gy = make_float2(fmaxf(fmaxf(gya.x, gyb.x), 0.f), fmaxf(fmaxf(gya.y, gyb.y), 0.f));
+  const float2 gz = make_float2(fmaxf(fmaxf(gza.x, gzb.x), 0.f), fmaxf(fmaxf(gza.y, gzb.y), 0.f));
+  return __ffma2_rn(gz, gz, __ffma2_rn(gy, gy, __fmul2_rn(gx, gx)));
+}
 // squared distance from a point to an axis-aligned box (0 inside), fp32
 __device__ __forceinline__ float box_d2(float x, float y, float z, const float4& lo, const float4& hi) {
   const float gx = fmaxf(fmaxf(lo.x - x, x - hi.x), 0.0f);
@@ -1413,6 +1427,7 @@ k_cull_rows(int64_t n, const float4* __restrict__ aux, const int* __restrict__ p
   if (l == 0 && b * kCullRB < n) rnegm[b] = v;
 }
 
+
 // ------------------------------------------------------------------ K2 ----
 // fp64: partial c_j = sum_i exp(((-C'_ij) + p_j) - M_i) * w_i  (dual.cpp:36,41)
 __global__ void __launch_bounds__(kColThreads)
@@ -1488,6 +1503,239 @@ __device__ __forceinline__ void flush_acc(float2& acc01, float2& acc23, double* 
 // fp32: thread owns 4 consecutive columns, loops over the split's rows.  The
 // rows' shift / weight (aux) -- and, on the fly, the rows' points -- are
 // staged in shared memory per 256-row tile and read as broadcasts.
+// ---------------------------------------------- culled on-the-fly sweeps ----
+// Warp-independent forms of k_row_otf / k_col_fast<true> for the Morton-
+// ordered handle (P.cull): each warp tests a block with the point-to-box
+// bound, stages only live blocks in its own shared-memory slice and never
+// waits for the CTA's other warps (a CTA-wide tile barrier made every tile
+// cost its busiest warp).  Per pair the arithmetic is that of the dense
+// kernels; skipped blocks are exactly the ones whose every exponent is
+// below -127, where ex2.approx.ftz returns +0.
+
+// Rows: warp = 256 consecutive sorted rows (8 per lane, 4 packed pairs);
+// blocks of kCullCB sorted columns, flushed / max-tracked per kOtfBlk.
+__global__ void __launch_bounds__(kRowThreads, OTG_ROW_OTF_MINB)
+k_row_otf_cull(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
+               const double* __restrict__ dq, int64_t mpad, float kh,
+               const double* __restrict__ rowM2, const int* __restrict__ rowJ,
+               int64_t cols_per_split, RowPart* __restrict__ rpart, const Ctrl* __restrict__ ctrl) {
+  pdl_wait();
+  if (ctrl->done || !ctrl->shift_valid) return;
+  constexpr int NP = kOtfRT / 2;
+  constexpr int kW = kRowThreads / 32;
+  __shared__ float4 sA[kW][kCullCB];  // (-x, -x, -y, -y)
+  __shared__ float4 sB[kW][kCullCB];  // (-z, -z, V, V)
+  __shared__ float2 sE[kW][kCullCB];  // (2^F, 2^F)
+  __shared__ double sSS[kOtfRT][kRowThreads];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t rbase = static_cast<int64_t>(blockIdx.x) * (kRowThreads * kOtfRT) +
+                        warp * (32 * kOtfRT) + lane;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.y) * cols_per_split;
+  const int64_t j1 = min(j0 + cols_per_split, m);
+  const double dmax2 = ctrl->dmax2;
+  float2 X[NP], Y[NP], Z[NP], nS[NP], fs[NP];
+  float tm[kOtfRT];
+  int tj[kOtfRT];
+#pragma unroll
+  for (int pp = 0; pp < NP; ++pp) {
+    const int64_t p0 = min(rbase + (2 * pp) * 32, n - 1), p1 = min(rbase + (2 * pp + 1) * 32, n - 1);
+    const float4 x0 = src.Xs[p0], x1 = src.Xs[p1];
+    X[pp] = make_float2(x0.x, x1.x);
+    Y[pp] = make_float2(x0.y, x1.y);
+    Z[pp] = make_float2(x0.z, x1.z);
+    nS[pp] = make_float2(-row_shift_estimate(rowM2, rowJ, dq, dmax2, src.perm_r[p0]),
+                         -row_shift_estimate(rowM2, rowJ, dq, dmax2, src.perm_r[p1]));
+    fs[pp] = make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int r = 0; r < kOtfRT; ++r) {
+    tm[r] = -FLT_MAX;
+    tj[r] = static_cast<int>(j0);
+    sSS[r][threadIdx.x] = 0.0;
+  }
+  const float2 nkh2 = make_float2(-kh, -kh);
+  const float kcull = kh * kCullSlack;
+  const float* Ep = vq + 2 * mpad;
+  float4* wA = sA[warp];
+  float4* wB = sB[warp];
+  float2* wE = sE[warp];
+  for (int64_t b0 = j0; b0 < j1; b0 += kCullCB) {
+    const int64_t cbk = b0 / kCullCB;
+    {
+      const float4 lo = __ldg(src.cbox + 2 * cbk), hi = __ldg(src.cbox + 2 * cbk + 1);
+      const float vmax = __ldg(src.cvmax + cbk);
+      bool live = false;
+      const float2 nk2 = make_float2(-kcull, -kcull), vm2 = make_float2(vmax, vmax);
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) {
+        const float2 bnd = __ffma2_rn(nk2, box_d2x2(X[pp], Y[pp], Z[pp], lo, hi),
+                                      __fadd2_rn(vm2, nS[pp]));
+        live |= fmaxf(bnd.x, bnd.y) >= kCullT;
+      }
+      if (!__any_sync(0xffffffffu, live)) continue;  // every exponent below -127
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < kCullCB / 32; ++h) {  // stage the block: lane -> columns lane, lane + 32
+      const int k = lane + 32 * h;
+      const int64_t jp = b0 + k;
+      if (jp < j1) {
+        const int64_t j = src.perm_c[jp];
+        const float nx = src.Yn[jp], ny = src.Yn[src.ypad + jp], nz = src.Yn[2 * src.ypad + jp];
+        const float V = vq[j];
+        wA[k] = make_float4(nx, nx, ny, ny);
+        wB[k] = make_float4(nz, nz, V, V);
+        const float E = Ep[j];
+        wE[k] = make_float2(E, E);
+      } else {  // padding: t = -inf
+        wA[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        wB[k] = make_float4(0.f, 0.f, -INFINITY, -INFINITY);
+        wE[k] = make_float2(0.f, 0.f);
+      }
+    }
+    __syncwarp();
+    for (int kb = 0; kb < kCullCB && b0 + kb < j1; kb += kOtfBlk) {
+#pragma unroll kOtfUnroll
+      for (int k = kb; k < kb + kOtfBlk; ++k) {
+        const float4 A = wA[k], B = wB[k];
+        const float2 E2 = wE[k];
+        const float2 ax = make_float2(A.x, A.y), ay = make_float2(A.z, A.w);
+        const float2 az = make_float2(B.x, B.y), V2 = make_float2(B.z, B.w);
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) {
+          const float2 dx = __fadd2_rn(X[pp], ax), dy = __fadd2_rn(Y[pp], ay),
+                       dz = __fadd2_rn(Z[pp], az);
+          const float2 c = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+          const float2 t = __ffma2_rn(c, nkh2, __fadd2_rn(V2, nS[pp]));
+          fs[pp] = __ffma2_rn(make_float2(ex2_approx(t.x), ex2_approx(t.y)), E2, fs[pp]);
+        }
+      }
+      const int jb = static_cast<int>(b0 + kb);
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) {
+        sSS[2 * pp][threadIdx.x] += otf_cvt(fs[pp].x);
+        sSS[2 * pp + 1][threadIdx.x] += otf_cvt(fs[pp].y);
+        if (fs[pp].x > tm[2 * pp]) {
+          tm[2 * pp] = fs[pp].x;
+          tj[2 * pp] = jb;
+        }
+        if (fs[pp].y > tm[2 * pp + 1]) {
+          tm[2 * pp + 1] = fs[pp].y;
+          tj[2 * pp + 1] = jb;
+        }
+        fs[pp] = make_float2(0.f, 0.f);
+      }
+    }
+  }
+  RowPart* dst = rpart + static_cast<int64_t>(blockIdx.y) * n;
+#pragma unroll
+  for (int r = 0; r < kOtfRT; ++r) {
+    const int64_t pos = rbase + r * 32;
+    if (pos < n) {
+      RowPart rp;
+      rp.t = tm[r];
+      rp.jb = tj[r];  // sorted column position (k_row_otf_fin maps it)
+      rp.s = sSS[r][threadIdx.x];
+      dst[src.perm_r[pos]] = rp;
+    }
+  }
+}
+
+// Columns: thread = 4 consecutive sorted columns, warp = 128; rows of the
+// split in blocks of kCullRB sorted rows, staged per warp when live.
+__global__ void __launch_bounds__(256, OTG_COL_OTF_MINB)
+k_col_otf_cull(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
+               const float4* __restrict__ aux, int64_t row_lo, int64_t row_hi,
+               int64_t rows_per_split, double* __restrict__ part, int64_t mpad,
+               const Ctrl* __restrict__ ctrl) {
+  pdl_wait();
+  if (ctrl->done) return;
+  constexpr int NT = 256, kW = NT / 32;
+  __shared__ float4 sX[kW][kCullRB];
+  __shared__ float4 sAx[kW][kCullRB];
+  __shared__ double sAcc[4][NT];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x;
+  const int64_t j0 = 4 * q;  // sorted column positions j0 .. j0 + 3
+  const int64_t i0 = row_lo + static_cast<int64_t>(blockIdx.y) * rows_per_split;
+  const int64_t i1 = min(i0 + rows_per_split, row_hi);
+  float Vc[4], vf[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double pj = (j0 + k < m) ? p[src.perm_c[j0 + k]] : 0.0;
+    split_q(pj * kLog2e, Vc[k], vf[k]);
+  }
+  YQ y4;
+  y4.x = y4.y = y4.z = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (j0 < m) load_y4<true>(src, q, y4);
+  const float2 Vc01 = make_float2(Vc[0], Vc[1]), Vc23 = make_float2(Vc[2], Vc[3]);
+  const float2 nkh2 = make_float2(-kh, -kh), nkl2 = make_float2(0.f, 0.f);
+  float2 acc01 = make_float2(0.f, 0.f), acc23 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) sAcc[e][threadIdx.x] = 0.0;
+  const float kcull = kh * kCullSlack;
+  const float yx[4] = {-y4.x.x, -y4.x.y, -y4.x.z, -y4.x.w};
+  const float yy[4] = {-y4.y.x, -y4.y.y, -y4.y.z, -y4.y.w};
+  const float yz[4] = {-y4.z.x, -y4.z.y, -y4.z.z, -y4.z.w};
+  // (columns past m: V = 0 at the origin -- they may keep a block live, never wrong)
+  float4* wX = sX[warp];
+  float4* wAx = sAx[warp];
+  for (int64_t r0 = i0; r0 < i1; r0 += kCullRB) {
+    const int64_t rb = r0 / kCullRB;
+    {
+      const float4 lo = __ldg(src.rbox + 2 * rb), hi = __ldg(src.rbox + 2 * rb + 1);
+      const float nm = __ldg(src.rnegm + rb);
+      bool live = false;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        live |= fmaf(-kcull, box_d2(yx[e], yy[e], yz[e], lo, hi), Vc[e] + nm) >= kCullT;
+      if (!__any_sync(0xffffffffu, live)) continue;  // every exponent below -127
+    }
+    const int rn = static_cast<int>(min(static_cast<int64_t>(kCullRB), i1 - r0));
+    __syncwarp();
+    if (lane < kCullRB) {
+      if (lane < rn) {
+        const int64_t sp = r0 + lane;
+        float4 ax = aux[src.perm_r[sp]];
+        ax.z = ax.y == 0.0f ? ax.z : ax.z * exp2f(-ax.y);  // w' = w 2^-mf
+        wX[lane] = src.Xs[sp];
+        wAx[lane] = ax;
+      } else {  // (never read: rn bounds the loop)
+        wX[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+        wAx[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    __syncwarp();
+    if (rn == kCullRB) {
+#pragma unroll
+      for (int h = 0; h < kCullRB; h += kColUnroll) {
+        float4 c[kColUnroll];
+#pragma unroll
+        for (int r = 0; r < kColUnroll; ++r) c[r] = cost_quad<true>(src, 0, q, wX[h + r], y4);
+#pragma unroll
+        for (int r = 0; r < kColUnroll; ++r)
+          col_quad_step_nf(c[r], wAx[h + r], Vc01, Vc23, nkh2, nkl2, acc01, acc23);
+      }
+    } else {
+      for (int r = 0; r < rn; ++r) {
+        const float4 cv = cost_quad<true>(src, 0, q, wX[r], y4);
+        col_quad_step_nf(cv, wAx[r], Vc01, Vc23, nkh2, nkl2, acc01, acc23);
+      }
+    }
+    // fp32 partials into the fp64 totals once per block (kCullRB = kFlushRows rows)
+    sAcc[0][threadIdx.x] += otf_cvt(acc01.x);
+    sAcc[1][threadIdx.x] += otf_cvt(acc01.y);
+    sAcc[2][threadIdx.x] += otf_cvt(acc23.x);
+    sAcc[3][threadIdx.x] += otf_cvt(acc23.y);
+    acc01 = make_float2(0.f, 0.f);
+    acc23 = make_float2(0.f, 0.f);
+  }
+  double* dst = part + static_cast<int64_t>(blockIdx.y) * mpad;
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    if (j0 + e < m) dst[src.perm_c[j0 + e]] = sAcc[e][threadIdx.x] * exp2(static_cast<double>(vf[e]));
+}
+
 template <bool OTF, int NT, bool CULL = false>
 __global__ void __launch_bounds__(NT, (!OTF && NT == 256) ? OTG_COL_MINB
                                       : (OTF && NT == 256) ? OTG_COL_OTF_MINB : 1)
@@ -2634,6 +2882,10 @@ void configure_sweeps(Problem& P) {
     }
   }
   splits = std::max<int64_t>(1, std::min<int64_t>(splits, max_splits));
+  // culled on-the-fly column pass: per-CTA work varies with the geometry, so
+  // many more CTAs than slots let the scheduler balance them
+  if (P.cull && P.storage == OTG_STORE_ON_THE_FLY && env_s <= 0)
+    splits = std::max<int64_t>(1, std::min<int64_t>(OTG_CULL_COL_SPLITS, (shard_rows + 255) / 256));
   P.col_splits = static_cast<int>(splits);
   P.rows_per_split = (shard_rows + splits - 1) / splits;
   if (P.cull) P.rows_per_split = (P.rows_per_split + kCullRB - 1) / kCullRB * kCullRB;  // whole blocks
@@ -2647,7 +2899,7 @@ void configure_sweeps(Problem& P) {
     OTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.device));
     const int64_t rb = (P.n_local + kRowThreads * kOtfRT - 1) / (kRowThreads * kOtfRT);
     const int64_t slots = std::max<int64_t>(1, static_cast<int64_t>(occ) * sms);
-    int64_t S = (8 * slots + rb - 1) / rb;
+    int64_t S = (OTG_CULL_ROW_WAVES * (P.cull ? 1 : 0) + 8 * (P.cull ? 0 : 1)) * slots / rb + 1;
     S = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(S, 128), (P.m + 255) / 256));
     int64_t cps = (P.m + S - 1) / S;
     cps = (cps + kOtfBlk - 1) / kOtfBlk * kOtfBlk;
@@ -2789,8 +3041,8 @@ void launch_row_pass(Problem& P) {
         launch_k(k_cull_cols, static_cast<unsigned>((P.m + 8 * kCullCB - 1) / (8 * kCullCB)), 256, 0,
                  P.stream, P.m, static_cast<const float*>(P.vq), static_cast<const int*>(P.perm_c),
                  P.cvmax, static_cast<const Ctrl*>(P.ctrl));
-        launch_k(k_row_otf<true>, g, kRowThreads, 0, P.stream, cull_src(P), P.n_local, P.m,
-                 static_cast<const float*>(P.vq), static_cast<const double*>(P.dq), P.mpad, kh, kl,
+        launch_k(k_row_otf_cull, g, kRowThreads, 0, P.stream, cull_src(P), P.n_local, P.m,
+                 static_cast<const float*>(P.vq), static_cast<const double*>(P.dq), P.mpad, kh,
                  static_cast<const double*>(P.rowM2), static_cast<const int*>(P.rowJ),
                  P.row_cols_per_split, rp, static_cast<const Ctrl*>(P.ctrl));
         fsrc.perm_c = P.perm_c;  // (the heaviest block's columns, in sorted order)
@@ -2845,8 +3097,8 @@ void launch_col_pass(Problem& P) {
         launch_k(k_cull_rows, static_cast<unsigned>((P.n_local + 16 * kCullRB - 1) / (16 * kCullRB)),
                  256, 0, P.stream, P.n_local, static_cast<const float4*>(P.aux),
                  static_cast<const int*>(P.perm_r), P.rnegm, static_cast<const Ctrl*>(P.ctrl));
-        launch_k(k_col_fast<true, 256, true>, grid, 256, 0, P.stream, cull_src(P), P.m, P.p, kh, kl,
-                 P.aux, lo, hi, P.rows_per_split, part, P.mpad, P.ctrl, P.fused);
+        launch_k(k_col_otf_cull, grid, 256, 0, P.stream, cull_src(P), P.m, P.p, kh, P.aux, lo, hi,
+                 P.rows_per_split, part, P.mpad, P.ctrl);
       } else if (NT == 512) {
         if (otf) { OTG_COL(true, 512); } else { OTG_COL(false, 512); }
       } else if (NT == 256) {

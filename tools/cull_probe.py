@@ -113,3 +113,24 @@ for CBk in (16, 64):
             kept_t += int(live[:L].view(-1, RTk, nbk).any(1).sum()) * RTk + int(live[L:].any(0).sum()) * (live.shape[0] - L)
         print(f"per-row box test, {CBk}-column blocks: row-level kept {kept_r / n / nbk:.4f}, "
               f"{RTk}-row tiles kept {kept_t / n / nbk:.4f}")
+
+# column pass: per-column point-to-box test against 16/32-row sorted blocks,
+# skip decided per warp of W consecutive sorted columns
+for RBk in (16, 32):
+    rlo, rhi = boxes(Xs, RBk)
+    nmax = tile_red(-Ss, RBk, "max")
+    nrb = rlo.shape[0]
+    for W in (32, 64, 128):
+        kept_c = 0
+        kept_w = 0
+        for k0 in range(0, n, 4096):
+            cols = torch.arange(k0, min(n, k0 + 4096), device=dev)
+            yc = Ys[cols]
+            gap = torch.clamp(torch.maximum(rlo[None] - yc[:, None], yc[:, None] - rhi[None]), min=0)
+            d2 = (gap.double() ** 2).sum(-1)
+            live = (Vs[cols][:, None] + nmax[None] - kh * d2) >= -128  # cols x row blocks
+            kept_c += int(live.sum())
+            L = live.shape[0] // W * W
+            kept_w += int(live[:L].view(-1, W, nrb).any(1).sum()) * W + int(live[L:].any(0).sum()) * (live.shape[0] - L)
+        print(f"column pass, {RBk}-row blocks: column-level kept {kept_c / n / nrb:.4f}, "
+              f"{W}-column warps kept {kept_w / n / nrb:.4f}")
