@@ -406,6 +406,16 @@ otg_status otg_gen_config(int cfg, int64_t n, int64_t m, uint64_t seed, double* 
 otg_status otg_gen_config4(int64_t count, uint64_t seed, int64_t d, int32_t* n, int32_t* m,
                            float* x_cat, float* y_cat);
 
+/* ---- test hooks ---- */
+/* On-the-fly handles visit rows and columns in Morton order in their
+ * steady-state sweeps and skip blocks whose every exponent is provably below
+ * -127 (ex2.approx.ftz returns +0 there: the skip is bitwise invisible).
+ * mode 1 (default): culled; 0: same sorted order, every block visited (the
+ * bitwise reference for the skip); -1: handles created afterwards keep the
+ * caller's order (the dense original sweeps).  Returns the previous mode.
+ * No reference counterpart (internal to the GPU sweeps). */
+int otg_debug_cull(int mode);
+
 #ifdef __cplusplus
 }
 #endif

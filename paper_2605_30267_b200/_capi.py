@@ -123,6 +123,7 @@ SIGNATURES = {
     "otg_gen_synthetic_instance": (C.c_int, [I64, I64, C.c_uint64, VP, VP, VP]),
     "otg_gen_config": (C.c_int, [C.c_int, I64, I64, C.c_uint64, VP, VP, VP]),
     "otg_gen_config4": (C.c_int, [I64, C.c_uint64, I64, VP, VP, VP, VP]),
+    "otg_debug_cull": (C.c_int, [C.c_int]),
 }
 
 _lib = None

@@ -271,10 +271,12 @@ static void upload_marginals(Problem& P, const double* a, const double* b) {
 // columns, 16 sorted rows).  Only the two steady-state on-the-fly sweep
 // kernels visit rows / columns in these orders; every array the API sees
 // stays in the caller's order.
+int& cull_mode();  // sweep.cu (test hook otg_debug_cull)
+
 static void setup_cull(Problem& P, const std::vector<float>& hx, const std::vector<float>& hy) {
   constexpr int64_t kCB = 64, kRB = 16;
   const int64_t n = P.n_local, m = P.m;
-  if (!OTG_CULL || n < 4096 || m < 4096) return;
+  if (!OTG_CULL || cull_mode() < 0 || n < 4096 || m < 4096) return;
   float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
   for (int64_t i = 0; i < n; ++i)
     for (int k = 0; k < 3; ++k) lo[k] = std::min(lo[k], hx[i * 4 + k]), hi[k] = std::max(hi[k], hx[i * 4 + k]);

@@ -345,6 +345,7 @@ struct CostSrc {
   const float* cvmax;  // per kCullCB sorted columns: max V (this evaluation)
   const float4* rbox;  // per kCullRB sorted rows: (lo, hi) boxes
   const float* rnegm;  // per kCullRB sorted rows: max -M (this evaluation)
+  int skip;            // 0: visit every block in the sorted order (test hook)
 };
 
 constexpr int kCullCB = 64;  // columns per culling block (row pass)
@@ -1572,7 +1573,7 @@ k_row_otf_cull(const CostSrc src, int64_t n, int64_t m, const float* __restrict_
                                       __fadd2_rn(vm2, nS[pp]));
         live |= fmaxf(bnd.x, bnd.y) >= kCullT;
       }
-      if (!__any_sync(0xffffffffu, live)) continue;  // every exponent below -127
+      if (src.skip && !__any_sync(0xffffffffu, live)) continue;  // every exponent below -127
     }
     __syncwarp();
 #pragma unroll
@@ -1689,7 +1690,7 @@ k_col_otf_cull(const CostSrc src, int64_t m, const double* __restrict__ p, float
 #pragma unroll
       for (int e = 0; e < 4; ++e)
         live |= fmaf(-kcull, box_d2(yx[e], yy[e], yz[e], lo, hi), Vc[e] + nm) >= kCullT;
-      if (!__any_sync(0xffffffffu, live)) continue;  // every exponent below -127
+      if (src.skip && !__any_sync(0xffffffffu, live)) continue;  // every exponent below -127
     }
     const int rn = static_cast<int>(min(static_cast<int64_t>(kCullRB), i1 - r0));
     __syncwarp();
@@ -2911,6 +2912,14 @@ void configure_sweeps(Problem& P) {
 }
 
 static CostSrc cost_src(const Problem& P);
+// Test hook (otg_debug_cull): 1 = culled sweeps (default), 0 = the same
+// sorted sweeps visiting every block, -1 = handles created from now on keep
+// the caller's order (no culling set up).
+int& cull_mode() {
+  static int mode = 1;
+  return mode;
+}
+
 // the culled sweeps' view: sorted coordinates, orders, block boxes / bounds
 static CostSrc cull_src(const Problem& P) {
   CostSrc s = cost_src(P);
@@ -2922,6 +2931,7 @@ static CostSrc cull_src(const Problem& P) {
   s.cvmax = P.cvmax;
   s.rbox = reinterpret_cast<const float4*>(P.rbox);
   s.rnegm = P.rnegm;
+  s.skip = cull_mode() > 0 ? 1 : 0;
   return s;
 }
 
@@ -2938,6 +2948,7 @@ static CostSrc cost_src(const Problem& P) {
   s.Xs = nullptr;
   s.cbox = s.rbox = nullptr;
   s.cvmax = s.rnegm = nullptr;
+  s.skip = 0;
   return s;
 }
 
@@ -3355,3 +3366,9 @@ void launch_apply(Problem& P) {
 int64_t rowpart_len(const Problem& P) { return row_blocks(P); }
 
 }  // namespace otg
+
+extern "C" int otg_debug_cull(int mode) {
+  const int prev = otg::cull_mode();
+  otg::cull_mode() = mode;
+  return prev;
+}
