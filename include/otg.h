@@ -415,6 +415,11 @@ otg_status otg_gen_config4(int64_t count, uint64_t seed, int64_t d, int32_t* n, 
  * caller's order (the dense original sweeps).  Returns the previous mode.
  * No reference counterpart (internal to the GPU sweeps). */
 int otg_debug_cull(int mode);
+/* Fraction of (warp tile x block) pairs the culled sweeps visit at the
+ * handle's current state: out[0] row pass (256 sorted rows x 64 sorted
+ * columns), out[1] column pass (128 sorted columns x 16 sorted rows); -1 when
+ * the handle is not culled.  Diagnostic (bench roofline). */
+otg_status otg_cull_stats(otg_problem h, double out[2]);
 
 #ifdef __cplusplus
 }

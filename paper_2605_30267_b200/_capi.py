@@ -124,6 +124,7 @@ SIGNATURES = {
     "otg_gen_config": (C.c_int, [C.c_int, I64, I64, C.c_uint64, VP, VP, VP]),
     "otg_gen_config4": (C.c_int, [I64, C.c_uint64, I64, VP, VP, VP, VP]),
     "otg_debug_cull": (C.c_int, [C.c_int]),
+    "otg_cull_stats": (C.c_int, [H, VP]),
 }
 
 _lib = None

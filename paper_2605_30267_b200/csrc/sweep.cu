@@ -1428,6 +1428,43 @@ k_cull_rows(int64_t n, const float4* __restrict__ aux, const int* __restrict__ p
   if (l == 0 && b * kCullRB < n) rnegm[b] = v;
 }
 
+// otg_cull_stats: the fraction of (warp tile x block) pairs the culled sweeps
+// would visit at the handle's current state -- the same bound, per pair.
+__global__ void k_cull_prep(int64_t n, int64_t m, const int* __restrict__ perm_r,
+                            const int* __restrict__ perm_c, const double* __restrict__ rowM2,
+                            const int* __restrict__ rowJ, const double* __restrict__ dq,
+                            const double* __restrict__ p, const float* __restrict__ Yns,
+                            int64_t ypad, const Ctrl* __restrict__ ctrl, float* __restrict__ nS,
+                            float* __restrict__ Vc, float4* __restrict__ Ys) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < n) nS[t] = -row_shift_estimate(rowM2, rowJ, dq, ctrl->dmax2, perm_r[t]);
+  if (t < m) {
+    float hi, lo;
+    split_q(p[perm_c[t]] * kLog2e, hi, lo);
+    Vc[t] = hi;
+    Ys[t] = make_float4(-Yns[t], -Yns[ypad + t], -Yns[2 * ypad + t], 0.f);
+  }
+}
+__global__ void k_cull_stat(int64_t npts, const float4* __restrict__ pts,
+                            const float* __restrict__ val, int tile, const float4* __restrict__ box,
+                            const float* __restrict__ bnd, int64_t nblocks, float kcull,
+                            unsigned long long* __restrict__ kept) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t groups = (npts + tile - 1) / tile;
+  if (idx >= groups * nblocks) return;
+  const int64_t g = idx / nblocks, b = idx % nblocks;
+  const float4 lo = box[2 * b], hi = box[2 * b + 1];
+  const float bb = bnd[b];
+  bool live = false;
+  for (int k = 0; k < tile && !live; ++k) {
+    const int64_t s = g * tile + k;
+    if (s >= npts) break;
+    const float4 q = pts[s];
+    live = fmaf(-kcull, box_d2(q.x, q.y, q.z, lo, hi), bb + val[s]) >= kCullT;
+  }
+  if (live) atomicAdd(kept, 1ull);
+}
+
 
 // ------------------------------------------------------------------ K2 ----
 // fp64: partial c_j = sum_i exp(((-C'_ij) + p_j) - M_i) * w_i  (dual.cpp:36,41)
@@ -3371,4 +3408,55 @@ extern "C" int otg_debug_cull(int mode) {
   const int prev = otg::cull_mode();
   otg::cull_mode() = mode;
   return prev;
+}
+
+extern "C" otg_status otg_cull_stats(otg_problem h, double out[2]) {
+  using namespace otg;
+  return guard([&] {
+    if (!out) fail(OTG_E_DIMENSION, "out is NULL");
+    if (!h) fail(OTG_E_DIMENSION, "NULL problem handle");
+    Problem& P = h->P;
+    OTG_CUDA(cudaSetDevice(P.device));
+    out[0] = out[1] = -1.0;
+    if (!P.cull) return;
+    const int64_t n = P.n_local, m = P.m;
+    float *nS = nullptr, *Vc = nullptr;
+    float4* Ys = nullptr;
+    unsigned long long* kept = nullptr;
+    OTG_CUDA(cudaMalloc(&nS, n * sizeof(float)));
+    OTG_CUDA(cudaMalloc(&Vc, m * sizeof(float)));
+    OTG_CUDA(cudaMalloc(&Ys, m * sizeof(float4)));
+    OTG_CUDA(cudaMalloc(&kept, 2 * sizeof(unsigned long long)));
+    OTG_CUDA(cudaMemsetAsync(kept, 0, 2 * sizeof(unsigned long long), P.stream));
+    const int64_t big = std::max(n, m);
+    k_cull_prep<<<static_cast<unsigned>((big + 255) / 256), 256, 0, P.stream>>>(
+        n, m, P.perm_r, P.perm_c, static_cast<const double*>(P.rowM2),
+        static_cast<const int*>(P.rowJ), static_cast<const double*>(P.dq), P.p, P.Yns, P.mpad,
+        static_cast<const Ctrl*>(P.ctrl), nS, Vc, Ys);
+    k_cull_cols<<<static_cast<unsigned>((m + 8 * kCullCB - 1) / (8 * kCullCB)), 256, 0, P.stream>>>(
+        m, static_cast<const float*>(P.vq), P.perm_c, P.cvmax, static_cast<const Ctrl*>(P.ctrl));
+    k_cull_rows<<<static_cast<unsigned>((n + 16 * kCullRB - 1) / (16 * kCullRB)), 256, 0, P.stream>>>(
+        n, static_cast<const float4*>(P.aux), P.perm_r, P.rnegm, static_cast<const Ctrl*>(P.ctrl));
+    const float kh = static_cast<float>(P.kappa * kLog2e);
+    const float kcull = kh * kCullSlack;
+    const int64_t rt = 32 * kOtfRT, cbn = (m + kCullCB - 1) / kCullCB;
+    const int64_t rp = ((n + rt - 1) / rt) * cbn;
+    k_cull_stat<<<static_cast<unsigned>((rp + 255) / 256), 256, 0, P.stream>>>(
+        n, reinterpret_cast<const float4*>(P.Xs), nS, static_cast<int>(rt),
+        reinterpret_cast<const float4*>(P.cbox), P.cvmax, cbn, kcull, kept);
+    const int64_t ct = 128, rbn = (n + kCullRB - 1) / kCullRB;
+    const int64_t cp = ((m + ct - 1) / ct) * rbn;
+    k_cull_stat<<<static_cast<unsigned>((cp + 255) / 256), 256, 0, P.stream>>>(
+        m, Ys, Vc, static_cast<int>(ct), reinterpret_cast<const float4*>(P.rbox), P.rnegm, rbn,
+        kcull, kept + 1);
+    unsigned long long hk[2] = {0, 0};
+    OTG_CUDA(cudaMemcpyAsync(hk, kept, sizeof hk, cudaMemcpyDeviceToHost, P.stream));
+    OTG_CUDA(cudaStreamSynchronize(P.stream));
+    cudaFree(nS);
+    cudaFree(Vc);
+    cudaFree(Ys);
+    cudaFree(kept);
+    out[0] = static_cast<double>(hk[0]) / static_cast<double>(rp);
+    out[1] = static_cast<double>(hk[1]) / static_cast<double>(cp);
+  });
 }

@@ -970,6 +970,15 @@ def time_sweeps(p: TransportProblem, v, reps=10):
     return list(ms), list(by)
 
 
+def cull_stats(p: TransportProblem):
+    """On-the-fly handles with culled sweeps: the fraction of (warp tile x
+    block) pairs the row / column pass visits at the handle's current state
+    (otg_cull_stats); (-1, -1) when the handle is not culled."""
+    out = (C.c_double * 2)()
+    _check(_lib().otg_cull_stats(p.handle.raw, out))
+    return float(out[0]), float(out[1])
+
+
 # ------------------------------------------------------------ inputs -----
 
 

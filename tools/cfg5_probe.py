@@ -17,4 +17,4 @@ t = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=min(it
                       time_sweeps=True)
 print(f"n={n} iters={r.iterations} it/s {r.iterations / r.device_seconds:.2f} "
       f"row {1e3 * t.row_pass_seconds / t.evaluations:.2f} ms col {1e3 * t.col_pass_seconds / t.evaluations:.2f} ms "
-      f"| v[0:3] {r.potentials.v[:3]} viol {r.final_violation:.3e} cull {p.handle.info.__dict__.get('cull', '?') if hasattr(p.handle.info, '__dict__') else '?'}")
+      f"| v[0:3] {r.potentials.v[:3]} viol {r.final_violation:.3e} blocks visited (row, col) {ot.cull_stats(p)}")
