@@ -258,6 +258,8 @@ struct Problem {
   float* rbox = nullptr;  // 2 float4 per 16 sorted rows
   float* cvmax = nullptr;
   float* rnegm = nullptr;
+  float* ves = nullptr;   // float2 per sorted column: (V, 2^F), per evaluation
+  float* auxs = nullptr;  // float4 per sorted row: aux (w pre-scaled), per evaluation
 
   // marginals (fp64)
   double *a = nullptr, *loga = nullptr, *b = nullptr, *logb = nullptr;

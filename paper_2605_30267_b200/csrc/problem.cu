@@ -145,7 +145,7 @@ void problem_free(Problem& P) {
                   P.y, P.grad, P.prev_grad,
                   P.prev_x, P.prev_y, P.flag_idx, P.fb_cols, P.fb_part, P.part, P.e1_part,
                   P.e2_part, P.epi_part, P.sp_rec, P.sp_bad_rows, P.sp_bad_count, P.ctrl, P.trace, P.vstar, P.bounds, P.fbA, P.fbS, P.fbT, P.red, P.sp_sums, P.sp_cnt,
-                  P.perm_r, P.perm_c, P.Xs, P.Yns, P.cbox, P.rbox, P.cvmax, P.rnegm};
+                  P.perm_r, P.perm_c, P.Xs, P.Yns, P.cbox, P.rbox, P.cvmax, P.rnegm, P.ves, P.auxs};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (P.ctrl_host) cudaFreeHost(P.ctrl_host);
@@ -332,6 +332,8 @@ static void setup_cull(Problem& P, const std::vector<float>& hx, const std::vect
   P.rbox = dalloc<float>(P, rb.size());
   P.cvmax = dalloc<float>(P, cb.size() / 8);
   P.rnegm = dalloc<float>(P, rb.size() / 8);
+  P.ves = dalloc<float>(P, 2 * m);
+  P.auxs = dalloc<float>(P, 4 * n);
   OTG_CUDA(cudaMemcpyAsync(P.perm_r, pr.data(), n * 4, cudaMemcpyHostToDevice, P.stream));
   OTG_CUDA(cudaMemcpyAsync(P.perm_c, pc.data(), m * 4, cudaMemcpyHostToDevice, P.stream));
   OTG_CUDA(cudaMemcpyAsync(P.Xs, xs.data(), xs.size() * 4, cudaMemcpyHostToDevice, P.stream));

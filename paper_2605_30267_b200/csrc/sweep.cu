@@ -346,6 +346,8 @@ struct CostSrc {
   const float4* rbox;  // per kCullRB sorted rows: (lo, hi) boxes
   const float* rnegm;  // per kCullRB sorted rows: max -M (this evaluation)
   int skip;            // 0: visit every block in the sorted order (test hook)
+  const float2* ves;   // per sorted column: (V, 2^F) of this evaluation
+  const float4* auxs;  // per sorted row: aux with w' = w 2^-mf, this evaluation
 };
 
 constexpr int kCullCB = 64;  // columns per culling block (row pass)
@@ -1399,8 +1401,8 @@ k_row_otf_fin(const CostSrc src, int64_t n, int64_t m, const float* __restrict__
 // potential (base 2, hi part) of each 64-column sorted block, and the largest
 // -M (negated row shift) of each 16-row sorted block.
 __global__ void __launch_bounds__(256)
-k_cull_cols(int64_t m, const float* __restrict__ vq, const int* __restrict__ perm_c,
-            float* __restrict__ cvmax, const Ctrl* __restrict__ ctrl) {
+k_cull_cols(int64_t m, int64_t mpad, const float* __restrict__ vq, const int* __restrict__ perm_c,
+            float* __restrict__ cvmax, float2* __restrict__ ves, const Ctrl* __restrict__ ctrl) {
   pdl_wait();
   if (ctrl->done) return;
   const int64_t b = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
@@ -1409,7 +1411,12 @@ k_cull_cols(int64_t m, const float* __restrict__ vq, const int* __restrict__ per
   float v = -INFINITY;
   for (int k = lane; k < kCullCB; k += 32) {
     const int64_t s = b * kCullCB + k;
-    if (s < m) v = fmaxf(v, vq[perm_c[s]]);
+    if (s < m) {
+      const int64_t j = perm_c[s];
+      const float V = vq[j];
+      v = fmaxf(v, V);
+      if (ves) ves[s] = make_float2(V, vq[2 * mpad + j]);  // (V, 2^F) in sorted order
+    }
   }
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   if (lane == 0) cvmax[b] = v;
@@ -1417,13 +1424,21 @@ k_cull_cols(int64_t m, const float* __restrict__ vq, const int* __restrict__ per
 
 __global__ void __launch_bounds__(256)
 k_cull_rows(int64_t n, const float4* __restrict__ aux, const int* __restrict__ perm_r,
-            float* __restrict__ rnegm, const Ctrl* __restrict__ ctrl) {
+            float* __restrict__ rnegm, float4* __restrict__ auxs, const Ctrl* __restrict__ ctrl) {
   pdl_wait();
   if (ctrl->done) return;
   const int64_t b = static_cast<int64_t>(blockIdx.x) * 16 + (threadIdx.x >> 4);
   const int l = threadIdx.x & 15;
   const int64_t s = b * kCullRB + l;
-  float v = s < n ? -aux[perm_r[s]].x : -INFINITY;
+  float v = -INFINITY;
+  if (s < n) {
+    float4 ax = aux[perm_r[s]];
+    v = -ax.x;
+    if (auxs) {  // sorted copy for the column pass, weight pre-scaled w' = w 2^-mf
+      ax.z = ax.y == 0.0f ? ax.z : ax.z * exp2f(-ax.y);
+      auxs[s] = ax;
+    }
+  }
   for (int o = 8; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   if (l == 0 && b * kCullRB < n) rnegm[b] = v;
 }
@@ -1593,7 +1608,6 @@ k_row_otf_cull(const CostSrc src, int64_t n, int64_t m, const float* __restrict_
   }
   const float2 nkh2 = make_float2(-kh, -kh);
   const float kcull = kh * kCullSlack;
-  const float* Ep = vq + 2 * mpad;
   float4* wA = sA[warp];
   float4* wB = sB[warp];
   float2* wE = sE[warp];
@@ -1618,13 +1632,11 @@ k_row_otf_cull(const CostSrc src, int64_t n, int64_t m, const float* __restrict_
       const int k = lane + 32 * h;
       const int64_t jp = b0 + k;
       if (jp < j1) {
-        const int64_t j = src.perm_c[jp];
         const float nx = src.Yn[jp], ny = src.Yn[src.ypad + jp], nz = src.Yn[2 * src.ypad + jp];
-        const float V = vq[j];
+        const float2 ve = src.ves[jp];
         wA[k] = make_float4(nx, nx, ny, ny);
-        wB[k] = make_float4(nz, nz, V, V);
-        const float E = Ep[j];
-        wE[k] = make_float2(E, E);
+        wB[k] = make_float4(nz, nz, ve.x, ve.x);
+        wE[k] = make_float2(ve.y, ve.y);
       } else {  // padding: t = -inf
         wA[k] = make_float4(0.f, 0.f, 0.f, 0.f);
         wB[k] = make_float4(0.f, 0.f, -INFINITY, -INFINITY);
@@ -1734,10 +1746,8 @@ k_col_otf_cull(const CostSrc src, int64_t m, const double* __restrict__ p, float
     if (lane < kCullRB) {
       if (lane < rn) {
         const int64_t sp = r0 + lane;
-        float4 ax = aux[src.perm_r[sp]];
-        ax.z = ax.y == 0.0f ? ax.z : ax.z * exp2f(-ax.y);  // w' = w 2^-mf
         wX[lane] = src.Xs[sp];
-        wAx[lane] = ax;
+        wAx[lane] = src.auxs[sp];  // (w' = w 2^-mf, sorted: k_cull_rows)
       } else {  // (never read: rn bounds the loop)
         wX[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
         wAx[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -2969,6 +2979,8 @@ static CostSrc cull_src(const Problem& P) {
   s.rbox = reinterpret_cast<const float4*>(P.rbox);
   s.rnegm = P.rnegm;
   s.skip = cull_mode() > 0 ? 1 : 0;
+  s.ves = reinterpret_cast<const float2*>(P.ves);
+  s.auxs = reinterpret_cast<const float4*>(P.auxs);
   return s;
 }
 
@@ -2986,6 +2998,8 @@ static CostSrc cost_src(const Problem& P) {
   s.cbox = s.rbox = nullptr;
   s.cvmax = s.rnegm = nullptr;
   s.skip = 0;
+  s.ves = nullptr;
+  s.auxs = nullptr;
   return s;
 }
 
@@ -3087,8 +3101,9 @@ void launch_row_pass(Problem& P) {
       CostSrc fsrc = src;
       if (P.cull) {
         launch_k(k_cull_cols, static_cast<unsigned>((P.m + 8 * kCullCB - 1) / (8 * kCullCB)), 256, 0,
-                 P.stream, P.m, static_cast<const float*>(P.vq), static_cast<const int*>(P.perm_c),
-                 P.cvmax, static_cast<const Ctrl*>(P.ctrl));
+                 P.stream, P.m, P.mpad, static_cast<const float*>(P.vq),
+                 static_cast<const int*>(P.perm_c), P.cvmax, reinterpret_cast<float2*>(P.ves),
+                 static_cast<const Ctrl*>(P.ctrl));
         launch_k(k_row_otf_cull, g, kRowThreads, 0, P.stream, cull_src(P), P.n_local, P.m,
                  static_cast<const float*>(P.vq), static_cast<const double*>(P.dq), P.mpad, kh,
                  static_cast<const double*>(P.rowM2), static_cast<const int*>(P.rowJ),
@@ -3144,7 +3159,8 @@ void launch_col_pass(Problem& P) {
         // culled on-the-fly column pass (sorted rows / columns, exact skips)
         launch_k(k_cull_rows, static_cast<unsigned>((P.n_local + 16 * kCullRB - 1) / (16 * kCullRB)),
                  256, 0, P.stream, P.n_local, static_cast<const float4*>(P.aux),
-                 static_cast<const int*>(P.perm_r), P.rnegm, static_cast<const Ctrl*>(P.ctrl));
+                 static_cast<const int*>(P.perm_r), P.rnegm, reinterpret_cast<float4*>(P.auxs),
+                 static_cast<const Ctrl*>(P.ctrl));
         launch_k(k_col_otf_cull, grid, 256, 0, P.stream, cull_src(P), P.m, P.p, kh, P.aux, lo, hi,
                  P.rows_per_split, part, P.mpad, P.ctrl);
       } else if (NT == 512) {
@@ -3434,9 +3450,11 @@ extern "C" otg_status otg_cull_stats(otg_problem h, double out[2]) {
         static_cast<const int*>(P.rowJ), static_cast<const double*>(P.dq), P.p, P.Yns, P.mpad,
         static_cast<const Ctrl*>(P.ctrl), nS, Vc, Ys);
     k_cull_cols<<<static_cast<unsigned>((m + 8 * kCullCB - 1) / (8 * kCullCB)), 256, 0, P.stream>>>(
-        m, static_cast<const float*>(P.vq), P.perm_c, P.cvmax, static_cast<const Ctrl*>(P.ctrl));
+        m, P.mpad, static_cast<const float*>(P.vq), P.perm_c, P.cvmax, nullptr,
+        static_cast<const Ctrl*>(P.ctrl));
     k_cull_rows<<<static_cast<unsigned>((n + 16 * kCullRB - 1) / (16 * kCullRB)), 256, 0, P.stream>>>(
-        n, static_cast<const float4*>(P.aux), P.perm_r, P.rnegm, static_cast<const Ctrl*>(P.ctrl));
+        n, static_cast<const float4*>(P.aux), P.perm_r, P.rnegm, nullptr,
+        static_cast<const Ctrl*>(P.ctrl));
     const float kh = static_cast<float>(P.kappa * kLog2e);
     const float kcull = kh * kCullSlack;
     const int64_t rt = 32 * kOtfRT, cbn = (m + kCullCB - 1) / kCullCB;
