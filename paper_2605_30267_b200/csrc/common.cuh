@@ -41,6 +41,15 @@
 #ifndef OTG_CULL_ROW_WAVES
 #define OTG_CULL_ROW_WAVES 16   // culled on-the-fly row pass: waves of column splits
 #endif
+#ifndef OTG_CULL_ROW_T
+#define OTG_CULL_ROW_T 128  // culled row pass: threads per CTA (warps are independent)
+#endif
+#ifndef OTG_CULL_RT
+#define OTG_CULL_RT 4       // culled row pass: rows per thread (warp tile = 32 x this)
+#endif
+#ifndef OTG_CULL_COL_T
+#define OTG_CULL_COL_T 128  // culled column pass: threads per CTA
+#endif
 #ifndef OTG_FIN_SORTED_FB
 #define OTG_FIN_SORTED_FB 0  // k_finalize's folded fallback: column-sorted work items (32 KB smem)
 #endif

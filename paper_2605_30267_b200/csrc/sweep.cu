@@ -351,6 +351,8 @@ struct CostSrc {
 };
 
 constexpr int kCullCB = 64;  // columns per culling block (row pass)
+constexpr int kCullRowT = OTG_CULL_ROW_T;  // threads per CTA of the culled row pass (warp-independent)
+constexpr int kCullColT = OTG_CULL_COL_T;  // threads per CTA of the culled column pass
 constexpr int kCullRB = 16;  // rows per culling block (column pass)
 constexpr float kCullT = -127.0f;  // bound below which a block is skipped (FTZ below -126)
 constexpr float kCullSlack = 1.0f - 1.0f / 65536.0f;  // relative slack on the box distance
@@ -1567,28 +1569,29 @@ __device__ __forceinline__ void flush_acc(float2& acc01, float2& acc23, double* 
 
 // Rows: warp = 256 consecutive sorted rows (8 per lane, 4 packed pairs);
 // blocks of kCullCB sorted columns, flushed / max-tracked per kOtfBlk.
-__global__ void __launch_bounds__(kRowThreads, OTG_ROW_OTF_MINB)
+__global__ void __launch_bounds__(kCullRowT, (OTG_CULL_RT == 8 ? 512 : 768) / kCullRowT)
 k_row_otf_cull(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
                const double* __restrict__ dq, int64_t mpad, float kh,
                const double* __restrict__ rowM2, const int* __restrict__ rowJ,
                int64_t cols_per_split, RowPart* __restrict__ rpart, const Ctrl* __restrict__ ctrl) {
   pdl_wait();
   if (ctrl->done || !ctrl->shift_valid) return;
-  constexpr int NP = kOtfRT / 2;
-  constexpr int kW = kRowThreads / 32;
+  constexpr int kCRT = OTG_CULL_RT;
+  constexpr int NP = kCRT / 2;
+  constexpr int kW = kCullRowT / 32;
   __shared__ float4 sA[kW][kCullCB];  // (-x, -x, -y, -y)
   __shared__ float4 sB[kW][kCullCB];  // (-z, -z, V, V)
   __shared__ float2 sE[kW][kCullCB];  // (2^F, 2^F)
-  __shared__ double sSS[kOtfRT][kRowThreads];
+  __shared__ double sSS[kCRT][kCullRowT];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t rbase = static_cast<int64_t>(blockIdx.x) * (kRowThreads * kOtfRT) +
-                        warp * (32 * kOtfRT) + lane;
+  const int64_t rbase = static_cast<int64_t>(blockIdx.x) * (kCullRowT * kCRT) +
+                        warp * (32 * kCRT) + lane;
   const int64_t j0 = static_cast<int64_t>(blockIdx.y) * cols_per_split;
   const int64_t j1 = min(j0 + cols_per_split, m);
   const double dmax2 = ctrl->dmax2;
   float2 X[NP], Y[NP], Z[NP], nS[NP], fs[NP];
-  float tm[kOtfRT];
-  int tj[kOtfRT];
+  float tm[kCRT];
+  int tj[kCRT];
 #pragma unroll
   for (int pp = 0; pp < NP; ++pp) {
     const int64_t p0 = min(rbase + (2 * pp) * 32, n - 1), p1 = min(rbase + (2 * pp + 1) * 32, n - 1);
@@ -1601,7 +1604,7 @@ k_row_otf_cull(const CostSrc src, int64_t n, int64_t m, const float* __restrict_
     fs[pp] = make_float2(0.f, 0.f);
   }
 #pragma unroll
-  for (int r = 0; r < kOtfRT; ++r) {
+  for (int r = 0; r < kCRT; ++r) {
     tm[r] = -FLT_MAX;
     tj[r] = static_cast<int>(j0);
     sSS[r][threadIdx.x] = 0.0;
@@ -1679,7 +1682,7 @@ k_row_otf_cull(const CostSrc src, int64_t n, int64_t m, const float* __restrict_
   }
   RowPart* dst = rpart + static_cast<int64_t>(blockIdx.y) * n;
 #pragma unroll
-  for (int r = 0; r < kOtfRT; ++r) {
+  for (int r = 0; r < kCRT; ++r) {
     const int64_t pos = rbase + r * 32;
     if (pos < n) {
       RowPart rp;
@@ -1693,14 +1696,14 @@ k_row_otf_cull(const CostSrc src, int64_t n, int64_t m, const float* __restrict_
 
 // Columns: thread = 4 consecutive sorted columns, warp = 128; rows of the
 // split in blocks of kCullRB sorted rows, staged per warp when live.
-__global__ void __launch_bounds__(256, OTG_COL_OTF_MINB)
+__global__ void __launch_bounds__(kCullColT, 512 / kCullColT)
 k_col_otf_cull(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
                const float4* __restrict__ aux, int64_t row_lo, int64_t row_hi,
                int64_t rows_per_split, double* __restrict__ part, int64_t mpad,
                const Ctrl* __restrict__ ctrl) {
   pdl_wait();
   if (ctrl->done) return;
-  constexpr int NT = 256, kW = NT / 32;
+  constexpr int NT = kCullColT, kW = NT / 32;
   __shared__ float4 sX[kW][kCullRB];
   __shared__ float4 sAx[kW][kCullRB];
   __shared__ double sAcc[4][NT];
@@ -3104,7 +3107,9 @@ void launch_row_pass(Problem& P) {
                  P.stream, P.m, P.mpad, static_cast<const float*>(P.vq),
                  static_cast<const int*>(P.perm_c), P.cvmax, reinterpret_cast<float2*>(P.ves),
                  static_cast<const Ctrl*>(P.ctrl));
-        launch_k(k_row_otf_cull, g, kRowThreads, 0, P.stream, cull_src(P), P.n_local, P.m,
+        const dim3 gc(static_cast<unsigned>((P.n_local + kCullRowT * OTG_CULL_RT - 1) / (kCullRowT * OTG_CULL_RT)),
+                      static_cast<unsigned>(P.row_splits));
+        launch_k(k_row_otf_cull, gc, kCullRowT, 0, P.stream, cull_src(P), P.n_local, P.m,
                  static_cast<const float*>(P.vq), static_cast<const double*>(P.dq), P.mpad, kh,
                  static_cast<const double*>(P.rowM2), static_cast<const int*>(P.rowJ),
                  P.row_cols_per_split, rp, static_cast<const Ctrl*>(P.ctrl));
@@ -3161,7 +3166,8 @@ void launch_col_pass(Problem& P) {
                  256, 0, P.stream, P.n_local, static_cast<const float4*>(P.aux),
                  static_cast<const int*>(P.perm_r), P.rnegm, reinterpret_cast<float4*>(P.auxs),
                  static_cast<const Ctrl*>(P.ctrl));
-        launch_k(k_col_otf_cull, grid, 256, 0, P.stream, cull_src(P), P.m, P.p, kh, P.aux, lo, hi,
+        const dim3 gcc(static_cast<unsigned>((P.m + 4 * kCullColT - 1) / (4 * kCullColT)), P.col_splits);
+        launch_k(k_col_otf_cull, gcc, kCullColT, 0, P.stream, cull_src(P), P.m, P.p, kh, P.aux, lo, hi,
                  P.rows_per_split, part, P.mpad, P.ctrl);
       } else if (NT == 512) {
         if (otf) { OTG_COL(true, 512); } else { OTG_COL(false, 512); }
@@ -3457,7 +3463,7 @@ extern "C" otg_status otg_cull_stats(otg_problem h, double out[2]) {
         static_cast<const Ctrl*>(P.ctrl));
     const float kh = static_cast<float>(P.kappa * kLog2e);
     const float kcull = kh * kCullSlack;
-    const int64_t rt = 32 * kOtfRT, cbn = (m + kCullCB - 1) / kCullCB;
+    const int64_t rt = 32 * OTG_CULL_RT, cbn = (m + kCullCB - 1) / kCullCB;
     const int64_t rp = ((n + rt - 1) / rt) * cbn;
     k_cull_stat<<<static_cast<unsigned>((rp + 255) / 256), 256, 0, P.stream>>>(
         n, reinterpret_cast<const float4*>(P.Xs), nS, static_cast<int>(rt),
