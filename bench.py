@@ -422,7 +422,7 @@ def main():
     if cfg == 3:
         roofline = hbm_roofline(info, row_ms, col_ms, bytes_sw, ms_sw, rows_local, M)
     else:
-        roofline = otf_roofline(row_ms, col_ms, rows_local, M, clk.summary())
+        roofline = otf_roofline(row_ms, col_ms, rows_local, M, clk.summary(), ot.cull_stats(p))
     roofline["epilogue_ms"] = epi_ms
 
     # ---- time to tolerance (fresh solve from v = 0) ----
@@ -516,11 +516,16 @@ def hbm_roofline(info, row_ms, col_ms, bytes_sw, ms_sw, rows, m):
             "isolated_ms": {"row": ms_sw[0], "col": ms_sw[1], "merge": ms_sw[2]}}
 
 
-def otf_roofline(row_ms, col_ms, rows, m, clocks):
+def otf_roofline(row_ms, col_ms, rows, m, clocks, visited=(-1.0, -1.0)):
     """On the fly: pair evaluations per second against the MUFU ex2 rate (one
     ex2 per pair, 16 / clk / SM) and the combined MUFU + FMA-pipe bound of
     BASELINE.md §2 (5 FP32 ops per pair, 8-op polynomial exp2 offload), both
-    at the max SM clock (the measured clock is reported beside them)."""
+    at the max SM clock (the measured clock is reported beside them).
+    `achieved` counts the ALGORITHMIC pairs (n x m per pass, the reference's
+    work); the culled sweeps skip blocks whose every exponent is provably
+    below -127 (ex2.approx.ftz would return +0), so it can exceed the peak --
+    `visited` (otg_cull_stats) and `visited_frac` give the pairs actually
+    evaluated and their rate against the same peak."""
     sms, f = 148, 1.965e9
     r_mufu = 16 * sms * f
     r_fma = 128 * sms * f
@@ -533,7 +538,10 @@ def otf_roofline(row_ms, col_ms, rows, m, clocks):
             "frac": achieved / r_mufu, "frac_combined_bound": achieved / combined,
             "combined_peak": combined / 1e12, "traffic": None,
             "algorithmic_pairs_per_launch": pairs, "avg_launch_ms": per_pass_ms,
-            "row_pass_ms": row_ms, "col_pass_ms": col_ms, "sm_mhz": clocks.get("sm_mhz")}
+            "row_pass_ms": row_ms, "col_pass_ms": col_ms, "sm_mhz": clocks.get("sm_mhz"),
+            "visited": {"row_pass": visited[0], "col_pass": visited[1]} if visited[0] >= 0 else None,
+            "visited_frac": ((visited[0] if row_ms >= col_ms else visited[1]) * pairs
+                             / (per_pass_ms * 1e-3) / r_mufu) if visited[0] >= 0 else None}
 
 
 if __name__ == "__main__":
