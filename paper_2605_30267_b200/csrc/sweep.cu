@@ -842,9 +842,11 @@ k_sp_redo(const CostSrc src, int64_t n, int64_t m, const double* __restrict__ p,
           double* __restrict__ rowM, double* __restrict__ rowS, double* __restrict__ u,
           double* __restrict__ wrow, float4* __restrict__ aux, double* __restrict__ rowM2,
           int* __restrict__ rowJ, const int* __restrict__ bad_rows,
-          const int* __restrict__ bad_count, int ncl, int64_t cap, Ctrl* __restrict__ ctrl) {
+          const int* __restrict__ bad_count, int ncl, int64_t cap,
+          const unsigned* __restrict__ total, Ctrl* __restrict__ ctrl) {
   pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done || !ctrl->shift_valid) return;
+  if (*total == 0u) return;  // (the single pass's count of listed rows)
   for (int c = 0; c < ncl; ++c) {
     const int nb = bad_count[c];
     const int64_t base = cap * c;
@@ -3192,7 +3194,7 @@ void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int n
   launch_k(k_sp_redo, 148, kRowThreads, 0, P.stream, cost_src(P), P.n_local, P.m, P.p, P.kappa, P.a,
                                                 P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,
                                                 P.rowM2, P.rowJ, bad_rows, bad_count, ncl, cap,
-                                                P.ctrl);
+                                                static_cast<const unsigned*>(P.sp_cnt + 2), P.ctrl);
 }
 
 int partial_rows(const Problem& P) { return P.vshards * P.col_splits; }
