@@ -128,8 +128,7 @@ typedef struct {
   double cost_raw_max;     /* CostMatrix::raw_max                           */
   int64_t device_bytes;    /* device memory held by the handle              */
   int world_size, rank, device;
-  int sweep_mode;          /* 0: fp64 two-pass, 1: fp32 two-pass, 2: fp32 single pass (band
-                             pipeline, k_sweep1), 3: fp32 single pass (whole rows, k_strip1) */
+  int sweep_mode;          /* 0: fp64 two-pass, 1: fp32 two-pass, 2: fp32 single pass (k_sweep1) */
   int sweep_clusters;      /* fused: co-resident 8-CTA clusters (persistent)  */
   int col_splits;          /* two-pass: row splits of the column pass         */
 } otg_problem_info;

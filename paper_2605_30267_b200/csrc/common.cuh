@@ -297,7 +297,6 @@ struct Problem {
   int two_pass = 0;             // otg_device_opts.sweep == 1: never the single pass
   int force_single_pass = 0;    // otg_device_opts.sweep == 2: single pass whenever it applies
   int sp_group = 0;             // CTAs (SMs) sharing one row band
-  int sp_strip = 0;             // whole-row single pass (k_strip1): its quads per thread, else 0
   int sp_fix = 28;              // fixed-point scale 2^sp_fix of the row sums
   int sp_bw = 0, sp_nbox = 0;   // TMA box: chunk width (columns), chunks per slice
   alignas(64) unsigned char sp_tmap[128] = {};  // CUtensorMap of the stored cost (2-D)

@@ -166,9 +166,6 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 #ifndef SP_POLL_NS
 #define SP_POLL_NS 128    // sleep between polls of a band's row-sum words
 #endif
-#ifndef SP_FOLD_PIPE
-#define SP_FOLD_PIPE 0  // column fold: next row's tensor-memory load in flight during the FMAs
-#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   unsigned spins = 0;
   while (!mbar_try(bar, parity)) {
@@ -329,50 +326,6 @@ __device__ __forceinline__ void tmem_st16f(uint32_t taddr, const float (&v)[16])
       "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
       "f"(v[15])
       : "memory");
-}
-__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, float (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-      "%11, %12, %13, %14, %15}, [%16];"
-      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
-        "=f"(v[7]), "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]),
-        "=f"(v[14]), "=f"(v[15])
-      : "r"(taddr)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_wait_ld16(float (&v)[16]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]),
-                 "+f"(v[6]), "+f"(v[7]), "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]),
-                 "+f"(v[12]), "+f"(v[13]), "+f"(v[14]), "+f"(v[15])
-               :
-               : "memory");
-}
-__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, float (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
-      "%28, %29, %30, %31}, [%32];"
-      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
-        "=f"(v[7]), "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]),
-        "=f"(v[14]), "=f"(v[15]), "=f"(v[16]), "=f"(v[17]), "=f"(v[18]), "=f"(v[19]),
-        "=f"(v[20]), "=f"(v[21]), "=f"(v[22]), "=f"(v[23]), "=f"(v[24]), "=f"(v[25]),
-        "=f"(v[26]), "=f"(v[27]), "=f"(v[28]), "=f"(v[29]), "=f"(v[30]), "=f"(v[31])
-      : "r"(taddr)
-      : "memory");
-}
-// wait for this thread's outstanding tensor-memory loads; the registers of
-// `v` (and of any earlier load) are defined only after it
-__device__ __forceinline__ void tmem_wait_ld32(float (&v)[32]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]),
-                 "+f"(v[6]), "+f"(v[7]), "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]),
-                 "+f"(v[12]), "+f"(v[13]), "+f"(v[14]), "+f"(v[15]), "+f"(v[16]), "+f"(v[17]),
-                 "+f"(v[18]), "+f"(v[19]), "+f"(v[20]), "+f"(v[21]), "+f"(v[22]), "+f"(v[23]),
-                 "+f"(v[24]), "+f"(v[25]), "+f"(v[26]), "+f"(v[27]), "+f"(v[28]), "+f"(v[29]),
-                 "+f"(v[30]), "+f"(v[31])
-               :
-               : "memory");
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   asm volatile(
@@ -705,39 +658,6 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
       float a32[4 * kQPL];
 #pragma unroll
       for (int e = 0; e < 4 * kQPL; ++e) a32[e] = 0.0f;
-#if SP_FOLD_PIPE
-      // one row (16 columns) per tensor-memory load, the next row's load in
-      // flight while this one is folded (tcgen05.wait::ld waits for all of
-      // this thread's loads: only one is outstanding at each wait)
-      {
-        float Ea[16], Eb[16];
-        auto fold16 = [&](const float (&E)[16], int r) {
-          const float wr = __shfl_sync(0xffffffffu, w_l, r);
-          if (wr != 0.0f) {  // uniform over the warp (one row); 0 = loose or absent row
-            const float2 w2 = make_float2(wr, wr);
-#pragma unroll
-            for (int e = 0; e < 4 * kQPL; e += 2) {
-              const float2 r2 = __ffma2_rn(make_float2(E[e], E[e + 1]), w2,
-                                           make_float2(a32[e], a32[e + 1]));
-              a32[e] = r2.x;
-              a32[e + 1] = r2.y;
-            }
-          }
-        };
-        tmem_ld16_nowait(taddr, Ea);
-#pragma unroll
-        for (int r = 0; r < kR; r += 2) {
-          tmem_wait_ld16(Ea);
-          if (r + 1 < kR) tmem_ld16_nowait(taddr + static_cast<uint32_t>((r + 1) * 16), Eb);
-          fold16(Ea, r);
-          if (r + 1 < kR) {
-            tmem_wait_ld16(Eb);
-            if (r + 2 < kR) tmem_ld16_nowait(taddr + static_cast<uint32_t>((r + 2) * 16), Ea);
-            fold16(Eb, r + 1);
-          }
-        }
-      }
-#else
 #pragma unroll 2
       for (int rp = 0; rp < kR / 2; ++rp) {
         float E[32];
@@ -757,7 +677,6 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
           }
         }
       }
-#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.tempty[ts]);
@@ -828,268 +747,6 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
         A.state[0] = par ^ 1u;
         __threadfence();
       }
-    }
-  }
-}
-
-// ---- whole-row single pass (short rows: m <= kStripMaxM) ---------------------
-// When a whole row of the cost fits in shared memory (cfg2: 8192 columns =
-// 32 KB) no CTA needs another CTA's partial row sums: each CTA (one per SM)
-// owns whole rows i = c, c + H, c + 2H, ... of the cost, streamed through a
-// ring of row slots (one 1-D bulk copy per row plus its 32-byte record, both
-// on the slot's `full` barrier).  Each of the 16 warps owns 1/16 of the
-// columns (lane quads warp*32 + lane + 512 kq) and, per row k,
-//   exps      e_ij = ex2(t_ij) against the row's shift estimate (the
-//             k_row_shift / k_sweep1 exponent, bitwise), written back IN
-//             PLACE over the cost (a lane touches only its own quads); the
-//             warp's row partial as a 2^-28 fixed-point integer (redux.sync on
-//             24-bit limbs: k_sweep1's representation) and its (max, argmax
-//             quad) key -> smem, arrive on the slot's `sums` barrier
-//   fold      kLag rows later: wait for row k - kLag's `sums` (the other
-//             warps published them long ago), S = the 16 partials (integer:
-//             deterministic), w = a / S, acc_j += w e_ij from the lane's own
-//             quads (fp32 over 8 rows, then fp64); the last warp to fold a
-//             row refills its slot (row + nslots)
-// No CTA-wide barrier: warps drift freely within the lag.  The CTA's fp64
-// column sums are row c of `part` (k_merge sums the H rows + the patch row).
-// Rows whose sum leaves [1/4, 2^20) are listed for k_sp_redo / k_sp_patch
-// exactly as in k_sweep1.  The cost is read once; no grid-wide dependency.
-constexpr int kStripWarps = 16;
-constexpr int kStripThreads = 32 * kStripWarps;
-constexpr int kStripMaxM = 4 * 4 * kStripThreads;  // 8192 columns (4 quads per lane)
-#ifndef SP_STRIP_LAG
-#define SP_STRIP_LAG 2
-#endif
-constexpr int kLag = SP_STRIP_LAG;  // rows between a row's exponentials and its fold
-constexpr int kStripSlotsMax = 32;
-
-struct alignas(16) StripShared {
-  uint64_t full[kStripSlotsMax];                     // cost row + record landed (TMA)
-  uint64_t sums[kStripSlotsMax];                     // the 16 warps' partials published
-  unsigned long long psum[kStripSlotsMax][kStripWarps];  // fixed-point warp partials
-  unsigned long long pkey[kStripSlotsMax][kStripWarps];  // (max, ~quad) warp keys
-  RowRec srec[kStripSlotsMax];                       // each slot's row record
-  int folded[kStripSlotsMax];                        // warps done with the slot's row
-};
-
-__device__ __forceinline__ void bulk_load_1d(void* smem_dst, const void* src, uint32_t bytes,
-                                             uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-template <int QPT, bool FULL>  // FULL: every lane's QPT quads exist (m = 4 QPT kStripThreads)
-__global__ void __launch_bounds__(kStripThreads, 1)
-k_strip1(const S1Args A, const Ctrl* __restrict__ ctrl) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  StripShared& S = *reinterpret_cast<StripShared*>(smem_raw);
-  float4* ring = reinterpret_cast<float4*>(smem_raw + ((sizeof(StripShared) + 127) / 128) * 128);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int H = gridDim.x, c = blockIdx.x;
-  const int nslots = A.nslots;
-  const int nr = A.n > c ? static_cast<int>((A.n - c + H - 1) / H) : 0;  // rows of this CTA
-  const int nq = static_cast<int>((A.m + 3) / 4);
-  const int rs4 = (nq + 3) / 4 * 4;  // float4 per slot (64-byte rows)
-  const uint32_t bytes = static_cast<uint32_t>(nq) * 16u;
-  auto row_of = [&](int k) { return static_cast<int64_t>(c) + static_cast<int64_t>(H) * k; };
-  auto load_row = [&](int k, int s) {  // row k of this CTA and its record into slot s
-    mbar_expect_tx(&S.full[s], bytes + static_cast<uint32_t>(sizeof(RowRec)));
-    bulk_load_1d(ring + s * rs4, A.C + row_of(k) * A.ldc, bytes, &S.full[s]);
-    bulk_load_1d(&S.srec[s], A.rec + row_of(k), sizeof(RowRec), &S.full[s]);
-  };
-  if (tid == 0) {
-    for (int s = 0; s < nslots; ++s) {
-      mbar_init(&S.full[s], 1);
-      mbar_init(&S.sums[s], kStripWarps);
-      S.folded[s] = 0;
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  pdl_wait();  // programmatic dependent launch: after k_sp_prep
-  if (ctrl->done || !ctrl->shift_valid) return;  // uniform
-  const unsigned par = A.state[0];
-  if (tid == 0)
-    for (int k = 0; k < nr && k < nslots; ++k) load_row(k, k);
-  // the lane's quads: warp 32 + lane + 512 kq (coalesced 16-byte smem accesses)
-  bool qv[QPT];
-  int qa[QPT];
-  float V[QPT][4], F[QPT][4];
-#pragma unroll
-  for (int kq = 0; kq < QPT; ++kq) {
-    const int qi = tid + kStripThreads * kq;
-    qv[kq] = FULL || qi < nq;
-    qa[kq] = qv[kq] ? qi : 0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int64_t j = 4 * static_cast<int64_t>(qi) + e;
-      const bool ok = qv[kq] && j < A.m;
-      V[kq][e] = ok ? A.vq[j] : -INFINITY;
-      F[kq][e] = ok ? A.vq[A.mpad + j] : 0.0f;
-    }
-  }
-  const float2 nkh2 = make_float2(-A.kh, -A.kh), nkl2 = make_float2(-A.kl, -A.kl);
-  double acc[4 * QPT];
-  float a32[4 * QPT];
-#pragma unroll
-  for (int e = 0; e < 4 * QPT; ++e) {
-    acc[e] = 0.0;
-    a32[e] = 0.0f;
-  }
-  int nbad = 0;
-  int* bad_list = A.bad_rows + static_cast<int64_t>(c) * kColWarps * A.cap;
-  const double scale = ldexp(1.0, -kFix);
-  int se = 0, sf = 0;           // slots of the next row to exponentiate / to fold
-  uint32_t phe = 0u, phf = 0u;  // their barrier phases
-  for (int k = 0; k < nr + kLag; ++k) {
-    if (k < nr) {
-      // ---------------------------------------------- exponentials of row k --
-      mbar_wait(&S.full[se], phe);
-      float4* row = ring + se * rs4;
-      const float sc = S.srec[se].shift;
-      const float2 nS = make_float2(-sc, -sc);
-      float2 ps = make_float2(0.f, 0.f);
-      float mx = -INFINITY;
-      int qb = 0;
-#pragma unroll
-      for (int kq = 0; kq < QPT; ++kq) {
-        const float4 cv = row[qa[kq]];
-        const float2 c01 = make_float2(cv.x, cv.y), c23 = make_float2(cv.z, cv.w);
-        const float2 t01 = __fadd2_rn(
-            __ffma2_rn(c01, nkh2, __fadd2_rn(make_float2(V[kq][0], V[kq][1]), nS)),
-            __ffma2_rn(c01, nkl2, make_float2(F[kq][0], F[kq][1])));
-        const float2 t23 = __fadd2_rn(
-            __ffma2_rn(c23, nkh2, __fadd2_rn(make_float2(V[kq][2], V[kq][3]), nS)),
-            __ffma2_rn(c23, nkl2, make_float2(F[kq][2], F[kq][3])));
-        const float e0 = ex2_approx(t01.x), e1 = ex2_approx(t01.y);
-        const float e2 = ex2_approx(t23.x), e3 = ex2_approx(t23.y);
-        if (qv[kq]) row[qa[kq]] = make_float4(e0, e1, e2, e3);
-        ps = __fadd2_rn(ps, __fadd2_rn(make_float2(e0, e1), make_float2(e2, e3)));
-        const float mq = fmaxf(fmaxf(t01.x, t01.y), fmaxf(t23.x, t23.y));
-        if (mq > mx) {  // lowest quad of equal maxima (kq ascending)
-          mx = mq;
-          qb = qa[kq];
-        }
-      }
-      // fixed-point partial (as k_sweep1: saturated at the loose-row bound)
-      const unsigned long long v0 = __float2ull_rn((ps.x + ps.y) * 268435456.0f);
-      const unsigned long long v = v0 < kFixSat ? v0 : kFixSat;
-      const unsigned slo = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(v & 0xffffffull));
-      const unsigned shi = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(v >> 24));
-      const unsigned hk = qv[0] ? ordered_key(mx) : 0u;
-      const unsigned hmax = __reduce_max_sync(0xffffffffu, hk);
-      const unsigned qmin =
-          __reduce_min_sync(0xffffffffu, hk == hmax ? static_cast<unsigned>(qb) : ~0u);
-      if (lane == 0) {
-        S.psum[se][warp] = (static_cast<unsigned long long>(shi) << 24) + slo;
-        S.pkey[se][warp] = (static_cast<unsigned long long>(hmax) << 32) | ~qmin;
-        mbar_arrive(&S.sums[se]);  // (release: the partials and the in-place exponentials)
-      }
-      if (++se == nslots) {
-        se = 0;
-        phe ^= 1u;
-      }
-    }
-    const int j = k - kLag;
-    if (j >= 0) {
-      // ------------------------------------------------------- fold row j --
-      mbar_wait(&S.sums[sf], phf);
-      unsigned long long tot = S.psum[sf][lane & 15];
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-      const double Sv = static_cast<double>(tot < kFixSat ? tot : kFixSat) * scale;
-      const bool bad = !(Sv >= 0.25 && Sv < 1048576.0);  // outside the fixed-point range: redo
-      const RowRec rc = S.srec[sf];
-      const double wi = rc.a / Sv;
-      const float wf = bad ? 0.0f : static_cast<float>(wi);
-      if (warp == 0 && lane == 0) {  // row outputs, loose rows in row order
-        const int64_t i = row_of(j);
-        unsigned long long key = 0ull;
-#pragma unroll
-        for (int w = 0; w < kStripWarps; ++w) {
-          const unsigned long long kw = S.pkey[sf][w];
-          key = kw > key ? kw : key;
-        }
-        if (!bad) {
-          const double M = static_cast<double>(rc.shift) * kLn2;
-          A.rowM[i] = M;
-          A.rowS[i] = Sv;
-          A.u[i] = (rc.loga - M) - log(Sv);
-          A.wrow[i] = wi;
-          A.rowJ[i] = -1;  // base-2 max + argmax quad: from this pass's key (k_sp_prep)
-          A.aux[i] = make_float4(rc.shift, 0.0f, wf, 0.0f);
-        } else {
-          bad_list[nbad++] = static_cast<int>(i);
-        }
-        A.tkey[static_cast<int64_t>(par) * A.n + i] = key;
-      }
-      if (wf != 0.0f) {
-        const float4* row = ring + sf * rs4;
-        const float2 w2 = make_float2(wf, wf);
-#pragma unroll
-        for (int kq = 0; kq < QPT; ++kq) {
-          const float4 ev = row[qa[kq]];
-          const float2 r01 = __ffma2_rn(make_float2(ev.x, ev.y), w2,
-                                        make_float2(a32[4 * kq], a32[4 * kq + 1]));
-          const float2 r23 = __ffma2_rn(make_float2(ev.z, ev.w), w2,
-                                        make_float2(a32[4 * kq + 2], a32[4 * kq + 3]));
-          a32[4 * kq] = r01.x;
-          a32[4 * kq + 1] = r01.y;
-          a32[4 * kq + 2] = r23.x;
-          a32[4 * kq + 3] = r23.y;
-        }
-      }
-      if ((j & 7) == 7) {
-#pragma unroll
-        for (int e = 0; e < 4 * QPT; ++e) {
-          acc[e] += static_cast<double>(a32[e]);
-          a32[e] = 0.0f;
-        }
-      }
-      // the last warp done with the slot refills it (row j + nslots)
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence_block();  // the warp's reads of the slot before the count
-        if (atomicAdd(&S.folded[sf], 1) == kStripWarps - 1) {
-          __threadfence_block();
-          S.folded[sf] = 0;
-          if (j + nslots < nr) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            load_row(j + nslots, sf);
-          }
-        }
-      }
-      if (++sf == nslots) {
-        sf = 0;
-        phf ^= 1u;
-      }
-    }
-  }
-  // the CTA's column sums: row c of the partials
-#pragma unroll
-  for (int kq = 0; kq < QPT; ++kq) {
-    const int qi = tid + kStripThreads * kq;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int64_t jj = 4 * static_cast<int64_t>(qi) + e;
-      if (qv[kq] && jj < A.m)
-        A.part[static_cast<int64_t>(c) * A.mpad + jj] = acc[4 * kq + e] + static_cast<double>(a32[4 * kq + e]);
-    }
-  }
-  if (tid < kColWarps) A.bad_count[c * kColWarps + tid] = tid == 0 ? nbad : 0;
-  if (tid == 0 && nbad) atomicAdd(A.state + 2, static_cast<unsigned>(nbad));
-  // flip the buffer parity after the last CTA
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    unsigned* fin = A.state + 1;
-    if (atomicAdd(fin, 1u) == static_cast<unsigned>(H - 1)) {
-      *fin = 0u;
-      A.state[0] = par ^ 1u;
-      __threadfence();
     }
   }
 }
@@ -1165,51 +822,11 @@ SpLayout sp_layout(int64_t m, int sms) {
 // fp32 stored cost, no virtual shards (they use the two-pass kernels), the
 // layout exists and the handle did not ask for the two-pass kernels
 // (otg_device_opts.sweep = 1: A/B and cross-checks).
-// Whole-row single pass (k_strip1) when a row fits in a ring slot: one CTA
-// per SM (at most one per row), kStripSlotsMax slots at most.
-static bool strip_configure(Problem& P, int sms) {
-  if (P.m > kStripMaxM) return false;
-  const int64_t min_rows = P.force_single_pass ? 1 : 8;  // rows per CTA, at least (auto)
-  if (P.n_local < min_rows * sms && !(P.force_single_pass && P.n_local >= 1)) return false;
-  const int nq = static_cast<int>((P.m + 3) / 4);
-  const int qpt = (nq + kStripThreads - 1) / kStripThreads;
-  const int Q = qpt <= 1 ? 1 : (qpt <= 2 ? 2 : 4);
-  const int64_t head = ((sizeof(StripShared) + 127) / 128) * 128;
-  const int64_t slot = static_cast<int64_t>((nq + 3) / 4 * 4) * 16;
-  const int nslots = static_cast<int>(std::min<int64_t>(kStripSlotsMax, (220 * 1024 - head) / slot));
-  if (nslots < kLag + 2) return false;
-  const int smem = static_cast<int>(head + nslots * slot);
-  const bool full = P.m == 4LL * Q * kStripThreads;
-  auto kern = Q == 1 ? k_strip1<1, false>
-                     : (Q == 2 ? k_strip1<2, false> : (full ? k_strip1<4, true> : k_strip1<4, false>));
-  // (the attribute is per kernel, not per handle: the largest size any handle can ask for)
-  OTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
-  int occ = 0;
-  OTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kStripThreads, smem));
-  if (occ < 1) return false;
-  P.fused = 1;
-  P.sp_strip = full ? 5 : Q;  // (5: Q = 4 with every quad present)
-  P.fused_clusters = static_cast<int>(std::min<int64_t>(sms, P.n_local));  // CTAs = partial rows
-  P.sp_group = 1;
-  P.fused_slots = nslots;
-  P.fused_smem = smem;
-  // loose-row lists: list 0 of each CTA's kColWarps (whole CTA, row order)
-  P.sp_cap = (P.n_local + P.fused_clusters - 1) / P.fused_clusters + 1;
-  if (getenv("OTG_VERBOSE"))
-    fprintf(stderr, "[otg] single-pass (whole rows): %d CTAs, %d quads per thread, smem %d, ring %d\n",
-            P.fused_clusters, Q, smem, nslots);
-  return true;
-}
-
 bool fused_configure(Problem& P) {
   P.fused = 0;
-  P.sp_strip = 0;
   if (P.storage != OTG_STORE_F32 || P.vshards != 1 || P.two_pass) return false;
   int sms = 0;
   OTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.device));
-#ifndef SP_NO_STRIP
-  if (strip_configure(P, sms)) return true;
-#endif
   const SpLayout L = sp_layout(P.m, sms);
   // the grid-wide band pipeline needs a long run of bands per group to pay
   // for its fill (B200: 8192^2 in 9 groups of 57 bands 0.18 ms vs two-pass
@@ -1333,14 +950,6 @@ void launch_fused(Problem& P, float kh, float kl) {
   A.nch = P.sp_nbox;
   A.dbg = sp_trace_buf();
   const int ctas = P.fused_clusters * P.sp_group;
-  if (P.sp_strip) {
-    // whole rows per CTA: no grid-wide dependency (a plain launch)
-    auto kern = P.sp_strip == 1 ? k_strip1<1, false>
-                : (P.sp_strip == 2 ? k_strip1<2, false>
-                                   : (P.sp_strip == 5 ? k_strip1<4, true> : k_strip1<4, false>));
-    launch_k(kern, ctas, kStripThreads, P.fused_smem, P.stream, A,
-             static_cast<const Ctrl*>(P.ctrl));
-  } else {
   // co-residency of the whole grid is required (grid-wide band counters):
   // a cooperative launch guarantees it or fails
   cudaLaunchConfig_t cfg = {};
@@ -1355,7 +964,6 @@ void launch_fused(Problem& P, float kh, float kl) {
   cfg.numAttrs = 1;
   OTG_CUDA(cudaLaunchKernelEx(&cfg, k_sweep1, A, *reinterpret_cast<const CUtensorMap*>(P.sp_tmap),
                               static_cast<const Ctrl*>(P.ctrl)));
-  }
   launch_sp_redo(P, P.sp_bad_rows, P.sp_bad_count, ctas * kColWarps, P.sp_cap);
   const unsigned g = static_cast<unsigned>((P.m + kPatchThreads - 1) / kPatchThreads);
   launch_k(k_sp_patch, g, kPatchThreads, 0, P.stream, P.C32, P.ldc, P.m, P.p, kh, kl, P.aux,

@@ -593,7 +593,7 @@ otg_status otg_problem_info_get(otg_problem h, otg_problem_info* out) {
     out->world_size = P.world;
     out->rank = P.rank;
     out->device = P.device;
-    out->sweep_mode = P.storage == OTG_STORE_F64 ? 0 : (P.fused ? (P.sp_strip ? 3 : 2) : 1);
+    out->sweep_mode = P.storage == OTG_STORE_F64 ? 0 : (P.fused ? 2 : 1);
     out->sweep_clusters = P.fused_clusters;
     out->col_splits = P.col_splits;
   });

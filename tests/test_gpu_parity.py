@@ -354,18 +354,17 @@ def test_fused_eval_matches_oracle_and_two_pass(n, m):
         assert abs(e.f_value - r["f_value"]) <= 1e-6 * max(1.0, abs(r["f_value"]))
 
 
-@pytest.mark.parametrize("n,m,eps,mode", [
-    (300, 4100, 2e-3, 3), (257, 65536, 1e-3, 2), (2048, 2048, 5e-4, 3),
-    (150, 8192, 1e-3, 3), (1000, 1001, 2e-3, 3), (4099, 5003, 1e-3, 3), (37, 777, 5e-3, 3)])
-def test_fused_single_pass_matches_two_pass_solve(n, m, eps, mode):
-    """Steady-state single-pass kernels against the two-pass kernels: mode 2
-    = the grid-wide band pipeline (k_sweep1: tensor-memory staging), mode 3 =
-    whole rows per CTA (k_strip1: rows of <= 8192 columns, ragged quads, fewer
-    rows than SMs); both with shift estimates and the loose-row redo + column
-    patch."""
+@pytest.mark.parametrize("n,m,eps", [
+    (300, 4100, 2e-3), (257, 65536, 1e-3), (2048, 2048, 5e-4),
+    (150, 8192, 1e-3), (1000, 1001, 2e-3), (4099, 5003, 1e-3), (37, 777, 5e-3)])
+def test_fused_single_pass_matches_two_pass_solve(n, m, eps):
+    """Steady-state single-pass kernel (grid-wide band pipeline, tensor-memory
+    staging, shift estimates, loose-row redo + column patch) against the
+    two-pass kernels, including ragged slices (m not a multiple of the slice
+    width) and partial last bands."""
     pf = _points_problem(n, m, 11, eps, True)
     p2 = _points_problem(n, m, 11, eps, False)
-    assert pf.handle.info.sweep_mode == mode and p2.handle.info.sweep_mode == 1
+    assert pf.handle.info.sweep_mode == 2 and p2.handle.info.sweep_mode == 1
     cfg = ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=40)
     gf = ot.homotopy_solve(pf, cfg)
     g2 = ot.homotopy_solve(p2, cfg)
