@@ -197,6 +197,15 @@ __device__ __forceinline__ float key_to_float(unsigned k) {
 }
 
 constexpr int kFix = 28;  // fixed-point scale 2^kFix of the row sums
+// Row keys carry the largest QUAD SUM of exponentials (and its quad) instead
+// of the largest exponent: 1 FADD per quad instead of 3 FMNMX.  The next
+// evaluation's shift estimate takes M2 = s + log2(quad sum), an upper bound on
+// the row's base-2 max within +2 (the estimate's upper bound U = M2 + dmax2
+// stays valid), and the quad -- which holds an element within 2 of the max --
+// for the lower bound L (an actual element of the new row, as before).
+#ifndef SP_QSUM
+#define SP_QSUM 1
+#endif
 constexpr unsigned long long kFixSat = 1ull << 48;  // = 2^20 in real units: the loose-row bound
 static_assert(kFix == 28, "band_rows scales by 268435456.0f = 2^28");
 
@@ -279,8 +288,13 @@ k_sp_prep(int64_t n, int64_t m, const float* __restrict__ C, int64_t ldc,
     int J = rowJ[i];
     if (J == -1) {
       const unsigned long long kk = prev[i];
+#if SP_QSUM
+      const double qs = static_cast<double>(key_to_float(static_cast<unsigned>(kk >> 32)));
+      M2 = static_cast<double>(rec[i].shift) + (qs > 0.0 ? log2(qs) : 0.0);
+#else
       M2 = static_cast<double>(rec[i].shift) +
            static_cast<double>(key_to_float(static_cast<unsigned>(kk >> 32)));
+#endif
       J = 4 * static_cast<int>(~static_cast<unsigned>(kk & 0xffffffffull));
       rowM2[i] = M2;
       rowJ[i] = J;
@@ -384,8 +398,14 @@ __device__ __forceinline__ void row_pair(const float4* __restrict__ slot,
       E[16 * h + 4 * kq + 1] = e1;
       E[16 * h + 4 * kq + 2] = e2;
       E[16 * h + 4 * kq + 3] = e3;
+#if SP_QSUM
+      const float2 s2 = __fadd2_rn(make_float2(e0, e1), make_float2(e2, e3));
+      ps = __fadd2_rn(ps, s2);
+      mq[kq] = s2.x + s2.y;  // the quad's sum: max element <= it <= 4 x max element
+#else
       ps = __fadd2_rn(ps, __fadd2_rn(make_float2(e0, e1), make_float2(e2, e3)));
       mq[kq] = fmaxf(fmaxf(t01.x, t01.y), fmaxf(t23.x, t23.y));
+#endif
     }
     // argmax quad: the lowest of equal maxima
     const float m01 = fmaxf(mq[0], mq[1]), m23 = fmaxf(mq[2], mq[3]);
