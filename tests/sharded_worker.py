@@ -29,6 +29,12 @@ def instance(case):
         x, y = ot.gen_config(5, n, m, 5)
         return dict(kind="points", x=x, y=y, a=np.full(n, 1 / n), b=np.full(m, 1 / m),
                     eps=0.1, storage="on_the_fly", norm="none", tol=1e-6, iters=60)
+    if case == "otf_cull":  # cfg5-shaped at eps 1e-3, large enough for the culled sweeps
+        # (>= 4096 local rows and columns): each rank Morton-orders its own rows
+        n, m = 9000, 6000
+        x, y = ot.gen_config(5, n, m, 5)
+        return dict(kind="points", x=x, y=y, a=np.full(n, 1 / n), b=np.full(m, 1 / m),
+                    eps=1e-3, storage="on_the_fly", norm="none", tol=1e-5, iters=40)
     if case == "f64_dense":  # dense fp64 rows through the dense contract
         n, m = 700, 500
         a, b, C = ot.synthetic_instance(n, m, 11)
@@ -86,7 +92,8 @@ def main():
              tol_it=tol.iterations, tol_conv=tol.converged, tol_fb=tol.fallback_columns,
              fixed_fb=fixed.fallback_columns, cost=st.primal_cost,
              viol=st.marginal_violation_l1, ev_v=ev.v_next, ev_u=ev.u, ev_f=ev.f_value,
-             ev_g=ev.grad_l1, n_local=p.handle.info.n_local)
+             ev_g=ev.grad_l1, n_local=p.handle.info.n_local,
+             culled=inst.get("storage") == "on_the_fly" and ot.cull_stats(p)[0] >= 0.0)
     p.close()
     dist.barrier()
     dist.destroy_process_group()
