@@ -506,6 +506,7 @@ otg_status otg_batch_get_cost(otg_batch h, float* out) {
 otg_status otg_batch_homotopy_solve(otg_batch h, const otg_homotopy_config* cfg,
                                     otg_batch_result* res) {
   return guard([&] {
+    OTG_RANGE("otg_batch_homotopy_solve");
     if (!h || !cfg || !res) fail(OTG_E_DIMENSION, "NULL argument");
     if (!(cfg->mu0 > 0.0) || !(cfg->mu0 < 1.0) || cfg->m0 < 1 || cfg->max_outer < 1)
       fail(OTG_E_OT, "homotopy schedule needs mu0 in (0, 1), m0 >= 1, max_outer >= 1");

@@ -8,6 +8,7 @@
 // <u, a> partial) once per evaluation; it is issued on the
 // handle's stream, so it is captured into the solver's chunk graph.
 #include <dlfcn.h>
+#include <unistd.h>
 
 #include <cstring>
 #include <mutex>
@@ -32,6 +33,8 @@ struct NcclApi {
   nccl_result_t (*all_reduce)(const void*, void*, size_t, int, int, nccl_comm_t,
                               cudaStream_t) = nullptr;
   const char* (*error_string)(nccl_result_t) = nullptr;
+  nccl_result_t (*get_async_error)(nccl_comm_t, nccl_result_t*) = nullptr;
+  nccl_result_t (*abort)(nccl_comm_t) = nullptr;
 };
 
 constexpr int kNcclDouble = 8;  // ncclFloat64
@@ -53,6 +56,9 @@ NcclApi& api() {
     a.destroy = reinterpret_cast<decltype(a.destroy)>(dlsym(a.lib, "ncclCommDestroy"));
     a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(a.lib, "ncclAllReduce"));
     a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(a.lib, "ncclGetErrorString"));
+    a.get_async_error =
+        reinterpret_cast<decltype(a.get_async_error)>(dlsym(a.lib, "ncclCommGetAsyncError"));
+    a.abort = reinterpret_cast<decltype(a.abort)>(dlsym(a.lib, "ncclCommAbort"));
   });
   if (!a.lib || !a.init_rank || !a.all_reduce)
     fail(OTG_E_NCCL, "libnccl.so.2 not loadable (import torch first, or add it to LD_LIBRARY_PATH)");
@@ -160,6 +166,33 @@ void comm_destroy(Problem& P) {
     api().destroy(static_cast<nccl_comm_t>(P.nccl_comm));
   }
   P.nccl_comm = nullptr;
+}
+
+// Host-side wait for the handle's stream that keeps polling the NCCL
+// communicator's asynchronous error state (a peer rank that died or a broken
+// link leaves the all-reduce -- and a plain stream synchronize -- waiting
+// forever): on an error the communicator is aborted, which releases the
+// stream, and the call fails with OTG_E_NCCL.  Host-callback handles and
+// unsharded handles just synchronize.
+void comm_sync(Problem& P) {
+  if (!P.sharded || P.ar_fn || !P.nccl_comm || !api().get_async_error) {
+    OTG_CUDA(cudaStreamSynchronize(P.stream));
+    return;
+  }
+  for (unsigned spins = 0;; ++spins) {
+    const cudaError_t q = cudaStreamQuery(P.stream);
+    if (q == cudaSuccess) return;
+    if (q != cudaErrorNotReady) OTG_CUDA(q);
+    nccl_result_t r = 0;
+    api().get_async_error(static_cast<nccl_comm_t>(P.nccl_comm), &r);
+    if (r != 0 && r != 7 /* ncclInProgress */) {
+      const char* s = api().error_string ? api().error_string(r) : "?";
+      if (api().abort) api().abort(static_cast<nccl_comm_t>(P.nccl_comm));
+      P.nccl_comm = nullptr;  // aborted: nothing left to destroy
+      fail(OTG_E_NCCL, std::string("NCCL asynchronous error: ") + s);
+    }
+    if (spins > 64) usleep(20);  // (after a short spin: chunks are ~ms long)
+  }
 }
 
 int comm_failed(Problem& P) {

@@ -57,7 +57,18 @@
 #define OTG_EPI_FUSED 0      // one-kernel epilogue with grid barriers (measured slower)
 #endif
 
+#include <nvtx3/nvToolsExt.h>  // (header-only NVTX v3: ranges cost nothing without a tool)
+
 namespace otg {
+
+// NVTX range over a C-ABI call or a chunk replay (nsys / ncu --nvtx timelines)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define OTG_RANGE(name) ::otg::NvtxRange otg_nvtx_range_(name)
 
 // ---------------------------------------------------------------- errors --
 struct Error {
@@ -392,6 +403,7 @@ int partial_rows(const Problem& P);  // rows of P.part the merge sums
 void comm_init(Problem& P, const otg_device_opts* opts);
 void comm_destroy(Problem& P);
 int comm_failed(Problem& P);  // a host all-reduce callback returned non-zero
+void comm_sync(Problem& P);    // stream wait; sharded NCCL handles poll the async error state
 void comm_allreduce_sum(Problem& P, const double* send, double* recv, size_t count);
 void comm_allreduce_max(Problem& P, const double* send, double* recv, size_t count);
 inline void comm_allreduce_sum(Problem& P, double* buf, size_t count) {

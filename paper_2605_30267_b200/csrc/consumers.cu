@@ -343,6 +343,7 @@ extern "C" {
 otg_status otg_plan_barycentric(otg_problem h, const double* u, const double* v,
                                 const double* src, int d, double* out, double* col_mass) {
   return guard([&] {
+    OTG_RANGE("otg_plan_barycentric");
     Problem& P = problem_of(h);
     if (d < 1 || d > kMaxFeat) fail(OTG_E_DIMENSION, "barycentric features: 1 <= d <= 8");
     if (!src || !out) fail(OTG_E_DIMENSION, "NULL feature / output buffer");
@@ -412,6 +413,7 @@ otg_status otg_plan_row_argmax(otg_problem h, const double* u, const double* v, 
 otg_status otg_plan_topk(otg_problem h, const double* u, const double* v, const int* rows,
                          int64_t nrows, int k, int* out) {
   return guard([&] {
+    OTG_RANGE("otg_plan_topk");
     Problem& P = problem_of(h);
     if (k < 1) fail(OTG_E_OT, "topk needs k >= 1");
     if (nrows < 0 || (nrows > 0 && (!rows || !out))) fail(OTG_E_DIMENSION, "NULL rows / output");
@@ -527,6 +529,7 @@ otg_status otg_dual_F(otg_problem h, const double* u, const double* v, double* o
 
 otg_status otg_hessian_f(otg_problem h, const double* v, double* H) {
   return guard([&] {  // dual.cpp:118-136
+    OTG_RANGE("otg_hessian_f");
     Problem& P = problem_of(h);
     if (!H) fail(OTG_E_DIMENSION, "NULL output");
     const int64_t n = P.n_local, m = P.m;

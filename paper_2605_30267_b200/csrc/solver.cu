@@ -67,7 +67,7 @@ void put_ctrl(Problem& P, const Ctrl& c) {
 
 void get_ctrl(Problem& P) {
   OTG_CUDA(cudaMemcpyAsync(P.ctrl_host, P.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, P.stream));
-  OTG_CUDA(cudaStreamSynchronize(P.stream));
+  comm_sync(P);  // (sharded NCCL handles: polls the communicator's async error state)
 }
 
 void h2d(Problem& P, double* dst, const double* src, int64_t count) {
@@ -150,9 +150,12 @@ LoopOut run_loop(Problem& P, otg_solve_result* res, bool timed) {
   long long ev_before = P.ctrl_host->evaluations;
   OTG_CUDA(cudaEventRecord(t0, P.stream));
   for (;;) {
-    OTG_CUDA(cudaGraphLaunch(timed ? P.chunk_exec_timed : P.chunk_exec, P.stream));
-    lo.launches += timed ? P.chunk_kernels_timed : P.chunk_kernels;
-    get_ctrl(P);
+    {
+      OTG_RANGE("otg chunk (8 evaluations)");
+      OTG_CUDA(cudaGraphLaunch(timed ? P.chunk_exec_timed : P.chunk_exec, P.stream));
+      lo.launches += timed ? P.chunk_kernels_timed : P.chunk_kernels;
+      get_ctrl(P);
+    }
     if (P.sharded && comm_failed(P)) fail(OTG_E_NCCL, "host all-reduce callback failed");
     if (P.ctrl_host->done == kPaused) {
       // a sharded evaluation flagged columns: finish it eagerly (exact
@@ -319,6 +322,7 @@ extern "C" {
 
 otg_status otg_row_solve_marginals(otg_problem h, const double* v, double* u, double* col) {
   return guard([&] {
+    OTG_RANGE("otg_row_solve_marginals");
     Problem& P = get(h);
     check_finite_vec(v, P.m, "v");
     Ctrl c = base_ctrl(P);
@@ -337,6 +341,7 @@ otg_status otg_row_solve_marginals(otg_problem h, const double* v, double* u, do
 otg_status otg_row_solve_marginals_log(otg_problem h, const double* v, double* u, double* col,
                                        double* col_log) {
   return guard([&] {
+    OTG_RANGE("otg_row_solve_marginals_log");
     Problem& P = get(h);
     one_eval(P, v, true);
     d2h(P, u, P.u, P.n_local);
@@ -348,6 +353,7 @@ otg_status otg_row_solve_marginals_log(otg_problem h, const double* v, double* u
 
 otg_status otg_eval_normalized_step(otg_problem h, const double* v, otg_step_eval* out) {
   return guard([&] {
+    OTG_RANGE("otg_eval_normalized_step");
     Problem& P = get(h);
     one_eval(P, v, true);
     if (out) {
@@ -364,6 +370,7 @@ otg_status otg_eval_normalized_step(otg_problem h, const double* v, otg_step_eva
 otg_status otg_sinkhorn_solve(otg_problem h, const double* v0, const otg_solve_config* cfg,
                               otg_solve_result* res) {
   return guard([&] {
+    OTG_RANGE("otg_sinkhorn_solve");
     Problem& P = get(h);
     validate_solve_config(cfg);
     std::vector<double> zero;
@@ -412,6 +419,7 @@ static void start_acc(Problem& P, Ctrl& c, const double* x0, const double* w0, d
 otg_status otg_acc_solve(otg_problem h, const double* v0, double mu, const otg_solve_config* cfg,
                          otg_solve_result* res) {
   return guard([&] {
+    OTG_RANGE("otg_acc_solve");
     Problem& P = get(h);
     validate_solve_config(cfg);
     if (!(mu > 0.0) || !(mu < 1.0)) fail(OTG_E_OT, "mu must lie in (0, 1)");
@@ -439,6 +447,7 @@ otg_status otg_acc_run(otg_problem h, const double* x0, const double* w0, double
                        int64_t m_steps, int record_trace, int64_t trace_stride,
                        const otg_instr* instr, otg_solve_result* res) {
   return guard([&] {
+    OTG_RANGE("otg_acc_run");
     Problem& P = get(h);
     if (m_steps < 0) fail(OTG_E_OT, "acc_run needs m >= 0");
     check_finite_vec(x0, P.m, "x0");
@@ -462,6 +471,7 @@ otg_status otg_acc_run(otg_problem h, const double* x0, const double* w0, double
 otg_status otg_homotopy_solve(otg_problem h, const otg_homotopy_config* cfg,
                               const otg_instr* instr, otg_solve_result* res) {
   return guard([&] {
+    OTG_RANGE("otg_homotopy_solve");
     Problem& P = get(h);
     if (!cfg) fail(OTG_E_OT, "homotopy config is NULL");
     if (!(cfg->mu0 > 0.0) || !(cfg->mu0 < 1.0) || cfg->m0 < 1 || cfg->max_outer < 1)
@@ -490,6 +500,7 @@ otg_status otg_homotopy_solve(otg_problem h, const otg_homotopy_config* cfg,
 
 otg_status otg_plan_stats(otg_problem h, const double* u, const double* v, otg_plan_summary* out) {
   return guard([&] {
+    OTG_RANGE("otg_plan_stats");
     Problem& P = get(h);
     if (!out) fail(OTG_E_DIMENSION, "NULL output");
     check_finite_vec(u, P.n_local, "u");
