@@ -371,6 +371,10 @@ T* dalloc(Problem& P, size_t count) {
   void* ptr = nullptr;
   OTG_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
   P.device_bytes += static_cast<int64_t>(count * sizeof(T));
+  // per-row / per-column state starts zeroed (no kernel or diagnostic can
+  // read uninitialised indices); the cost itself (>= 1 GiB) is written in full
+  if (count * sizeof(T) < (size_t{1} << 30))
+    OTG_CUDA(cudaMemsetAsync(ptr, 0, count * sizeof(T), P.stream));
   return static_cast<T*>(ptr);
 }
 

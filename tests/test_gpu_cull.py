@@ -48,3 +48,20 @@ def test_cull_matches_dense_order():
     assert float(np.max(np.abs(culled.potentials.v - dense.potentials.v))) / scale < 2e-6
     assert ct.iterations == dt.iterations and ct.converged and dt.converged
     assert abs(ct.final_violation - dt.final_violation) <= 1e-6 * dt.final_violation + 1e-12
+
+
+@pytest.mark.gpu
+def test_cull_stats_needs_an_evaluated_handle():
+    """The culling bound uses the shift estimates of an evaluated state: on a
+    fresh handle otg_cull_stats refuses (it once read uninitialised argmax
+    indices there: an illegal address), and the context stays usable."""
+    n = m = 4096
+    x, y = ot.gen_config(5, n, m, 5)
+    p = ot.TransportProblem.from_points(np.full(n, 1 / n), np.full(m, 1 / m), x, y, 1e-3,
+                                        norm="none", storage="on_the_fly")
+    with pytest.raises(ot.OtError):
+        ot.cull_stats(p)
+    ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=3))
+    rows, cols = ot.cull_stats(p)
+    assert 0.0 < rows <= 1.0 and 0.0 < cols <= 1.0
+    p.close()
