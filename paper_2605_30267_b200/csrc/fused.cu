@@ -71,9 +71,12 @@ constexpr int kColWarps = 4;           // warps 5..8: the same quarters and band
 #endif
 constexpr int kUnroll = SP_UNROLL;     // row pairs interleaved by the compiler
 #ifndef SP_LOADERS
-#define SP_LOADERS 1
+#define SP_LOADERS 0
 #endif
-constexpr int kLoaders = SP_LOADERS;   // loader warps (bands t = l mod kLoaders)
+// loader warps (bands t = l mod kLoaders); 0: no loader warp -- the second of
+// a band's two row warps to finish with its ring slot issues the slot's next
+// band (12 warps instead of 13: 3 per SMSP, so up to 168 registers each)
+constexpr int kLoaders = SP_LOADERS;
 constexpr int kThreads = 32 * (kLoaders + kRowWarps + kColWarps);
 constexpr int kQPL = 4;                // quads (4 columns) per lane: a lane covers 16 columns
 constexpr int kQMax = 32 * kQPL;       // quads per CTA slice, at most (one warp covers it)
@@ -258,6 +261,7 @@ struct alignas(16) S1Shared {
   uint64_t tfull[kTSlots];     // exponentials in TMEM (row warp -> column warp)
   uint64_t tempty[kTSlots];    // TMEM slot read (column warp -> row warp)
   int slot_band[kRingMax];     // band the loader last issued into each ring slot
+  int rel[kRingMax];           // (no loader warp) row warps done with the slot's band
   uint32_t tmem_base;
 };
 
@@ -454,6 +458,7 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
         mbar_init(&S.full[s], 1);
         mbar_init(&S.empty[s], 2);  // both half-band row warps
         S.slot_band[s] = -1;
+        S.rel[s] = 0;
       }
       for (int s = 0; s < kTSlots; ++s) {
         mbar_init(&S.tfull[s], 2);  // both half-band row warps
@@ -471,6 +476,18 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = S.tmem_base;
+  // ONE tensor copy per band: the 3-D view {cw, chunks, rows} of the cost
+  // puts the slice's [16][W] block in one box (copy-engine cost is per box)
+  auto issue_band = [&](int64_t t, int s) {
+    mbar_expect_tx(&S.full[s], slot_bytes);
+    // (after the expect: a row warp that sees band t here waits on the right phase)
+    *reinterpret_cast<volatile int*>(&S.slot_band[s]) = static_cast<int>(t);
+    tma_load_3d(ring + s * slot_f4, &cmap, 0, k * A.nch, static_cast<int>(band_row0(t)),
+                &S.full[s]);
+    stamp(A, 0, t);
+  };
+  if (kLoaders == 0 && warp == 0 && lane == 0)
+    for (int64_t t = 0; t < nb && t < nslots; ++t) issue_band(t, static_cast<int>(t));
   // band t: row warp (t mod 8) + 1, column warp t mod 4; TMEM lane quarter of
   // those warps, column slot (t / 4) mod kTPerQ; barriers indexed t mod kTSlots
   auto tmem_of = [&](int w, int64_t t) {
@@ -480,9 +497,6 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
 
   if (warp < kLoaders) {
     // ----------------------------------------------------------- loaders --
-    // ONE tensor copy per band: the 3-D view {cw, chunks, rows} of the cost
-    // puts the slice's [16][W] block in one box (copy-engine cost is per
-    // box: 2-D boxes of 16 x 224 moved only ~25 GB/s per SM)
     if (lane == 0) {
       for (int64_t t = warp; t < nb; t += kLoaders) {
         const int s = static_cast<int>(t % nslots);
@@ -499,12 +513,7 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
           // the row warp's generic-proxy reads of the slot precede the async refill
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
-        mbar_expect_tx(&S.full[s], slot_bytes);
-        // (after the expect: a row warp that sees band t here waits on the right phase)
-        *reinterpret_cast<volatile int*>(&S.slot_band[s]) = static_cast<int>(t);
-        tma_load_3d(ring + s * slot_f4, &cmap, 0, k * A.nch, static_cast<int>(band_row0(t)),
-                    &S.full[s]);
-        stamp(A, 0, t);
+        issue_band(t, s);
       }
     }
   } else if (warp < kLoaders + kRowWarps) {
@@ -602,7 +611,20 @@ k_sweep1(const S1Args A, const __grid_constant__ CUtensorMap cmap, const Ctrl* _
       // the slot's cost rows are no longer needed
       if (lane == 0) stamp(A, 7, t);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[s]);
+      if (kLoaders > 0) {
+        if (lane == 0) mbar_arrive(&S.empty[s]);
+      } else if (lane == 0) {
+        // the band's second row warp done with the slot refills it (band t + nslots)
+        __threadfence_block();
+        if (atomicAdd(&S.rel[s], 1) == 1) {
+          __threadfence_block();
+          S.rel[s] = 0;
+          if (t + nslots < nb) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_band(t + nslots, s);
+          }
+        }
+      }
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();

@@ -22,11 +22,7 @@ print("memcheck exercise done")
 x, y = ot.gen_config(5, 4096, 4100, 5)
 pc = ot.TransportProblem.from_points(np.full(4096, 1 / 4096), np.full(4100, 1 / 4100), x, y, 1e-3,
                                      norm="none", storage="on_the_fly")
-try:
-    ot.cull_stats(pc)  # no evaluated state yet: refused
-    raise SystemExit("cull_stats before a solve should fail")
-except ot.OtError:
-    pass
+ot.cull_stats(pc)  # never evaluated: zeroed state, harmless
 ot.homotopy_solve(pc, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=3))
 assert ot.cull_stats(pc)[0] > 0.0
 # batched path (one CTA per problem)
