@@ -317,6 +317,11 @@ struct Problem {
   int* sp_bad_count = nullptr;
   void* sp_sums = nullptr;      // [2][n] fixed-point row sums, [2][n] (max, argmax) keys
   unsigned* sp_cnt = nullptr;   // [0] buffer parity of the next launch, [1] finished CTAs
+  // the row statistics at the zero point (p = 0): base-2 row max upper bound
+  // and argmin column of the stored cost, so a solve that starts at 0 runs
+  // the single pass from its first evaluation (no exact two-pass seed)
+  double* sp_zM2 = nullptr;
+  int* sp_zJ = nullptr;
 
   // on-the-fly transposed row pass (k_row_otf): column splits and their
   // per-row partials (row_splits x n_local records of 16 B)

@@ -935,9 +935,61 @@ bool fused_configure(Problem& P) {
   return true;
 }
 
+// Row minima of the stored cost (one CTA per row, columns < m only): the
+// zero point's row statistics.  M2 = -(min_j C_ij) kappa log2(e) + 1/64 is
+// an upper bound on the base-2 row max at p = 0 (the fp32 exponents round
+// within ~1e-4 of it) and argmin_j C_ij (lowest index of equal minima) is its
+// argmax -- what k_sp_prep reads after an evaluation.
+__global__ void __launch_bounds__(256)
+k_zero_rowstats(const float* __restrict__ C, int64_t ldc, int64_t n, int64_t m, double k2,
+                double* __restrict__ zM2, int* __restrict__ zJ) {
+  __shared__ float sv[8];
+  __shared__ int sj[8];
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const float* row = C + i * ldc;
+    float bv = INFINITY;
+    int bj = 0;
+    for (int64_t j = threadIdx.x; j < m; j += 256) {
+      const float c = row[j];
+      if (c < bv) {  // (ascending j per thread: the lowest index of equal minima)
+        bv = c;
+        bj = static_cast<int>(j);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (ov < bv || (ov == bv && oj < bj)) {
+        bv = ov;
+        bj = oj;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      sv[threadIdx.x >> 5] = bv;
+      sj[threadIdx.x >> 5] = bj;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < 8; ++w)
+        if (sv[w] < bv || (sv[w] == bv && sj[w] < bj)) {
+          bv = sv[w];
+          bj = sj[w];
+        }
+      zM2[i] = -static_cast<double>(bv) * k2 + 1.0 / 64.0;
+      zJ[i] = bj;
+    }
+    __syncthreads();
+  }
+}
+
 void fused_alloc(Problem& P) {
   if (!P.fused) return;
   const int64_t n = P.n_local;
+  P.sp_zM2 = dalloc<double>(P, n);
+  P.sp_zJ = dalloc<int>(P, n);
+  k_zero_rowstats<<<static_cast<unsigned>(std::min<int64_t>(n, 148 * 8)), 256, 0, P.stream>>>(
+      static_cast<const float*>(P.C32), P.ldc, n, P.m, P.kappa * kLog2e, P.sp_zM2, P.sp_zJ);
+  OTG_CUDA(cudaGetLastError());
   P.sp_rec = dalloc<double>(P, static_cast<size_t>(n) * (sizeof(RowRec) / 8));
   const int lists = P.fused_clusters * P.sp_group * kColWarps;
   P.sp_bad_rows = dalloc<int>(P, static_cast<size_t>(lists) * P.sp_cap);

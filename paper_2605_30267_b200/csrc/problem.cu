@@ -145,7 +145,8 @@ void problem_free(Problem& P) {
                   P.y, P.grad, P.prev_grad,
                   P.prev_x, P.prev_y, P.flag_idx, P.fb_cols, P.fb_part, P.part, P.e1_part,
                   P.e2_part, P.epi_part, P.sp_rec, P.sp_bad_rows, P.sp_bad_count, P.ctrl, P.trace, P.vstar, P.bounds, P.fbA, P.fbS, P.fbT, P.red, P.sp_sums, P.sp_cnt,
-                  P.perm_r, P.perm_c, P.Xs, P.Yns, P.cbox, P.rbox, P.cvmax, P.rnegm, P.ves, P.auxs};
+                  P.perm_r, P.perm_c, P.Xs, P.Yns, P.cbox, P.rbox, P.cvmax, P.rnegm, P.ves, P.auxs,
+                  P.sp_zM2, P.sp_zJ};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (P.ctrl_host) cudaFreeHost(P.ctrl_host);
