@@ -385,3 +385,26 @@ def test_fused_homotopy_cost_and_iterations():
     cg = ot.plan_stats(pf, g.potentials.u, g.potentials.v).primal_cost
     co = O.plan_stats(q, o.u, o.v, eps)["primal_cost"]
     assert abs(cg - co) <= REL32 * abs(co)
+
+
+@pytest.mark.parametrize("solver", ["sinkhorn", "acc", "acc_warm"])
+def test_single_pass_zero_point_seed(solver):
+    """Solves on a single-pass handle that start at the zero point skip the
+    exact two-pass seed evaluation (the row statistics of p = 0 come from the
+    cost's row minima); a warm start (acc_warm: nonzero v0) takes the exact
+    seed.  Both agree with the two-pass handle to the fp32 bar."""
+    n, m, eps = 300, 4100, 2e-3
+    pf = _points_problem(n, m, 13, eps, True)
+    p2 = _points_problem(n, m, 13, eps, False)
+    assert pf.handle.info.sweep_mode == 2 and p2.handle.info.sweep_mode == 1
+    cfg = ot.SolveConfig(tol_l1=1e-300, max_iters=40)
+    v0 = None
+    if solver == "acc_warm":
+        v0 = O.random_zero_sum(O.Rng(3), m, 5.0)
+    if solver == "sinkhorn":
+        gf, g2 = ot.sinkhorn_solve(pf, v0, cfg), ot.sinkhorn_solve(p2, v0, cfg)
+    else:
+        gf, g2 = ot.acc_solve(pf, v0, 0.5, cfg), ot.acc_solve(p2, v0, 0.5, cfg)
+    assert gf.iterations == g2.iterations == 40
+    assert rel(gf.potentials.v, g2.potentials.v) <= 2e-6
+    assert rel(gf.potentials.u, g2.potentials.u) <= 2e-6
