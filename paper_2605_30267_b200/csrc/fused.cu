@@ -870,12 +870,14 @@ bool fused_configure(Problem& P) {
   int sms = 0;
   OTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.device));
   const SpLayout L = sp_layout(P.m, sms);
-  // the grid-wide band pipeline needs a long run of bands per group to pay
-  // for its fill (B200: 8192^2 in 9 groups of 57 bands 0.18 ms vs two-pass
-  // 0.11 ms; 2048 x 65536, 128 bands 0.27 vs 0.20; 65536^2, 4096 bands 3.5 vs 5.1)
+  // the grid-wide band pipeline needs a run of bands per group to pay for its
+  // fill (B200, round-2 kernel, us per evaluation single / two-pass,
+  // tools/sp_crossover.py: 2048 x 8192 (14 bands per group) 78 / 81, 4096 x
+  // 8192 (28) 105 / 104, 8192^2 (57) 115 / 136, 8192 x 2048 67 / 89, 65536 x
+  // 1024 126 / 416, 2048 x 65536 208 / 259, 65536^2 3400 / 5100)
   const int64_t bands_per_group = ((P.n_local + kR - 1) / kR + L.H - 1) / std::max(L.H, 1);
   if (!L.ok || P.ldc % L.cw != 0 || P.n_local < 2 * kR) return false;
-  if (bands_per_group < 512 && !P.force_single_pass) return false;
+  if (bands_per_group < 32 && !P.force_single_pass) return false;
   const int64_t W = static_cast<int64_t>(L.cw) * L.nch;
   const int64_t head = ((sizeof(S1Shared) + 127) / 128) * 128;
   const int64_t slot = kR * W * 4;
