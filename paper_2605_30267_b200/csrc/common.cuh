@@ -367,6 +367,11 @@ struct Problem {
   size_t ar_host_len = 0;
   double* red = nullptr;      // sharded: this rank's merged column partials (+ <u, a>)
   int capturing = 0;          // launch_eval is being captured into the chunk graph
+  // single-pass handles: a second chunk graph for evaluations that follow one
+  // (shift estimates valid): no exact-path kernels, merge folded into the patch
+  int steady_capture = 0;     // the steady graph is being captured
+  cudaGraphExec_t chunk_exec_steady = nullptr;
+  int chunk_kernels_steady = 0;
 };
 
 // allocation helpers (track bytes)
@@ -405,6 +410,10 @@ bool fused_configure(Problem& P);
 void fused_alloc(Problem& P);
 void launch_fused(Problem& P, float kh, float kl);
 void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int ncl, int64_t cap);
+// unsharded single pass: the loose rows' column patch + the merge of the
+// partial rows + the underflow flags + <u, a> in one kernel (sweep.cu)
+void launch_sp_patch_merge(Problem& P, float kh, float kl, int nlists);
+inline bool patch_merges(const Problem& P) { return P.fused && !P.sharded; }
 int partial_rows(const Problem& P);  // rows of P.part the merge sums
 
 // collectives of a sharded handle (comm.cpp).  recv may equal send.  Both

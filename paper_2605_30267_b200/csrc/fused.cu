@@ -280,9 +280,18 @@ k_sp_prep(int64_t n, int64_t m, const float* __restrict__ C, int64_t ldc,
           double* __restrict__ rowM2, int* __restrict__ rowJ, const double* __restrict__ a,
           const double* __restrict__ loga, RowRec* __restrict__ rec,
           const unsigned long long* __restrict__ tkey, unsigned* __restrict__ state,
-          const Ctrl* __restrict__ ctrl) {
+          Ctrl* __restrict__ ctrl, int steady) {
   pdl_wait();  // programmatic dependent launch: after the previous kernel
-  if (ctrl->done || !ctrl->shift_valid) return;
+  if (ctrl->done) return;
+  if (!ctrl->shift_valid) {
+    // the steady graph has no exact-path kernels: an evaluation without shift
+    // estimates there (a non-finite step) ends the solve with an error
+    if (steady && blockIdx.x == 0 && threadIdx.x == 0) {
+      ctrl->error = OTG_E_OT;
+      ctrl->done = 1;
+    }
+    return;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) state[2] = 0u;  // loose rows listed by this evaluation
   const double dmax2 = ctrl->dmax2;
   const unsigned long long* prev = tkey + static_cast<int64_t>(state[0] ^ 1u) * n;
@@ -1013,7 +1022,7 @@ void launch_fused(Problem& P, float kh, float kl) {
   launch_k(k_sp_prep, 296, 256, 0, P.stream, P.n_local, P.m, static_cast<const float*>(P.C32), P.ldc,
            static_cast<const float*>(P.vq), P.mpad, kh, kl, P.rowM2, P.rowJ, P.a, P.loga, rec,
            static_cast<const unsigned long long*>(sums + 2 * P.n_local),
-           P.sp_cnt, P.ctrl);
+           P.sp_cnt, P.ctrl, P.steady_capture);
   S1Args A;
   A.dbg = nullptr;
   A.rec = rec;
@@ -1061,6 +1070,11 @@ void launch_fused(Problem& P, float kh, float kl) {
   OTG_CUDA(cudaLaunchKernelEx(&cfg, k_sweep1, A, *reinterpret_cast<const CUtensorMap*>(P.sp_tmap),
                               static_cast<const Ctrl*>(P.ctrl)));
   launch_sp_redo(P, P.sp_bad_rows, P.sp_bad_count, ctas * kColWarps, P.sp_cap);
+  if (patch_merges(P)) {  // patch + merge + flags + <u, a> in one kernel
+    launch_sp_patch_merge(P, kh, kl, ctas * kColWarps);
+    OTG_CUDA(cudaGetLastError());
+    return;
+  }
   const unsigned g = static_cast<unsigned>((P.m + kPatchThreads - 1) / kPatchThreads);
   launch_k(k_sp_patch, g, kPatchThreads, 0, P.stream, P.C32, P.ldc, P.m, P.p, kh, kl, P.aux,
            P.sp_bad_rows, P.sp_bad_count, ctas * kColWarps, P.sp_cap,

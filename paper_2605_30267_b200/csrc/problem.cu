@@ -152,6 +152,7 @@ void problem_free(Problem& P) {
   if (P.ctrl_host) cudaFreeHost(P.ctrl_host);
   if (P.chunk_exec) cudaGraphExecDestroy(P.chunk_exec);
   if (P.chunk_exec_timed) cudaGraphExecDestroy(P.chunk_exec_timed);
+  if (P.chunk_exec_steady) cudaGraphExecDestroy(P.chunk_exec_steady);
   for (cudaEvent_t e : P.chunk_events) cudaEventDestroy(e);
   if (P.nccl_comm) comm_destroy(P);
   if (P.stream) cudaStreamDestroy(P.stream);

@@ -107,8 +107,8 @@ void raise_device_error(const Ctrl& c) {
   if (c.error) fail(static_cast<otg_status>(c.error), "device-side error");
 }
 
-void build_graph(Problem& P, bool timed) {
-  cudaGraphExec_t& exec = timed ? P.chunk_exec_timed : P.chunk_exec;
+void build_graph(Problem& P, bool timed, bool steady = false) {
+  cudaGraphExec_t& exec = steady ? P.chunk_exec_steady : (timed ? P.chunk_exec_timed : P.chunk_exec);
   if (exec) return;
   if (timed && P.chunk_events.empty()) {
     P.chunk_events.resize(5 * kChunk);
@@ -117,6 +117,7 @@ void build_graph(Problem& P, bool timed) {
   cudaGraph_t g = nullptr;
   OTG_CUDA(cudaStreamBeginCapture(P.stream, cudaStreamCaptureModeThreadLocal));
   P.capturing = 1;
+  P.steady_capture = steady ? 1 : 0;
   try {
     for (int k = 0; k < kChunk; ++k) {
       launch_eval(P, true, timed, timed ? &P.chunk_events[5 * k] : nullptr);
@@ -127,11 +128,13 @@ void build_graph(Problem& P, bool timed) {
     }
   } catch (...) {
     P.capturing = 0;
+    P.steady_capture = 0;
     cudaStreamEndCapture(P.stream, &g);
     if (g) cudaGraphDestroy(g);
     throw;
   }
   P.capturing = 0;
+  P.steady_capture = 0;
   OTG_CUDA(cudaStreamEndCapture(P.stream, &g));
   size_t nn = 0;
   OTG_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
@@ -143,7 +146,7 @@ void build_graph(Problem& P, bool timed) {
     OTG_CUDA(cudaGraphNodeGetType(nd, &t));
     kernels += (t == cudaGraphNodeTypeKernel);
   }
-  (timed ? P.chunk_kernels_timed : P.chunk_kernels) = kernels;
+  (steady ? P.chunk_kernels_steady : (timed ? P.chunk_kernels_timed : P.chunk_kernels)) = kernels;
   OTG_CUDA(cudaGraphInstantiate(&exec, g, 0));
   cudaGraphDestroy(g);
   P.chunk_len = kChunk;
@@ -160,6 +163,11 @@ struct LoopOut {
 // the trace ring into res->trace after every chunk.
 LoopOut run_loop(Problem& P, otg_solve_result* res, bool timed) {
   build_graph(P, timed);
+  // unsharded single-pass handles replay the steady graph (no exact-path
+  // kernels, merge in the patch kernel) for chunks that start after an
+  // evaluation (or at the zero point: zero_start)
+  const bool use_steady = patch_merges(P) && !timed;
+  if (use_steady) build_graph(P, false, true);
   cudaEvent_t t0, t1;
   OTG_CUDA(cudaEventCreate(&t0));
   OTG_CUDA(cudaEventCreate(&t1));
@@ -170,8 +178,12 @@ LoopOut run_loop(Problem& P, otg_solve_result* res, bool timed) {
   for (;;) {
     {
       OTG_RANGE("otg chunk (8 evaluations)");
-      OTG_CUDA(cudaGraphLaunch(timed ? P.chunk_exec_timed : P.chunk_exec, P.stream));
-      lo.launches += timed ? P.chunk_kernels_timed : P.chunk_kernels;
+      const bool steady = use_steady && P.ctrl_host->shift_valid;
+      OTG_CUDA(cudaGraphLaunch(steady ? P.chunk_exec_steady
+                                      : (timed ? P.chunk_exec_timed : P.chunk_exec),
+                               P.stream));
+      lo.launches += steady ? P.chunk_kernels_steady
+                            : (timed ? P.chunk_kernels_timed : P.chunk_kernels);
       get_ctrl(P);
     }
     if (P.sharded && comm_failed(P)) fail(OTG_E_NCCL, "host all-reduce callback failed");

@@ -1976,9 +1976,10 @@ k_merge(const double* __restrict__ part, int nshards, int splits, int64_t m, int
         double* __restrict__ col, double* __restrict__ col_log, int* __restrict__ flag_idx,
         int* __restrict__ fb_cols, const double* __restrict__ u, const double* __restrict__ a,
         int64_t nrows, int do_merge, int flag, Ctrl* __restrict__ ctrl, int fused_rows,
-        int ua_n) {
+        int ua_n, int patch_merged) {
   pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done) return;
+  if (patch_merged && ctrl->shift_valid) return;  // k_sp_patch_merge did this evaluation's merge
   __shared__ double sh[kEThreads / 32];
   merge_body(part, nshards, splits, m, mpad, col, col_log, flag_idx, fb_cols, u, a, nrows,
              do_merge, flag, ctrl, blockIdx.x, gridDim.x, sh, fused_rows, ua_n);
@@ -3090,11 +3091,12 @@ void launch_row_pass(Problem& P) {
                                                      P.rowM2, P.rowJ, P.redo_rows, P.ctrl)
     const bool otf = P.storage == OTG_STORE_ON_THE_FLY;
     if (P.fused) {
-      // exact first evaluation (two-pass), then the single-pass kernel
-      launch_k(k_row_exact<4, false>, resident_grid(P, k_row_exact<4, false>, blocks), kRowThreads,
-               0, P.stream, 
-          src, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM, P.rowS, P.u, P.wrow, P.aux,
-          P.rowM2, P.rowJ, P.ctrl, P.vq, P.mpad);
+      // exact first evaluation (two-pass), then the single-pass kernel (the
+      // steady graph follows an evaluation: no exact-path kernel)
+      if (!P.steady_capture)
+        launch_k(k_row_exact<4, false>, resident_grid(P, k_row_exact<4, false>, blocks),
+                 kRowThreads, 0, P.stream, src, P.n_local, P.m, P.p, P.kappa, P.a, P.loga, P.rowM,
+                 P.rowS, P.u, P.wrow, P.aux, P.rowM2, P.rowJ, P.ctrl, P.vq, P.mpad);
       launch_fused(P, kh, kl);
     } else if (otf && P.row_splits > 0 && R == 8) {
       launch_k(k_row_exact<8, true>, resident_grid(P, k_row_exact<8, true>, blocks), kRowThreads, 0,
@@ -3147,6 +3149,7 @@ void launch_col_pass(Problem& P) {
   const double k2 = P.kappa * kLog2e;
   const float kh = static_cast<float>(k2);
   const float kl = static_cast<float>(k2 - static_cast<double>(kh));
+  if (P.fused && P.steady_capture) return;  // the single pass did the columns
   for (int s = 0; s < P.vshards; ++s) {
     const int64_t lo = s * shard_rows, hi = std::min(P.n_local, lo + shard_rows);
     double* part = P.part + static_cast<int64_t>(s) * P.col_splits * P.mpad;
@@ -3197,6 +3200,79 @@ void launch_sp_redo(Problem& P, const int* bad_rows, const int* bad_count, int n
                                                 static_cast<const unsigned*>(P.sp_cnt + 2), P.ctrl);
 }
 
+int64_t merge_blocks(const Problem& P);
+
+// Unsharded single pass, steady state: column j's patch (the rows the pass
+// listed as loose, in list order -- k_sp_patch's formula), then the merge of
+// the H group rows + that patch row with merge_body's 8-chain tree (bitwise
+// the k_merge result), the underflow flag and <u, a> slice blk: one kernel
+// instead of k_sp_patch + k_merge.
+__global__ void __launch_bounds__(kEThreads)
+k_sp_patch_merge(const float* __restrict__ C, int64_t ldc, int64_t m, int64_t mpad,
+                 const double* __restrict__ p, float kh, float kl, const float4* __restrict__ aux,
+                 const int* __restrict__ bad_rows, const int* __restrict__ bad_count, int nlists,
+                 int64_t cap, const unsigned* __restrict__ total, double* __restrict__ part, int H,
+                 double* __restrict__ col, double* __restrict__ col_log, int* __restrict__ flag_idx,
+                 int* __restrict__ fb_cols, const double* __restrict__ u,
+                 const double* __restrict__ a, int64_t nrows, int ua_n, Ctrl* __restrict__ ctrl) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
+  if (ctrl->done || !ctrl->shift_valid) return;
+  __shared__ double sh[kEThreads / 32];
+  const int blk = blockIdx.x;
+  if (blk < ua_n) {  // <u, a> over row slice blk of ua_n (as merge_body)
+    const int64_t r0 = nrows * blk / ua_n, r1 = nrows * (blk + 1) / ua_n;
+    double t = 0.0;
+    for (int64_t k = r0 + threadIdx.x; k < r1; k += kEThreads) t += u[k] * a[k];
+    t = block_sum<kEThreads>(t, sh);
+    if (threadIdx.x == 0) col[mpad + 1 + blk] = t;
+  }
+  const int64_t j = static_cast<int64_t>(blk) * kEThreads + threadIdx.x;
+  if (j >= m) return;
+  double patch = 0.0;
+  if (*total != 0u) {
+    const double x2 = p[j] * kLog2e;
+    const double h = rint(x2 * 256.0) * (1.0 / 256.0);
+    const float Vc = static_cast<float>(h), vf = static_cast<float>(x2 - h);
+    for (int c = 0; c < nlists; ++c) {
+      const int nbad = bad_count[c];
+      for (int q = 0; q < nbad; ++q) {
+        const int64_t i = bad_rows[c * cap + q];
+        const float4 ax = aux[i];
+        const float cc = C[i * ldc + j];
+        const float Aq = Vc - ax.x;
+        const float gq = fmaf(-cc, kl, vf - ax.y);
+        const float tt = fmaf(-cc, kh, Aq) + gq;
+        patch += static_cast<double>(ax.z * ex2_approx(tt));
+      }
+    }
+  }
+  part[static_cast<int64_t>(H) * mpad + j] = patch;
+  double l[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int k = 0; k < H; ++k) l[k & 7] += part[static_cast<int64_t>(k) * mpad + j];
+  l[H & 7] += patch;
+  const double c = 0.0 + (((l[0] + l[1]) + (l[2] + l[3])) + ((l[4] + l[5]) + (l[6] + l[7])));
+  col[j] = c;
+  if (c >= ctrl->tiny) {
+    col_log[j] = log(c);
+    flag_idx[j] = -1;
+  } else {
+    const unsigned slot = atomicAdd(&ctrl->fb_count, 1u);
+    fb_cols[slot] = static_cast<int>(j);
+    flag_idx[j] = static_cast<int>(slot);
+  }
+}
+
+void launch_sp_patch_merge(Problem& P, float kh, float kl, int nlists) {
+  const unsigned g = static_cast<unsigned>(merge_blocks(P));
+  launch_k(k_sp_patch_merge, g, kEThreads, 0, P.stream, static_cast<const float*>(P.C32), P.ldc,
+           P.m, P.mpad, static_cast<const double*>(P.p), kh, kl,
+           static_cast<const float4*>(P.aux), static_cast<const int*>(P.sp_bad_rows),
+           static_cast<const int*>(P.sp_bad_count), nlists, P.sp_cap,
+           static_cast<const unsigned*>(P.sp_cnt + 2), P.part, P.fused_clusters, P.col, P.col_log,
+           P.flag_idx, P.fb_cols, static_cast<const double*>(P.u),
+           static_cast<const double*>(P.a), P.n_local, static_cast<int>(merge_blocks(P)), P.ctrl);
+}
+
 int partial_rows(const Problem& P) { return P.vshards * P.col_splits; }
 
 int64_t merge_blocks(const Problem& P) { return (P.m + kEThreads - 1) / kEThreads; }
@@ -3212,7 +3288,8 @@ static void launch_merge(Problem& P, bool merge, bool flag) {
                                               P.col_log, P.flag_idx, P.fb_cols, P.u, P.a,
                                               P.n_local, merge ? 1 : 0, flag ? 1 : 0, P.ctrl,
                                               P.fused ? P.fused_clusters + 1 : 0,
-                                              static_cast<int>(merge_blocks(P)));
+                                              static_cast<int>(merge_blocks(P)),
+                                              patch_merges(P) ? 1 : 0);
   OTG_CUDA(cudaGetLastError());
 }
 
@@ -3222,7 +3299,7 @@ void launch_merge_nolog(Problem& P) { launch_merge(P, true, false); }
 static void launch_merge_into(Problem& P, double* dst) {
   launch_k(k_merge, merge_grid(P), kEThreads, 0, P.stream, P.part, P.vshards, P.col_splits,
            P.m, P.mpad, dst, P.col_log, P.flag_idx, P.fb_cols, P.u, P.a, P.n_local, 1, 0,
-           P.ctrl, P.fused ? P.fused_clusters + 1 : 0, static_cast<int>(merge_blocks(P)));
+           P.ctrl, P.fused ? P.fused_clusters + 1 : 0, static_cast<int>(merge_blocks(P)), 0);
   OTG_CUDA(cudaGetLastError());
 }
 
@@ -3374,7 +3451,7 @@ void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
       P.apply_pending = 1;
       return;
     }
-  } else {
+  } else if (!(P.steady_capture && patch_merges(P))) {
     launch_merge(P, true, with_log);
   }
   if (!with_log) return;
