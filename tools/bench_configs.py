@@ -98,8 +98,14 @@ def cfg2(cpu):
                        iters_per_s=r.iterations / r.device_seconds,
                        sweep_mode=int(p.handle.info.sweep_mode),
                        row_ms=1e3 * row, col_ms=1e3 * col,
-                       row_frac=bytes_pass / row / 1e9 / peak if row > 0 else None,
-                       col_frac=bytes_pass / col / 1e9 / peak if col > 0 else None,
+                       # two-pass: each pass reads the cost once; single pass
+                       # (mode 2): ONE read for the whole evaluation sweep
+                       row_frac=(bytes_pass / row / 1e9 / peak
+                                 if row > 0 and p.handle.info.sweep_mode != 2 else None),
+                       col_frac=(bytes_pass / col / 1e9 / peak
+                                 if col > 0 and p.handle.info.sweep_mode != 2 else None),
+                       sweep_frac=(bytes_pass / (row + col) / 1e9 / peak
+                                   if p.handle.info.sweep_mode == 2 and row + col > 0 else None),
                        clocks=clk.summary())
             if cpu:
                 q = O.Problem(a, a, C32, cost_div=eps)
