@@ -188,6 +188,7 @@ struct Ctrl {
   int is_step;        // the eval in flight is an accelerated step (not a seed)
   int have_prev;      // stability: previous observation stored
   int live_e2;        // finalize -> apply handoff for the current eval
+  int fin_done;       // steady single pass: k_sp_patch_merge finalized this eval (no flags)
   long long k;        // observation index (sinkhorn / acc / acc_run)
   long long evaluations;
   long long iterations;

@@ -292,7 +292,10 @@ k_sp_prep(int64_t n, int64_t m, const float* __restrict__ C, int64_t ldc,
     }
     return;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) state[2] = 0u;  // loose rows listed by this evaluation
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    state[2] = 0u;       // loose rows listed by this evaluation
+    ctrl->fin_done = 0;  // (k_sp_patch_merge may finalize this evaluation)
+  }
   const double dmax2 = ctrl->dmax2;
   const unsigned long long* prev = tkey + static_cast<int64_t>(state[0] ^ 1u) * n;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; i < n;

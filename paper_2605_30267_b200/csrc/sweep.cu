@@ -2478,7 +2478,7 @@ __device__ __forceinline__ void fallback_all(const FinArgs& A, unsigned nf, doub
 __global__ void __launch_bounds__(kEThreads, 2)
 k_finalize(const FinArgs A, Ctrl* __restrict__ ctrl) {
   pdl_wait();  // programmatic dependent launch: after the previous kernel
-  if (ctrl->done) return;
+  if (ctrl->done || ctrl->fin_done) return;  // (fin_done: k_sp_patch_merge finalized it)
   __shared__ double sh[kEThreads / 32 * 8];
   __shared__ bool last;
   // K5 folded in (unsharded): every CTA takes its share of the flagged
@@ -3214,10 +3214,12 @@ k_sp_patch_merge(const float* __restrict__ C, int64_t ldc, int64_t m, int64_t mp
                  int64_t cap, const unsigned* __restrict__ total, double* __restrict__ part, int H,
                  double* __restrict__ col, double* __restrict__ col_log, int* __restrict__ flag_idx,
                  int* __restrict__ fb_cols, const double* __restrict__ u,
-                 const double* __restrict__ a, int64_t nrows, int ua_n, Ctrl* __restrict__ ctrl) {
+                 const double* __restrict__ a, int64_t nrows, int ua_n, const FinArgs F,
+                 int fin_fuse, Ctrl* __restrict__ ctrl) {
   pdl_wait();  // programmatic dependent launch: after the previous kernel
   if (ctrl->done || !ctrl->shift_valid) return;
-  __shared__ double sh[kEThreads / 32];
+  __shared__ double sh[kEThreads / 32 * 8];
+  __shared__ bool last;
   const int blk = blockIdx.x;
   if (blk < ua_n) {  // <u, a> over row slice blk of ua_n (as merge_body)
     const int64_t r0 = nrows * blk / ua_n, r1 = nrows * (blk + 1) / ua_n;
@@ -3227,50 +3229,78 @@ k_sp_patch_merge(const float* __restrict__ C, int64_t ldc, int64_t m, int64_t mp
     if (threadIdx.x == 0) col[mpad + 1 + blk] = t;
   }
   const int64_t j = static_cast<int64_t>(blk) * kEThreads + threadIdx.x;
-  if (j >= m) return;
-  double patch = 0.0;
-  if (*total != 0u) {
-    const double x2 = p[j] * kLog2e;
-    const double h = rint(x2 * 256.0) * (1.0 / 256.0);
-    const float Vc = static_cast<float>(h), vf = static_cast<float>(x2 - h);
-    for (int c = 0; c < nlists; ++c) {
-      const int nbad = bad_count[c];
-      for (int q = 0; q < nbad; ++q) {
-        const int64_t i = bad_rows[c * cap + q];
-        const float4 ax = aux[i];
-        const float cc = C[i * ldc + j];
-        const float Aq = Vc - ax.x;
-        const float gq = fmaf(-cc, kl, vf - ax.y);
-        const float tt = fmaf(-cc, kh, Aq) + gq;
-        patch += static_cast<double>(ax.z * ex2_approx(tt));
+  E1Acc e;
+  if (j < m) {
+    double patch = 0.0;
+    if (*total != 0u) {
+      const double x2 = p[j] * kLog2e;
+      const double h = rint(x2 * 256.0) * (1.0 / 256.0);
+      const float Vc = static_cast<float>(h), vf = static_cast<float>(x2 - h);
+      for (int c = 0; c < nlists; ++c) {
+        const int nbad = bad_count[c];
+        for (int q = 0; q < nbad; ++q) {
+          const int64_t i = bad_rows[c * cap + q];
+          const float4 ax = aux[i];
+          const float cc = C[i * ldc + j];
+          const float Aq = Vc - ax.x;
+          const float gq = fmaf(-cc, kl, vf - ax.y);
+          const float tt = fmaf(-cc, kh, Aq) + gq;
+          patch += static_cast<double>(ax.z * ex2_approx(tt));
+        }
       }
     }
+    part[static_cast<int64_t>(H) * mpad + j] = patch;
+    double l[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < H; ++k) l[k & 7] += part[static_cast<int64_t>(k) * mpad + j];
+    l[H & 7] += patch;
+    const double c = 0.0 + (((l[0] + l[1]) + (l[2] + l[3])) + ((l[4] + l[5]) + (l[6] + l[7])));
+    col[j] = c;
+    if (c >= ctrl->tiny) {
+      col_log[j] = log(c);
+      flag_idx[j] = -1;
+      // steady graph: finalize the column now (flagged columns wait for the
+      // exact LSE: k_finalize then redoes the whole evaluation's finalize)
+      if (fin_fuse) finalize_col(F, j, -1, e);
+    } else {
+      const unsigned slot = atomicAdd(&ctrl->fb_count, 1u);
+      fb_cols[slot] = static_cast<int>(j);
+      flag_idx[j] = static_cast<int>(slot);
+    }
   }
-  part[static_cast<int64_t>(H) * mpad + j] = patch;
-  double l[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  for (int k = 0; k < H; ++k) l[k & 7] += part[static_cast<int64_t>(k) * mpad + j];
-  l[H & 7] += patch;
-  const double c = 0.0 + (((l[0] + l[1]) + (l[2] + l[3])) + ((l[4] + l[5]) + (l[6] + l[7])));
-  col[j] = c;
-  if (c >= ctrl->tiny) {
-    col_log[j] = log(c);
-    flag_idx[j] = -1;
-  } else {
-    const unsigned slot = atomicAdd(&ctrl->fb_count, 1u);
-    fb_cols[slot] = static_cast<int>(j);
-    flag_idx[j] = static_cast<int>(slot);
+  if (!fin_fuse) return;
+  // the E1 partials of this CTA's columns; the last CTA runs the solver's
+  // control step unless a column was flagged (then k_finalize does it all)
+  store_e1<kEThreads>(F, blk, e, sh);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&ctrl->e1_counter, 1u) == gridDim.x - 1;
   }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (*reinterpret_cast<volatile unsigned*>(&ctrl->fb_count) != 0u) {
+    if (threadIdx.x == 0) ctrl->e1_counter = 0;
+    return;
+  }
+  finalize_tail<kEThreads>(F, static_cast<int>(gridDim.x), sh, ctrl);
+  if (threadIdx.x == 0) ctrl->fin_done = 1;
 }
+
+static FinArgs fin_args(const Problem& P, int64_t ua_slices);
 
 void launch_sp_patch_merge(Problem& P, float kh, float kl, int nlists) {
   const unsigned g = static_cast<unsigned>(merge_blocks(P));
+  // the finalize folds in only in the steady graph, with k_finalize's own
+  // column partition (one 256-column work unit per CTA)
+  const int fin_fuse = (P.steady_capture && merge_blocks(P) == P.e_blocks) ? 1 : 0;
   launch_k(k_sp_patch_merge, g, kEThreads, 0, P.stream, static_cast<const float*>(P.C32), P.ldc,
            P.m, P.mpad, static_cast<const double*>(P.p), kh, kl,
            static_cast<const float4*>(P.aux), static_cast<const int*>(P.sp_bad_rows),
            static_cast<const int*>(P.sp_bad_count), nlists, P.sp_cap,
            static_cast<const unsigned*>(P.sp_cnt + 2), P.part, P.fused_clusters, P.col, P.col_log,
            P.flag_idx, P.fb_cols, static_cast<const double*>(P.u),
-           static_cast<const double*>(P.a), P.n_local, static_cast<int>(merge_blocks(P)), P.ctrl);
+           static_cast<const double*>(P.a), P.n_local, static_cast<int>(merge_blocks(P)),
+           fin_args(P, merge_blocks(P)), fin_fuse, P.ctrl);
 }
 
 int partial_rows(const Problem& P) { return P.vshards * P.col_splits; }
