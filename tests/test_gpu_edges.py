@@ -155,3 +155,31 @@ def test_many_flagged_columns_sorted_fallback():
     # the exact column LSE ran for (at least) the far columns
     s = ot.homotopy_solve(p, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=1))
     assert s.fallback_columns >= m - m // 3
+
+
+@pytest.mark.parametrize("sweep", ["single_pass"])
+def test_flagged_columns_in_the_steady_single_pass_graph(sweep):
+    """Underflowed columns on a single-pass handle: the solve starts at the
+    zero point, so its first evaluations already run the steady chunk graph
+    (no exact-path kernels, finalize folded into the patch/merge kernel);
+    evaluations with flagged columns must fall through to k_finalize's exact
+    column LSE.  Against the two-pass handle and the oracle."""
+    rng = np.random.default_rng(5)
+    n, m = 384, 3000
+    x = rng.uniform(0.0, 0.1, size=(n, 3))
+    y = np.concatenate([rng.uniform(0.0, 0.1, size=(m // 3, 3)),
+                        rng.uniform(0.9, 1.0, size=(m - m // 3, 3))])
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    ps = ot.TransportProblem.from_points(a, b, x, y, 5e-4, sweep=sweep)
+    p2 = ot.TransportProblem.from_points(a, b, x, y, 5e-4, sweep="two_pass")
+    assert ps.handle.info.sweep_mode == 2 and p2.handle.info.sweep_mode == 1
+    s1 = ot.homotopy_solve(ps, ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=1))
+    assert s1.fallback_columns >= m - m // 3
+    cfg = ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=30)
+    gs, g2 = ot.homotopy_solve(ps, cfg), ot.homotopy_solve(p2, cfg)
+    assert gs.fallback_columns == g2.fallback_columns > 0
+    assert gs.iterations == g2.iterations == 30
+    assert rel(gs.potentials.v, g2.potentials.v) <= 2e-6
+    q = O.Problem(a, b, ps.stored_cost(), cost_div=5e-4)
+    o = O.homotopy_solve(q, tol_l1=1e-300, max_total_inner=30)
+    assert rel(gs.potentials.v, o.v) <= 2e-6
