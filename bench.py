@@ -350,6 +350,9 @@ def main():
     torch.cuda.set_device(local_rank)
     distributed = world > 1 or args.shard
     if distributed:
+        if "RANK" not in os.environ:  # --shard at one rank without torchrun
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0",
+                              MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     x, y = ot.gen_config(cfg, N, M, C["seed"])
     a = np.full(N, 1.0 / N)
