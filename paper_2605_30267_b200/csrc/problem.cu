@@ -202,6 +202,10 @@ void problem_alloc_state(Problem& P) {
   P.ctrl = dalloc<Ctrl>(P, 1);
   P.trace = dalloc<double>(P, kTraceCap * kTraceCols);
   P.bounds = dalloc<double>(P, kBoundaryCap * kBoundCols);
+  // the reference solution's v* (energy / radii): allocated with the handle --
+  // the cached chunk graphs capture this pointer, so a later instrumented
+  // solve on the same handle must find it at the same address
+  P.vstar = dalloc<double>(P, P.mpad);
   OTG_CUDA(cudaMallocHost(&P.ctrl_host, sizeof(Ctrl)));
   OTG_CUDA(cudaMemsetAsync(P.p, 0, mp * sizeof(double), P.stream));
   OTG_CUDA(cudaMemsetAsync(P.wacc, 0, mp * sizeof(double), P.stream));

@@ -429,7 +429,6 @@ static void attach_reference(Problem& P, Ctrl& c, const double* v_star, double f
   if (!v_star) return;
   check_finite_vec(v_star, P.m, "reference v_star");
   if (!std::isfinite(f_star)) fail(OTG_E_OT, "reference f_star is not finite");
-  if (!P.vstar) P.vstar = dalloc<double>(P, P.mpad);
   h2d(P, P.vstar, v_star, P.m);
   c.have_ref = 1;
   c.f_star = f_star;

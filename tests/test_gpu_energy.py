@@ -110,3 +110,19 @@ def test_fp32_points_energy_columns():
     k = min(len(h.result.trace.records), len(o.trace))
     ge = np.array([r.energy for r in h.result.trace.records[:k]])
     assert np.all(np.abs(ge - o.trace[:k, 12]) <= 1e-5 * np.maximum(1.0, np.abs(o.trace[:k, 12])))
+
+
+def test_reference_solve_after_a_plain_solve_on_the_same_handle():
+    """The chunk graph is cached per handle: a reference-instrumented solve
+    after a plain one must find v* where the graph looks for it (round 2
+    fix: v* allocated with the handle, not at the first reference solve)."""
+    q = O.synthetic_rescaled(40, 30, 9, 0.05)
+    vs, fs = O.reference_solve(q, 1e-12)
+    p = ot.synthetic_rescaled(40, 30, 9, 0.05)
+    cfg = ot.HomotopyConfig(tol_l1=1e-9, record_trace=True)
+    plain = ot.homotopy_solve_instrumented(p, cfg, None)
+    instr = ot.AccelInstrumentation(reference=ot.ReferenceSolution(vs, fs), stability=True)
+    h = ot.homotopy_solve_instrumented(p, cfg, instr)
+    o = O.homotopy_solve(q, tol_l1=1e-9, record_trace=True, stability=True, reference=(vs, fs))
+    assert plain.result.iterations == h.result.iterations == o.iterations
+    close(h.result.trace.as_array(), o.trace, 1e-9)

@@ -408,3 +408,29 @@ def test_single_pass_zero_point_seed(solver):
     assert gf.iterations == g2.iterations == 40
     assert rel(gf.potentials.v, g2.potentials.v) <= 2e-6
     assert rel(gf.potentials.u, g2.potentials.u) <= 2e-6
+
+
+def test_single_pass_instrumented_trace_matches_two_pass():
+    """The steady single-pass graph runs the solver's control step inside the
+    patch/merge kernel: an instrumented homotopy solve (trace rows, stability
+    conditions, energy / radii against a reference solution) on a single-pass
+    handle matches the two-pass handle's trace to the fp32 bar, with the same
+    iteration count and condition counters."""
+    n, m, eps = 300, 4100, 2e-3
+    pf = _points_problem(n, m, 17, eps, True)
+    p2 = _points_problem(n, m, 17, eps, False)
+    assert pf.handle.info.sweep_mode == 2 and p2.handle.info.sweep_mode == 1
+    ref = ot.homotopy_solve(p2, ot.HomotopyConfig(tol_l1=1e-5, max_total_inner=3000))
+    instr = ot.AccelInstrumentation(
+        reference=ot.ReferenceSolution(ref.potentials.v, ref.final_reduced_f), stability=True)
+    cfg = ot.HomotopyConfig(tol_l1=1e-300, max_total_inner=40, record_trace=True)
+    hf = ot.homotopy_solve_instrumented(pf, cfg, instr)
+    h2 = ot.homotopy_solve_instrumented(p2, cfg, instr)
+    assert hf.result.iterations == h2.result.iterations == 40
+    assert hf.conditions_checked == h2.conditions_checked
+    tf, t2 = hf.result.trace.as_array(), h2.result.trace.as_array()
+    assert tf.shape == t2.shape and tf.shape[0] > 0
+    fin = np.isfinite(t2)
+    assert np.array_equal(np.isfinite(tf), fin)
+    d = np.abs(tf[fin] - t2[fin]) / np.maximum(1.0, np.abs(t2[fin]))
+    assert d.max() <= 1e-5, float(d.max())
