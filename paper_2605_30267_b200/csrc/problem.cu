@@ -65,34 +65,40 @@ __global__ void k_div_rows(double* __restrict__ C, int64_t ldc, int64_t n, int64
 }
 
 // raw cost of one pair, fp64, left-to-right without contraction (data.cpp:75-77, 98-99)
+// D > 0: the dimension as a compile-time constant (the same operations in the
+// same order, unrolled); D = 0: runtime d
+template <int D = 0>
 __device__ __forceinline__ double raw_cost(const double* __restrict__ x,
-                                           const double* __restrict__ y, int64_t d, int cost) {
+                                           const double* __restrict__ y, int64_t d_rt, int cost) {
+  const int64_t d = D > 0 ? D : d_rt;
   double s = 0.0;
   if (cost == OTG_COST_SQEUCLID) {
+#pragma unroll
     for (int64_t k = 0; k < d; ++k) {
       const double diff = __dsub_rn(x[k], y[k]);
       s = __dadd_rn(s, __dmul_rn(diff, diff));
     }
     return s;
   }
+#pragma unroll
   for (int64_t k = 0; k < d; ++k) s = __dadd_rn(s, __dmul_rn(x[k], y[k]));
   return __dadd_rn(-s, 1.0);
 }
 
 // pass 1: per-block (min, max) of the raw cost
+template <int D>
 __global__ void k_cost_minmax(const double* __restrict__ X, const double* __restrict__ Y,
                               int64_t n, int64_t m, int64_t d, int cost,
                               double2* __restrict__ out) {
   __shared__ double smn[kT], smx[kT];
   double mn = DBL_MAX, mx = -DBL_MAX;
-  const int64_t total = n * m;
-  for (int64_t t = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; t < total;
-       t += static_cast<int64_t>(gridDim.x) * kT) {
-    const int64_t i = t / m, j = t % m;
-    const double c = raw_cost(X + i * d, Y + j * d, d, cost);
-    mn = fmin(mn, c);
-    mx = fmax(mx, c);
-  }
+  // rows over the grid, columns over the CTA (no index division per pair)
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x)
+    for (int64_t j = threadIdx.x; j < m; j += kT) {
+      const double c = raw_cost<D>(X + i * d, Y + j * d, d, cost);
+      mn = fmin(mn, c);
+      mx = fmax(mx, c);
+    }
   smn[threadIdx.x] = mn;
   smx[threadIdx.x] = mx;
   __syncthreads();
@@ -108,14 +114,14 @@ __global__ void k_cost_minmax(const double* __restrict__ X, const double* __rest
 
 // pass 2: normalise and store. norm: NONE, MAX (c / mx), MINMAX ((c-mn)/(mx-mn)),
 // HALFRANGE (c / 2); then fp64 storage divides by eps (rescale), fp32 rounds.
-template <typename T>
+template <typename T, int D>
 __global__ void k_cost_store(const double* __restrict__ X, const double* __restrict__ Y,
                              int64_t n, int64_t m, int64_t d, int cost, int norm, double mn,
                              double mx, double eps_div, T* __restrict__ C, int64_t ldc) {
   for (int64_t i = blockIdx.y; i < n; i += gridDim.y)
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
        j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    double c = raw_cost(X + i * d, Y + j * d, d, cost);
+    double c = raw_cost<D>(X + i * d, Y + j * d, d, cost);
     if (norm == OTG_NORM_MAX) {
       if (mx > 0.0) c = c / mx;
     } else if (norm == OTG_NORM_MINMAX) {
@@ -511,7 +517,10 @@ otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const doub
       const int blocks = 148 * 8;
       double2* part = nullptr;
       OTG_CUDA(cudaMalloc(&part, blocks * sizeof(double2)));
-      k_cost_minmax<<<blocks, kT, 0, P.stream>>>(dX, dY, nl, m, d, cost, part);
+      if (d == 3)
+        k_cost_minmax<3><<<blocks, kT, 0, P.stream>>>(dX, dY, nl, m, d, cost, part);
+      else
+        k_cost_minmax<0><<<blocks, kT, 0, P.stream>>>(dX, dY, nl, m, d, cost, part);
       OTG_CUDA(cudaGetLastError());
       std::vector<double2> hp(blocks);
       OTG_CUDA(cudaMemcpyAsync(hp.data(), part, blocks * sizeof(double2), cudaMemcpyDeviceToHost, P.stream));
@@ -545,14 +554,22 @@ otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const doub
       P.storage = OTG_STORE_F64;
       P.C64 = dalloc<double>(P, static_cast<size_t>(nl) * P.ldc);
       OTG_CUDA(cudaMemsetAsync(P.C64, 0, static_cast<size_t>(nl) * P.ldc * sizeof(double), P.stream));
-      k_cost_store<double><<<grid, kT, 0, P.stream>>>(dX, dY, nl, m, d, cost, norm, mn, mx,
-                                                      epsilon, P.C64, P.ldc);
+      if (d == 3)
+        k_cost_store<double, 3><<<grid, kT, 0, P.stream>>>(dX, dY, nl, m, d, cost, norm, mn, mx,
+                                                           epsilon, P.C64, P.ldc);
+      else
+        k_cost_store<double, 0><<<grid, kT, 0, P.stream>>>(dX, dY, nl, m, d, cost, norm, mn, mx,
+                                                           epsilon, P.C64, P.ldc);
     } else {
       P.storage = OTG_STORE_F32;
       P.C32 = dalloc<float>(P, static_cast<size_t>(nl) * P.ldc);
       OTG_CUDA(cudaMemsetAsync(P.C32, 0, static_cast<size_t>(nl) * P.ldc * sizeof(float), P.stream));
-      k_cost_store<float><<<grid, kT, 0, P.stream>>>(dX, dY, nl, m, d, cost, norm, mn, mx, 1.0,
-                                                     P.C32, P.ldc);
+      if (d == 3)
+        k_cost_store<float, 3><<<grid, kT, 0, P.stream>>>(dX, dY, nl, m, d, cost, norm, mn, mx,
+                                                          1.0, P.C32, P.ldc);
+      else
+        k_cost_store<float, 0><<<grid, kT, 0, P.stream>>>(dX, dY, nl, m, d, cost, norm, mn, mx,
+                                                          1.0, P.C32, P.ldc);
     }
     OTG_CUDA(cudaGetLastError());
     OTG_CUDA(cudaStreamSynchronize(P.stream));
