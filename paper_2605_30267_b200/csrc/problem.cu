@@ -119,8 +119,12 @@ __global__ void k_cost_store(const double* __restrict__ X, const double* __restr
                              int64_t n, int64_t m, int64_t d, int cost, int norm, double mn,
                              double mx, double eps_div, T* __restrict__ C, int64_t ldc) {
   for (int64_t i = blockIdx.y; i < n; i += gridDim.y)
-  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < ldc;
        j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (j >= m) {  // row padding: zero (no separate memset of the whole matrix)
+      C[i * ldc + j] = static_cast<T>(0);
+      continue;
+    }
     double c = raw_cost<D>(X + i * d, Y + j * d, d, cost);
     if (norm == OTG_NORM_MAX) {
       if (mx > 0.0) c = c / mx;
@@ -553,7 +557,6 @@ otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const doub
     if (storage == OTG_STORE_F64) {
       P.storage = OTG_STORE_F64;
       P.C64 = dalloc<double>(P, static_cast<size_t>(nl) * P.ldc);
-      OTG_CUDA(cudaMemsetAsync(P.C64, 0, static_cast<size_t>(nl) * P.ldc * sizeof(double), P.stream));
       if (d == 3)
         k_cost_store<double, 3><<<grid, kT, 0, P.stream>>>(dX, dY, nl, m, d, cost, norm, mn, mx,
                                                            epsilon, P.C64, P.ldc);
@@ -563,7 +566,6 @@ otg_status otg_problem_create_points(int64_t n, int64_t m, int64_t d, const doub
     } else {
       P.storage = OTG_STORE_F32;
       P.C32 = dalloc<float>(P, static_cast<size_t>(nl) * P.ldc);
-      OTG_CUDA(cudaMemsetAsync(P.C32, 0, static_cast<size_t>(nl) * P.ldc * sizeof(float), P.stream));
       if (d == 3)
         k_cost_store<float, 3><<<grid, kT, 0, P.stream>>>(dX, dY, nl, m, d, cost, norm, mn, mx,
                                                           1.0, P.C32, P.ldc);
