@@ -53,9 +53,6 @@
 #ifndef OTG_FIN_SORTED_FB
 #define OTG_FIN_SORTED_FB 0  // k_finalize's folded fallback: column-sorted work items (32 KB smem)
 #endif
-#ifndef OTG_EPI_FUSED
-#define OTG_EPI_FUSED 0      // one-kernel epilogue with grid barriers (measured slower)
-#endif
 
 #include <nvtx3/nvToolsExt.h>  // (header-only NVTX v3: ranges cost nothing without a tool)
 
@@ -202,7 +199,7 @@ struct Ctrl {
   long long cond_checked, cond_held;
   long long live_kernels;
   unsigned int e1_counter, e2_counter, fb_count, redo_count;
-  unsigned int bar_count, bar_gen;  // software grid barrier of k_epilogue
+  unsigned int bar_count, bar_gen;  // (unused: the round-1 one-kernel epilogue's grid barrier)
   // fp32 row pass: shift estimate from the previous evaluation (sweep.cu)
   int shift_valid;    // rowM2 / vq describe the previous point, dmax2 the step
   int pad1;
@@ -342,7 +339,6 @@ struct Problem {
   int e_blocks = 1;
   double* e1_part = nullptr;  // e_blocks x 8
   double* e2_part = nullptr;  // e_blocks x 8
-  double* epi_part = nullptr; // single-kernel epilogue: 2 x kEpiMaxGrid x 8
   Ctrl* ctrl = nullptr;
   Ctrl* ctrl_host = nullptr;  // pinned mirror
   double* trace = nullptr;    // ring: trace_cap x kTraceCols

@@ -154,7 +154,7 @@ void problem_free(Problem& P) {
                   P.col_log,
                   P.y, P.grad, P.prev_grad,
                   P.prev_x, P.prev_y, P.flag_idx, P.fb_cols, P.fb_part, P.part, P.e1_part,
-                  P.e2_part, P.epi_part, P.sp_rec, P.sp_bad_rows, P.sp_bad_count, P.ctrl, P.trace, P.vstar, P.bounds, P.fbA, P.fbS, P.fbT, P.red, P.sp_sums, P.sp_cnt,
+                  P.e2_part, P.sp_rec, P.sp_bad_rows, P.sp_bad_count, P.ctrl, P.trace, P.vstar, P.bounds, P.fbA, P.fbS, P.fbT, P.red, P.sp_sums, P.sp_cnt,
                   P.perm_r, P.perm_c, P.Xs, P.Yns, P.cbox, P.rbox, P.cvmax, P.rnegm, P.ves, P.auxs,
                   P.sp_zM2, P.sp_zJ};
   for (void* q : ptrs)
@@ -207,7 +207,6 @@ void problem_alloc_state(Problem& P) {
   if (P.row_splits > 0) P.rpart = dalloc<double2>(P, static_cast<int64_t>(P.row_splits) * n);
   P.e1_part = dalloc<double>(P, (P.e_blocks + 1) * 8 + row_blocks(P) + 8);
   P.e2_part = dalloc<double>(P, P.e_blocks * 16);
-  P.epi_part = dalloc<double>(P, kEpiMaxGrid * (8 + 16));
   fused_alloc(P);
   P.ctrl = dalloc<Ctrl>(P, 1);
   P.trace = dalloc<double>(P, kTraceCap * kTraceCols);

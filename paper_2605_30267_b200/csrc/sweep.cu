@@ -2778,82 +2778,6 @@ k_apply(const AppArgs A, Ctrl* __restrict__ ctrl) {
 }
 
 
-// ------------------------------------------------------ fused epilogue ----
-// Merge + flag, exact fallback, finalize + control step and the vector update
-// of one evaluation in ONE launch: a cooperative grid (one CTA per SM) with
-// software grid barriers instead of four kernel boundaries.  Opt-in
-// (OTG_EPI_FUSED=1): measured on B200 it is SLOWER than the four launches
-// (256^2: 30 vs 20 us per evaluation; 65536^2: 108 vs 98 us) -- five grid
-// barriers cost more than three graph kernel boundaries.  Unsharded only.
-__device__ __forceinline__ void grid_sync(Ctrl* ctrl) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* gen = &ctrl->bar_gen;
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(&ctrl->bar_count, 1u) == gridDim.x - 1) {
-      ctrl->bar_count = 0;
-      __threadfence();
-      atomicAdd(&ctrl->bar_gen, 1u);
-    } else {
-      while (*gen == g) __nanosleep(20);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-struct EpiArgs {
-  const double* part;
-  int nshards, splits;
-  int64_t nrows;
-  int* fb_cols;
-  const double* u;
-  const double* a;
-  const double* C64;
-  CostSrc src;
-  int64_t ldc;
-  double kappa;
-  double2* fb_part;
-  int storage;
-  int fused_rows;
-  FinArgs F;
-  AppArgs P;
-};
-
-__global__ void __launch_bounds__(kEThreads)
-k_epilogue(const EpiArgs E, Ctrl* __restrict__ ctrl) {
-  pdl_wait();  // programmatic dependent launch: after the previous kernel
-  if (ctrl->done) return;  // uniform: written by an earlier launch
-  __shared__ double sh[kEThreads / 32 * 16];
-  const int blk = blockIdx.x, nblk = gridDim.x;
-  merge_body(E.part, E.nshards, E.splits, E.F.m, E.F.mpad, E.F.col, E.F.col_log,
-             const_cast<int*>(E.F.flag_idx), E.fb_cols, E.u, E.a, E.nrows, 1, 1, ctrl, blk, nblk,
-             sh, E.fused_rows, nblk);
-  grid_sync(ctrl);
-  const unsigned nf = *static_cast<volatile unsigned*>(&ctrl->fb_count);
-  if (nf > 0) {
-    if (E.storage == OTG_STORE_F64)
-      fallback_body<true, false>(E.C64, E.src, E.ldc, E.nrows, E.kappa, E.u, E.F.p, E.fb_cols,
-                                 E.fb_part, nf, blk, nblk, sh);
-    else if (E.storage == OTG_STORE_ON_THE_FLY)
-      fallback_body<false, true>(E.C64, E.src, E.ldc, E.nrows, E.kappa, E.u, E.F.p, E.fb_cols,
-                                 E.fb_part, nf, blk, nblk, sh);
-    else
-      fallback_body<false, false>(E.C64, E.src, E.ldc, E.nrows, E.kappa, E.u, E.F.p, E.fb_cols,
-                                  E.fb_part, nf, blk, nblk, sh);
-    grid_sync(ctrl);
-  }
-  finalize_cols(E.F, blk, nblk, sh);
-  grid_sync(ctrl);
-  if (blk == 0) finalize_tail(E.F, nblk, sh, ctrl);
-  grid_sync(ctrl);
-  if (!*static_cast<volatile int*>(&ctrl->live_e2)) return;  // uniform after the barrier
-  apply_cols(E.P, ctrl, blk, nblk, sh);
-  grid_sync(ctrl);
-  if (blk == 0) apply_tail(E.P, nblk, sh, ctrl);
-}
-
 int e_grid(int64_t m) {
   const int64_t blocks = (m + kEThreads - 1) / kEThreads;
   return static_cast<int>(blocks < 296 ? blocks : 296);
@@ -3406,60 +3330,9 @@ static AppArgs app_args(const Problem& P) {
 }
 
 // CTAs of the single-kernel epilogue (co-resident: <= one per SM), 0 = off.
-static int epilogue_grid(Problem& P) {
-  constexpr int env = OTG_EPI_FUSED;
-  if (!env || P.sharded) return 0;
-  if (P.epi_grid == 0) {
-    int sms = 0, occ = 0;
-    OTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.device));
-    OTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_epilogue, kEThreads, 0));
-    P.epi_grid = occ >= 1 ? std::min(sms, kEpiMaxGrid) : -1;
-  }
-  return std::max(P.epi_grid, 0);
-}
-
-static void launch_epilogue(Problem& P, int grid) {
-  EpiArgs E;
-  E.part = P.part;
-  E.nshards = P.vshards;
-  E.splits = P.col_splits;
-  E.fused_rows = P.fused ? P.fused_clusters + 1 : 0;
-  E.nrows = P.n_local;
-  E.fb_cols = P.fb_cols;
-  E.u = P.u;
-  E.a = P.a;
-  E.C64 = P.C64;
-  E.src = cost_src(P);
-  E.ldc = P.ldc;
-  E.kappa = P.kappa;
-  E.fb_part = P.fb_part;
-  E.storage = P.storage;
-  E.F = fin_args(P, grid);
-  E.F.e1_part = P.epi_part;
-  E.P = app_args(P);
-  E.P.e2_part = P.epi_part + kEpiMaxGrid * 8;  // (kEpiMaxGrid x kE2 after the e1 rows)
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(kEThreads);
-  cfg.stream = P.stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  OTG_CUDA(cudaLaunchKernelEx(&cfg, k_epilogue, E, P.ctrl));
-}
-
 void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
   P.apply_pending = 0;
   launch_sweeps(P, timed, ev4);
-  if (with_log) {
-    const int grid = epilogue_grid(P);
-    if (grid > 0) {
-      launch_epilogue(P, grid);
-      return;
-    }
-  }
   if (P.sharded) {
     // local merge into `red`, then THE collective of the evaluation: one
     // out-of-place all-reduce of the m column sums + <u, a> slices into col
