@@ -386,6 +386,8 @@ T* dalloc(Problem& P, size_t count) {
 }
 
 void problem_free(Problem& P);
+// E1 (finalize) partials: one per group of 32 consecutive columns
+__host__ __device__ inline int64_t e1_groups_of(int64_t m) { return (m + 31) / 32; }
 Problem& problem_of(otg_problem h);  // handle -> problem (sets the device)
 void problem_alloc_state(Problem& P);
 

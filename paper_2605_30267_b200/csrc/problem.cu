@@ -205,7 +205,7 @@ void problem_alloc_state(Problem& P) {
                                        static_cast<size_t>(P.fused_clusters) + 1);
   P.part = dalloc<double>(P, prow * mp);
   if (P.row_splits > 0) P.rpart = dalloc<double2>(P, static_cast<int64_t>(P.row_splits) * n);
-  P.e1_part = dalloc<double>(P, (P.e_blocks + 1) * 8 + row_blocks(P) + 8);
+  P.e1_part = dalloc<double>(P, (e1_groups_of(P.m) + 1) * 8 + row_blocks(P) + 8);
   P.e2_part = dalloc<double>(P, P.e_blocks * 16);
   fused_alloc(P);
   P.ctrl = dalloc<Ctrl>(P, 1);

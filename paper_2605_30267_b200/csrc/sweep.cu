@@ -2405,20 +2405,43 @@ __device__ __forceinline__ void store_e1(const FinArgs& A, int part, E1Acc& e, d
   }
 }
 
-// Per-column finalize of work unit blk of nblk; its partials -> e1_part[blk].
+// The E1 partials are per group of 32 consecutive columns (group g =
+// columns 32 g .. 32 g + 31, one warp, a fixed shuffle tree): k_finalize,
+// k_merge_fin and k_sp_patch_merge all produce them identically, so every
+// path sums the same partials in the same order.
+__device__ __forceinline__ void store_e1_warp(const FinArgs& A, int64_t g, E1Acc& e) {
+  const double s0 = warp_sum(e.s_abs), s1 = warp_sum(e.s_y), s2 = warp_sum(e.s_pb);
+  const double m0 = warp_max(e.mx_p), m1 = warp_max(e.bad);
+  if ((threadIdx.x & 31) == 0) {
+    double* dst = A.e1_part + g * 8;
+    dst[0] = s0;
+    dst[1] = s1;
+    dst[2] = s2;
+    dst[3] = m0;
+    dst[4] = m1;
+  }
+}
+
+// Per-column finalize of the 32-column groups of warp slots blk x warps ..
+// (stride nblk x warps); each group's partials -> e1_part[group].
 // defer: flagged columns are left to the last CTA (their fallback partials
 // are complete only once every CTA has run its share of the fallback).
 template <int NT = kEThreads>
 __device__ __forceinline__ void finalize_cols(const FinArgs& A, int blk, int nblk, double* shm,
                                               bool defer = false) {
-  E1Acc e;
-  for (int64_t j = static_cast<int64_t>(blk) * NT + threadIdx.x; j < A.m;
-       j += static_cast<int64_t>(nblk) * NT) {
-    const int slot = A.flag_idx[j];
-    if (defer && slot >= 0) continue;
-    finalize_col(A, j, slot, e);
+  (void)shm;
+  constexpr int W = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t G = e1_groups_of(A.m);
+  for (int64_t g = static_cast<int64_t>(blk) * W + w; g < G; g += static_cast<int64_t>(nblk) * W) {
+    E1Acc e;
+    const int64_t j = g * 32 + lane;
+    if (j < A.m) {
+      const int slot = A.flag_idx[j];
+      if (!(defer && slot >= 0)) finalize_col(A, j, slot, e);
+    }
+    store_e1_warp(A, g, e);
   }
-  store_e1<NT>(A, blk, e, shm);
 }
 
 template <int NT = kEThreads>
@@ -2509,7 +2532,7 @@ k_finalize(const FinArgs A, Ctrl* __restrict__ ctrl) {
   __syncthreads();
   if (!last) return;
   __threadfence();
-  int parts = gridDim.x;
+  int parts = static_cast<int>(e1_groups_of(A.m));
   if (nf > 0) {  // the flagged columns, in list order: one more partial
     E1Acc e;
     for (unsigned f = threadIdx.x; f < nf; f += kEThreads) {
@@ -2521,6 +2544,79 @@ k_finalize(const FinArgs A, Ctrl* __restrict__ ctrl) {
     ++parts;
   }
   finalize_tail(A, parts, sh, ctrl);
+}
+
+// Unsharded, single-shard solver evaluations (inside the chunk graph): the
+// merge of k_merge (one 32-column group per CTA, 8 warps over the splits,
+// the same 8-chain tree), its underflow flags and <u, a> slice, then warp 0
+// finalizes the group's unflagged columns into the group's E1 partial and
+// the last CTA runs the control step -- unless a column was flagged (then
+// k_finalize redoes the whole finalize with the exact column LSE).  Saves
+// k_finalize's launch and last-CTA round trip (cfg1: latency-bound).
+__global__ void __launch_bounds__(kEThreads)
+k_merge_fin(const double* __restrict__ part, int splits, int64_t m, int64_t mpad,
+            double* __restrict__ col, double* __restrict__ col_log, int* __restrict__ flag_idx,
+            int* __restrict__ fb_cols, const double* __restrict__ u, const double* __restrict__ a,
+            int64_t nrows, Ctrl* __restrict__ ctrl, int fused_rows, int ua_n, int patch_merged,
+            const FinArgs F) {
+  pdl_wait();  // programmatic dependent launch: after the previous kernel
+  if (ctrl->done) return;
+  if (patch_merged && ctrl->shift_valid) return;  // k_sp_patch_merge did this evaluation's merge
+  if (fused_rows && ctrl->shift_valid) splits = fused_rows;
+  __shared__ double sh[kEThreads / 32 * 8];
+  __shared__ double chain[kEThreads / 32][32];
+  __shared__ bool last;
+  const int blk = blockIdx.x, nblk = gridDim.x;
+  if (blk < ua_n) {  // <u, a> over row slice blk of ua_n (as merge_body)
+    const int64_t r0 = nrows * blk / ua_n, r1 = nrows * (blk + 1) / ua_n;
+    double t = 0.0;
+    for (int64_t k = r0 + threadIdx.x; k < r1; k += kEThreads) t += u[k] * a[k];
+    t = block_sum<kEThreads>(t, sh);
+    if (threadIdx.x == 0) col[mpad + 1 + blk] = t;
+  }
+  const double tiny = ctrl->tiny;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t grp = blk; grp * 32 < m; grp += nblk) {
+    const int64_t j = grp * 32 + lane;
+    const bool in = j < m;
+    double l = 0.0;
+    if (in)
+      for (int k = w; k < splits; k += 8) l += part[static_cast<int64_t>(k) * mpad + j];
+    chain[w][lane] = l;
+    __syncthreads();
+    if (w == 0) {
+      const double c = 0.0 + (((chain[0][lane] + chain[1][lane]) + (chain[2][lane] + chain[3][lane])) +
+                              ((chain[4][lane] + chain[5][lane]) + (chain[6][lane] + chain[7][lane])));
+      E1Acc e;
+      if (in) {
+        col[j] = c;
+        if (c >= tiny) {
+          col_log[j] = log(c);
+          flag_idx[j] = -1;
+          finalize_col(F, j, -1, e);
+        } else {
+          const unsigned slot = atomicAdd(&ctrl->fb_count, 1u);
+          fb_cols[slot] = static_cast<int>(j);
+          flag_idx[j] = static_cast<int>(slot);
+        }
+      }
+      store_e1_warp(F, grp, e);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&ctrl->e1_counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (*reinterpret_cast<volatile unsigned*>(&ctrl->fb_count) != 0u) {
+    if (threadIdx.x == 0) ctrl->e1_counter = 0;
+    return;
+  }
+  finalize_tail<kEThreads>(F, static_cast<int>(e1_groups_of(m)), sh, ctrl);
+  if (threadIdx.x == 0) ctrl->fin_done = 1;
 }
 
 // ------------------------------------------------------------------ E2 ----
@@ -2762,6 +2858,8 @@ __device__ __forceinline__ void apply_tail(const AppArgs& A, int nparts, double*
 __global__ void __launch_bounds__(kEThreads, 2)
 k_apply(const AppArgs A, Ctrl* __restrict__ ctrl) {
   pdl_wait();  // programmatic dependent launch: after the previous kernel
+  // (this evaluation's finalize is over: the next one starts unfinalized)
+  if (blockIdx.x == 0 && threadIdx.x == 0 && ctrl->fin_done) ctrl->fin_done = 0;
   if (!ctrl->live_e2) return;
   __shared__ double sh[kEThreads / 32 * 16];
   __shared__ bool last;
@@ -2962,7 +3060,7 @@ static unsigned resident_grid(const Problem& P, K kernel, int64_t blocks) {
 
 void launch_row_pass(Problem& P) {
   const int64_t blocks = row_blocks(P);
-  double* rowpart = P.e1_part + (P.e_blocks + 1) * 8;  // scratch after the E1 partials
+  double* rowpart = P.e1_part + (e1_groups_of(P.m) + 1) * 8;  // scratch after the E1 partials
   if (P.storage == OTG_STORE_F64) {
     const int G = precise_row_group(P);
     if (G == 32)
@@ -3192,9 +3290,10 @@ k_sp_patch_merge(const float* __restrict__ C, int64_t ldc, int64_t m, int64_t mp
     }
   }
   if (!fin_fuse) return;
-  // the E1 partials of this CTA's columns; the last CTA runs the solver's
-  // control step unless a column was flagged (then k_finalize does it all)
-  store_e1<kEThreads>(F, blk, e, sh);
+  // the E1 partials of this CTA's 32-column groups (one per warp); the last
+  // CTA runs the solver's control step unless a column was flagged (then
+  // k_finalize does it all)
+  store_e1_warp(F, static_cast<int64_t>(blk) * (kEThreads / 32) + (threadIdx.x >> 5), e);
   if (threadIdx.x == 0) {
     __threadfence();
     last = atomicAdd(&ctrl->e1_counter, 1u) == gridDim.x - 1;
@@ -3206,7 +3305,7 @@ k_sp_patch_merge(const float* __restrict__ C, int64_t ldc, int64_t m, int64_t mp
     if (threadIdx.x == 0) ctrl->e1_counter = 0;
     return;
   }
-  finalize_tail<kEThreads>(F, static_cast<int>(gridDim.x), sh, ctrl);
+  finalize_tail<kEThreads>(F, static_cast<int>(e1_groups_of(m)), sh, ctrl);
   if (threadIdx.x == 0) ctrl->fin_done = 1;
 }
 
@@ -3216,7 +3315,7 @@ void launch_sp_patch_merge(Problem& P, float kh, float kl, int nlists) {
   const unsigned g = static_cast<unsigned>(merge_blocks(P));
   // the finalize folds in only in the steady graph, with k_finalize's own
   // column partition (one 256-column work unit per CTA)
-  const int fin_fuse = (P.steady_capture && merge_blocks(P) == P.e_blocks) ? 1 : 0;
+  const int fin_fuse = P.steady_capture ? 1 : 0;
   launch_k(k_sp_patch_merge, g, kEThreads, 0, P.stream, static_cast<const float*>(P.C32), P.ldc,
            P.m, P.mpad, static_cast<const double*>(P.p), kh, kl,
            static_cast<const float4*>(P.aux), static_cast<const int*>(P.sp_bad_rows),
@@ -3234,10 +3333,21 @@ int64_t merge_blocks(const Problem& P) { return (P.m + kEThreads - 1) / kEThread
 // k_merge CTAs: 32 columns each (<u, a> slices: the first merge_blocks(P))
 static unsigned merge_grid(const Problem& P) { return static_cast<unsigned>((P.m + 31) / 32); }
 
+static FinArgs fin_args(const Problem& P, int64_t ua_slices);
+
 static void launch_merge(Problem& P, bool merge, bool flag) {
   const unsigned blocks = merge_grid(P);
   const int shards = P.vshards;
   const int splits = P.col_splits;
+  if (merge && flag && P.capturing && !P.sharded && P.vshards == 1) {
+    launch_k(k_merge_fin, blocks, kEThreads, 0, P.stream, P.part, splits, P.m, P.mpad, P.col,
+             P.col_log, P.flag_idx, P.fb_cols, static_cast<const double*>(P.u),
+             static_cast<const double*>(P.a), P.n_local, P.ctrl,
+             P.fused ? P.fused_clusters + 1 : 0, static_cast<int>(merge_blocks(P)),
+             patch_merges(P) ? 1 : 0, fin_args(P, merge_blocks(P)));
+    OTG_CUDA(cudaGetLastError());
+    return;
+  }
   launch_k(k_merge, blocks, kEThreads, 0, P.stream, P.part, shards, splits, P.m, P.mpad, P.col,
                                               P.col_log, P.flag_idx, P.fb_cols, P.u, P.a,
                                               P.n_local, merge ? 1 : 0, flag ? 1 : 0, P.ctrl,
