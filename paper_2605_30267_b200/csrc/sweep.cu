@@ -2506,7 +2506,7 @@ k_finalize(const FinArgs A, Ctrl* __restrict__ ctrl) {
   __shared__ bool last;
   // K5 folded in (unsharded): every CTA takes its share of the flagged
   // columns' exact LSE, the last CTA finalizes those columns
-  // flagged columns are finalized by the last CTA in list order whether the
+  // flagged columns are finalized by the last CTA in column order whether the
   // fallback ran here or (sharded) in k_fallback + the all-reduces, so the
   // two paths sum the E1 partials identically
   const unsigned nf = ctrl->fb_count;
@@ -2533,11 +2533,12 @@ k_finalize(const FinArgs A, Ctrl* __restrict__ ctrl) {
   if (!last) return;
   __threadfence();
   int parts = static_cast<int>(e1_groups_of(A.m));
-  if (nf > 0) {  // the flagged columns, in list order: one more partial
+  if (nf > 0) {  // the flagged columns, in COLUMN order (the list's slot order
+                 // comes from atomics): one more partial, deterministic
     E1Acc e;
-    for (unsigned f = threadIdx.x; f < nf; f += kEThreads) {
-      const int64_t j = A.fb_cols[f];
-      finalize_col(A, j, static_cast<int>(f), e);
+    for (int64_t j = threadIdx.x; j < A.m; j += kEThreads) {
+      const int slot = A.flag_idx[j];
+      if (slot >= 0) finalize_col(A, j, slot, e);
     }
     store_e1(A, parts, e, sh);
     __syncthreads();
