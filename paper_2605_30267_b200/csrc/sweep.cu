@@ -2613,7 +2613,13 @@ k_merge_fin(const double* __restrict__ part, int splits, int64_t m, int64_t mpad
   if (!last) return;
   __threadfence();
   if (*reinterpret_cast<volatile unsigned*>(&ctrl->fb_count) != 0u) {
-    if (threadIdx.x == 0) ctrl->e1_counter = 0;
+    // underflowed columns need the exact column LSE: pause the chunk (every
+    // later kernel of it returns); the host finishes this evaluation eagerly
+    // (k_finalize with the fallback, k_apply) and keeps replaying
+    if (threadIdx.x == 0) {
+      ctrl->e1_counter = 0;
+      ctrl->done = kPaused;
+    }
     return;
   }
   finalize_tail<kEThreads>(F, static_cast<int>(e1_groups_of(m)), sh, ctrl);
@@ -3303,7 +3309,13 @@ k_sp_patch_merge(const float* __restrict__ C, int64_t ldc, int64_t m, int64_t mp
   if (!last) return;
   __threadfence();
   if (*reinterpret_cast<volatile unsigned*>(&ctrl->fb_count) != 0u) {
-    if (threadIdx.x == 0) ctrl->e1_counter = 0;
+    // underflowed columns need the exact column LSE: pause the chunk (every
+    // later kernel of it returns); the host finishes this evaluation eagerly
+    // (k_finalize with the fallback, k_apply) and keeps replaying
+    if (threadIdx.x == 0) {
+      ctrl->e1_counter = 0;
+      ctrl->done = kPaused;
+    }
     return;
   }
   finalize_tail<kEThreads>(F, static_cast<int>(e1_groups_of(m)), sh, ctrl);
@@ -3316,7 +3328,7 @@ void launch_sp_patch_merge(Problem& P, float kh, float kl, int nlists) {
   const unsigned g = static_cast<unsigned>(merge_blocks(P));
   // the finalize folds in only in the steady graph, with k_finalize's own
   // column partition (one 256-column work unit per CTA)
-  const int fin_fuse = P.steady_capture ? 1 : 0;
+  const int fin_fuse = P.capturing ? 1 : 0;
   launch_k(k_sp_patch_merge, g, kEThreads, 0, P.stream, static_cast<const float*>(P.C32), P.ldc,
            P.m, P.mpad, static_cast<const double*>(P.p), kh, kl,
            static_cast<const float4*>(P.aux), static_cast<const int*>(P.sp_bad_rows),
@@ -3476,6 +3488,13 @@ void launch_eval(Problem& P, bool with_log, bool timed, cudaEvent_t* ev4) {
 // of flagged columns (sharded: local (top, sum) per column, MAX then SUM
 // all-reduce), then finalize.
 void launch_fallback_and_finalize(Problem& P) {
+  if (!P.sharded && P.capturing && P.vshards == 1) {
+    // the merge kernel (k_merge_fin / k_sp_patch_merge) finalizes every
+    // captured evaluation; one with underflowed columns pauses the chunk and
+    // the host runs this function eagerly (P.capturing = 0) for it
+    P.apply_pending = 1;
+    return;
+  }
   if (!P.sharded) {
     // K5 runs inside k_finalize (fin_args: fold_fb) -- no separate launch
     launch_k(k_finalize, P.e_blocks, kEThreads, 0, P.stream, fin_args(P, merge_blocks(P)), P.ctrl);
