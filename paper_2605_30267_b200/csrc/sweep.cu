@@ -1571,7 +1571,10 @@ __device__ __forceinline__ void flush_acc(float2& acc01, float2& acc23, double* 
 
 // Rows: warp = 256 consecutive sorted rows (8 per lane, 4 packed pairs);
 // blocks of kCullCB sorted columns, flushed / max-tracked per kOtfBlk.
-__global__ void __launch_bounds__(kCullRowT, (OTG_CULL_RT == 8 ? 512 : 768) / kCullRowT)
+#ifndef OTG_CULL_ROW_THREADS_PER_SM
+#define OTG_CULL_ROW_THREADS_PER_SM (OTG_CULL_RT == 8 ? 512 : 768)  // culled row pass: resident threads per SM
+#endif
+__global__ void __launch_bounds__(kCullRowT, OTG_CULL_ROW_THREADS_PER_SM / kCullRowT)
 k_row_otf_cull(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
                const double* __restrict__ dq, int64_t mpad, float kh,
                const double* __restrict__ rowM2, const int* __restrict__ rowJ,
@@ -1698,7 +1701,10 @@ k_row_otf_cull(const CostSrc src, int64_t n, int64_t m, const float* __restrict_
 
 // Columns: thread = 4 consecutive sorted columns, warp = 128; rows of the
 // split in blocks of kCullRB sorted rows, staged per warp when live.
-__global__ void __launch_bounds__(kCullColT, 512 / kCullColT)
+#ifndef OTG_CULL_COL_THREADS_PER_SM
+#define OTG_CULL_COL_THREADS_PER_SM 1024  // culled column pass: resident threads per SM the registers allow (64 regs; 512: 6.25 -> 1024: 6.06 ms at cfg5)
+#endif
+__global__ void __launch_bounds__(kCullColT, OTG_CULL_COL_THREADS_PER_SM / kCullColT)
 k_col_otf_cull(const CostSrc src, int64_t m, const double* __restrict__ p, float kh,
                const float4* __restrict__ aux, int64_t row_lo, int64_t row_hi,
                int64_t rows_per_split, double* __restrict__ part, int64_t mpad,
