@@ -1572,7 +1572,7 @@ __device__ __forceinline__ void flush_acc(float2& acc01, float2& acc23, double* 
 // Rows: warp = 256 consecutive sorted rows (8 per lane, 4 packed pairs);
 // blocks of kCullCB sorted columns, flushed / max-tracked per kOtfBlk.
 #ifndef OTG_CULL_ROW_THREADS_PER_SM
-#define OTG_CULL_ROW_THREADS_PER_SM (OTG_CULL_RT == 8 ? 512 : 768)  // culled row pass: resident threads per SM
+#define OTG_CULL_ROW_THREADS_PER_SM 512  // culled row pass: resident threads per SM (768: 6.14 -> 512: 6.10 ms at cfg5)
 #endif
 __global__ void __launch_bounds__(kCullRowT, OTG_CULL_ROW_THREADS_PER_SM / kCullRowT)
 k_row_otf_cull(const CostSrc src, int64_t n, int64_t m, const float* __restrict__ vq,
